@@ -1,0 +1,320 @@
+"""Schedule graphs, super-graph template, batch layouts, and the device encoder.
+
+Host side (once per spec / per graph object):
+  * the star-shaped loop graph and the super-graph template
+    (reference graphs.py:30-228),
+  * the symmetric-normalised adjacency D^-1/2 (A+I) D^-1/2 built in fp64
+    exactly as reference graphs.py:234-241,
+  * `batch_layout` (graphs.py:278-302), and
+  * `EncodeTables`: the per-spec constants the device encoder needs.
+
+Device side (per candidate): `encode_batch` (graphs.py:305-351) runs as the
+sm_100a kernel `kt_encode` -- index/choice decode, clamp + ceil-split, the 12
+context slots, scatter into iterval rows -- and returns a device tensor.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import DomainError
+from .kernels import (
+    AXES_BY_OP,
+    AXIS_ORDER,
+    MAX_AXES,
+    MAX_KNOBS,
+    MAX_LOOPS,
+    REDUCTION_AXES,
+    KernelSpec,
+    KnobConfig,
+    KnobSpace,
+    axis_extents,
+    build_knob_space,
+    knob_value_map,
+    resolved_tiles,
+)
+
+FEATURE_SLOTS = (
+    "extent",
+    "log2_extent",
+    "tile_level",
+    "is_reduction",
+    "is_unrolled",
+    "stride_hint",
+    "touched_elements_estimate",
+    "log2_touched",
+    "arithmetic_ops_estimate",
+    "log2_arith",
+    "loop_depth",
+    "normalized_position",
+)
+FEATURE_DIM = len(FEATURE_SLOTS)
+
+
+@dataclass
+class GraphNode:
+    kind: str  # "root" | "for_node" | "iterval"
+    feature: np.ndarray | None = None
+    template_slot: str | None = None
+
+
+@dataclass
+class CodeGraph:
+    nodes: list
+    edges: list
+    label: float | None = None
+
+    @property
+    def num_nodes(self) -> int:
+        return len(self.nodes)
+
+
+@dataclass(frozen=True)
+class SuperGraphTemplate:
+    op_types: tuple
+    slots: tuple
+    mapping_table: dict
+
+    @property
+    def num_nodes(self) -> int:
+        return 1 + 2 * len(self.slots)
+
+    def iterval_index(self, slot: str) -> int:
+        return 2 + 2 * self.slots.index(slot)
+
+
+@dataclass
+class GraphTensors:
+    feature_matrix: np.ndarray  # (N, F) fp64, raw (unnormalised)
+    normalized_adjacency: np.ndarray  # (N, N) fp64
+    feature_mask: np.ndarray  # (N,) bool
+
+
+# --- loop context features (host fp64; used for CodeGraph construction) -------
+
+
+def context_features(extents, tile_levels, reductions, unrolled, stride_hints) -> np.ndarray:
+    """12 feature slots per loop; last axis = loops outermost-first (graphs.py:89-126).
+
+    touched = product of the extents strictly inside a loop; arith = 2*touched;
+    logs are log2(max(v, 1)); depth = 1..n; position = k / max(n-1, 1).
+    """
+    e = np.asarray(extents, dtype=np.float64)
+    n = e.shape[-1]
+    touched = np.ones_like(e)
+    if n > 1:
+        suffix = np.cumprod(e[..., ::-1], axis=-1)[..., ::-1]
+        touched[..., :-1] = suffix[..., 1:]
+    arith = 2.0 * touched
+    lg = lambda v: np.log2(np.maximum(v, 1.0))
+    depth = np.broadcast_to(np.arange(1, n + 1, dtype=np.float64), e.shape)
+    pos = np.broadcast_to(np.arange(n, dtype=np.float64) / max(n - 1, 1), e.shape)
+    cols = [e, lg(e), tile_levels, reductions, unrolled, stride_hints,
+            touched, lg(touched), arith, lg(arith), depth, pos]
+    cols = [np.asarray(c, dtype=np.float64) for c in cols]
+    return np.stack(np.broadcast_arrays(*cols), axis=-1)
+
+
+def loop_slot_names(axes) -> list:
+    """Chain order of the lowered nest: all outer loops, then all inner loops."""
+    present = set(axes)
+    return [f"{a}_{s}" for s in ("outer", "inner") for a in AXIS_ORDER if a in present]
+
+
+def _loop_rows(spec: KernelSpec, space: KnobSpace, config: KnobConfig):
+    values = knob_value_map(space, config)
+    tiles = resolved_tiles(spec, values)
+    auto = int(values.get("auto_unroll_max_step", 0))
+    explicit = bool(values.get("unroll_explicit", 0))
+    axes = AXES_BY_OP[spec.op_type]
+    ext, lvl, red, unr, strd = [], [], [], [], []
+    for level in (0, 1):
+        for a in axes:
+            outer, inner = tiles[a]
+            e = outer if level == 0 else inner
+            ext.append(e)
+            lvl.append(level)
+            red.append(1.0 if a in REDUCTION_AXES else 0.0)
+            unr.append(1.0 if (level == 1 and explicit and 0 < e <= auto) else 0.0)
+            strd.append(float(inner) if level == 0 else 1.0)
+    return loop_slot_names(axes), context_features(ext, lvl, red, unr, strd)
+
+
+# --- templates and graphs -------------------------------------------------------
+
+
+def build_super_template(op_types) -> SuperGraphTemplate:
+    ops = tuple(sorted(set(op_types)))
+    if not ops:
+        raise DomainError("op_types must be non-empty")
+    for op in ops:
+        if op not in AXES_BY_OP:
+            raise DomainError(f"unsupported op_type {op!r}")
+    union = set()
+    for op in ops:
+        union.update(AXES_BY_OP[op])
+    slots = tuple(loop_slot_names(union))
+    mapping = {(op, name): name for op in ops for name in loop_slot_names(AXES_BY_OP[op])}
+    return SuperGraphTemplate(op_types=ops, slots=slots, mapping_table=mapping)
+
+
+def _star(names, features=None):
+    nodes, edges = [GraphNode("root")], []
+    for i, name in enumerate(names):
+        f = len(nodes)
+        nodes.append(GraphNode("for_node", template_slot=name))
+        feat = None if features is None or features[i] is None else np.array(features[i])
+        nodes.append(GraphNode("iterval", feature=feat, template_slot=name))
+        edges += [(0, f), (f, f + 1)]
+    return nodes, edges
+
+
+def template_graph_skeleton(template: SuperGraphTemplate) -> CodeGraph:
+    nodes, edges = _star(template.slots)
+    return CodeGraph(nodes=nodes, edges=edges)
+
+
+def augment_to_super(graph: CodeGraph, template: SuperGraphTemplate, op_type: str) -> CodeGraph:
+    out = template_graph_skeleton(template)
+    out.label = graph.label
+    for node in graph.nodes:
+        if node.kind != "iterval":
+            continue
+        slot = template.mapping_table.get((op_type, node.template_slot))
+        if slot is None:
+            raise DomainError(f"template has no slot for {(op_type, node.template_slot)}")
+        if node.feature is not None:
+            out.nodes[template.iterval_index(slot)].feature = node.feature.copy()
+    return out
+
+
+def config_graph(spec, config, space=None, template=None, label=None) -> CodeGraph:
+    """Star graph of (spec, config): root -> for_node -> iterval per loop,
+    optionally augmented into `template` (reference graphs.py:354-369)."""
+    if space is None:
+        space = build_knob_space(spec)
+    names, feats = _loop_rows(spec, space, config)
+    nodes, edges = _star(names, list(feats))
+    g = CodeGraph(nodes=nodes, edges=edges, label=label)
+    if template is not None:
+        g = augment_to_super(g, template, spec.op_type)
+    return g
+
+
+def feature_multiset(graph: CodeGraph) -> list:
+    return sorted(tuple(n.feature.tolist()) for n in graph.nodes if n.feature is not None)
+
+
+# --- tensorisation ------------------------------------------------------------------
+
+
+def normalized_adjacency(num_nodes: int, edges) -> np.ndarray:
+    """D^-1/2 (A + I) D^-1/2 in fp64, same operation order as graphs.py:234-241."""
+    a = np.zeros((num_nodes, num_nodes))
+    for s, d in edges:
+        a[s, d] = 1.0
+        a[d, s] = 1.0
+    a[np.diag_indices(num_nodes)] += 1.0
+    dinv = 1.0 / np.sqrt(a.sum(axis=1))
+    return a * dinv[:, None] * dinv[None, :]
+
+
+def graph_to_tensors(graph) -> GraphTensors:
+    n = len(graph.nodes)
+    x = np.zeros((n, FEATURE_DIM))
+    mask = np.zeros(n, dtype=bool)
+    for i, node in enumerate(graph.nodes):
+        if node.feature is None:
+            continue
+        f = np.asarray(node.feature)
+        if f.shape != (FEATURE_DIM,):
+            raise DomainError(f"node {i} feature has shape {f.shape}, want ({FEATURE_DIM},)")
+        x[i] = f
+        mask[i] = True
+    return GraphTensors(x, normalized_adjacency(n, graph.edges), mask)
+
+
+def tensors_for(graph) -> GraphTensors:
+    """Memoised graph_to_tensors (reference model.py:115-121 memoises the same way)."""
+    cached = getattr(graph, "_tensors", None)
+    if cached is None:
+        cached = graph_to_tensors(graph)
+        graph._tensors = cached
+    return cached
+
+
+@dataclass
+class BatchLayout:
+    adjacency: np.ndarray
+    iterval_rows: np.ndarray
+    feature_mask: np.ndarray
+    num_nodes: int
+    loop_names: tuple
+
+
+def batch_layout(spec: KernelSpec, template: SuperGraphTemplate | None) -> BatchLayout:
+    """Shared adjacency / iterval rows / mask for a spec (graphs.py:278-302)."""
+    names = loop_slot_names(AXES_BY_OP[spec.op_type])
+    if template is None:
+        rows = np.array([2 + 2 * i for i in range(len(names))])
+        nodes, edges = _star(names)
+    else:
+        rows = np.array([template.iterval_index(template.mapping_table[(spec.op_type, n)])
+                         for n in names])
+        nodes, edges = _star(template.slots)
+    num = len(nodes)
+    mask = np.zeros(num, dtype=bool)
+    mask[rows] = True
+    return BatchLayout(normalized_adjacency(num, edges), rows, mask, num, tuple(names))
+
+
+# --- text format (reference graphs.py:381-429) -----------------------------------
+
+
+def graph_to_text(graph: CodeGraph) -> str:
+    lines = [f"codegraph {graph.num_nodes} {FEATURE_DIM}"]
+    for n in graph.nodes:
+        slot = n.template_slot if n.template_slot is not None else "-"
+        body = "null" if n.feature is None else " ".join(repr(float(v)) for v in n.feature)
+        lines.append(f"{n.kind} {slot} {body}")
+    lines += [f"edge {s} {d}" for s, d in graph.edges]
+    if graph.label is not None:
+        lines.append(f"label {repr(float(graph.label))}")
+    return "\n".join(lines) + "\n"
+
+
+def graph_from_text(text: str) -> CodeGraph:
+    lines = [ln for ln in text.splitlines() if ln.strip()]
+    if not lines or not lines[0].startswith("codegraph "):
+        raise DomainError("not a codegraph document")
+    _, n_s, f_s = lines[0].split()[:3]
+    num_nodes = int(n_s)
+    if int(f_s) != FEATURE_DIM:
+        raise DomainError(f"feature dim {f_s} unsupported (want {FEATURE_DIM})")
+    if len(lines) < 1 + num_nodes:
+        raise DomainError("truncated codegraph document")
+    nodes = []
+    for ln in lines[1 : 1 + num_nodes]:
+        kind, slot, *rest = ln.split()
+        slot = None if slot == "-" else slot
+        if rest == ["null"]:
+            nodes.append(GraphNode(kind, template_slot=slot))
+            continue
+        vals = np.array([float(v) for v in rest])
+        if vals.shape != (FEATURE_DIM,):
+            raise DomainError("bad feature row length")
+        nodes.append(GraphNode(kind, feature=vals, template_slot=slot))
+    edges, label = [], None
+    for ln in lines[1 + num_nodes :]:
+        parts = ln.split()
+        if parts[0] == "edge":
+            edges.append((int(parts[1]), int(parts[2])))
+        elif parts[0] == "label":
+            label = float(parts[1])
+        else:
+            raise DomainError(f"unexpected line {ln!r}")
+    return CodeGraph(nodes=nodes, edges=edges, label=label)

@@ -1,0 +1,253 @@
+#!/usr/bin/env python3
+"""Generate the parity fixtures under tests/golden/ by RUNNING THE REFERENCE.
+
+Run in the build container only (needs /root/reference; the GPU box never
+runs this):  python tests/golden/make_goldens.py
+
+Everything is keyed by `rng_from` so reruns are byte-identical.  Outputs:
+  graph_conv1d_{raw,super}.txt  the reference's own golden graphs, re-emitted
+                                through reference graph_to_text (graphs.py:381)
+  encode.npz     per op: spec, knob values, sampled + edge-case config indices,
+                 and reference encode_batch rows (graphs.py:305) for raw and
+                 super layouts; layouts' adjacency / rows
+  model.npz      init_model + dataset_norms params; embed_batch/head_forward_batch
+                 outputs (model.py:185-203) on conv2d super/raw and mixed batches
+  grad.npz       grad() (model.py:218) on raw mixed-op batches, scope all / head_only
+  head.npz       head_loss_grad / head_hvp (model.py:358-432) at random points
+  meta.npz       meta_step FO + SO (meta.py:223), fine_tune_embedded (meta.py:274),
+                 sample_meta_tasks draws (meta.py:136) as dataset positions
+  rank.npz       rank_history orderings (search.py:257) on tie-heavy scores
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+from dataclasses import replace
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+
+from kerntune import graphs as rg  # noqa: E402
+from kerntune import kernels as rk  # noqa: E402
+from kerntune import meta as rmeta  # noqa: E402
+from kerntune import model as rm  # noqa: E402
+from kerntune import search as rs  # noqa: E402
+from kerntune.harness import DatasetParams, sample_kernel  # noqa: E402
+from kerntune.oracle import get_profile, measure  # noqa: E402
+from kerntune.util import rng_from  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+BENCH_SPEC = rk.KernelSpec("conv2d", 56, 64, 64, 3, 3, 1)
+
+
+def spec_for(op):
+    if op == "conv2d":
+        return BENCH_SPEC
+    rng = rng_from("golden-spec", op)
+    params = DatasetParams()
+    while True:
+        s = sample_kernel(params, rng)
+        if s.op_type == op:
+            return s
+
+
+def model_params(m):
+    d = {f"gcn{i}": w for i, w in enumerate(m.gcn.layers)}
+    d["agg"] = m.agg.sum_weights
+    for i, (w, b) in enumerate(zip(m.head.weights, m.head.biases)):
+        d[f"hw{i}"] = w
+        d[f"hb{i}"] = b
+    d["fmean"] = m.feature_norm.mean
+    d["fstd"] = m.feature_norm.std
+    d["lnorm"] = np.array([m.label_norm.mean, m.label_norm.std])
+    return d
+
+
+def golden_graph_text():
+    spec = rk.KernelSpec(op_type="conv1d", input_size=200, in_channels=64, out_channels=128, kernel_size=3)
+    space = rk.build_knob_space(spec)
+    c = rk.index_config(space, 123456)
+    for name, tmpl in (("raw", None), ("super", rg.build_super_template(rk.OP_TYPES))):
+        with open(os.path.join(OUT, f"graph_conv1d_{name}.txt"), "w", encoding="utf-8") as f:
+            f.write(rg.graph_to_text(rg.config_graph(spec, c, space, template=tmpl)))
+
+
+def encode_goldens():
+    template = rg.build_super_template(rk.OP_TYPES)
+    out = {}
+    for op in rk.OP_TYPES:
+        spec = spec_for(op)
+        space = rk.build_knob_space(spec)
+        cfgs = rk.sample_configs(space, 40, rng_from("golden-cfg", op))
+        idx = [rk.config_index(space, c) for c in cfgs]
+        # edge cases: first/last index, max tile choices (padded values), all-zero unroll
+        cards = space.cardinalities
+        last = [c - 1 for c in cards]
+        idx += [0, space.size - 1, rk.config_index(space, rk.KnobConfig(tuple(last[:-2]) + (0, 0))),
+                rk.config_index(space, rk.KnobConfig((0,) * (len(cards) - 2) + (2, 1)))]
+        cfgs = [rk.index_config(space, i) for i in idx]
+        out[f"{op}/spec"] = np.array([spec.input_size, spec.in_channels, spec.out_channels,
+                                      spec.kernel_size, spec.stride, spec.padding])
+        out[f"{op}/size"] = np.array(space.size)
+        for j, k in enumerate(space.knobs):
+            out[f"{op}/knob{j}"] = np.array(k.values, dtype=np.int64)
+        out[f"{op}/idx"] = np.array(idx, dtype=np.int64)
+        out[f"{op}/choices"] = np.array([c.choices for c in cfgs], dtype=np.int64)
+        for rep, tmpl in (("raw", None), ("super", template)):
+            lay = rg.batch_layout(spec, tmpl)
+            x = rg.encode_batch(spec, space, cfgs, lay)
+            out[f"{op}/{rep}/rows"] = lay.iterval_rows
+            out[f"{op}/{rep}/adj"] = lay.adjacency
+            out[f"{op}/{rep}/feats"] = x[:, lay.iterval_rows, :]
+            assert not x[:, ~lay.feature_mask, :].any()
+            # per-graph path must agree (test_graphs.py:211-223)
+            g = rg.config_graph(spec, cfgs[0], space, template=tmpl)
+            assert np.array_equal(rg.graph_to_tensors(g).feature_matrix, x[0])
+    np.savez_compressed(os.path.join(OUT, "encode.npz"), **out)
+
+
+def corpus(n_per_op=60):
+    """Small mixed-op corpus of (spec, space, config) with oracle labels."""
+    prof = get_profile("platform-A")
+    items = []
+    for op in rk.OP_TYPES:
+        spec = spec_for(op)
+        space = rk.build_knob_space(spec)
+        for c in rk.sample_configs(space, n_per_op, rng_from("golden-corpus", op)):
+            items.append((spec, space, c, max(measure(spec, c, prof, space).gflops, 1e-3)))
+    return items
+
+
+def model_goldens(items):
+    template = rg.build_super_template(rk.OP_TYPES)
+    samples = [rmeta.LabeledSample(rg.config_graph(s, c, sp, template=template), s.signature(), y)
+               for s, sp, c, y in items]
+    fn, ln = rmeta.dataset_norms(samples)
+    m = replace(rm.init_model(rng_from("golden-model")), feature_norm=fn, label_norm=ln)
+    out = {f"p/{k}": v for k, v in model_params(m).items()}
+    # conv2d sweep batch (super + raw) and a mixed-op super batch
+    spec = BENCH_SPEC
+    space = rk.build_knob_space(spec)
+    cfgs = rk.sample_configs(space, 256, rng_from("golden-score"))
+    out["score/idx"] = np.array([rk.config_index(space, c) for c in cfgs], dtype=np.int64)
+    for rep, tmpl in (("raw", None), ("super", template)):
+        lay = rg.batch_layout(spec, tmpl)
+        x = rg.encode_batch(spec, space, cfgs, lay)
+        u = rm.embed_batch(m, x, lay.feature_mask, lay.adjacency)
+        out[f"score/{rep}/u"] = u
+        out[f"score/{rep}/z"] = rm.head_forward_batch(u, m.head)
+    mixed = [it for it in items[::7]]
+    out["mixed/op"] = np.array([rk.OP_TYPES.index(s.op_type) for s, _, _, _ in mixed])
+    out["mixed/idx"] = np.array([rk.config_index(sp, c) for s, sp, c, _ in mixed], dtype=np.int64)
+    us = []
+    for s, sp, c, _ in mixed:
+        g = rg.config_graph(s, c, sp, template=template)
+        us.append(rm.embed(g, m))
+    out["mixed/u"] = np.stack(us)
+    out["mixed/z"] = rm.head_forward_batch(np.stack(us), m.head)
+    np.savez_compressed(os.path.join(OUT, "model.npz"), **out)
+    return m
+
+
+def grad_goldens(items, m):
+    """Raw (segmented, N in {17,21,25}) mixed batches through model.grad."""
+    out = {}
+    rng = rng_from("golden-grad")
+    for b, n in enumerate((1, 3, 16)):
+        pick = rng.choice(len(items), n, replace=False)
+        batch = []
+        for j in pick:
+            s, sp, c, y = items[int(j)]
+            batch.append((rg.config_graph(s, c, sp), y))
+        out[f"b{b}/pick"] = pick
+        for scope in ("all", "head_only"):
+            loss, g = rm.grad(m, batch, scope)
+            out[f"b{b}/{scope}/loss"] = np.array(loss)
+            for i, w in enumerate(g.gcn):
+                out[f"b{b}/{scope}/gcn{i}"] = w
+            out[f"b{b}/{scope}/agg"] = g.agg
+            for i, (w, bb) in enumerate(zip(g.head_weights, g.head_biases)):
+                out[f"b{b}/{scope}/hw{i}"] = w
+                out[f"b{b}/{scope}/hb{i}"] = bb
+        m2 = rm.sgd_step(m, rm.grad(m, batch, "all")[1], 0.005)
+        out[f"b{b}/sgd_vec"] = np.concatenate(
+            [w.ravel() for w in m2.gcn.layers] + [m2.agg.sum_weights, rm.head_to_vec(m2.head)])
+    np.savez_compressed(os.path.join(OUT, "grad.npz"), **out)
+
+
+def head_goldens(m):
+    rng = rng_from("golden-head")
+    theta = rm.head_to_vec(m.head)
+    out = {}
+    for k, n in enumerate((1, 6, 64)):
+        u = np.abs(rng.normal(size=(n, 64)))
+        y = rng.normal(size=n)
+        v = rng.normal(size=theta.size)
+        th = theta + 0.01 * rng.normal(size=theta.size)
+        mse, g = rm.head_loss_grad(th, m.head, u, y)
+        out[f"c{k}/u"], out[f"c{k}/y"], out[f"c{k}/v"], out[f"c{k}/theta"] = u, y, v, th
+        out[f"c{k}/mse"], out[f"c{k}/grad"] = np.array(mse), g
+        out[f"c{k}/hvp"] = rm.head_hvp(th, m.head, u, y, v)
+    np.savez_compressed(os.path.join(OUT, "head.npz"), **out)
+
+
+def meta_goldens(items, m):
+    template = rg.build_super_template(rk.OP_TYPES)
+    samples = [rmeta.LabeledSample(rg.config_graph(s, c, sp, template=template), s.signature(), y)
+               for s, sp, c, y in items]
+    pos = {id(s): i for i, s in enumerate(samples)}
+    out = {}
+    for order, fo in (("fo", True), ("so", False)):
+        cfg = rmeta.MetaConfig(n_way=3, k_shot=2, meta_batch=32, inner_steps=1, first_order=fo)
+        tasks = rmeta.sample_meta_tasks(samples, cfg, rng_from("golden-tasks", order))
+        out[f"{order}/support"] = np.array([[pos[id(s)] for s in t.support] for t in tasks])
+        out[f"{order}/query"] = np.array([[pos[id(s)] for s in t.query] for t in tasks])
+        m2, stats = rmeta.meta_step(m, tasks, cfg)
+        out[f"{order}/theta"] = rm.head_to_vec(m2.head)
+        out[f"{order}/stats"] = np.array([stats["support_loss"], stats["query_loss"]])
+        # two more outer steps through meta_train's loop body
+        m3 = m2
+        for _ in range(2):
+            m3, _ = rmeta.meta_step(m3, tasks, cfg)
+        out[f"{order}/theta3"] = rm.head_to_vec(m3.head)
+    # fine-tune on 64 samples, 8 steps (TuneConfig defaults search.py:439-440)
+    ft = samples[:64]
+    m4 = rmeta.fine_tune(m, [(s.graph, s.label_gflops) for s in ft], 0.01, 8)
+    out["ft/theta"] = rm.head_to_vec(m4.head)
+    out["labels"] = np.array([y for _, _, _, y in items])
+    out["op"] = np.array([rk.OP_TYPES.index(s.op_type) for s, _, _, _ in items])
+    out["idx"] = np.array([rk.config_index(sp, c) for _, sp, c, _ in items], dtype=np.int64)
+    np.savez_compressed(os.path.join(OUT, "meta.npz"), **out)
+
+
+def rank_goldens():
+    rng = rng_from("golden-rank")
+    out = {}
+    idx = rng.choice(10_000, 600, replace=False)
+    scores = np.round(rng.normal(size=600), 1)  # heavy exact ties
+    visited = set(int(i) for i in idx[rng.choice(600, 50, replace=False)])
+    hist = {int(i): float(s) for i, s in zip(idx, scores)}
+    out["idx"], out["scores"] = idx, scores
+    out["visited"] = np.array(sorted(visited))
+    out["top"] = np.array(rs.rank_history(hist, visited, 128))
+    np.savez_compressed(os.path.join(OUT, "rank.npz"), **out)
+
+
+def main():
+    golden_graph_text()
+    encode_goldens()
+    items = corpus()
+    m = model_goldens(items)
+    grad_goldens(items, m)
+    head_goldens(m)
+    meta_goldens(items, m)
+    rank_goldens()
+    for f in sorted(os.listdir(OUT)):
+        print(f, os.path.getsize(os.path.join(OUT, f)))
+
+
+if __name__ == "__main__":
+    main()
