@@ -1,0 +1,373 @@
+#!/usr/bin/env python3
+"""Headline benchmark: candidate graphs/sec scored (C5 sweep), one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Workload (BASELINE.json configs[4], weak-scaled): every rank scores its own
+shard of 1,048,576 conv2d schedule graphs per step (spec conv2d 56x64x64 k3
+s3 p1, super-graph layout N=25, random config indices from
+rng_from("sweep", rank)) through the fused sm_100a scorer and keeps the top-512
+by (score desc, index asc); with N>1 the per-rank top-k lists are all-gathered
+over NCCL and merged on device (the only exchange step of the path).
+`value` = N x 1,048,576 / (max over ranks of the device time per step).
+`e2e` repeats the step through the public API with the indices in pinned host
+memory and the scores + top-k copied back (Sweeper.run_host).
+Timed steps rotate over a 192 MiB index pool (> 126 MB L2).
+`--impl reference` times the oracle port of the reference's scoring path
+(fp64 numpy, all host cores) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "candidate graphs/sec scored; MAML meta-train tasks/sec at 1/2/4/8 B200"
+BATCH = 1 << 20
+TOPK = 512
+POOL_SLICES = 24
+SPEC_ARGS = ("conv2d", 56, 64, 64, 3, 3, 1)
+FLOP_PER_GRAPH = 2 * (12 * 12 * 32 + 12 * 32 * 32 + 64 * 64 + 64 * 64 + 64)  # star-factored MACs x 2
+REF_FLOP_PER_GRAPH = 95065  # dense 25-node evaluation
+FP32_PEAK_TFLOPS = 71.4  # measured in-repo, tools/fma_peak.cu (profiles/r01_fp32_peak.md)
+LABEL_NORM = (-5.62, 7.08)  # conftest corpus statistics
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# --- setup ------------------------------------------------------------------------
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")), ws
+
+
+def bench_model(dev):
+    """init_model(rng_from("bench-model")) with feature norms of the bench corpus."""
+    import torch
+
+    from paper_2102_04199_b200 import graphs as pg
+    from paper_2102_04199_b200 import kernels as pk
+    from paper_2102_04199_b200 import model as pm
+    from paper_2102_04199_b200.util import rng_from
+
+    m = pm.init_model(rng_from("bench-model"), device=dev)
+    tmpl = pg.build_super_template(pk.OP_TYPES)
+    rows = []
+    for op in ("conv2d", "winograd", "depthwise"):
+        spec = pk.KernelSpec(op, 56, 64, 64, 3, 3, 1)
+        space = pk.build_knob_space(spec)
+        lay = pg.batch_layout(spec, tmpl)
+        idx = rng_from("bench-norms", op).integers(0, space.size, 4096)
+        x = pg.encode_batch(spec, space, idx, lay, device=dev).cpu().numpy()
+        rows.append(x[:, lay.iterval_rows, :].reshape(-1, 12))
+    stacked = np.concatenate(rows)
+    std = stacked.std(axis=0)
+    fn = pm.FeatureNorm(stacked.mean(axis=0), np.where(std < 1e-12, 1.0, std))
+    return pm.model_from_flat(m._flat, m, feature_norm=fn, label_norm=pm.LabelNorm(*LABEL_NORM))
+
+
+def oracle_params(m):
+    """fp64 copy of the device model for the CPU oracle (exact upcast of fp32)."""
+    h = lambda t: t.detach().double().cpu().numpy()
+    return {"gcn": [h(w) for w in m.gcn.layers], "agg": h(m.agg.sum_weights),
+            "head_w": [h(w) for w in m.head.weights], "head_b": [h(b) for b in m.head.biases],
+            "fmean": m.feature_norm.mean, "fstd": m.feature_norm.std,
+            "lmean": m.label_norm.mean, "lstd": m.label_norm.std}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(gpu_index), "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], 0, set()
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                s, m_ = float(parts[0]), float(parts[1])
+            except ValueError:
+                continue
+            sm.append(s)
+            mx = max(mx, m_)
+            for name, v in zip(self.NAMES, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        load = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": float(np.median(load)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "r01_ncu_score.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        if int(d.get("batch", 0)) == BATCH:
+            return float(d["dram_bytes_per_launch"])
+    except (OSError, ValueError, KeyError):
+        pass
+    return None
+
+
+# --- CPU arms -------------------------------------------------------------------------
+
+
+def cpu_sweep(m_params, n, seed_rank=0):
+    from oracle import cpu_baseline
+    from paper_2102_04199_b200.util import rng_from
+
+    idx = rng_from("sweep", seed_rank).integers(0, 451_584_000, n)
+    secs, procs, _ = cpu_baseline.time_sweep(m_params, SPEC_ARGS[0], SPEC_ARGS[1:], True, idx)
+    return n / secs, procs, secs
+
+
+def run_reference(args):
+    """--impl reference: oracle port of the reference scoring path on host cores."""
+    rank, _, ws = dist_env()
+    if rank != 0:
+        return 0
+    import torch
+
+    from oracle import cpu_baseline, kt_oracle as ko
+    from paper_2102_04199_b200.util import rng_from
+
+    # same model as our arm, built on the host (fp64 draws; norms from the oracle encoder)
+    p = ko.init_params(rng_from("bench-model"))
+    p = {k: ([np.float32(w).astype(np.float64) for w in v] if isinstance(v, list) else v) for k, v in p.items()}
+    op, sargs = SPEC_ARGS[0], SPEC_ARGS[1:]
+    rows = []
+    for o in ("conv2d", "winograd", "depthwise"):
+        ext = ko.extents(o, *sargs)
+        knobs = ko.knob_lists(o, ext)
+        adj, rr, mask = ko.layout(o, True)
+        size = int(np.prod([len(v) for _, v in knobs]))
+        ch = ko.decode([len(v) for _, v in knobs], rng_from("bench-norms", o).integers(0, size, 4096))
+        rows.append(ko.loop_features(o, ext, knobs, ch).reshape(-1, 12))
+    st = np.concatenate(rows)
+    p["fmean"], p["fstd"] = st.mean(axis=0), np.where(st.std(axis=0) < 1e-12, 1.0, st.std(axis=0))
+    p["lmean"], p["lstd"] = LABEL_NORM
+    # bounded per-step sample so W + K steps stay within a few minutes of CPU time
+    n = args.ref_sample or (65536 if args.steps + args.warmup <= 40 else 16384)
+    sp = cpu_baseline.SweepPool(p, op, sargs, True)
+    procs = sp.procs
+    gen = rng_from("sweep", 0)
+    times = []
+    for i in range(args.warmup + args.steps):
+        secs, _ = sp.time(gen.integers(0, 451_584_000, n))
+        if i >= args.warmup:
+            times.append(secs)
+    sp.close()
+    ms = 1e3 * float(np.mean(times))
+    value = n / (ms / 1e3)
+    sample = f"{n} random conv2d candidates per step, 4096-candidate chunks, {procs} processes x 1 BLAS thread"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "graphs/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C5 candidate-scoring sweep (oracle port of meta_scores, bounded sample)",
+                       "spec": "conv2d/56/64/64/3/3 p1", "layout": "super N=25", "sample": n},
+            "cpu_baseline": {"value": value, "unit": "graphs/s", "cores": procs, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "graphs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --- our arm ----------------------------------------------------------------------------
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2102_04199_b200 import _lib
+    from paper_2102_04199_b200 import graphs as pg
+    from paper_2102_04199_b200 import kernels as pk
+    from paper_2102_04199_b200 import search as ps
+    from paper_2102_04199_b200.util import rng_from
+
+    rank, local, ws = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _lib.load()
+
+    m = bench_model(dev)
+    spec = pk.KernelSpec(*SPEC_ARGS)
+    space = pk.build_knob_space(spec)
+    lay = pg.batch_layout(spec, pg.build_super_template(pk.OP_TYPES))
+    sw = ps.Sweeper(m, spec, space, lay, BATCH, k=TOPK, chunks=4)
+
+    gen = rng_from("sweep", rank)
+    pool_host = torch.from_numpy(gen.integers(0, space.size, POOL_SLICES * BATCH))
+    pool = pool_host.to(dev)
+    gather_s = torch.empty(ws * TOPK, dtype=torch.float32, device=dev)
+    gather_i = torch.empty(ws * TOPK, dtype=torch.int64, device=dev)
+
+    def step(i):
+        ti, ts = sw.run_device(pool[(i % POOL_SLICES) * BATCH : (i % POOL_SLICES + 1) * BATCH])
+        if ws > 1:
+            dist.all_gather_into_tensor(gather_s, ts)
+            dist.all_gather_into_tensor(gather_i, ti)
+            ps.topk_merge(gather_s, gather_i, TOPK)
+
+    # per-step score-kernel timing: events around the score launch on the launching stream
+    cur = torch.cuda.current_stream(dev)
+    k0s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    k1s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if int(sw.err.item()):
+        raise RuntimeError("bad config index in pool")
+
+    sampler = ClockSampler(local) if rank == 0 else None
+    time.sleep(0.2)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.kt_launch_count()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for i in range(args.steps):
+        sl = pool[((i + args.warmup) % POOL_SLICES) * BATCH : ((i + args.warmup) % POOL_SLICES + 1) * BATCH]
+        k0s[i].record()
+        sw._score(sl.data_ptr(), 0, BATCH, sw.z.data_ptr(), cur.cuda_stream)
+        k1s[i].record()
+        sw._topk(sl.data_ptr(), 0, BATCH, cur.cuda_stream)
+        if ws > 1:
+            dist.all_gather_into_tensor(gather_s, sw.top_score)
+            dist.all_gather_into_tensor(gather_i, sw.top_idx)
+            ps.topk_merge(gather_s, gather_i, TOPK)
+    t1.record()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    launches = lib.kt_launch_count() - launches0
+    ms_local = t0.elapsed_time(t1) / args.steps
+    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in zip(k0s, k1s)]))
+    ms = ms_local
+    if ws > 1:
+        t = torch.tensor([ms_local], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    clocks = sampler.stop() if sampler else None
+    value = ws * BATCH / (ms / 1e3)
+
+    # ---- e2e through the public API: pinned host indices in, host scores + top-k out
+    host_slices = [pool_host[j * BATCH : (j + 1) * BATCH].pin_memory() for j in range(4)]
+    for j in range(3):
+        sw.run_host(host_slices[j % 4])
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = time.perf_counter()
+    h0 = torch.cuda.Event(enable_timing=True)
+    h1 = torch.cuda.Event(enable_timing=True)
+    h0.record()
+    for i in range(args.steps):
+        z_h, ti_h, ts_h = sw.run_host(host_slices[i % 4], check=False)
+        if ws > 1:
+            dist.all_gather_into_tensor(gather_s, sw.top_score)
+            dist.all_gather_into_tensor(gather_i, sw.top_idx)
+            mi, _ = ps.topk_merge(gather_s, gather_i, TOPK)
+            mi.cpu()
+    h1.record()
+    torch.cuda.synchronize()
+    e2e_ms = max(h0.elapsed_time(h1), 1e3 * (time.perf_counter() - e0)) / args.steps
+    if ws > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = {"value": ws * BATCH / (e2e_ms / 1e3), "unit": "graphs/s", "h2d_bytes_per_step": BATCH * 8,
+           "d2h_bytes_per_step": BATCH * 4 + TOPK * 12, "ms_per_step": e2e_ms}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        g_s, procs, secs = cpu_sweep(oracle_params(m), args.cpu_sample)
+        cpu = {"value": g_s, "unit": "graphs/s", "cores": procs, "kind": "port",
+               "sample": f"{args.cpu_sample} random conv2d candidates (oracle port of meta_scores, fp64 numpy, "
+                         f"4096-candidate chunks, {procs} processes x 1 BLAS thread), {secs:.1f} s"}
+
+    achieved = FLOP_PER_GRAPH * BATCH / (kern_ms / 1e3) / 1e12
+    traffic = load_traffic()
+    line = {
+        "metric": METRIC, "value": value, "unit": "graphs/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+        "config": {"workload": "C5 candidate-scoring sweep: 1,048,576 conv2d schedule graphs per GPU per step "
+                               "+ top-512 (score desc, index asc); N>1: NCCL all-gather of per-rank top-k + merge",
+                   "spec": "conv2d/56/64/64/3/3 p1 (space 451,584,000)", "layout": "super-graph N=25, nnz 73",
+                   "model": "GCN 12->32->32, sum+max readout, FC 64->64->64->1 (random init, bench-model)",
+                   "parallelism": f"dp{ws} (candidate shards)",
+                   "l2": f"timed steps rotate over a {POOL_SLICES * BATCH * 8 >> 20} MiB index pool (> 126 MB L2)"},
+        "roofline": {"bound": "fp32", "kernel": "score_star_kernel", "achieved": achieved,
+                     "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
+                     "traffic": traffic, "kernel_ms": kern_ms,
+                     "flop_per_graph": FLOP_PER_GRAPH, "ref_formula_flop_per_graph": REF_FLOP_PER_GRAPH,
+                     "peak_source": "measured in-repo FFMA peak (tools/fma_peak.cu); not in MEASURED_PEAKS.json"},
+        "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 18)
+    ap.add_argument("--ref-sample", type=int, default=0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,165 @@
+/*
+ * kerntune_b200.h -- C-ABI of the B200 (sm_100a) MetaTune cost-model library.
+ *
+ * The reference (arXiv 2102.04199, package `kerntune`, pure Python/numpy) has
+ * no native FFI; its hot path is a set of Python functions.  Each entry point
+ * below is the device replacement of one of them and cites the reference
+ * function it stands in for (path relative to /root/reference/pkg/src/kerntune).
+ * The Python package `paper_2102_04199_b200` binds these with ctypes
+ * (`_lib.py`) and keeps the reference's Python names and signatures.
+ *
+ * Conventions
+ *   - every pointer argument is a DEVICE pointer unless named `host_*`;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream);
+ *   - no entry point allocates memory; scratch comes from the caller
+ *     (`*_workspace_bytes` queries give the size);
+ *   - all launches are stream-ordered and asynchronous; nothing synchronises
+ *     the host except kt_sync_check;
+ *   - return 0 (KT_OK) or a KT_E_* code; kt_last_error() describes the last
+ *     failure on the calling thread.  The Python layer maps KT_E_SHAPE /
+ *     KT_E_EMPTY / KT_E_RANGE / KT_E_UNSUPPORTED to DomainError and
+ *     KT_E_CUDA / KT_E_NUMERIC to NumericError (reference errors.py:10-19).
+ *
+ * Flat parameter vector (fp32, device), layout described by kt_dims:
+ *   [ gcn W_0 (F x d_1), ..., gcn W_{L-1}, agg (d_L),
+ *     head W_0 (2 d_L x h_1), b_0, W_1, b_1, ..., W_H (h_H x 1), b_H ]
+ * i.e. the GCN layers, the aggregation weights, then exactly the reference's
+ * flat head vector head_to_vec() order (model.py:328-333).
+ */
+#ifndef KERNTUNE_B200_H
+#define KERNTUNE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KT_OK 0
+#define KT_E_SHAPE 1       /* shape / length mismatch           -> DomainError */
+#define KT_E_EMPTY 2       /* empty batch                       -> DomainError */
+#define KT_E_RANGE 3       /* config index out of space         -> DomainError */
+#define KT_E_UNSUPPORTED 4 /* dims beyond the compiled limits   -> DomainError */
+#define KT_E_CUDA 5        /* CUDA launch / runtime failure     -> NumericError */
+#define KT_E_NUMERIC 6     /* non-finite result                 -> NumericError */
+#define KT_E_ARG 7         /* null pointer / bad argument       -> DomainError */
+
+#define KT_F 12            /* FEATURE_DIM (graphs.py:30-44) */
+#define KT_MAX_KNOBS 8
+#define KT_MAX_AXES 6
+#define KT_MAX_LOOPS 12
+#define KT_MAX_CARD 160
+#define KT_MAX_LAYERS 4    /* GCN layers and head layers, each */
+#define KT_MAX_DIM 64      /* widest GCN / head layer the general kernels take */
+#define KT_MAX_NODES 64    /* largest graph the general kernels take */
+
+/* Per-spec encode table (built on the host by graphs.EncodeTables, uploaded
+ * once per (spec, layout, feature norm)).  Replaces the per-call Python work
+ * of encode_batch (graphs.py:305-351) + index_config (kernels.py:278-286). */
+typedef struct kt_spec_table {
+  int32_t n_knobs, n_axes, n_loops, n_nodes;
+  int32_t n_pairs;                       /* (for, iterval) pairs in the layout */
+  int32_t auto_knob, expl_knob;          /* knob index or -1 */
+  int32_t pad0;
+  uint64_t space_size;
+  uint32_t card[KT_MAX_KNOBS];           /* cardinalities, knob 0 most significant */
+  int32_t axis_knob[KT_MAX_AXES];        /* knob index of tile_<axis> or -1 */
+  int32_t axis_reduce[KT_MAX_AXES];
+  int32_t loop_row[KT_MAX_LOOPS];        /* iterval node row of loop k */
+  int32_t auto_vals[4];
+  int32_t expl_vals[2];
+  int32_t pad1[2];
+  int32_t outer[KT_MAX_AXES][KT_MAX_CARD];  /* ceil(e / clamp(t)) per tile choice */
+  int32_t inner[KT_MAX_AXES][KT_MAX_CARD];  /* clamp(t, 1, e) per tile choice */
+  double raw_log2[2][KT_MAX_AXES][KT_MAX_CARD]; /* numpy log2 of outer/inner extents */
+  /* normalised (fp64 (x-mean)/std cast to fp32, computed by numpy on the host) */
+  float nrm_ext[KT_MAX_LOOPS][KT_MAX_CARD];      /* slot 0 per loop and choice */
+  float nrm_log2ext[KT_MAX_LOOPS][KT_MAX_CARD];  /* slot 1 */
+  float nrm_stride[KT_MAX_LOOPS][KT_MAX_CARD];   /* slot 5 (outer loops: t) */
+  float nrm_const[KT_MAX_LOOPS][KT_F];           /* slots 2,3,5(inner),10,11 (+4 when 0) */
+  float nrm_unroll1[KT_MAX_LOOPS];               /* slot 4 when unrolled */
+  double fmean[KT_F], fstd[KT_F];
+} kt_spec_table;
+
+/* Model dimensions and flat-vector offsets (in floats). */
+typedef struct kt_dims {
+  int32_t F;
+  int32_t n_gcn;
+  int32_t gcn[KT_MAX_LAYERS + 1];   /* gcn[0] = F, gcn[i+1] = d_{i+1} */
+  int32_t n_head;                   /* number of affine head layers (>= 1) */
+  int32_t head[KT_MAX_LAYERS + 2];  /* head[0] = 2 d_L, ..., head[n_head] = 1 */
+  int32_t off_gcn[KT_MAX_LAYERS];
+  int32_t off_agg;
+  int32_t off_hw[KT_MAX_LAYERS + 1];
+  int32_t off_hb[KT_MAX_LAYERS + 1];
+  int32_t off_head;                 /* start of the head part (= off_hw[0]) */
+  int32_t n_head_params;
+  int32_t n_params;
+} kt_dims;
+
+/* ---- library ---------------------------------------------------------------- */
+int kt_version(void);
+const char* kt_last_error(void);
+/* Number of kernels this library has launched in the process (bench evidence). */
+int64_t kt_launch_count(void);
+/* Synchronise `stream` and report any sticky device error. */
+int kt_sync_check(void* stream);
+
+/* ---- encoding ---------------------------------------------------------------- */
+/* encode_batch (graphs.py:305-351) from config indices (index_config decode on
+ * device): raw fp64 features (B, n_nodes, 12), zeros off the iterval rows.
+ * Indices outside [0, space_size) set *err_flag = 1 and write zero rows. */
+int kt_encode_raw(const kt_spec_table* tab, const int64_t* idx, int64_t B,
+                  double* feats_out, int32_t* err_flag, void* stream);
+/* Same from a choice matrix (B, n_knobs) int64 (the list[KnobConfig] form). */
+int kt_encode_raw_choices(const kt_spec_table* tab, const int64_t* choices, int64_t B,
+                          double* feats_out, int32_t* err_flag, void* stream);
+
+/* ---- candidate scoring (the predictor of search.py:534-541) ------------------------ */
+/* Fused encode -> GCN(12->32->32) -> weighted-sum+max readout -> head(64->64->64->1)
+ * for graphs on the star layouts batch_layout (graphs.py:278) produces; equals
+ * head_forward_batch(embed_batch(encode_batch(...))) (model.py:185-203).
+ * Requires the default dims (F=12, gcn (32,32), head (64,64)).  `idx` may be NULL:
+ * then candidate i is config index idx_base + i (a contiguous sweep shard).
+ * If u_out != NULL the (B, 64) embeddings are written too (fine-tune rows). */
+int kt_score_indices(const kt_spec_table* tab, const kt_dims* dims, const float* params,
+                     const int64_t* idx, int64_t idx_base, int64_t B,
+                     float* z_out, float* u_out, int32_t* err_flag, void* stream);
+
+/* ---- general forward (arbitrary adjacency, segmented batches) ------------------------ */
+/* embed_batch (model.py:185-194) generalised to CSR batches.
+ * Shared pattern (nodes_per_graph > 0, node_ptr NULL): every graph has the same
+ *   n = nodes_per_graph nodes and adjacency; row_ptr (n+1) / col (local ids) /
+ *   val describe it once and mask is (n,).
+ * Segmented (nodes_per_graph == 0): graph g owns nodes [node_ptr[g], node_ptr[g+1]);
+ *   row_ptr is indexed by global node, col holds global node ids, mask is per node.
+ * feats: (total nodes, F) fp64 RAW features (normalised on device, model.py:108-112);
+ * val: fp32 entries of the fp64 normalised adjacency; max_nodes bounds any graph.
+ * Writes u (B, 2 d_L); if z_out != NULL also head_forward_batch (model.py:197-203). */
+int kt_embed_csr(const kt_dims* dims, const float* params, const double* fmean, const double* fstd,
+                 const double* feats, const uint8_t* mask, const int64_t* node_ptr,
+                 int32_t nodes_per_graph, int32_t max_nodes,
+                 const int32_t* row_ptr, const int32_t* col, const float* val, int64_t B,
+                 float* u_out, float* z_out, void* stream);
+/* head_forward_batch (model.py:197-203): u (B, head[0]) -> z (B). */
+int kt_head_forward(const kt_dims* dims, const float* params, const float* u, int64_t B,
+                    float* z_out, void* stream);
+
+/* ---- ranking (search.py:257-264) ------------------------------------------------------ */
+/* Top-k of (score desc, index asc) over B candidates; `visited` (sorted int64,
+ * n_visited entries, may be NULL) are excluded.  Outputs k indices and scores
+ * (fewer valid entries are padded with index -1).  idx == NULL means idx_base + i. */
+int64_t kt_topk_workspace_bytes(int64_t B, int32_t k);
+int kt_topk(const float* scores, const int64_t* idx, int64_t idx_base, int64_t B,
+            const int64_t* visited, int64_t n_visited, int32_t k,
+            int64_t* top_idx, float* top_score, void* workspace, int64_t workspace_bytes,
+            void* stream);
+/* Merge world x k (score, index) candidate lists (the all-gathered per-rank top-k). */
+int kt_topk_merge(const float* scores, const int64_t* idx, int64_t n, int32_t k,
+                  int64_t* top_idx, float* top_score, void* workspace, int64_t workspace_bytes,
+                  void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KERNTUNE_B200_H */

@@ -318,3 +318,159 @@ def graph_from_text(text: str) -> CodeGraph:
         else:
             raise DomainError(f"unexpected line {ln!r}")
     return CodeGraph(nodes=nodes, edges=edges, label=label)
+
+
+# --- device encode tables ----------------------------------------------------------
+
+
+def _norm32(x, mean, std, slot):
+    """np.float32((x - mean[slot]) / std[slot]) in fp64 -- the reference's order
+    of operations (model.py:111), so table entries are bit-exact."""
+    return np.float32((np.float64(x) - mean[slot]) / std[slot])
+
+
+def build_spec_table(spec: KernelSpec, space: KnobSpace, layout: BatchLayout,
+                     fmean=None, fstd=None):
+    """Host-side `kt_spec_table` for (spec, space, layout, feature norm).
+
+    Everything that depends on a single tile choice or only on the loop
+    position is tabulated here with numpy fp64 (so it is bit-identical to
+    encode_batch + normalize_features); the device computes the rest.
+    """
+    from . import _lib
+
+    fmean = np.zeros(FEATURE_DIM) if fmean is None else np.asarray(fmean, dtype=np.float64)
+    fstd = np.ones(FEATURE_DIM) if fstd is None else np.asarray(fstd, dtype=np.float64)
+    axes = AXES_BY_OP[spec.op_type]
+    ext = axis_extents(spec)
+    na, nl = len(axes), 2 * len(axes)
+    if len(space.knobs) > MAX_KNOBS:
+        raise DomainError("knob space has too many knobs for the device encoder")
+    if layout.num_nodes > _lib.KT_MAX_NODES:
+        raise DomainError("layout has too many nodes for the device encoder")
+    if space.size >= 2**63:
+        raise DomainError("knob space too large")
+    t = _lib.SpecTable()
+    t.n_knobs, t.n_axes, t.n_loops, t.n_nodes = len(space.knobs), na, nl, layout.num_nodes
+    t.n_pairs = (layout.num_nodes - 1) // 2
+    t.space_size = space.size
+    names = [k.name for k in space.knobs]
+    for j, k in enumerate(space.knobs):
+        if len(k.values) > _lib.KT_MAX_CARD:
+            raise DomainError(f"knob {k.name} has more than {_lib.KT_MAX_CARD} values")
+        t.card[j] = len(k.values)
+    t.auto_knob = names.index("auto_unroll_max_step") if "auto_unroll_max_step" in names else -1
+    t.expl_knob = names.index("unroll_explicit") if "unroll_explicit" in names else -1
+    if t.auto_knob >= 0:
+        for c, v in enumerate(space.knobs[t.auto_knob].values):
+            t.auto_vals[c] = int(v)
+    if t.expl_knob >= 0:
+        for c, v in enumerate(space.knobs[t.expl_knob].values):
+            t.expl_vals[c] = int(v)
+    rows = [int(r) for r in layout.iterval_rows]
+    if len(rows) != nl:
+        raise DomainError("layout does not match the spec's loop count")
+    for k, r in enumerate(rows):
+        t.loop_row[k] = r
+    for s in range(FEATURE_DIM):
+        t.fmean[s], t.fstd[s] = float(fmean[s]), float(fstd[s])
+    for a, axis in enumerate(axes):
+        e = ext[axis]
+        kname = f"tile_{axis}"
+        t.axis_knob[a] = names.index(kname) if kname in names else -1
+        t.axis_reduce[a] = 1 if axis in REDUCTION_AXES else 0
+        tiles = space.knobs[t.axis_knob[a]].values if t.axis_knob[a] >= 0 else (1,)
+        clamped = np.clip(np.asarray(tiles, dtype=np.int64), 1, e)
+        outer = -(-e // clamped)
+        lg_out = np.log2(np.maximum(outer.astype(np.float64), 1.0))
+        lg_in = np.log2(np.maximum(clamped.astype(np.float64), 1.0))
+        for c in range(len(tiles)):
+            t.outer[a][c], t.inner[a][c] = int(outer[c]), int(clamped[c])
+            t.raw_log2[0][a][c], t.raw_log2[1][a][c] = float(lg_out[c]), float(lg_in[c])
+            ko, ki = a, na + a  # outer / inner loop positions
+            t.nrm_ext[ko][c] = _norm32(outer[c], fmean, fstd, 0)
+            t.nrm_ext[ki][c] = _norm32(clamped[c], fmean, fstd, 0)
+            t.nrm_log2ext[ko][c] = _norm32(lg_out[c], fmean, fstd, 1)
+            t.nrm_log2ext[ki][c] = _norm32(lg_in[c], fmean, fstd, 1)
+            t.nrm_stride[ko][c] = _norm32(clamped[c], fmean, fstd, 5)
+        for k, level in ((a, 0), (na + a, 1)):
+            consts = {2: float(level), 3: float(t.axis_reduce[a]), 4: 0.0, 5: 1.0,
+                      10: float(k + 1), 11: float(k) / max(nl - 1, 1)}
+            for s, v in consts.items():
+                t.nrm_const[k][s] = _norm32(v, fmean, fstd, s)
+            t.nrm_unroll1[k] = _norm32(1.0, fmean, fstd, 4)
+    return t
+
+
+_TABLE_CACHE: dict = {}
+
+
+def device_spec_table(spec, space, layout, fmean=None, fstd=None, device=None):
+    """Uploaded kt_spec_table (uint8 device tensor), cached per content."""
+    import ctypes
+
+    import torch
+
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    key = (spec, tuple(k.values for k in space.knobs), layout.num_nodes,
+           tuple(int(r) for r in layout.iterval_rows),
+           None if fmean is None else np.asarray(fmean, dtype=np.float64).tobytes(),
+           None if fstd is None else np.asarray(fstd, dtype=np.float64).tobytes(), str(dev))
+    hit = _TABLE_CACHE.get(key)
+    if hit is not None:
+        return hit
+    t = build_spec_table(spec, space, layout, fmean, fstd)
+    raw = np.frombuffer(ctypes.string_at(ctypes.addressof(t), ctypes.sizeof(t)), dtype=np.uint8)
+    buf = torch.from_numpy(raw.copy()).to(dev)
+    if len(_TABLE_CACHE) > 256:
+        _TABLE_CACHE.clear()
+    _TABLE_CACHE[key] = buf
+    return buf
+
+
+def configs_to_indices(space: KnobSpace, configs) -> np.ndarray:
+    """Vectorised config_index over list[KnobConfig] (validated on the host)."""
+    cards = np.array(space.cardinalities, dtype=np.int64)
+    ch = np.array([c.choices for c in configs], dtype=np.int64).reshape(len(configs), -1)
+    if ch.shape[1] != len(cards):
+        raise DomainError(f"config has {ch.shape[1]} choices, space has {len(cards)} knobs")
+    if (ch < 0).any() or (ch >= cards).any():
+        raise DomainError("choice out of range for its knob")
+    mult = np.ones(len(cards), dtype=np.int64)
+    for j in range(len(cards) - 2, -1, -1):
+        mult[j] = mult[j + 1] * cards[j + 1]
+    return ch @ mult
+
+
+def encode_batch(spec: KernelSpec, space: KnobSpace, configs, layout: BatchLayout, *, device=None):
+    """encode_batch (graphs.py:305-351) on the GPU: raw fp64 features (B, N, 12).
+
+    `configs` is a list of KnobConfig (as in the reference) or an int64 tensor /
+    array of config indices.  Returns a device tensor.
+    """
+    import torch
+
+    from . import _lib
+
+    tab = device_spec_table(spec, space, layout, device=device)
+    dev = tab.device
+    if isinstance(configs, torch.Tensor):
+        idx = configs.to(dev, torch.int64)
+    elif isinstance(configs, np.ndarray):
+        idx = torch.from_numpy(configs.astype(np.int64)).to(dev)
+    else:
+        if len(configs) == 0:
+            raise DomainError("empty batch")
+        idx = torch.from_numpy(configs_to_indices(space, configs)).to(dev)
+    b = idx.numel()
+    if b == 0:
+        raise DomainError("empty batch")
+    out = torch.empty((b, layout.num_nodes, FEATURE_DIM), dtype=torch.float64, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    lib = _lib.load()
+    with torch.cuda.device(dev):
+        _lib.check(lib.kt_encode_raw(_lib.ptr(tab), _lib.ptr(idx), b, _lib.ptr(out), _lib.ptr(err),
+                                     _lib.stream_handle()), "encode_batch")
+    if int(err.item()):
+        raise DomainError("config index out of range for the knob space")
+    return out

@@ -1,0 +1,535 @@
+"""GCN + MLP cost model on the GPU: the drop-in for the reference's model.py.
+
+Same names, signatures and semantics as the reference (kerntune/model.py:54-477):
+  ModelState / GcnParams / AggParams / HeadParams / FeatureNorm / LabelNorm /
+  Gradients, init_model, normalize_label, denormalize_label, embed_batch,
+  head_forward_batch, embed, forward, predict_gflops, loss, grad, sgd_step,
+  head_to_vec, vec_to_head, head_loss_grad, head_hvp, save_model, load_model.
+Differences, by design:
+  * parameters live on the device as fp32 views into ONE flat vector laid out
+    [gcn W_i..., agg, head W0, b0, W1, b1, W2, b2] (include/kerntune_b200.h);
+    the head part is exactly head_to_vec's order, so MAML/fine-tune update the
+    tail of the flat vector in place of the reference's numpy concatenations;
+  * FeatureNorm / LabelNorm stay fp64 numpy on the host (they feed the fp64
+    encoder tables and the GFLOPS de-normalisation);
+  * batch outputs (u, z, gradients) are device tensors; scalars (loss) are
+    Python floats, as in the reference.
+All compute goes through libkerntune_b200.so; nothing here falls back to CPU.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import DomainError
+from .graphs import FEATURE_DIM, tensors_for
+
+LABEL_FLOOR_GFLOPS = 1e-3
+
+
+@dataclass
+class GcnParams:
+    layers: list  # (d_in, d_out) fp32 device views
+
+
+@dataclass
+class AggParams:
+    sum_weights: torch.Tensor  # (d_last,)
+
+
+@dataclass
+class HeadParams:
+    weights: list  # [(2*d_last, h1), (h1, h2), (h2, 1)]
+    biases: list
+
+
+@dataclass
+class FeatureNorm:
+    mean: np.ndarray
+    std: np.ndarray
+
+
+@dataclass
+class LabelNorm:
+    mean: float
+    std: float
+
+
+@dataclass
+class ModelState:
+    gcn: GcnParams
+    agg: AggParams
+    head: HeadParams
+    feature_norm: FeatureNorm
+    label_norm: LabelNorm
+    _flat: torch.Tensor | None = field(default=None, repr=False, compare=False)
+
+
+@dataclass
+class Gradients:
+    gcn: list
+    agg: torch.Tensor
+    head_weights: list
+    head_biases: list
+    _flat: torch.Tensor | None = field(default=None, repr=False, compare=False)
+
+
+# --- layout of the flat parameter vector ---------------------------------------------
+
+
+def make_dims(feature_dim: int, gcn_dims, head_hidden) -> _lib.Dims:
+    gcn_dims, head_hidden = tuple(gcn_dims), tuple(head_hidden)
+    if not gcn_dims or len(gcn_dims) > _lib.KT_MAX_LAYERS or len(head_hidden) + 1 > _lib.KT_MAX_LAYERS + 1:
+        raise DomainError("model depth beyond the compiled limits")
+    d = _lib.Dims()
+    d.F = feature_dim
+    d.n_gcn = len(gcn_dims)
+    dims = (feature_dim,) + gcn_dims
+    for i, v in enumerate(dims):
+        d.gcn[i] = v
+    off = 0
+    for i in range(len(gcn_dims)):
+        d.off_gcn[i] = off
+        off += dims[i] * dims[i + 1]
+    d.off_agg = off
+    off += dims[-1]
+    hd = (2 * dims[-1],) + head_hidden + (1,)
+    d.n_head = len(hd) - 1
+    for i, v in enumerate(hd):
+        d.head[i] = v
+    d.off_head = off
+    for i in range(len(hd) - 1):
+        d.off_hw[i] = off
+        off += hd[i] * hd[i + 1]
+        d.off_hb[i] = off
+        off += hd[i + 1]
+    d.n_head_params = off - d.off_head
+    d.n_params = off
+    return d
+
+
+def head_only_dims(head_shapes) -> _lib.Dims:
+    """Dims whose offsets index a bare flat head vector (head_to_vec layout)."""
+    d = _lib.Dims()
+    hd = [head_shapes[0][0]] + [s[1] for s in head_shapes]
+    d.n_head = len(head_shapes)
+    for i, v in enumerate(hd):
+        d.head[i] = v
+    off = 0
+    for i in range(len(head_shapes)):
+        d.off_hw[i] = off
+        off += hd[i] * hd[i + 1]
+        d.off_hb[i] = off
+        off += hd[i + 1]
+    d.n_head_params = d.n_params = off
+    d.n_gcn = 1
+    d.F = d.gcn[0] = d.gcn[1] = 1
+    return d
+
+
+def dims_of(m: ModelState) -> _lib.Dims:
+    gcn = [tuple(w.shape) for w in m.gcn.layers]
+    return make_dims(gcn[0][0], [s[1] for s in gcn], [w.shape[1] for w in m.head.weights[:-1]])
+
+
+def _shapes(m) -> list:
+    return ([tuple(w.shape) for w in m.gcn.layers] + [tuple(m.agg.sum_weights.shape)]
+            + [s for w, b in zip(m.head.weights, m.head.biases) for s in (tuple(w.shape), tuple(b.shape))])
+
+
+def _tensors(m) -> list:
+    return (list(m.gcn.layers) + [m.agg.sum_weights]
+            + [t for w, b in zip(m.head.weights, m.head.biases) for t in (w, b)])
+
+
+def _views(flat: torch.Tensor, shapes: list) -> list:
+    out, off = [], 0
+    for s in shapes:
+        n = int(np.prod(s))
+        out.append(flat[off : off + n].view(s))
+        off += n
+    if off != flat.numel():
+        raise DomainError("flat parameter vector has the wrong length")
+    return out
+
+
+def _assemble(cls_state, flat: torch.Tensor, shapes, n_gcn: int, n_head: int, **extra):
+    v = _views(flat, shapes)
+    gcn, agg, rest = v[:n_gcn], v[n_gcn], v[n_gcn + 1 :]
+    hw, hb = rest[0::2], rest[1::2]
+    if cls_state is ModelState:
+        return ModelState(GcnParams(gcn), AggParams(agg), HeadParams(hw, hb), extra["feature_norm"],
+                          extra["label_norm"], _flat=flat)
+    return Gradients(gcn=gcn, agg=agg, head_weights=hw, head_biases=hb, _flat=flat)
+
+
+def _is_packed(obj, tensors) -> bool:
+    flat = obj._flat
+    if flat is None:
+        return False
+    base = flat.data_ptr()
+    es = flat.element_size()
+    off = 0
+    for t in tensors:
+        if not isinstance(t, torch.Tensor) or t.device != flat.device or t.dtype != flat.dtype:
+            return False
+        if t.data_ptr() != base + off * es or not t.is_contiguous():
+            return False
+        off += t.numel()
+    return off == flat.numel()
+
+
+def flat_params(m: ModelState) -> torch.Tensor:
+    """The model's flat fp32 device vector; re-packed if the user swapped tensors."""
+    ts = _tensors(m)
+    if _is_packed(m, ts):
+        return m._flat
+    dev = m._flat.device if m._flat is not None else _device_of(ts)
+    return torch.cat([torch.as_tensor(t, dtype=torch.float32, device=dev).reshape(-1) for t in ts])
+
+
+def _device_of(ts) -> torch.device:
+    for t in ts:
+        if isinstance(t, torch.Tensor) and t.is_cuda:
+            return t.device
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def model_from_flat(flat: torch.Tensor, like: ModelState, feature_norm=None, label_norm=None) -> ModelState:
+    return _assemble(ModelState, flat, _shapes(like), len(like.gcn.layers), len(like.head.weights),
+                     feature_norm=like.feature_norm if feature_norm is None else feature_norm,
+                     label_norm=like.label_norm if label_norm is None else label_norm)
+
+
+def grads_from_flat(flat: torch.Tensor, like: ModelState) -> Gradients:
+    return _assemble(Gradients, flat, _shapes(like), len(like.gcn.layers), len(like.head.weights))
+
+
+def flat_grads(g: Gradients) -> torch.Tensor:
+    ts = list(g.gcn) + [g.agg] + [t for w, b in zip(g.head_weights, g.head_biases) for t in (w, b)]
+    if _is_packed(g, ts):
+        return g._flat
+    return torch.cat([torch.as_tensor(t, dtype=torch.float32).reshape(-1) for t in ts])
+
+
+# --- construction -----------------------------------------------------------------------
+
+
+def init_model(rng, feature_dim: int = FEATURE_DIM, gcn_dims: tuple = (32, 32),
+               head_hidden: tuple = (64, 64), *, device=None) -> ModelState:
+    """U(-1/sqrt(fan_in), +) init drawn from `rng` in the reference's order
+    (model.py:71-96: gcn layers, then (w_i, b_i) pairs), cast to fp32 on device."""
+    def u(fan_in, shape):
+        s = 1.0 / math.sqrt(fan_in)
+        return rng.uniform(-s, s, size=shape)
+
+    dims = (feature_dim,) + tuple(gcn_dims)
+    parts = [u(dims[i], (dims[i], dims[i + 1])) for i in range(len(dims) - 1)]
+    parts.append(np.ones(dims[-1]))
+    hd = (2 * dims[-1],) + tuple(head_hidden) + (1,)
+    for i in range(len(hd) - 1):
+        parts.append(u(hd[i], (hd[i], hd[i + 1])))
+        parts.append(u(hd[i], (hd[i + 1],)))
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    flat = torch.from_numpy(np.concatenate([p.ravel() for p in parts]).astype(np.float32)).to(dev)
+    shapes = [p.shape for p in parts]
+    return _assemble(ModelState, flat, shapes, len(gcn_dims), len(hd) - 1,
+                     feature_norm=FeatureNorm(np.zeros(feature_dim), np.ones(feature_dim)),
+                     label_norm=LabelNorm(0.0, 1.0))
+
+
+def from_reference(ref_state, *, device=None) -> ModelState:
+    """Adopt a reference (numpy fp64) ModelState: same field layout, cast to fp32."""
+    parts = (list(ref_state.gcn.layers) + [ref_state.agg.sum_weights]
+             + [t for w, b in zip(ref_state.head.weights, ref_state.head.biases) for t in (w, b)])
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    flat = torch.from_numpy(np.concatenate([np.asarray(p).ravel() for p in parts]).astype(np.float32)).to(dev)
+    return _assemble(ModelState, flat, [np.asarray(p).shape for p in parts], len(ref_state.gcn.layers),
+                     len(ref_state.head.weights),
+                     feature_norm=FeatureNorm(np.asarray(ref_state.feature_norm.mean, dtype=np.float64).copy(),
+                                              np.asarray(ref_state.feature_norm.std, dtype=np.float64).copy()),
+                     label_norm=LabelNorm(float(ref_state.label_norm.mean), float(ref_state.label_norm.std)))
+
+
+def normalize_label(m: ModelState, gflops: float) -> float:
+    return (math.log2(max(gflops, LABEL_FLOOR_GFLOPS)) - m.label_norm.mean) / m.label_norm.std
+
+
+def denormalize_label(m: ModelState, z):
+    """2^(z sigma + mu); works on floats and tensors."""
+    if isinstance(z, torch.Tensor):
+        return torch.exp2(z.double() * m.label_norm.std + m.label_norm.mean)
+    return 2.0 ** (z * m.label_norm.std + m.label_norm.mean)
+
+
+def loss(preds, labels_normalized) -> float:
+    p = np.atleast_1d(np.asarray(_host(preds), dtype=np.float64))
+    y = np.atleast_1d(np.asarray(_host(labels_normalized), dtype=np.float64))
+    if p.shape != y.shape:
+        raise DomainError("prediction/label shape mismatch")
+    if p.size == 0:
+        raise DomainError("empty batch")
+    return float(np.mean((p - y) ** 2))
+
+
+def _host(x):
+    return x.detach().cpu().numpy() if isinstance(x, torch.Tensor) else x
+
+
+# --- device helpers -----------------------------------------------------------------------
+
+_NORM_CACHE: dict = {}
+
+
+def _norm_tensors(m: ModelState, dev):
+    key = (m.feature_norm.mean.tobytes(), m.feature_norm.std.tobytes(), str(dev))
+    hit = _NORM_CACHE.get(key)
+    if hit is None:
+        hit = (torch.from_numpy(np.asarray(m.feature_norm.mean, dtype=np.float64)).to(dev),
+               torch.from_numpy(np.asarray(m.feature_norm.std, dtype=np.float64)).to(dev))
+        if len(_NORM_CACHE) > 64:
+            _NORM_CACHE.clear()
+        _NORM_CACHE[key] = hit
+    return hit
+
+
+_CSR_CACHE: dict = {}
+
+
+def shared_csr(adj: np.ndarray, dev):
+    """CSR (row_ptr, col, fp32 val) of one N x N adjacency, cached per content."""
+    adj = np.asarray(adj, dtype=np.float64)
+    key = (adj.shape, adj.tobytes(), str(dev))
+    hit = _CSR_CACHE.get(key)
+    if hit is None:
+        rows, cols = np.nonzero(adj)
+        row_ptr = np.zeros(adj.shape[0] + 1, dtype=np.int32)
+        np.add.at(row_ptr, rows + 1, 1)
+        row_ptr = np.cumsum(row_ptr).astype(np.int32)
+        hit = (torch.from_numpy(row_ptr).to(dev), torch.from_numpy(cols.astype(np.int32)).to(dev),
+               torch.from_numpy(adj[rows, cols].astype(np.float32)).to(dev))
+        if len(_CSR_CACHE) > 64:
+            _CSR_CACHE.clear()
+        _CSR_CACHE[key] = hit
+    return hit
+
+
+def _as_device(x, dev, dtype):
+    if isinstance(x, torch.Tensor):
+        return x.to(device=dev, dtype=dtype).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.dtype(str(dtype).split(".")[-1]))).to(dev)
+
+
+@dataclass
+class PackedGraphs:
+    """Segmented-CSR batch of CodeGraphs (device), built by pack_graphs."""
+    feats: torch.Tensor      # (total_nodes, F) fp64 raw
+    mask: torch.Tensor       # (total_nodes,) uint8
+    node_ptr: torch.Tensor   # (B+1,) int64
+    row_ptr: torch.Tensor    # (total_nodes+1,) int32
+    col: torch.Tensor        # (nnz,) int32 global node ids
+    val: torch.Tensor        # (nnz,) fp32
+    max_nodes: int
+    n_graphs: int
+
+
+def pack_graphs(graphs, dev) -> PackedGraphs:
+    """Host packing of [CodeGraph] into one segmented CSR batch (memoised per graph
+    through tensors_for, like the reference's model.py:115-121)."""
+    if not graphs:
+        raise DomainError("empty batch")
+    ts = [tensors_for(g) for g in graphs]
+    sizes = np.array([t.feature_matrix.shape[0] for t in ts], dtype=np.int64)
+    if sizes.max() > _lib.KT_MAX_NODES:
+        raise DomainError(f"graph with {sizes.max()} nodes exceeds the device limit {_lib.KT_MAX_NODES}")
+    node_ptr = np.concatenate([[0], np.cumsum(sizes)])
+    feats = np.concatenate([t.feature_matrix for t in ts])
+    if feats.shape[1] != FEATURE_DIM:
+        raise DomainError("feature width mismatch")
+    mask = np.concatenate([t.feature_mask for t in ts]).astype(np.uint8)
+    rows, cols, vals = [], [], []
+    for base, t in zip(node_ptr[:-1], ts):
+        r, c = np.nonzero(t.normalized_adjacency)
+        rows.append(r + base)
+        cols.append(c + base)
+        vals.append(t.normalized_adjacency[r, c])
+    rows, cols, vals = np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
+    row_ptr = np.zeros(node_ptr[-1] + 1, dtype=np.int64)
+    np.add.at(row_ptr, rows + 1, 1)
+    row_ptr = np.cumsum(row_ptr)
+    up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)
+    return PackedGraphs(up(feats, np.float64), up(mask, np.uint8), up(node_ptr, np.int64),
+                        up(row_ptr, np.int32), up(cols, np.int32), up(vals, np.float32),
+                        int(sizes.max()), len(graphs))
+
+
+# --- batched forward ----------------------------------------------------------------------
+
+
+def embed_batch(m: ModelState, feats, mask, adj) -> torch.Tensor:
+    """Embeddings (B, 2 d) for (B, N, F) raw features sharing one mask/adjacency
+    (model.py:185-194); feats may be numpy or a device tensor (e.g. encode_batch's)."""
+    flat = flat_params(m)
+    dev = flat.device
+    x = _as_device(feats, dev, torch.float64)
+    if x.dim() != 3 or x.shape[2] != m.gcn.layers[0].shape[0]:
+        raise DomainError(f"feats must be (B, N, {m.gcn.layers[0].shape[0]})")
+    b, n = x.shape[0], x.shape[1]
+    if b == 0:
+        raise DomainError("empty batch")
+    adj = np.asarray(_host(adj), dtype=np.float64)
+    msk = np.asarray(_host(mask), dtype=bool)
+    if adj.shape != (n, n) or msk.shape != (n,):
+        raise DomainError("adjacency / mask shape does not match feats")
+    if n > _lib.KT_MAX_NODES:
+        raise DomainError(f"graphs of {n} nodes exceed the device limit {_lib.KT_MAX_NODES}")
+    rp, col, val = shared_csr(adj, dev)
+    mean, std = _norm_tensors(m, dev)
+    mk = torch.from_numpy(msk.astype(np.uint8)).to(dev)
+    d = dims_of(m)
+    u = torch.empty((b, 2 * d.gcn[d.n_gcn]), dtype=torch.float32, device=dev)
+    lib = _lib.load()
+    with torch.cuda.device(dev):
+        _lib.check(lib.kt_embed_csr(d, _lib.ptr(flat), _lib.ptr(mean), _lib.ptr(std), _lib.ptr(x),
+                                    _lib.ptr(mk), None, n, n, _lib.ptr(rp), _lib.ptr(col), _lib.ptr(val), b,
+                                    _lib.ptr(u), None, _lib.stream_handle()), "embed_batch")
+    return u
+
+
+def head_forward_batch(u, head: HeadParams) -> torch.Tensor:
+    """(B,) head outputs (model.py:197-203)."""
+    shapes = [tuple(w.shape) for w in head.weights]
+    vec = head_to_vec(head)
+    dev = vec.device
+    uu = _as_device(u, dev, torch.float32)
+    if uu.dim() != 2 or uu.shape[1] != shapes[0][0]:
+        raise DomainError("u width does not match the head")
+    if uu.shape[0] == 0:
+        raise DomainError("empty batch")
+    z = torch.empty(uu.shape[0], dtype=torch.float32, device=dev)
+    lib = _lib.load()
+    with torch.cuda.device(dev):
+        _lib.check(lib.kt_head_forward(head_only_dims(shapes), _lib.ptr(vec), _lib.ptr(uu), uu.shape[0],
+                                       _lib.ptr(z), _lib.stream_handle()), "head_forward_batch")
+    return z
+
+
+def embed_graphs(m: ModelState, graphs, with_scores: bool = False):
+    """Embeddings (and optionally scores) of a list of CodeGraphs of any sizes."""
+    flat = flat_params(m)
+    dev = flat.device
+    pk = pack_graphs(graphs, dev)
+    mean, std = _norm_tensors(m, dev)
+    d = dims_of(m)
+    u = torch.empty((pk.n_graphs, 2 * d.gcn[d.n_gcn]), dtype=torch.float32, device=dev)
+    z = torch.empty(pk.n_graphs, dtype=torch.float32, device=dev) if with_scores else None
+    lib = _lib.load()
+    with torch.cuda.device(dev):
+        _lib.check(lib.kt_embed_csr(d, _lib.ptr(flat), _lib.ptr(mean), _lib.ptr(std), _lib.ptr(pk.feats),
+                                    _lib.ptr(pk.mask), _lib.ptr(pk.node_ptr), 0, pk.max_nodes,
+                                    _lib.ptr(pk.row_ptr), _lib.ptr(pk.col), _lib.ptr(pk.val), pk.n_graphs,
+                                    _lib.ptr(u), _lib.ptr(z), _lib.stream_handle()), "embed_graphs")
+    return (u, z) if with_scores else u
+
+
+def embed(graph, m: ModelState) -> torch.Tensor:
+    """Aggregated embedding of one graph (model.py:153-160)."""
+    return embed_graphs(m, [graph])[0]
+
+
+def forward(graph, m: ModelState) -> float:
+    """Prediction on the normalised log scale (model.py:163-165)."""
+    return float(embed_graphs(m, [graph], with_scores=True)[1][0].item())
+
+
+def predict_gflops(graph, m: ModelState) -> float:
+    return denormalize_label(m, forward(graph, m))
+
+
+# --- flat head parameterisation (model.py:328-355) -------------------------------------------
+
+
+def head_to_vec(head: HeadParams) -> torch.Tensor:
+    """Flat [W0, b0, W1, b1, ...] vector; a view when the head already is one."""
+    parts = [t for w, b in zip(head.weights, head.biases) for t in (w, b)]
+    if all(isinstance(t, torch.Tensor) for t in parts):
+        base, off, ok = parts[0], 0, True
+        for t in parts:
+            if (not t.is_contiguous() or t.dtype != base.dtype or t.device != base.device
+                    or t.data_ptr() != base.data_ptr() + off * base.element_size()):
+                ok = False
+                break
+            off += t.numel()
+        if ok:
+            return torch.as_strided(base, (off,), (1,))
+    dev = _device_of(parts)
+    return torch.cat([torch.as_tensor(t, dtype=torch.float32, device=dev).reshape(-1) for t in parts])
+
+
+def vec_to_head(vec, like: HeadParams) -> HeadParams:
+    vec = torch.as_tensor(vec)
+    ws, bs, off = [], [], 0
+    for w, b in zip(like.weights, like.biases):
+        nw, nb = int(np.prod(w.shape)), int(np.prod(b.shape))
+        ws.append(vec[off : off + nw].view(tuple(w.shape)))
+        off += nw
+        bs.append(vec[off : off + nb].view(tuple(b.shape)))
+        off += nb
+    if off != vec.numel():
+        raise DomainError("flat head vector has the wrong length")
+    return HeadParams(weights=ws, biases=bs)
+
+
+def with_head_vec(m: ModelState, head_vec: torch.Tensor) -> ModelState:
+    """New ModelState sharing gcn/agg values with m and taking `head_vec` as its head."""
+    d = dims_of(m)
+    flat = flat_params(m)
+    new = torch.cat([flat[: d.off_head], head_vec.reshape(-1).to(flat.dtype)])
+    return model_from_flat(new, m)
+
+
+# --- checkpoints (model.py:438-477, npz v1) ----------------------------------------------------
+
+CHECKPOINT_VERSION = 1
+
+
+def save_model(m: ModelState, path) -> None:
+    """npz v1, interchangeable with the reference; fp32 weights are stored as fp64."""
+    h = lambda t: np.asarray(_host(t), dtype=np.float64)
+    arrays = {
+        "version": np.array(CHECKPOINT_VERSION),
+        "n_gcn": np.array(len(m.gcn.layers)),
+        "agg_w": h(m.agg.sum_weights),
+        "feat_mean": np.asarray(m.feature_norm.mean, dtype=np.float64),
+        "feat_std": np.asarray(m.feature_norm.std, dtype=np.float64),
+        "label_norm": np.array([m.label_norm.mean, m.label_norm.std]),
+    }
+    for i, w in enumerate(m.gcn.layers):
+        arrays[f"gcn_{i}"] = h(w)
+    for i, (w, b) in enumerate(zip(m.head.weights, m.head.biases)):
+        arrays[f"head_w{i}"] = h(w)
+        arrays[f"head_b{i}"] = h(b)
+    np.savez(path, **arrays)
+
+
+def load_model(path, *, device=None) -> ModelState:
+    with np.load(path) as z:
+        if int(z["version"]) != CHECKPOINT_VERSION:
+            raise DomainError(f"unsupported checkpoint version {int(z['version'])}")
+        n_gcn = int(z["n_gcn"])
+        parts = [z[f"gcn_{i}"] for i in range(n_gcn)] + [z["agg_w"]]
+        i = 0
+        while f"head_w{i}" in z:
+            parts += [z[f"head_w{i}"], z[f"head_b{i}"]]
+            i += 1
+        label = z["label_norm"]
+        fn = FeatureNorm(z["feat_mean"].copy(), z["feat_std"].copy())
+        ln = LabelNorm(float(label[0]), float(label[1]))
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    flat = torch.from_numpy(np.concatenate([p.ravel() for p in parts]).astype(np.float32)).to(dev)
+    return _assemble(ModelState, flat, [p.shape for p in parts], n_gcn, i, feature_norm=fn, label_norm=ln)

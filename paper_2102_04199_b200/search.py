@@ -1,0 +1,241 @@
+"""The predictor seam of the tuner, on the GPU.
+
+The reference's proposers take the cost model as a plain callable
+`predict(list[KnobConfig]) -> scores` (search.py:9-10, sa_explore 202-254), and
+`tune` builds it as meta_scores / meta_energy = encode_batch -> embed_batch ->
+head_forward_batch (search.py:534-541).  `CostModelPredictor` is that callable
+backed by the fused sm_100a scorer (kt_score_indices), and `rank_history`
+keeps the reference's (-score, index) ordering (search.py:257-264).  For large
+candidate sets `score_indices` + `topk` stay on the device end to end.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import DomainError
+from .graphs import BatchLayout, batch_layout, configs_to_indices, device_spec_table
+from .kernels import KernelSpec, KnobSpace
+from .model import ModelState, dims_of, flat_params
+
+DEFAULT_DIMS = (12, (32, 32), (64, 64))
+
+
+def _default_model(m: ModelState) -> bool:
+    d = dims_of(m)
+    return (d.F, tuple(d.gcn[1 : d.n_gcn + 1]), tuple(d.head[1 : d.n_head])) == DEFAULT_DIMS
+
+
+def score_indices(m: ModelState, spec: KernelSpec, space: KnobSpace, layout: BatchLayout, idx=None, *,
+                  base: int = 0, count: int | None = None, want_u: bool = False, check: bool = True,
+                  z_out=None, u_out=None, err=None):
+    """Scores z (fp32 device, normalised log2 GFLOPS) of config indices.
+
+    `idx` is an int64 device tensor (or array-like); with idx=None the candidates
+    are the contiguous range [base, base+count).  Equals
+    head_forward_batch(embed_batch(m, encode_batch(...), mask, adj), head).
+    """
+    flat = flat_params(m)
+    dev = flat.device
+    if not _default_model(m):
+        return _score_general(m, spec, space, layout, idx, base, count, want_u)
+    if idx is not None and not isinstance(idx, torch.Tensor):
+        idx = torch.from_numpy(np.ascontiguousarray(idx, dtype=np.int64)).to(dev)
+    b = int(idx.numel()) if idx is not None else int(count or 0)
+    if b <= 0:
+        raise DomainError("empty batch")
+    tab = device_spec_table(spec, space, layout, m.feature_norm.mean, m.feature_norm.std, device=dev)
+    z = z_out if z_out is not None else torch.empty(b, dtype=torch.float32, device=dev)
+    u = None
+    if want_u:
+        u = u_out if u_out is not None else torch.empty((b, 64), dtype=torch.float32, device=dev)
+    e = err if err is not None else torch.zeros(1, dtype=torch.int32, device=dev)
+    lib = _lib.load()
+    with torch.cuda.device(dev):
+        _lib.check(lib.kt_score_indices(_lib.ptr(tab), dims_of(m), _lib.ptr(flat), _lib.ptr(idx), base, b,
+                                        _lib.ptr(z), _lib.ptr(u), _lib.ptr(e), _lib.stream_handle()),
+                   "score_indices")
+    if check and int(e.item()):
+        raise DomainError("config index out of range for the knob space")
+    return (z, u) if want_u else z
+
+
+def _score_general(m, spec, space, layout, idx, base, count, want_u):
+    from .graphs import encode_batch
+    from .model import embed_batch, head_forward_batch
+
+    dev = flat_params(m).device
+    if idx is None:
+        idx = torch.arange(base, base + int(count), dtype=torch.int64, device=dev)
+    feats = encode_batch(spec, space, idx, layout, device=dev)
+    u = embed_batch(m, feats, layout.feature_mask, layout.adjacency)
+    z = head_forward_batch(u, m.head)
+    return (z, u) if want_u else z
+
+
+class CostModelPredictor:
+    """`predict(configs) -> np.ndarray` for sa_explore / tune (search.py:202-254, 534-541).
+
+    `meta_scores(configs)` returns (z, u) like the reference closure; both are
+    host numpy arrays (float64 scores in input order), so this object is a
+    drop-in wherever the reference passes `meta_energy`.
+    """
+
+    def __init__(self, m: ModelState, spec: KernelSpec, space: KnobSpace, layout: BatchLayout | None = None,
+                 template=None):
+        self.m = m
+        self.spec = spec
+        self.space = space
+        self.layout = layout if layout is not None else batch_layout(spec, template)
+
+    def meta_scores(self, configs):
+        idx = configs_to_indices(self.space, configs)
+        z, u = score_indices(self.m, self.spec, self.space, self.layout, idx, want_u=True, check=False)
+        return z.double().cpu().numpy(), u.double().cpu().numpy()
+
+    def __call__(self, configs) -> np.ndarray:
+        idx = configs_to_indices(self.space, configs)
+        z = score_indices(self.m, self.spec, self.space, self.layout, idx, check=False)
+        return z.double().cpu().numpy()
+
+
+def rank_history(history: dict, visited: set, count: int) -> list:
+    """Best `count` unvisited indices, highest score first, ties -> lower index."""
+    ranked = sorted(((i, e) for i, e in history.items() if i not in visited), key=lambda t: (-t[1], t[0]))
+    return [i for i, _ in ranked[:count]]
+
+
+def topk(scores: torch.Tensor, k: int, idx: torch.Tensor | None = None, *, base: int = 0, visited=None):
+    """Device rank_history: the k best (score desc, index asc) candidates, visited excluded.
+
+    Returns (indices int64, scores fp32) device tensors of length k (index -1 pads
+    when fewer than k candidates survive)."""
+    dev = scores.device
+    b = scores.numel()
+    if b == 0:
+        raise DomainError("empty candidate set")
+    vis = None
+    if visited:
+        vis = torch.from_numpy(np.array(sorted(int(v) for v in visited), dtype=np.int64)).to(dev)
+    lib = _lib.load()
+    ws_bytes = int(lib.kt_topk_workspace_bytes(b, k))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    ti = torch.empty(k, dtype=torch.int64, device=dev)
+    ts = torch.empty(k, dtype=torch.float32, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(lib.kt_topk(_lib.ptr(scores), _lib.ptr(idx), base, b, _lib.ptr(vis),
+                               0 if vis is None else vis.numel(), k, _lib.ptr(ti), _lib.ptr(ts), _lib.ptr(ws),
+                               ws_bytes, _lib.stream_handle()), "topk")
+    return ti, ts
+
+
+def topk_merge(scores: torch.Tensor, idx: torch.Tensor, k: int):
+    """Merge concatenated per-rank (score, index) top-k lists into the global top-k."""
+    dev = scores.device
+    n = scores.numel()
+    lib = _lib.load()
+    ws_bytes = int(lib.kt_topk_workspace_bytes(n, k))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    ti = torch.empty(k, dtype=torch.int64, device=dev)
+    ts = torch.empty(k, dtype=torch.float32, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(lib.kt_topk_merge(_lib.ptr(scores), _lib.ptr(idx), n, k, _lib.ptr(ti), _lib.ptr(ts),
+                                     _lib.ptr(ws), ws_bytes, _lib.stream_handle()), "topk_merge")
+    return ti, ts
+
+
+class Sweeper:
+    """Candidate-scoring sweep (C5): score a shard of config indices and keep the
+    top-k by (score desc, index asc) -- rank_history over the whole shard.
+
+    Everything per call is pre-resolved (spec table, dims, flat params, device
+    buffers, streams, events), so a step is a handful of C-ABI calls.
+    `run_device` takes device-resident indices; `run_host` is the end-to-end
+    form: pinned host indices in, host scores + top-k out, with the H2D copy,
+    the scoring and the D2H copy of `chunks` slices overlapped on three streams.
+    """
+
+    def __init__(self, m: ModelState, spec: KernelSpec, space: KnobSpace, layout: BatchLayout,
+                 max_batch: int, k: int = 512, chunks: int = 4):
+        if not _default_model(m):
+            raise DomainError("Sweeper needs the default model dims (use score_indices otherwise)")
+        self.lib = _lib.load()
+        self.flat = flat_params(m)
+        self.dev = self.flat.device
+        self.dims = dims_of(m)
+        self.tab = device_spec_table(spec, space, layout, m.feature_norm.mean, m.feature_norm.std,
+                                     device=self.dev)
+        self.space_size = space.size
+        self.max_batch, self.k, self.chunks = max_batch, k, chunks
+        dev = self.dev
+        self.z = torch.empty(max_batch, dtype=torch.float32, device=dev)
+        self.idx = torch.empty(max_batch, dtype=torch.int64, device=dev)
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.ws_bytes = int(self.lib.kt_topk_workspace_bytes(max_batch, k))
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        self.top_idx = torch.empty(k, dtype=torch.int64, device=dev)
+        self.top_score = torch.empty(k, dtype=torch.float32, device=dev)
+        self.h_z = torch.empty(max_batch, dtype=torch.float32, pin_memory=True)
+        self.h_top_idx = torch.empty(k, dtype=torch.int64, pin_memory=True)
+        self.h_top_score = torch.empty(k, dtype=torch.float32, pin_memory=True)
+        self.s_h2d = torch.cuda.Stream(dev)
+        self.s_d2h = torch.cuda.Stream(dev)
+        self.ev_in = [torch.cuda.Event() for _ in range(chunks)]
+        self.ev_out = [torch.cuda.Event() for _ in range(chunks)]
+        self.ev_done = torch.cuda.Event()
+        self._p = dict(tab=self.tab.data_ptr(), flat=self.flat.data_ptr(), err=self.err.data_ptr(),
+                       ws=self.ws.data_ptr(), ti=self.top_idx.data_ptr(), ts=self.top_score.data_ptr())
+
+    def _score(self, idx_ptr, base, n, z_ptr, stream):
+        _lib.check(self.lib.kt_score_indices(self._p["tab"], self.dims, self._p["flat"], idx_ptr, base, n, z_ptr,
+                                             None, self._p["err"], stream), "sweep score")
+
+    def _topk(self, idx_ptr, base, n, stream, visited=None):
+        vp = None if visited is None else visited.data_ptr()
+        nv = 0 if visited is None else visited.numel()
+        _lib.check(self.lib.kt_topk(self.z.data_ptr(), idx_ptr, base, n, vp, nv, self.k, self._p["ti"],
+                                    self._p["ts"], self._p["ws"], self.ws_bytes, stream), "sweep topk")
+
+    def run_device(self, idx: torch.Tensor | None = None, *, base: int = 0, count: int | None = None,
+                   visited: torch.Tensor | None = None):
+        """Scores into self.z[:n]; returns (top_idx, top_score) device views."""
+        n = idx.numel() if idx is not None else int(count)
+        if n > self.max_batch or n <= 0:
+            raise DomainError("sweep batch size out of range")
+        st = torch.cuda.current_stream(self.dev).cuda_stream
+        ip = None if idx is None else idx.data_ptr()
+        self._score(ip, base, n, self.z.data_ptr(), st)
+        self._topk(ip, base, n, st, visited)
+        return self.top_idx, self.top_score
+
+    def run_host(self, idx_host: torch.Tensor, check: bool = True):
+        """End to end: pinned host int64 indices -> (host scores, host top-k idx, scores)."""
+        n = idx_host.numel()
+        if n > self.max_batch or n <= 0:
+            raise DomainError("sweep batch size out of range")
+        comp = torch.cuda.current_stream(self.dev)
+        step = -(-n // self.chunks)
+        bounds = [(a, min(a + step, n)) for a in range(0, n, step)]
+        with torch.cuda.stream(self.s_h2d):
+            self.s_h2d.wait_stream(comp)
+            for i, (a, b) in enumerate(bounds):
+                self.idx[a:b].copy_(idx_host[a:b], non_blocking=True)
+                self.ev_in[i].record(self.s_h2d)
+        for i, (a, b) in enumerate(bounds):
+            comp.wait_event(self.ev_in[i])
+            self._score(self.idx.data_ptr() + 8 * a, 0, b - a, self.z.data_ptr() + 4 * a, comp.cuda_stream)
+            self.ev_out[i].record(comp)
+            with torch.cuda.stream(self.s_d2h):
+                self.s_d2h.wait_event(self.ev_out[i])
+                self.h_z[a:b].copy_(self.z[a:b], non_blocking=True)
+        self._topk(self.idx.data_ptr(), 0, n, comp.cuda_stream)
+        self.h_top_idx.copy_(self.top_idx, non_blocking=True)
+        self.h_top_score.copy_(self.top_score, non_blocking=True)
+        comp.wait_stream(self.s_d2h)
+        self.ev_done.record(comp)
+        self.ev_done.synchronize()
+        if check and int(self.err.item()):
+            raise DomainError("config index out of range for the knob space")
+        return self.h_z[:n], self.h_top_idx, self.h_top_score

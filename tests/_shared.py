@@ -56,3 +56,22 @@ def corpus_graphs(g_meta, super_graph=True):
         x = ko.encode(op, ext, knobs, ch, adj.shape[0], rows)[0]
         out.append((x, adj, mask))
     return out
+
+
+class _NS:
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+
+def device_model(g_model, device=None):
+    """Product ModelState (fp32, device) holding the golden fp64 parameters."""
+    from paper_2102_04199_b200.model import from_reference
+
+    p = oracle_params(g_model)
+    ref = _NS(
+        gcn=_NS(layers=p["gcn"]), agg=_NS(sum_weights=p["agg"]),
+        head=_NS(weights=p["head_w"], biases=p["head_b"]),
+        feature_norm=_NS(mean=p["fmean"], std=p["fstd"]),
+        label_norm=_NS(mean=p["lmean"], std=p["lstd"]),
+    )
+    return from_reference(ref, device=device)
