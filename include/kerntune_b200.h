@@ -79,6 +79,7 @@ typedef struct kt_spec_table {
   float nrm_const[KT_MAX_LOOPS][KT_F];           /* slots 2,3,5(inner),10,11 (+4 when 0) */
   float nrm_unroll1[KT_MAX_LOOPS];               /* slot 4 when unrolled */
   double fmean[KT_F], fstd[KT_F];
+  uint64_t card_magic[KT_MAX_KNOBS];    /* floor(2^64 / card) + 1 (card >= 2): exact u32 division */
 } kt_spec_table;
 
 /* Model dimensions and flat-vector offsets (in floats). */

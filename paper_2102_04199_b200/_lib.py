@@ -56,6 +56,7 @@ class SpecTable(ctypes.Structure):
         ("nrm_unroll1", f32 * KT_MAX_LOOPS),
         ("fmean", f64 * KT_F),
         ("fstd", f64 * KT_F),
+        ("card_magic", u64 * KT_MAX_KNOBS),
     ]
 
 

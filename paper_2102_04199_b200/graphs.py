@@ -359,6 +359,7 @@ def build_spec_table(spec: KernelSpec, space: KnobSpace, layout: BatchLayout,
         if len(k.values) > _lib.KT_MAX_CARD:
             raise DomainError(f"knob {k.name} has more than {_lib.KT_MAX_CARD} values")
         t.card[j] = len(k.values)
+        t.card_magic[j] = (2**64 // len(k.values) + 1) if len(k.values) >= 2 else 0
     t.auto_knob = names.index("auto_unroll_max_step") if "auto_unroll_max_step" in names else -1
     t.expl_knob = names.index("unroll_explicit") if "unroll_explicit" in names else -1
     if t.auto_knob >= 0:

@@ -39,7 +39,7 @@ def score_indices(m: ModelState, spec: KernelSpec, space: KnobSpace, layout: Bat
     """
     flat = flat_params(m)
     dev = flat.device
-    if not _default_model(m):
+    if not _default_model(m) or space.size >= 2**32:
         return _score_general(m, spec, space, layout, idx, base, count, want_u)
     if idx is not None and not isinstance(idx, torch.Tensor):
         idx = torch.from_numpy(np.ascontiguousarray(idx, dtype=np.int64)).to(dev)
@@ -159,8 +159,8 @@ class Sweeper:
 
     def __init__(self, m: ModelState, spec: KernelSpec, space: KnobSpace, layout: BatchLayout,
                  max_batch: int, k: int = 512, chunks: int = 4):
-        if not _default_model(m):
-            raise DomainError("Sweeper needs the default model dims (use score_indices otherwise)")
+        if not _default_model(m) or space.size >= 2**32:
+            raise DomainError("Sweeper needs the default model dims and a space < 2^32 (use score_indices)")
         self.lib = _lib.load()
         self.flat = flat_params(m)
         self.dev = self.flat.device

@@ -1,0 +1,13 @@
+#!/bin/bash
+# Quick gpurun: forward parity tests, bench without CPU baseline, one ncu capture of the scorer.
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests -q -m gpu -p no:cacheprovider ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/pytest_gpu.txt 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_gpu.txt
+timeout 300 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err
+echo "bench rc=$?" >> gpurun_out/bench.err
+if [ "${NCU:-1}" = "1" ]; then
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:${NCU_K:-score_star} -s 3 -c 1 \
+  -o gpurun_out/prof_score -f python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
+fi
+echo done
