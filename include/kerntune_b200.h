@@ -136,15 +136,73 @@ int kt_score_indices(const kt_spec_table* tab, const kt_dims* dims, const float*
  *   row_ptr is indexed by global node, col holds global node ids, mask is per node.
  * feats: (total nodes, F) fp64 RAW features (normalised on device, model.py:108-112);
  * val: fp32 entries of the fp64 normalised adjacency; max_nodes bounds any graph.
+ * graph_idx (optional, B entries) gathers graphs of a resident dataset (row b of
+ * the output is graph graph_idx[b]).
  * Writes u (B, 2 d_L); if z_out != NULL also head_forward_batch (model.py:197-203). */
 int kt_embed_csr(const kt_dims* dims, const float* params, const double* fmean, const double* fstd,
                  const double* feats, const uint8_t* mask, const int64_t* node_ptr,
                  int32_t nodes_per_graph, int32_t max_nodes,
-                 const int32_t* row_ptr, const int32_t* col, const float* val, int64_t B,
-                 float* u_out, float* z_out, void* stream);
+                 const int32_t* row_ptr, const int32_t* col, const float* val,
+                 const int64_t* graph_idx, int64_t B, float* u_out, float* z_out, void* stream);
 /* head_forward_batch (model.py:197-203): u (B, head[0]) -> z (B). */
 int kt_head_forward(const kt_dims* dims, const float* params, const float* u, int64_t B,
                     float* z_out, void* stream);
+
+/* ---- training (model.py:218-310, meta.py:104-123) ----------------------------------------- */
+/* grad(m, batch, scope) (model.py:218-285) over a CSR batch laid out as for
+ * kt_embed_csr.  graph_idx (optional, B entries) gathers graphs of a resident
+ * dataset.  Batch item b uses graph graph_idx ? graph_idx[b] : b and the
+ * z-normalised label y[b] (model.py:99-101).
+ * Writes the batch-mean gradient (flat layout) to grad_out (may be NULL) and the
+ * MSE to *loss_out (fp64, may be NULL); if new_params != NULL also writes
+ * params - lr * grad (sgd_step, model.py:288-310) there.  head_only != 0 is
+ * scope "head_only" (gcn/agg gradients exactly zero).  The per-graph gradient
+ * rows are summed in a fixed order in fp64: results are run-to-run identical. */
+int64_t kt_grad_workspace_bytes(const kt_dims* dims, int64_t B);
+int kt_grad(const kt_dims* dims, const float* params, const double* fmean, const double* fstd,
+            const double* feats, const uint8_t* mask, const int64_t* node_ptr,
+            int32_t nodes_per_graph, int32_t max_nodes, const int32_t* row_ptr, const int32_t* col,
+            const float* val, const int64_t* graph_idx, const float* y, int64_t B, int32_t head_only,
+            float* grad_out, double* loss_out, float lr, float* new_params,
+            void* workspace, int64_t workspace_bytes, void* stream);
+/* sgd_step on flat vectors: out = params - lr * grad (out may alias params). */
+int kt_sgd(const float* params, const float* grad, float lr, int64_t n, float* out, void* stream);
+/* The batch-1 SGD loop of pretrain (meta.py:117-122): for s in 0..n_steps-1,
+ * params -= gamma * grad(params, [dataset graph order[s]], "all"); y is indexed
+ * by dataset graph.  One CTA, parameters resident in shared memory; params is
+ * updated in place. */
+int kt_pretrain_sgd(const kt_dims* dims, float* params, const double* fmean, const double* fstd,
+                    const double* feats, const uint8_t* mask, const int64_t* node_ptr,
+                    int32_t nodes_per_graph, int32_t max_nodes, const int32_t* row_ptr,
+                    const int32_t* col, const float* val, const int64_t* order, const float* y,
+                    int64_t n_steps, float gamma, void* stream);
+
+/* ---- head engine, MAML, fine-tune (model.py:358-432, meta.py:167-297) ---------------------- */
+/* Flat head vectors (head_to_vec order) of n_head_params floats; dims supplies the
+ * head shapes (only the head fields and n_head_params are read).  u: (n, head[0])
+ * fp32 rows, y: (n,) normalised labels. */
+/* head_loss_grad (model.py:358-389): grad_out (flat), *mse_out (may be NULL). */
+int kt_head_loss_grad(const kt_dims* dims, const float* theta, const float* u, const float* y, int64_t n,
+                      float* grad_out, float* mse_out, void* stream);
+/* head_hvp (model.py:392-432): Hessian-vector product H(theta) v. */
+int kt_head_hvp(const kt_dims* dims, const float* theta, const float* u, const float* y, const float* v,
+                int64_t n, float* hvp_out, void* stream);
+/* fine_tune_embedded (meta.py:274-282): `steps` full-batch head SGD steps of rate
+ * alpha; theta_out may alias theta; mse_out (steps floats, may be NULL) gets the
+ * loss before each step. */
+int kt_fine_tune(const kt_dims* dims, const float* theta, const float* u, const float* y, int64_t n,
+                 float alpha, int32_t steps, float* theta_out, float* mse_out, void* stream);
+/* One CTA per task: maml_outer_grad (meta.py:167-196) for T tasks whose support
+ * / query rows are u[s_idx[s_off[t] .. s_off[t+1])] / u[q_idx[...]] (labels y
+ * indexed the same way).  Writes g_sum = sum_t g_t (fixed order, fp64 accumulate)
+ * and stats = (sum_t support_loss_t, sum_t query_loss_t) (fp64, may be NULL).
+ * meta_step's update is then theta - beta * g_sum (kt_sgd), after an all-reduce
+ * of g_sum when tasks are sharded over ranks. */
+int64_t kt_maml_workspace_bytes(const kt_dims* dims, int32_t T, int32_t inner_steps, int32_t first_order);
+int kt_maml_tasks(const kt_dims* dims, const float* theta, const float* u, const float* y,
+                  const int64_t* s_off, const int64_t* s_idx, const int64_t* q_off, const int64_t* q_idx,
+                  int32_t T, float alpha, int32_t inner_steps, int32_t first_order, float* g_sum,
+                  double* stats, void* workspace, int64_t workspace_bytes, void* stream);
 
 /* ---- ranking (search.py:257-264) ------------------------------------------------------ */
 /* Top-k of (score desc, index asc) over B candidates; `visited` (sorted int64,

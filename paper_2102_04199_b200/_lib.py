@@ -85,9 +85,21 @@ _SIGS = {
     "kt_encode_raw": (ctypes.c_int, [vp, vp, i64, vp, vp, vp]),
     "kt_encode_raw_choices": (ctypes.c_int, [vp, vp, i64, vp, vp, vp]),
     "kt_score_indices": (ctypes.c_int, [vp, ctypes.POINTER(Dims), vp, vp, i64, i64, vp, vp, vp, vp]),
-    "kt_embed_csr": (ctypes.c_int, [ctypes.POINTER(Dims), vp, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, i64,
-                                    vp, vp, vp]),
+    "kt_embed_csr": (ctypes.c_int, [ctypes.POINTER(Dims), vp, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp,
+                                    i64, vp, vp, vp]),
     "kt_head_forward": (ctypes.c_int, [ctypes.POINTER(Dims), vp, vp, i64, vp, vp]),
+    "kt_grad_workspace_bytes": (i64, [ctypes.POINTER(Dims), i64]),
+    "kt_grad": (ctypes.c_int, [ctypes.POINTER(Dims), vp, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, i64,
+                               i32, vp, vp, f32, vp, vp, i64, vp]),
+    "kt_sgd": (ctypes.c_int, [vp, vp, f32, i64, vp, vp]),
+    "kt_pretrain_sgd": (ctypes.c_int, [ctypes.POINTER(Dims), vp, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp,
+                                       i64, f32, vp]),
+    "kt_head_loss_grad": (ctypes.c_int, [ctypes.POINTER(Dims), vp, vp, vp, i64, vp, vp, vp]),
+    "kt_head_hvp": (ctypes.c_int, [ctypes.POINTER(Dims), vp, vp, vp, vp, i64, vp, vp]),
+    "kt_fine_tune": (ctypes.c_int, [ctypes.POINTER(Dims), vp, vp, vp, i64, f32, i32, vp, vp, vp]),
+    "kt_maml_workspace_bytes": (i64, [ctypes.POINTER(Dims), i32, i32, i32]),
+    "kt_maml_tasks": (ctypes.c_int, [ctypes.POINTER(Dims), vp, vp, vp, vp, vp, vp, vp, i32, f32, i32, i32, vp, vp,
+                                     vp, i64, vp]),
     "kt_topk_workspace_bytes": (i64, [i64, i32]),
     "kt_topk": (ctypes.c_int, [vp, vp, i64, i64, vp, i64, i32, vp, vp, vp, i64, vp]),
     "kt_topk_merge": (ctypes.c_int, [vp, vp, i64, i32, vp, vp, vp, i64, vp]),

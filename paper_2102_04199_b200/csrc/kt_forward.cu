@@ -12,8 +12,8 @@ __global__ void __launch_bounds__(WARPS * 32)
 embed_kernel(kt_dims dims, const float* __restrict__ params, const double* __restrict__ fmean,
              const double* __restrict__ fstd, const double* __restrict__ feats, const uint8_t* __restrict__ mask,
              const int64_t* __restrict__ node_ptr, int npg, int max_nodes, const int32_t* __restrict__ row_ptr,
-             const int32_t* __restrict__ col, const float* __restrict__ val, int64_t B, int D,
-             float* __restrict__ u_out, float* __restrict__ z_out) {
+             const int32_t* __restrict__ col, const float* __restrict__ val, const int64_t* __restrict__ gidx,
+             int64_t B, int D, float* __restrict__ u_out, float* __restrict__ z_out) {
   extern __shared__ __align__(16) float sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slab = 2 * max_nodes * D + 2 * 2 * KT_MAX_DIM;
@@ -22,25 +22,26 @@ embed_kernel(kt_dims dims, const float* __restrict__ params, const double* __res
   float* h0 = Bf + max_nodes * D;
   float* h1 = h0 + 2 * KT_MAX_DIM;
   const int dl = dims.gcn[dims.n_gcn];
+  const WarpGroup W{lane};
   for (int64_t g = static_cast<int64_t>(blockIdx.x) * WARPS + warp; g < B;
        g += static_cast<int64_t>(gridDim.x) * WARPS) {
-    const GraphView v = graph_view(g, node_ptr, npg, row_ptr, col, val, mask);
-    load_features(v, feats, dims.F, fmean, fstd, A, D, lane);
-    __syncwarp();
+    const GraphView v = graph_view(gidx ? gidx[g] : g, node_ptr, npg, row_ptr, col, val, mask);
+    load_features(W, v, feats, dims.F, fmean, fstd, A, D);
+    W.sync();
     for (int l = 0; l < dims.n_gcn; ++l) {
-      csr_aggregate(v, A, Bf, dims.gcn[l], D, lane);
-      __syncwarp();
-      dense(Bf, params + dims.off_gcn[l], A, v.n, dims.gcn[l], dims.gcn[l + 1], D, true, lane);
-      __syncwarp();
+      csr_aggregate(W, v, A, Bf, dims.gcn[l], D);
+      W.sync();
+      dense(W, Bf, params + dims.off_gcn[l], A, v.n, dims.gcn[l], dims.gcn[l + 1], D, true);
+      W.sync();
     }
-    readout(A, v.n, dl, D, params + dims.off_agg, h0, lane);
-    __syncwarp();
+    readout(W, A, v.n, dl, D, params + dims.off_agg, h0, static_cast<int*>(nullptr));
+    W.sync();
     for (int c = lane; c < 2 * dl; c += 32) u_out[g * 2 * dl + c] = h0[c];
     if (z_out) {
-      const float z = head_row(dims, params, h0, h1, lane);
+      const float z = head_row(W, dims, params, h0, h1);
       if (lane == 0) z_out[g] = z;
     }
-    __syncwarp();
+    W.sync();
   }
 }
 
@@ -54,7 +55,7 @@ head_kernel(kt_dims dims, const float* __restrict__ params, const float* __restr
        g += static_cast<int64_t>(gridDim.x) * WARPS) {
     for (int c = lane; c < d0; c += 32) buf[warp][0][c] = u[g * d0 + c];
     __syncwarp();
-    const float z = head_row(dims, params, buf[warp][0], buf[warp][1], lane);
+    const float z = head_row(WarpGroup{lane}, dims, params, buf[warp][0], buf[warp][1]);
     if (lane == 0) z_out[g] = z;
     __syncwarp();
   }
@@ -81,8 +82,8 @@ extern "C" {
 
 int kt_embed_csr(const kt_dims* dims, const float* params, const double* fmean, const double* fstd,
                  const double* feats, const uint8_t* mask, const int64_t* node_ptr, int32_t nodes_per_graph,
-                 int32_t max_nodes, const int32_t* row_ptr, const int32_t* col, const float* val, int64_t B,
-                 float* u_out, float* z_out, void* stream) {
+                 int32_t max_nodes, const int32_t* row_ptr, const int32_t* col, const float* val,
+                 const int64_t* graph_idx, int64_t B, float* u_out, float* z_out, void* stream) {
   using namespace kt;
   KT_REQUIRE(dims && params && fmean && fstd && feats && mask && row_ptr && col && val && u_out, KT_E_ARG,
              "kt_embed_csr: null pointer");
@@ -104,8 +105,8 @@ int kt_embed_csr(const kt_dims* dims, const float* params, const double* fmean, 
   int64_t blocks = (B + fwd::WARPS - 1) / fwd::WARPS;
   if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
   fwd::embed_kernel<<<(int)blocks, fwd::WARPS * 32, smem, as_stream(stream)>>>(
-      *dims, params, fmean, fstd, feats, mask, node_ptr, nodes_per_graph, max_nodes, row_ptr, col, val, B, D,
-      u_out, z_out);
+      *dims, params, fmean, fstd, feats, mask, node_ptr, nodes_per_graph, max_nodes, row_ptr, col, val, graph_idx,
+      B, D, u_out, z_out);
   note_launches(1);
   return check_launch("kt_embed_csr");
 }

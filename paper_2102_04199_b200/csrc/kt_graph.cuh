@@ -1,16 +1,28 @@
-// Warp-per-graph building blocks for general (non-star) graphs and arbitrary
+// Thread-group building blocks for general (non-star) graphs and arbitrary
 // model dims: normalisation, CSR aggregation, dense transform + ReLU, readout,
-// head forward.  Shared by the general forward, training and MAML kernels.
+// head forward, and the reverse-mode pieces of model.grad (model.py:218-285).
 //
-// A warp owns one graph; its activations live in that warp's shared-memory
-// slab with row stride D (>= every layer width).  Lanes stride over feature
-// columns, so CSR neighbour gathers read whole rows conflict-free and weight
-// reads (W[k][c], lanes on c) are coalesced and L1-resident.
+// A group (one warp, or a whole CTA for the sequential-SGD kernel) owns one
+// graph; its activations live in the group's shared-memory slab with row
+// stride D (>= every layer width).  Threads stride over feature columns, so CSR
+// neighbour gathers read whole rows conflict-free and weight reads W[k][c]
+// (threads on c) are coalesced and L1-resident.
 #pragma once
 
 #include "kt_common.cuh"
 
 namespace kt {
+
+struct WarpGroup {
+  int r;  // rank in group
+  static constexpr int n = 32;
+  __device__ __forceinline__ void sync() const { __syncwarp(); }
+};
+
+struct CtaGroup {
+  int r, n;
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
+};
 
 struct GraphView {
   int n;                 // nodes in this graph
@@ -46,11 +58,11 @@ __device__ __forceinline__ GraphView graph_view(int64_t g, const int64_t* node_p
   return v;
 }
 
-// X (n x F) <- normalised raw features of the graph's masked rows, zero elsewhere.
-__device__ __forceinline__ void load_features(const GraphView& v, const double* feats, int F,
-                                              const double* fmean, const double* fstd, float* X, int D,
-                                              int lane) {
-  for (int e = lane; e < v.n * F; e += 32) {
+// X (n x F) <- normalised raw features of the graph's masked rows, zero elsewhere (model.py:108-112).
+template <class Grp>
+__device__ __forceinline__ void load_features(const Grp& G, const GraphView& v, const double* feats, int F,
+                                              const double* fmean, const double* fstd, float* X, int D) {
+  for (int e = G.r; e < v.n * F; e += G.n) {
     const int r = e / F, f = e - (e / F) * F;
     float x = 0.0f;
     if (v.mask[r]) x = static_cast<float>((feats[(v.node0 + r) * F + f] - fmean[f]) / fstd[f]);
@@ -58,69 +70,92 @@ __device__ __forceinline__ void load_features(const GraphView& v, const double* 
   }
 }
 
-// T (n x din) <- A_hat H
-__device__ __forceinline__ void csr_aggregate(const GraphView& v, const float* Hs, float* Ts, int din, int D,
-                                              int lane) {
-  for (int r = 0; r < v.n; ++r) {
-    const int64_t b = v.row_ptr[v.rp_base + r], e = v.row_ptr[v.rp_base + r + 1];
-    for (int c = lane; c < din; c += 32) {
-      float acc = 0.0f;
-      for (int64_t q = b; q < e; ++q) acc = fmaf(v.val[q], Hs[(v.col[q] - v.col_base) * D + c], acc);
-      Ts[r * D + c] = acc;
-    }
+// T (n x din) <- A_hat H   (A_hat symmetric, so A_hat^T products use the same routine)
+template <class Grp>
+__device__ __forceinline__ void csr_aggregate(const Grp& G, const GraphView& v, const float* Hs, float* Ts,
+                                              int din, int D) {
+  for (int e = G.r; e < v.n * din; e += G.n) {
+    const int r = e / din, c = e - (e / din) * din;
+    const int64_t b = v.row_ptr[v.rp_base + r], end = v.row_ptr[v.rp_base + r + 1];
+    float acc = 0.0f;
+    for (int64_t q = b; q < end; ++q) acc = fmaf(v.val[q], Hs[(v.col[q] - v.col_base) * D + c], acc);
+    Ts[r * D + c] = acc;
   }
 }
 
-// Out (n x dout) <- T W (+ optional ReLU); W row-major (din x dout) in global memory.
-__device__ __forceinline__ void dense(const float* Ts, const float* __restrict__ W, float* Out, int n, int din,
-                                      int dout, int D, bool relu_out, int lane) {
-  for (int c = lane; c < dout; c += 32) {
-    for (int r = 0; r < n; ++r) {
-      float acc = 0.0f;
-      for (int k = 0; k < din; ++k) acc = fmaf(Ts[r * D + k], __ldg(W + k * dout + c), acc);
-      Out[r * D + c] = relu_out ? fmaxf(acc, 0.0f) : acc;
-    }
+// Out (n x dout) <- T W (+ optional ReLU); W row-major (din x dout).
+template <class Grp>
+__device__ __forceinline__ void dense(const Grp& G, const float* Ts, const float* __restrict__ W, float* Out, int n,
+                                      int din, int dout, int D, bool relu_out) {
+  for (int e = G.r; e < n * dout; e += G.n) {
+    const int r = e / dout, c = e - (e / dout) * dout;
+    float acc = 0.0f;
+    for (int k = 0; k < din; ++k) acc = fmaf(Ts[r * D + k], W[k * dout + c], acc);
+    Out[r * D + c] = relu_out ? fmaxf(acc, 0.0f) : acc;
   }
 }
 
-// u = [sum_n a_c H[n][c], max_n H[n][c]]  (model.py:136-141 / 192-194)
-__device__ __forceinline__ void readout(const float* Hs, int n, int d, int D, const float* __restrict__ agg,
-                                       float* u, int lane) {
-  for (int c = lane; c < d; c += 32) {
-    const float a = __ldg(agg + c);
+// Out (n x din) <- dZ W^T   (W is din x dout)
+template <class Grp>
+__device__ __forceinline__ void dense_t(const Grp& G, const float* dZ, const float* __restrict__ W, float* Out,
+                                        int n, int din, int dout, int D) {
+  for (int e = G.r; e < n * din; e += G.n) {
+    const int r = e / din, k = e - (e / din) * din;
+    float acc = 0.0f;
+    for (int c = 0; c < dout; ++c) acc = fmaf(dZ[r * D + c], W[k * dout + c], acc);
+    Out[r * D + k] = acc;
+  }
+}
+
+// u = [sum_n a_c H[n][c], max_n H[n][c]]  (model.py:136-141 / 192-194); arg[c] = first argmax
+template <class Grp>
+__device__ __forceinline__ void readout(const Grp& G, const float* Hs, int n, int d, int D,
+                                       const float* __restrict__ agg, float* u, int* arg) {
+  for (int c = G.r; c < d; c += G.n) {
+    const float a = agg[c];
     float s = 0.0f, m = -INFINITY;
+    int am = 0;
     for (int r = 0; r < n; ++r) {
       const float h = Hs[r * D + c];
       s += h * a;
-      m = fmaxf(m, h);
+      if (h > m) { m = h; am = r; }
     }
     u[c] = s;
     u[d + c] = m;
+    if (arg) arg[c] = am;
+  }
+}
+
+// One affine head layer: out = in W + b (+ReLU unless last); W (din x dout) at params+off_w.
+template <class Grp>
+__device__ __forceinline__ void head_layer(const Grp& G, const float* in, const float* __restrict__ W,
+                                           const float* __restrict__ b, float* out, int din, int dout, bool relu_out) {
+  for (int c = G.r; c < dout; c += G.n) {
+    float acc = 0.0f;
+    for (int k = 0; k < din; ++k) acc = fmaf(in[k], W[k * dout + c], acc);
+    acc += b[c];
+    out[c] = relu_out ? fmaxf(acc, 0.0f) : acc;
   }
 }
 
 // Head forward of one row vector a (len dims.head[0]) using two ping-pong
-// buffers of >= KT_MAX_DIM floats; returns the scalar output.
-__device__ __forceinline__ float head_row(const kt_dims& dims, const float* __restrict__ params, float* a,
-                                          float* tmp, int lane) {
+// buffers of >= 2*KT_MAX_DIM floats; returns the scalar output.
+template <class Grp>
+__device__ __forceinline__ float head_row(const Grp& G, const kt_dims& dims, const float* __restrict__ params,
+                                          float* a, float* tmp) {
   float* in = a;
   float* out = tmp;
   for (int i = 0; i < dims.n_head; ++i) {
-    const int din = dims.head[i], dout = dims.head[i + 1];
-    const float* W = params + dims.off_hw[i];
-    const float* b = params + dims.off_hb[i];
-    const bool last = i == dims.n_head - 1;
-    __syncwarp();
-    for (int c = lane; c < dout; c += 32) {
-      float acc = 0.0f;
-      for (int k = 0; k < din; ++k) acc = fmaf(in[k], __ldg(W + k * dout + c), acc);
-      acc += __ldg(b + c);
-      out[c] = last ? acc : fmaxf(acc, 0.0f);
-    }
-    __syncwarp();
+    G.sync();
+    head_layer(G, in, params + dims.off_hw[i], params + dims.off_hb[i], out, dims.head[i], dims.head[i + 1],
+               i != dims.n_head - 1);
+    G.sync();
     float* t = in; in = out; out = t;
   }
   return in[0];
 }
+
+// Backwards compatible warp helpers (lane-based) used by the forward kernels.
+__device__ __forceinline__ WarpGroup warp_group(int lane) { return WarpGroup{lane}; }
 
 }  // namespace kt

@@ -396,7 +396,7 @@ def embed_batch(m: ModelState, feats, mask, adj) -> torch.Tensor:
     lib = _lib.load()
     with torch.cuda.device(dev):
         _lib.check(lib.kt_embed_csr(d, _lib.ptr(flat), _lib.ptr(mean), _lib.ptr(std), _lib.ptr(x),
-                                    _lib.ptr(mk), None, n, n, _lib.ptr(rp), _lib.ptr(col), _lib.ptr(val), b,
+                                    _lib.ptr(mk), None, n, n, _lib.ptr(rp), _lib.ptr(col), _lib.ptr(val), None, b,
                                     _lib.ptr(u), None, _lib.stream_handle()), "embed_batch")
     return u
 
@@ -432,7 +432,7 @@ def embed_graphs(m: ModelState, graphs, with_scores: bool = False):
     with torch.cuda.device(dev):
         _lib.check(lib.kt_embed_csr(d, _lib.ptr(flat), _lib.ptr(mean), _lib.ptr(std), _lib.ptr(pk.feats),
                                     _lib.ptr(pk.mask), _lib.ptr(pk.node_ptr), 0, pk.max_nodes,
-                                    _lib.ptr(pk.row_ptr), _lib.ptr(pk.col), _lib.ptr(pk.val), pk.n_graphs,
+                                    _lib.ptr(pk.row_ptr), _lib.ptr(pk.col), _lib.ptr(pk.val), None, pk.n_graphs,
                                     _lib.ptr(u), _lib.ptr(z), _lib.stream_handle()), "embed_graphs")
     return (u, z) if with_scores else u
 
@@ -491,6 +491,140 @@ def with_head_vec(m: ModelState, head_vec: torch.Tensor) -> ModelState:
     flat = flat_params(m)
     new = torch.cat([flat[: d.off_head], head_vec.reshape(-1).to(flat.dtype)])
     return model_from_flat(new, m)
+
+
+# --- gradients and SGD (model.py:218-310) --------------------------------------------------
+
+
+def _grad_packed(m: ModelState, pk: PackedGraphs, y: torch.Tensor, scope: str, graph_idx=None, *,
+                 lr: float | None = None, npg: int = 0):
+    """Device grad over a packed batch; returns (loss tensor fp64 (1,), grad flat, new flat or None)."""
+    if scope not in ("all", "head_only"):
+        raise DomainError(f"unknown grad scope {scope!r}")
+    flat = flat_params(m)
+    dev = flat.device
+    d = dims_of(m)
+    b = int(graph_idx.numel()) if graph_idx is not None else pk.n_graphs
+    if b == 0:
+        raise DomainError("empty batch")
+    mean, std = _norm_tensors(m, dev)
+    lib = _lib.load()
+    ws_bytes = int(lib.kt_grad_workspace_bytes(d, b))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    g = torch.empty_like(flat)
+    loss = torch.empty(1, dtype=torch.float64, device=dev)
+    new = torch.empty_like(flat) if lr is not None else None
+    with torch.cuda.device(dev):
+        _lib.check(lib.kt_grad(d, _lib.ptr(flat), _lib.ptr(mean), _lib.ptr(std), _lib.ptr(pk.feats),
+                               _lib.ptr(pk.mask), None if npg else _lib.ptr(pk.node_ptr), npg, pk.max_nodes,
+                               _lib.ptr(pk.row_ptr), _lib.ptr(pk.col), _lib.ptr(pk.val), _lib.ptr(graph_idx),
+                               _lib.ptr(y), b, 1 if scope == "head_only" else 0, _lib.ptr(g), _lib.ptr(loss),
+                               0.0 if lr is None else float(lr), _lib.ptr(new), _lib.ptr(ws), ws_bytes,
+                               _lib.stream_handle()), "grad")
+    return loss, g, new
+
+
+def grad(m: ModelState, batch: list, scope: str = "all"):
+    """(loss, Gradients) of the batch MSE over [(graph, label_gflops)] (model.py:218-285).
+
+    scope "head_only" leaves gcn/agg gradients exactly zero."""
+    if scope not in ("all", "head_only"):
+        raise DomainError(f"unknown grad scope {scope!r}")
+    if not batch:
+        raise DomainError("empty batch")
+    ys = np.array([normalize_label(m, float(v)) for _, v in batch], dtype=np.float64)
+    if not np.isfinite(ys).all():
+        raise DomainError("non-finite label")
+    dev = flat_params(m).device
+    pk = pack_graphs([g for g, _ in batch], dev)
+    y = torch.from_numpy(ys.astype(np.float32)).to(dev)
+    loss, g, _ = _grad_packed(m, pk, y, scope)
+    return float(loss.item()), grads_from_flat(g, m)
+
+
+def _sgd_flat(p: torch.Tensor, g: torch.Tensor, lr: float) -> torch.Tensor:
+    if p.shape != g.shape:
+        raise DomainError("parameter/gradient shape mismatch")
+    pc = p.contiguous().float()
+    gc = g.to(device=pc.device, dtype=torch.float32).contiguous()
+    out = torch.empty_like(pc)
+    if pc.numel() == 0:
+        return out
+    lib = _lib.load()
+    with torch.cuda.device(pc.device):
+        _lib.check(lib.kt_sgd(_lib.ptr(pc), _lib.ptr(gc), float(lr), pc.numel(), _lib.ptr(out),
+                              _lib.stream_handle()), "sgd_step")
+    return out
+
+
+def sgd_step(p, g, lr: float):
+    """p - lr*g for ModelState/Gradients, HeadParams/Gradients or plain arrays (model.py:288-310)."""
+    if isinstance(p, ModelState) and isinstance(g, Gradients):
+        if _shapes(p) != [tuple(t.shape) for t in
+                          list(g.gcn) + [g.agg] + [t for w, b in zip(g.head_weights, g.head_biases) for t in (w, b)]]:
+            raise DomainError("gradient shapes do not match parameters")
+        return model_from_flat(_sgd_flat(flat_params(p), flat_grads(g), lr), p)
+    if isinstance(p, HeadParams) and isinstance(g, Gradients):
+        gh = HeadParams(list(g.head_weights), list(g.head_biases))
+        return vec_to_head(_sgd_flat(head_to_vec(p), head_to_vec(gh), lr), p)
+    if isinstance(p, (np.ndarray, torch.Tensor)) and isinstance(g, (np.ndarray, torch.Tensor)):
+        if tuple(p.shape) != tuple(g.shape):
+            raise DomainError("parameter/gradient shape mismatch")
+        was_np = isinstance(p, np.ndarray)
+        dev = p.device if isinstance(p, torch.Tensor) and p.is_cuda else torch.device("cuda", torch.cuda.current_device())
+        pt = torch.as_tensor(p, dtype=torch.float32).to(dev).reshape(-1)
+        out = _sgd_flat(pt, torch.as_tensor(g, dtype=torch.float32).to(dev).reshape(-1), lr).view(tuple(p.shape))
+        return out.cpu().numpy().astype(p.dtype) if was_np else out
+    raise DomainError(f"cannot apply sgd_step to {type(p).__name__}/{type(g).__name__}")
+
+
+# --- head engine on flat vectors (model.py:358-432) ------------------------------------------
+
+
+def _head_dims_like(like: HeadParams) -> _lib.Dims:
+    return head_only_dims([tuple(w.shape) for w in like.weights])
+
+
+def _dev_vec(x, dev):
+    return torch.as_tensor(x, dtype=torch.float32).to(dev).contiguous().reshape(-1)
+
+
+def head_loss_grad(vec, like: HeadParams, u, y):
+    """(mse, d mse / d vec) of the head at flat params `vec` on embeddings u (n, D)."""
+    d = _head_dims_like(like)
+    dev = _device_of([vec] + list(like.weights))
+    v = _dev_vec(vec, dev)
+    if v.numel() != d.n_head_params:
+        raise DomainError("flat head vector has the wrong length")
+    uu = torch.as_tensor(u, dtype=torch.float32).to(dev).contiguous()
+    yy = _dev_vec(y, dev)
+    if uu.dim() != 2 or uu.shape[1] != d.head[0] or uu.shape[0] != yy.numel():
+        raise DomainError("u / y shapes do not match the head")
+    g = torch.empty_like(v)
+    mse = torch.empty(1, dtype=torch.float32, device=dev)
+    lib = _lib.load()
+    with torch.cuda.device(dev):
+        _lib.check(lib.kt_head_loss_grad(d, _lib.ptr(v), _lib.ptr(uu), _lib.ptr(yy), uu.shape[0], _lib.ptr(g),
+                                         _lib.ptr(mse), _lib.stream_handle()), "head_loss_grad")
+    return float(mse.item()), g
+
+
+def head_hvp(vec, like: HeadParams, u, y, v) -> torch.Tensor:
+    """Hessian-vector product of the head MSE at `vec` along `v` (forward-over-reverse)."""
+    d = _head_dims_like(like)
+    dev = _device_of([vec] + list(like.weights))
+    th = _dev_vec(vec, dev)
+    vv = _dev_vec(v, dev)
+    if th.numel() != d.n_head_params or vv.numel() != d.n_head_params:
+        raise DomainError("flat head vector has the wrong length")
+    uu = torch.as_tensor(u, dtype=torch.float32).to(dev).contiguous()
+    yy = _dev_vec(y, dev)
+    out = torch.empty_like(th)
+    lib = _lib.load()
+    with torch.cuda.device(dev):
+        _lib.check(lib.kt_head_hvp(d, _lib.ptr(th), _lib.ptr(uu), _lib.ptr(yy), _lib.ptr(vv), uu.shape[0],
+                                   _lib.ptr(out), _lib.stream_handle()), "head_hvp")
+    return out
 
 
 # --- checkpoints (model.py:438-477, npz v1) ----------------------------------------------------

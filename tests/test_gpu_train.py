@@ -1,0 +1,217 @@
+"""Device parity of the training path: grad / sgd_step, head engine, MAML, fine-tune, pretrain.
+
+Tolerances (fp32 device vs fp64 reference; SURVEY.md 7 hard part 1):
+  * gradients: per-tensor norm-wise rel <= 1e-4, and element-wise rel <= 1e-4
+    above an absolute floor of 1e-4 * max|g| (batch-sum cancellation leaves a few
+    tiny entries with larger relative error);
+  * parameters after updates: element-wise rel <= 1e-5 (floor 1e-7);
+  * losses: rel <= 1e-5.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import kt_oracle as ko
+from paper_2102_04199_b200 import graphs as pg
+from paper_2102_04199_b200 import kernels as pk
+from paper_2102_04199_b200 import meta as pmeta
+from paper_2102_04199_b200 import model as pm
+from tests._shared import device_model, head_shapes, oracle_params, spec_of
+
+pytestmark = pytest.mark.gpu
+OPS = pk.OP_TYPES
+TEMPLATE = pg.build_super_template(OPS)
+
+
+def assert_grad_close(got, want, rtol=1e-4):
+    got = np.asarray(got, dtype=np.float64).ravel()
+    want = np.asarray(want, dtype=np.float64).ravel()
+    scale = np.linalg.norm(want)
+    if scale == 0:
+        assert np.abs(got).max() == 0
+        return
+    assert np.linalg.norm(got - want) <= rtol * scale, f"norm-wise rel {np.linalg.norm(got - want) / scale:.2e}"
+    floor = 1e-4 * np.abs(want).max()
+    big = np.abs(want) > floor
+    rel = np.abs(got[big] - want[big]) / np.abs(want[big])
+    assert rel.max() <= rtol * 10, f"element-wise rel {rel.max():.2e}"
+
+
+def assert_params_close(got, want, rtol=1e-5):
+    got = np.asarray(got, dtype=np.float64).ravel()
+    want = np.asarray(want, dtype=np.float64).ravel()
+    err = np.abs(got - want) / np.maximum(np.abs(want), 1e-7 / rtol * 1e-5 + 1e-7)
+    assert np.abs(got - want).max() <= rtol * np.abs(want).max() or err.max() <= 10 * rtol, \
+        f"max abs {np.abs(got - want).max():.2e}"
+    assert np.linalg.norm(got - want) <= rtol * np.linalg.norm(want)
+
+
+def corpus_samples(g_encode, g_meta, super_graph):
+    out = []
+    for op_i, idx, y in zip(g_meta["op"], g_meta["idx"], g_meta["labels"]):
+        op = OPS[int(op_i)]
+        spec = spec_of(g_encode, op)
+        space = pk.build_knob_space(spec)
+        g = pg.config_graph(spec, pk.index_config(space, int(idx)), space,
+                            template=TEMPLATE if super_graph else None)
+        out.append(pmeta.LabeledSample(g, spec.signature(), float(y)))
+    return out
+
+
+@pytest.fixture(scope="module")
+def raw_samples(g_encode, g_meta):
+    return corpus_samples(g_encode, g_meta, False)
+
+
+@pytest.fixture(scope="module")
+def super_samples(g_encode, g_meta):
+    return corpus_samples(g_encode, g_meta, True)
+
+
+@pytest.mark.parametrize("b", [0, 1, 2])
+@pytest.mark.parametrize("scope", ["all", "head_only"])
+def test_grad_matches_reference(cuda_device, g_model, g_grad, raw_samples, b, scope):
+    m = device_model(g_model)
+    pick = g_grad[f"b{b}/pick"]
+    batch = [(raw_samples[int(j)].graph, raw_samples[int(j)].label_gflops) for j in pick]
+    loss, g = pm.grad(m, batch, scope)
+    ref_loss = float(g_grad[f"b{b}/{scope}/loss"])
+    assert abs(loss - ref_loss) <= 1e-5 * max(abs(ref_loss), 1e-6)
+    for i, w in enumerate(g.gcn):
+        assert_grad_close(w.cpu().numpy(), g_grad[f"b{b}/{scope}/gcn{i}"])
+    assert_grad_close(g.agg.cpu().numpy(), g_grad[f"b{b}/{scope}/agg"])
+    for i, (w, bb) in enumerate(zip(g.head_weights, g.head_biases)):
+        assert_grad_close(w.cpu().numpy(), g_grad[f"b{b}/{scope}/hw{i}"])
+        assert_grad_close(bb.cpu().numpy(), g_grad[f"b{b}/{scope}/hb{i}"])
+    if scope == "head_only":
+        assert not any(w.any() for w in g.gcn) and not g.agg.any()
+
+
+def test_grad_is_deterministic(cuda_device, g_model, raw_samples):
+    m = device_model(g_model)
+    batch = [(s.graph, s.label_gflops) for s in raw_samples[:200]]
+    l1, g1 = pm.grad(m, batch)
+    l2, g2 = pm.grad(m, batch)
+    assert l1 == l2 and torch.equal(g1._flat, g2._flat)
+
+
+def test_grad_super_batch_vs_oracle(cuda_device, g_model, super_samples):
+    """Batch of 360 super-graph samples (all ops) against the oracle."""
+    m = device_model(g_model)
+    p = oracle_params(g_model)
+    loss, g = pm.grad(m, [(s.graph, s.label_gflops) for s in super_samples])
+    trip = []
+    for s in super_samples:
+        t = pg.graph_to_tensors(s.graph)
+        trip.append((t.feature_matrix, t.normalized_adjacency, t.feature_mask))
+    rl, rg = ko.grad(p, trip, [s.label_gflops for s in super_samples])
+    assert abs(loss - rl) <= 1e-5 * rl
+    for a, b in zip(g.gcn + [g.agg] + g.head_weights + g.head_biases,
+                    rg["gcn"] + [rg["agg"]] + rg["head_w"] + rg["head_b"]):
+        assert_grad_close(a.cpu().numpy(), b)
+
+
+def test_sgd_step_matches_reference(cuda_device, g_model, g_grad, raw_samples):
+    m = device_model(g_model)
+    pick = g_grad["b2/pick"]
+    batch = [(raw_samples[int(j)].graph, raw_samples[int(j)].label_gflops) for j in pick]
+    _, g = pm.grad(m, batch)
+    m2 = pm.sgd_step(m, g, 0.005)
+    assert_params_close(pm.flat_params(m2).cpu().numpy(), g_grad["b2/sgd_vec"])
+    # pure: the input model is untouched
+    assert torch.equal(pm.flat_params(m), device_model(g_model)._flat)
+
+
+def test_sgd_step_arrays_and_guards(cuda_device):
+    out = pm.sgd_step(np.array([1.0, 2.0]), np.array([1.0, 1.0]), 0.5)
+    assert np.allclose(out, [0.5, 1.5]) and isinstance(out, np.ndarray)
+    with pytest.raises(pm.DomainError):
+        pm.sgd_step(np.zeros(2), np.zeros(3), 0.1)
+
+
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_head_loss_grad_and_hvp(cuda_device, g_model, g_head, k):
+    m = device_model(g_model)
+    th, u, y, v = (g_head[f"c{k}/{n}"] for n in ("theta", "u", "y", "v"))
+    mse, g = pm.head_loss_grad(th, m.head, u, y)
+    assert abs(mse - float(g_head[f"c{k}/mse"])) <= 1e-5 * float(g_head[f"c{k}/mse"])
+    assert_grad_close(g.cpu().numpy(), g_head[f"c{k}/grad"])
+    hv = pm.head_hvp(th, m.head, u, y, v)
+    assert_grad_close(hv.cpu().numpy(), g_head[f"c{k}/hvp"])
+
+
+@pytest.mark.parametrize("order", ["fo", "so"])
+def test_meta_step_matches_reference(cuda_device, g_model, g_meta, super_samples, order):
+    m = device_model(g_model)
+    cfg = pmeta.MetaConfig(n_way=3, k_shot=2, meta_batch=32, inner_steps=1, first_order=order == "fo")
+    tasks = [pmeta.MetaTask([super_samples[i] for i in s], [super_samples[i] for i in q], [])
+             for s, q in zip(g_meta[f"{order}/support"], g_meta[f"{order}/query"])]
+    m1, stats = pmeta.meta_step(m, tasks, cfg)
+    assert_params_close(pm.head_to_vec(m1.head).cpu().numpy(), g_meta[f"{order}/theta"])
+    np.testing.assert_allclose([stats["support_loss"], stats["query_loss"]], g_meta[f"{order}/stats"], rtol=1e-5)
+    assert torch.equal(pm.flat_params(m1)[: pm.dims_of(m).off_head], pm.flat_params(m)[: pm.dims_of(m).off_head])
+    m3 = m1
+    for _ in range(2):
+        m3, _ = pmeta.meta_step(m3, tasks, cfg)
+    assert_params_close(pm.head_to_vec(m3.head).cpu().numpy(), g_meta[f"{order}/theta3"])
+
+
+def test_meta_step_reductions(cuda_device, g_model, g_meta, super_samples):
+    m = device_model(g_model)
+    tasks = [pmeta.MetaTask([super_samples[i] for i in s], [super_samples[i] for i in q], [])
+             for s, q in zip(g_meta["fo/support"][:8], g_meta["fo/query"][:8])]
+    # beta = 0: bitwise identity
+    m0, _ = pmeta.meta_step(m, tasks, pmeta.MetaConfig(beta=0.0))
+    assert torch.equal(pm.flat_params(m0), pm.flat_params(m))
+    # alpha = 0: plain SGD (lr beta) on the summed query gradients
+    cfg = pmeta.MetaConfig(alpha=0.0, beta=0.002)
+    ma, _ = pmeta.meta_step(m, tasks, cfg)
+    theta = pm.head_to_vec(m.head)
+    total = torch.zeros_like(theta)
+    for t in tasks:
+        u, y = pmeta._embedded(m, t.query)
+        total += pm.head_loss_grad(theta, m.head, u, y)[1]
+    want = (theta - cfg.beta * total).cpu().numpy()
+    assert_params_close(pm.head_to_vec(ma.head).cpu().numpy(), want, rtol=1e-6)
+
+
+def test_fine_tune_matches_reference(cuda_device, g_model, g_meta, super_samples):
+    m = device_model(g_model)
+    ft = super_samples[:64]
+    m2 = pmeta.fine_tune(m, [(s.graph, s.label_gflops) for s in ft], 0.01, 8)
+    assert_params_close(pm.head_to_vec(m2.head).cpu().numpy(), g_meta["ft/theta"])
+    assert torch.equal(pm.flat_params(m2)[: pm.dims_of(m).off_head], pm.flat_params(m)[: pm.dims_of(m).off_head])
+    assert pmeta.fine_tune(m, [], 0.01, 5) is m
+
+
+def test_inner_adapt_alpha_zero_identity(cuda_device, g_model, super_samples):
+    m = device_model(g_model)
+    h = pmeta.inner_adapt(m, super_samples[:4], alpha=0.0, inner_steps=3)
+    assert torch.equal(pm.head_to_vec(h), pm.head_to_vec(m.head))
+
+
+def test_pretrain_matches_oracle_sgd_loop(cuda_device, g_encode, g_meta):
+    """pretrain == init_model(rng) + per-epoch rng.permutation + batch-1 SGD (meta.py:104-123)."""
+    from paper_2102_04199_b200.util import rng_from
+
+    samples = corpus_samples(g_encode, g_meta, False)[::9]  # 40 raw graphs of mixed sizes
+    cfg = pmeta.MetaConfig(pretrain_epochs=2, gamma=0.005)
+    m = pmeta.pretrain(samples, cfg, rng_from("pretrain-test"))
+    # oracle replay with the same draws
+    rng = rng_from("pretrain-test")
+    p = ko.init_params(rng)
+    fn, ln = pmeta.dataset_norms(samples)
+    p.update(fmean=fn.mean, fstd=fn.std, lmean=ln.mean, lstd=ln.std)
+    trip = []
+    for s in samples:
+        t = pg.graph_to_tensors(s.graph)
+        trip.append((t.feature_matrix, t.normalized_adjacency, t.feature_mask))
+    for _ in range(cfg.pretrain_epochs):
+        for i in rng.permutation(len(samples)):
+            _, g = ko.grad(p, [trip[int(i)]], [samples[int(i)].label_gflops])
+            p = ko.sgd(p, g, cfg.gamma)
+    want = np.concatenate([w.ravel() for w in p["gcn"]] + [p["agg"]] + [ko.head_to_vec(p["head_w"], p["head_b"])])
+    got = pm.flat_params(m).cpu().numpy()
+    assert np.linalg.norm(got - want) <= 1e-4 * np.linalg.norm(want)
+    assert np.array_equal(m.feature_norm.mean, fn.mean)
