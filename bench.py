@@ -143,6 +143,148 @@ def load_traffic():
     return None
 
 
+# --- secondary configs (C2 pretrain step, C3 MAML, C4 fine-tune) ----------------------
+
+
+def synthetic_corpus(n_kernels=47, per_kernel=200, ops=None, seed="bench-corpus"):
+    """Conftest-shaped corpus (47 kernel classes x 200 configs, super-graph layout) with
+    synthetic labels: the oracle platform model is out of scope, throughput does not
+    depend on label values."""
+    from paper_2102_04199_b200 import graphs as pg
+    from paper_2102_04199_b200 import kernels as pk
+    from paper_2102_04199_b200.meta import LabeledSample
+    from paper_2102_04199_b200.util import rng_from
+
+    rng = rng_from(seed)
+    tmpl = pg.build_super_template(pk.OP_TYPES)
+    ops = ops or pk.OP_TYPES
+    out, seen = [], set()
+    while len(seen) < n_kernels:
+        op = ops[int(rng.integers(0, len(ops)))]
+        one_d = op in ("conv1d", "transpose1d")
+        spec = pk.KernelSpec(op, int(rng.integers(150, 601) if one_d else rng.integers(7, 225)),
+                             int(rng.integers(32, 129) if one_d else rng.integers(3, 129)),
+                             int(rng.integers(32, 513) if one_d else rng.integers(16, 129)),
+                             int((1, 3, 5, 7)[int(rng.integers(0, 4))]), 3, 1)
+        if spec.signature() in seen:
+            continue
+        seen.add(spec.signature())
+        space = pk.build_knob_space(spec)
+        for c in pk.sample_configs(space, per_kernel, rng):
+            g = pg.config_graph(spec, c, space, template=tmpl)
+            out.append(LabeledSample(g, spec.signature(), float(2.0 ** rng.uniform(-10.0, 12.0))))
+    return out
+
+
+def bench_maml(m, corpus, steps, warmup, first_order=True):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2102_04199_b200 import meta as pmeta
+    from paper_2102_04199_b200.util import rng_from
+
+    cfg = pmeta.MetaConfig(n_way=3, k_shot=2, meta_batch=32, inner_steps=1, first_order=first_order)
+    tr = pmeta.MetaTrainer(m, corpus, cfg)
+    rank, _, ws = dist_env()
+    plan = tr.plan(rng_from("metatrain", "super", 0), warmup + steps, shard=(rank, ws))
+    bufs = tr._buffers(plan)
+    for s in range(warmup):
+        tr.step(plan, bufs, s)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for s in range(warmup, warmup + steps):
+        tr.step(plan, bufs, s)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if ws > 1:
+        t = torch.tensor([ms], device=pm_device(m))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    st = tr.stats(plan, bufs)
+    return {"metric": "MAML meta-train tasks/sec", "value": 32 / (ms / 1e3), "unit": "tasks/s",
+            "ms_per_step": ms, "steps": steps,
+            "config": f"C3: 3-way 2-shot, 32 tasks/outer step, 1 inner step, {'FO' if first_order else 'SO'}, "
+                      "frozen GCN re-embedding the step's 384 task graphs every step (super N=25), "
+                      f"47x200 synthetic corpus; 3 launches/step; tasks sharded over {ws} GPU(s) with an NCCL "
+                      "all-reduce of sum_i g_i per step",
+            "final_query_loss": float(st[-1, 1])}
+
+
+def pm_device(m):
+    return m._flat.device
+
+
+def bench_pretrain_step(m, corpus, steps, warmup):
+    """C2: grad(m, batch 512, "all") + sgd_step, mixed conv2d/winograd/depthwise (super)."""
+    import torch
+
+    from paper_2102_04199_b200 import _lib
+    from paper_2102_04199_b200 import model as pm
+    from paper_2102_04199_b200.util import rng_from
+
+    dev = pm.flat_params(m).device
+    pk_ = pm.pack_graphs([s.graph for s in corpus], dev)
+    y_all = np.array([pm.normalize_label(m, s.label_gflops) for s in corpus], dtype=np.float32)
+    rng = rng_from("bench-pretrain")
+    batches = [rng.choice(len(corpus), 512, replace=False) for _ in range(warmup + steps)]
+    gidx = [torch.from_numpy(b.astype(np.int64)).to(dev) for b in batches]
+    ys = [torch.from_numpy(y_all[b]).to(dev) for b in batches]
+    lib = _lib.load()
+    d = pm.dims_of(m)
+    flat = pm.flat_params(m).clone()
+    nxt = torch.empty_like(flat)
+    mean, std = pm._norm_tensors(m, dev)
+    ws_bytes = int(lib.kt_grad_workspace_bytes(d, 512))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    loss = torch.empty(1, dtype=torch.float64, device=dev)
+    p = _lib.ptr
+
+    def step(i, a, b):
+        _lib.check(lib.kt_grad(d, p(a), p(mean), p(std), p(pk_.feats), p(pk_.mask), p(pk_.node_ptr), 0,
+                               pk_.max_nodes, p(pk_.row_ptr), p(pk_.col), p(pk_.val), p(gidx[i]), p(ys[i]), 512, 0,
+                               None, p(loss), 0.005, p(b), p(ws), ws_bytes, _lib.stream_handle()), "pretrain step")
+
+    bufs = [flat, nxt]
+    for i in range(warmup):
+        step(i, bufs[i % 2], bufs[(i + 1) % 2])
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(warmup, warmup + steps):
+        step(i, bufs[i % 2], bufs[(i + 1) % 2])
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    return {"metric": "supervised pretrain step", "value": 512 / (ms / 1e3), "unit": "graphs/s", "ms_per_step": ms,
+            "config": "C2: grad(batch 512, scope all) + sgd_step(0.005), mixed conv2d/winograd/depthwise super "
+                      "graphs, fixed-order fp64 gradient reduction"}
+
+
+def bench_fine_tune(m, corpus, reps=50):
+    """C4: fine_tune_embedded on 64 candidates x 8 steps (TuneConfig defaults)."""
+    import torch
+
+    from paper_2102_04199_b200 import meta as pmeta
+    from paper_2102_04199_b200 import model as pm
+
+    u, y = pmeta._embedded(m, corpus[:64])
+    theta = pm.head_to_vec(m.head)
+    for _ in range(3):
+        pmeta.fine_tune_vec(m, theta, u, y, 0.01, 8)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        pmeta.fine_tune_vec(m, theta, u, y, 0.01, 8)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    return {"metric": "online fine-tune call", "value": ms, "unit": "ms/call", "higher_is_better": False,
+            "config": "C4: fine_tune_embedded(u 64x64, y, alpha 0.01, 8 steps), one kernel"}
+
+
 # --- CPU arms -------------------------------------------------------------------------
 
 
@@ -345,6 +487,14 @@ def run_ours(args):
     }
     if cpu:
         line["cpu_baseline"] = cpu
+    if not args.no_extras:
+        corpus = synthetic_corpus()
+        line["maml"] = bench_maml(m, corpus, args.meta_steps, 10)
+        if ws == 1:
+            line["maml_so"] = bench_maml(m, corpus, max(args.meta_steps // 2, 10), 5, first_order=False)
+            line["pretrain"] = bench_pretrain_step(m, [s for s in corpus if s.kernel_class.split("/")[0] in
+                                                       ("conv2d", "winograd", "depthwise")], 50, 5)
+            line["fine_tune"] = bench_fine_tune(m, corpus)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -361,6 +511,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 18)
     ap.add_argument("--ref-sample", type=int, default=0)
+    ap.add_argument("--no-extras", action="store_true", help="skip the C2/C3/C4 secondary measurements")
+    ap.add_argument("--meta-steps", type=int, default=200)
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

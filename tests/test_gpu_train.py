@@ -215,3 +215,18 @@ def test_pretrain_matches_oracle_sgd_loop(cuda_device, g_encode, g_meta):
     got = pm.flat_params(m).cpu().numpy()
     assert np.linalg.norm(got - want) <= 1e-4 * np.linalg.norm(want)
     assert np.array_equal(m.feature_norm.mean, fn.mean)
+
+
+def test_meta_trainer_equals_meta_train(cuda_device, g_model, super_samples):
+    """Device-resident MetaTrainer (pre-drawn tasks, 3 launches/step) == meta_train."""
+    from paper_2102_04199_b200.util import rng_from
+
+    m = device_model(g_model)
+    cfg = pmeta.MetaConfig(n_way=3, k_shot=2, meta_batch=8, outer_steps=6)
+    want = pmeta.meta_train(m, super_samples, cfg, rng_from("mt-eq"))
+    tr = pmeta.MetaTrainer(m, super_samples, cfg)
+    plan = tr.plan(rng_from("mt-eq"), cfg.outer_steps)
+    bufs = tr.run(plan)
+    got = tr.model()
+    assert_params_close(pm.flat_params(got).cpu().numpy(), pm.flat_params(want).cpu().numpy(), rtol=1e-6)
+    assert np.isfinite(tr.stats(plan, bufs)).all()

@@ -8,6 +8,6 @@ timeout 300 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_
 echo "bench rc=$?" >> gpurun_out/bench.err
 if [ "${NCU:-1}" = "1" ]; then
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:${NCU_K:-score_star} -s 3 -c 1 \
-  -o gpurun_out/prof_score -f python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
+  -o gpurun_out/prof_score -f python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-extras > gpurun_out/ncu_full.log 2>&1
 fi
 echo done
