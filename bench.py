@@ -488,7 +488,12 @@ def run_ours(args):
     if cpu:
         line["cpu_baseline"] = cpu
     if not args.no_extras:
+        from paper_2102_04199_b200 import meta as pmeta
+        from paper_2102_04199_b200 import model as pm
+
         corpus = synthetic_corpus()
+        fn, ln = pmeta.dataset_norms(corpus)  # meta.py:81-101 over the corpus, as pretrain does
+        m = pm.model_from_flat(m._flat, m, feature_norm=fn, label_norm=ln)
         line["maml"] = bench_maml(m, corpus, args.meta_steps, 10)
         if ws == 1:
             line["maml_so"] = bench_maml(m, corpus, max(args.meta_steps // 2, 10), 5, first_order=False)

@@ -21,61 +21,55 @@ int check_dims(const kt_dims& d);
 namespace meta {
 
 constexpr int NT = 256;
-constexpr int RC = 8;               // rows per chunk
-constexpr int HMAX = 2 * KT_MAX_DIM; // widest head vector (input 2 d_L)
+constexpr int HMAX = 2 * KT_MAX_DIM;  // widest head vector (input 2 d_L)
 
 struct Head {
   int nh;
   int dim[KT_MAX_LAYERS + 2];
   int ow[KT_MAX_LAYERS + 1], ob[KT_MAX_LAYERS + 1];  // offsets into the flat head vector
   int P;
+  int HS;  // scratch row stride (widest layer, padded to 4)
+  int RC;  // rows per chunk
 };
 
-__host__ __device__ inline Head head_of(const kt_dims& d) {
+__host__ __device__ inline Head head_of(const kt_dims& d, int rc = 8) {
   Head h;
   h.nh = d.n_head;
-  for (int i = 0; i <= d.n_head; ++i) h.dim[i] = d.head[i];
+  int w = 1;
+  for (int i = 0; i <= d.n_head; ++i) {
+    h.dim[i] = d.head[i];
+    w = d.head[i] > w ? d.head[i] : w;
+  }
   for (int i = 0; i < d.n_head; ++i) {
     h.ow[i] = d.off_hw[i] - d.off_head;
     h.ob[i] = d.off_hb[i] - d.off_head;
   }
   h.P = d.n_head_params;
+  h.HS = (w + 3) & ~3;
+  h.RC = rc;
   return h;
 }
 
-// Row-chunk scratch: activations A[0..nh], pre-activations Z[0..nh-1], tangents,
-// deltas -- each RC x HMAX.
+// Row-chunk scratch carved arithmetically from one base pointer (no pointer
+// arrays -> no local-memory indirection in the hot loops):
+//   A(0..nh) activations, Z(0..nh-1) pre-activations, [TA(0..nh) tangents,]
+//   D(0..1) deltas [, D(2..3) tangent deltas] -- each RC x HS -- then NT floats.
 struct Scratch {
-  float* A[KT_MAX_LAYERS + 2];
-  float* Z[KT_MAX_LAYERS + 1];
-  float* TA[KT_MAX_LAYERS + 2];  // forward tangents (HVP only)
-  float* D0;
-  float* D1;
-  float* TD0;
-  float* TD1;
-  float* red;  // NT floats for block reductions
+  float* base;
+  int blk, nh, hvp;
+  __device__ __forceinline__ float* A(int i) const { return base + i * blk; }
+  __device__ __forceinline__ float* Z(int i) const { return base + (nh + 1 + i) * blk; }
+  __device__ __forceinline__ float* TA(int i) const { return base + (2 * nh + 1 + i) * blk; }
+  __device__ __forceinline__ float* D(int j) const { return base + ((hvp ? 3 * nh + 2 : 2 * nh + 1) + j) * blk; }
+  __device__ __forceinline__ float* red() const { return base + ((hvp ? 3 * nh + 2 : 2 * nh + 1) + (hvp ? 4 : 2)) * blk; }
 };
 
-__host__ __device__ inline int scratch_floats(int nh, bool hvp) {
-  return ((nh + 1) + nh + (hvp ? nh + 1 : 0) + (hvp ? 4 : 2)) * RC * HMAX + NT;
+__host__ __device__ inline int scratch_floats(const Head& h, bool hvp) {
+  return ((h.nh + 1) + h.nh + (hvp ? h.nh + 1 : 0) + (hvp ? 4 : 2)) * h.RC * h.HS + NT;
 }
 
-__device__ inline Scratch carve(float* p, int nh, bool hvp) {
-  Scratch s;
-  for (int i = 0; i <= nh; ++i) { s.A[i] = p; p += RC * HMAX; }
-  for (int i = 0; i < nh; ++i) { s.Z[i] = p; p += RC * HMAX; }
-  if (hvp)
-    for (int i = 0; i <= nh; ++i) { s.TA[i] = p; p += RC * HMAX; }
-  s.D0 = p; p += RC * HMAX;
-  s.D1 = p; p += RC * HMAX;
-  if (hvp) {
-    s.TD0 = p; p += RC * HMAX;
-    s.TD1 = p; p += RC * HMAX;
-  } else {
-    s.TD0 = s.TD1 = nullptr;
-  }
-  s.red = p;
-  return s;
+__device__ __forceinline__ Scratch carve(float* p, const Head& h, bool hvp) {
+  return Scratch{p, h.RC * h.HS, h.nh, hvp ? 1 : 0};
 }
 
 __device__ __forceinline__ float block_sum(float v, float* red) {
@@ -92,23 +86,13 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return s;
 }
 
-// Loads rows [r0, r0+nr) (gathered through ridx when given) into A[0].
-__device__ __forceinline__ void load_rows(const Head& h, const float* u, const int64_t* ridx, int r0, int nr,
-                                          float* A0) {
-  const int d0 = h.dim[0];
-  for (int e = threadIdx.x; e < nr * d0; e += NT) {
-    const int r = e / d0, c = e - (e / d0) * d0;
-    const int64_t row = ridx ? ridx[r0 + r] : r0 + r;
-    A0[r * HMAX + c] = u[row * d0 + c];
-  }
-}
-
 // grad (and mse) of the head MSE at theta over n rows; if v != nullptr computes
 // the Hessian-vector product H(theta) v instead (forward-over-reverse, ReLU masks
-// constant).  out (h.P floats, smem) is overwritten.  Returns the mse.
+// constant).  Rows are u[ridx[r]] (or u[r]) and labels y[ridx[r]] (or y[r]).
+// out (h.P floats, smem) is overwritten.  Returns the mse.
 __device__ float head_pass(const Head& h, const float* th, const float* v, const float* u, const int64_t* ridx,
-                           const float* y, const int64_t* yidx, int n, float* out, const Scratch& S) {
-  const int nh = h.nh;
+                           const float* y, int n, float* out, const Scratch& S) {
+  const int nh = h.nh, HS = h.HS, RC = h.RC;
   const bool hvp = v != nullptr;
   for (int e = threadIdx.x; e < h.P; e += NT) out[e] = 0.0f;
   float sq_local = 0.0f;
@@ -116,105 +100,139 @@ __device__ float head_pass(const Head& h, const float* th, const float* v, const
   for (int r0 = 0; r0 < n; r0 += RC) {
     const int nr = n - r0 < RC ? n - r0 : RC;
     __syncthreads();
-    load_rows(h, u, ridx, r0, nr, S.A[0]);
-    if (hvp)
-      for (int e = threadIdx.x; e < nr * h.dim[0]; e += NT) {
-        const int r = e / h.dim[0], c = e - (e / h.dim[0]) * h.dim[0];
-        S.TA[0][r * HMAX + c] = 0.0f;
+    {
+      const int d0 = h.dim[0];
+      float* A0 = S.A(0);
+      float* T0 = hvp ? S.TA(0) : nullptr;
+      for (int e = threadIdx.x; e < nr * d0; e += NT) {
+        const int r = e / d0, c = e - r * d0;
+        const int64_t row = ridx ? ridx[r0 + r] : r0 + r;
+        A0[r * HS + c] = u[row * d0 + c];
+        if (hvp) T0[r * HS + c] = 0.0f;
       }
+    }
     __syncthreads();
     // forward
     for (int i = 0; i < nh; ++i) {
       const int din = h.dim[i], dout = h.dim[i + 1];
-      const float* W = th + h.ow[i];
-      const float* b = th + h.ob[i];
+      const float* __restrict__ W = th + h.ow[i];
+      const float* __restrict__ b = th + h.ob[i];
+      const float* __restrict__ Ai = S.A(i);
+      float* __restrict__ Zi = S.Z(i);
+      float* __restrict__ An = S.A(i + 1);
       const bool last = i == nh - 1;
-      for (int e = threadIdx.x; e < nr * dout; e += NT) {
-        const int r = e / dout, c = e - (e / dout) * dout;
-        float acc = 0.0f;
-        for (int k = 0; k < din; ++k) acc = fmaf(S.A[i][r * HMAX + k], W[k * dout + c], acc);
-        acc += b[c];
-        S.Z[i][r * HMAX + c] = acc;
-        S.A[i + 1][r * HMAX + c] = last ? acc : fmaxf(acc, 0.0f);
-        if (hvp) {
-          const float* vW = v + h.ow[i];
-          float t = v[h.ob[i] + c];
+      if (!hvp) {
+        for (int e = threadIdx.x; e < nr * dout; e += NT) {
+          const int r = e / dout, c = e - r * dout;
+          const float* a = Ai + r * HS;
+          float acc = b[c];
+          for (int k = 0; k < din; ++k) acc = fmaf(a[k], W[k * dout + c], acc);
+          Zi[r * HS + c] = acc;
+          An[r * HS + c] = last ? acc : fmaxf(acc, 0.0f);
+        }
+      } else {
+        const float* __restrict__ vW = v + h.ow[i];
+        const float* __restrict__ TAi = S.TA(i);
+        float* __restrict__ TAn = S.TA(i + 1);
+        for (int e = threadIdx.x; e < nr * dout; e += NT) {
+          const int r = e / dout, c = e - r * dout;
+          const float* a = Ai + r * HS;
+          const float* ta = TAi + r * HS;
+          float acc = b[c], t = v[h.ob[i] + c];
           for (int k = 0; k < din; ++k) {
-            t = fmaf(S.TA[i][r * HMAX + k], W[k * dout + c], t);
-            t = fmaf(S.A[i][r * HMAX + k], vW[k * dout + c], t);
+            const float w = W[k * dout + c];
+            acc = fmaf(a[k], w, acc);
+            t = fmaf(ta[k], w, fmaf(a[k], vW[k * dout + c], t));
           }
-          S.TA[i + 1][r * HMAX + c] = (last || acc > 0.0f) ? t : 0.0f;
+          Zi[r * HS + c] = acc;
+          An[r * HS + c] = last ? acc : fmaxf(acc, 0.0f);
+          TAn[r * HS + c] = (last || acc > 0.0f) ? t : 0.0f;
         }
       }
       __syncthreads();
     }
     // output deltas (model.py:382-383 / 422-423)
-    for (int r = threadIdx.x; r < nr; r += NT) {
-      const float yy = yidx ? y[yidx[r0 + r]] : y[r0 + r];
-      const float resid = S.A[nh][r * HMAX] - yy;
-      sq_local += resid * resid;
-      S.D0[r * HMAX] = two_n * resid;
-      if (hvp) S.TD0[r * HMAX] = two_n * S.TA[nh][r * HMAX];
+    {
+      const float* An = S.A(nh);
+      float* D0 = S.D(0);
+      for (int r = threadIdx.x; r < nr; r += NT) {
+        const int64_t row = ridx ? ridx[r0 + r] : r0 + r;
+        const float resid = An[r * HS] - y[row];
+        sq_local += resid * resid;
+        D0[r * HS] = two_n * resid;
+        if (hvp) S.D(2)[r * HS] = two_n * S.TA(nh)[r * HS];
+      }
     }
     __syncthreads();
     // backward
-    float* da = S.D0;
-    float* dn = S.D1;
-    float* tda = S.TD0;
-    float* tdn = S.TD1;
+    int cur = 0;
     for (int i = nh - 1; i >= 0; --i) {
       const int din = h.dim[i], dout = h.dim[i + 1];
       const bool last = i == nh - 1;
-      // mask deltas in place: dz = da * (z > 0) (not on the linear output layer)
-      if (!last) {
+      float* __restrict__ da = S.D(cur);
+      float* __restrict__ dn = S.D(cur ^ 1);
+      float* __restrict__ tda = hvp ? S.D(2 + cur) : nullptr;
+      float* __restrict__ tdn = hvp ? S.D(2 + (cur ^ 1)) : nullptr;
+      const float* __restrict__ Zi = S.Z(i);
+      const float* __restrict__ Ai = S.A(i);
+      const float* __restrict__ TAi = hvp ? S.TA(i) : nullptr;
+      if (!last) {  // dz = da * (z > 0)
         for (int e = threadIdx.x; e < nr * dout; e += NT) {
-          const int r = e / dout, c = e - (e / dout) * dout;
-          if (!(S.Z[i][r * HMAX + c] > 0.0f)) {
-            da[r * HMAX + c] = 0.0f;
-            if (hvp) tda[r * HMAX + c] = 0.0f;
+          const int r = e / dout, c = e - r * dout;
+          if (!(Zi[r * HS + c] > 0.0f)) {
+            da[r * HS + c] = 0.0f;
+            if (hvp) tda[r * HS + c] = 0.0f;
           }
         }
         __syncthreads();
       }
-      // parameter gradient: out_w += A^T dz (grad) or TA^T dz + A^T tdz (hvp); out_b += sum dz / tdz
+      // out_w += A^T dz (grad) | TA^T dz + A^T tdz (hvp); out_b += sum dz | sum tdz
       float* gw = out + h.ow[i];
       for (int e = threadIdx.x; e < din * dout; e += NT) {
-        const int k = e / dout, c = e - (e / dout) * dout;
+        const int k = e / dout, c = e - k * dout;
         float acc = gw[e];
-        for (int r = 0; r < nr; ++r) {
-          if (hvp)
-            acc = fmaf(S.TA[i][r * HMAX + k], da[r * HMAX + c], fmaf(S.A[i][r * HMAX + k], tda[r * HMAX + c], acc));
-          else
-            acc = fmaf(S.A[i][r * HMAX + k], da[r * HMAX + c], acc);
+        if (hvp) {
+          for (int r = 0; r < nr; ++r)
+            acc = fmaf(TAi[r * HS + k], da[r * HS + c], fmaf(Ai[r * HS + k], tda[r * HS + c], acc));
+        } else {
+          for (int r = 0; r < nr; ++r) acc = fmaf(Ai[r * HS + k], da[r * HS + c], acc);
         }
         gw[e] = acc;
       }
       for (int c = threadIdx.x; c < dout; c += NT) {
         float acc = out[h.ob[i] + c];
-        for (int r = 0; r < nr; ++r) acc += hvp ? tda[r * HMAX + c] : da[r * HMAX + c];
+        const float* src = hvp ? tda : da;
+        for (int r = 0; r < nr; ++r) acc += src[r * HS + c];
         out[h.ob[i] + c] = acc;
       }
       // propagate: da' = dz W^T ; tda' = tdz W^T + dz vW^T
       if (i > 0) {
-        const float* W = th + h.ow[i];
+        const float* __restrict__ W = th + h.ow[i];
+        const float* __restrict__ vW = hvp ? v + h.ow[i] : nullptr;
         for (int e = threadIdx.x; e < nr * din; e += NT) {
-          const int r = e / din, k = e - (e / din) * din;
+          const int r = e / din, k = e - r * din;
+          const float* dr = da + r * HS;
+          const float* wk = W + k * dout;
           float acc = 0.0f, tacc = 0.0f;
-          for (int c = 0; c < dout; ++c) {
-            acc = fmaf(da[r * HMAX + c], W[k * dout + c], acc);
-            if (hvp)
-              tacc = fmaf(tda[r * HMAX + c], W[k * dout + c], fmaf(da[r * HMAX + c], v[h.ow[i] + k * dout + c], tacc));
+          if (hvp) {
+            const float* tdr = tda + r * HS;
+            const float* vk = vW + k * dout;
+            for (int c = 0; c < dout; ++c) {
+              acc = fmaf(dr[c], wk[c], acc);
+              tacc = fmaf(tdr[c], wk[c], fmaf(dr[c], vk[c], tacc));
+            }
+            tdn[r * HS + k] = tacc;
+          } else {
+            for (int c = 0; c < dout; ++c) acc = fmaf(dr[c], wk[c], acc);
           }
-          dn[r * HMAX + k] = acc;
-          if (hvp) tdn[r * HMAX + k] = tacc;
+          dn[r * HS + k] = acc;
         }
       }
       __syncthreads();
-      float* t = da; da = dn; dn = t;
-      t = tda; tda = tdn; tdn = t;
+      cur ^= 1;
     }
   }
-  const float sq = block_sum(sq_local, S.red);
+  const float sq = block_sum(sq_local, S.red());
   return sq / static_cast<float>(n);
 }
 
@@ -228,17 +246,17 @@ struct TaskSet {
 };
 
 __global__ void __launch_bounds__(NT)
-maml_task_kernel(kt_dims dims, const float* __restrict__ theta, TaskSet ts, int T, float alpha, int inner_steps,
-                 int first_order, float* __restrict__ theta_ws, float* __restrict__ g_out,
+maml_task_kernel(kt_dims dims, int rc, const float* __restrict__ theta, TaskSet ts, int T, float alpha,
+                 int inner_steps, int first_order, float* __restrict__ theta_ws, float* __restrict__ g_out,
                  float* __restrict__ loss_out) {
   extern __shared__ __align__(16) float sm[];
-  const Head h = head_of(dims);
+  const Head h = head_of(dims, rc);
   const int P4 = (h.P + 3) & ~3;
   float* th = sm;             // current theta_k
   float* th1 = th + P4;       // next theta / theta_0 for HVP
   float* gb = th1 + P4;       // support gradient / HVP output
   float* vb = gb + P4;        // query gradient v
-  const Scratch S = carve(vb + P4, h.nh, !first_order);
+  const Scratch S = carve(vb + P4, h, !first_order);
   const int t = blockIdx.x;
   if (t >= T) return;
   const int64_t s0 = ts.s_off[t], ns = ts.s_off[t + 1] - s0;
@@ -251,14 +269,14 @@ maml_task_kernel(kt_dims dims, const float* __restrict__ theta, TaskSet ts, int 
   for (int k = 0; k < inner_steps; ++k) {
     if (!first_order && inner_steps > 1)
       for (int e = threadIdx.x; e < h.P; e += NT) theta_ws[(static_cast<int64_t>(t) * inner_steps + k) * h.P + e] = cur[e];
-    const float ls = head_pass(h, cur, nullptr, ts.u, ts.s_idx + s0, ts.y, ts.s_idx + s0, static_cast<int>(ns), gb, S);
+    const float ls = head_pass(h, cur, nullptr, ts.u, ts.s_idx + s0, ts.y, static_cast<int>(ns), gb, S);
     if (k == 0) ls0 = ls;
     __syncthreads();
     for (int e = threadIdx.x; e < h.P; e += NT) nxt[e] = cur[e] - alpha * gb[e];
     __syncthreads();
     float* tmp = cur; cur = nxt; nxt = tmp;
   }
-  const float lq = head_pass(h, cur, nullptr, ts.u, ts.q_idx + q0, ts.y, ts.q_idx + q0, static_cast<int>(nq), vb, S);
+  const float lq = head_pass(h, cur, nullptr, ts.u, ts.q_idx + q0, ts.y, static_cast<int>(nq), vb, S);
   __syncthreads();
   if (!first_order) {
     for (int k = inner_steps - 1; k >= 0; --k) {
@@ -266,7 +284,7 @@ maml_task_kernel(kt_dims dims, const float* __restrict__ theta, TaskSet ts, int 
       for (int e = threadIdx.x; e < h.P; e += NT)
         nxt[e] = inner_steps > 1 ? theta_ws[(static_cast<int64_t>(t) * inner_steps + k) * h.P + e] : theta[e];
       __syncthreads();
-      head_pass(h, nxt, vb, ts.u, ts.s_idx + s0, ts.y, ts.s_idx + s0, static_cast<int>(ns), gb, S);
+      head_pass(h, nxt, vb, ts.u, ts.s_idx + s0, ts.y, static_cast<int>(ns), gb, S);
       __syncthreads();
       for (int e = threadIdx.x; e < h.P; e += NT) vb[e] -= alpha * gb[e];
       __syncthreads();
@@ -297,31 +315,31 @@ __global__ void task_sum_kernel(const float* __restrict__ g, int T, int P, float
 
 // head_loss_grad / head_hvp / fine-tune: one CTA on one theta.
 __global__ void __launch_bounds__(NT)
-head_kernel(kt_dims dims, const float* __restrict__ theta, const float* __restrict__ v, const float* __restrict__ u,
-            const float* __restrict__ y, int n, int steps, float alpha, float* __restrict__ out,
-            float* __restrict__ mse_out) {
+head_kernel(kt_dims dims, int rc, const float* __restrict__ theta, const float* __restrict__ v,
+            const float* __restrict__ u, const float* __restrict__ y, int n, int steps, float alpha,
+            float* __restrict__ out, float* __restrict__ mse_out) {
   extern __shared__ __align__(16) float sm[];
-  const Head h = head_of(dims);
+  const Head h = head_of(dims, rc);
   const int P4 = (h.P + 3) & ~3;
   float* th = sm;
   float* gb = th + P4;
   float* vb = gb + P4;
   const bool hvp = v != nullptr;
-  const Scratch S = carve(vb + P4, h.nh, hvp);
+  const Scratch S = carve(vb + P4, h, hvp);
   for (int e = threadIdx.x; e < h.P; e += NT) {
     th[e] = theta[e];
     if (hvp) vb[e] = v[e];
   }
   __syncthreads();
   if (steps <= 0) {  // single evaluation: grad (or hvp) -> out
-    const float mse = head_pass(h, th, hvp ? vb : nullptr, u, nullptr, y, nullptr, n, gb, S);
+    const float mse = head_pass(h, th, hvp ? vb : nullptr, u, nullptr, y, n, gb, S);
     __syncthreads();
     for (int e = threadIdx.x; e < h.P; e += NT) out[e] = gb[e];
     if (threadIdx.x == 0 && mse_out) mse_out[0] = mse;
     return;
   }
   for (int s = 0; s < steps; ++s) {  // fine_tune_embedded: theta -= alpha * grad, `steps` times
-    const float mse = head_pass(h, th, nullptr, u, nullptr, y, nullptr, n, gb, S);
+    const float mse = head_pass(h, th, nullptr, u, nullptr, y, n, gb, S);
     __syncthreads();
     for (int e = threadIdx.x; e < h.P; e += NT) th[e] -= alpha * gb[e];
     if (threadIdx.x == 0 && mse_out) mse_out[s] = mse;
@@ -330,8 +348,17 @@ head_kernel(kt_dims dims, const float* __restrict__ theta, const float* __restri
   for (int e = threadIdx.x; e < h.P; e += NT) out[e] = th[e];
 }
 
-static size_t task_smem(const Head& h, bool so) { return sizeof(float) * (4 * ((h.P + 3) & ~3) + scratch_floats(h.nh, so)); }
-static size_t head_smem(const Head& h, bool hvp) { return sizeof(float) * (3 * ((h.P + 3) & ~3) + scratch_floats(h.nh, hvp)); }
+static size_t task_smem(const Head& h, bool so) { return sizeof(float) * (4 * ((h.P + 3) & ~3) + scratch_floats(h, so)); }
+static size_t head_smem(const Head& h, bool hvp) { return sizeof(float) * (3 * ((h.P + 3) & ~3) + scratch_floats(h, hvp)); }
+
+// Largest row chunk (<= cap) whose shared-memory footprint fits.
+static Head fit_rows(const kt_dims& d, int cap, bool task, bool hvp) {
+  for (int rc = cap; rc >= 1; rc >>= 1) {
+    const Head h = head_of(d, rc);
+    if ((task ? task_smem(h, hvp) : head_smem(h, hvp)) <= 220 * 1024) return h;
+  }
+  return head_of(d, 1);
+}
 
 static int check_head(const kt_dims& d) {
   KT_REQUIRE(d.n_head >= 1 && d.n_head <= KT_MAX_LAYERS + 1, KT_E_UNSUPPORTED, "head depth beyond limits");
@@ -363,13 +390,13 @@ int kt_head_loss_grad(const kt_dims* dims, const float* theta, const float* u, c
   KT_REQUIRE(n > 0, KT_E_EMPTY, "kt_head_loss_grad: empty batch");
   int rc = meta::check_head(*dims);
   if (rc) return rc;
-  const meta::Head h = meta::head_of(*dims);
+  const meta::Head h = meta::fit_rows(*dims, 32, false, false);
   static size_t cached = 0;
   const size_t smem = meta::head_smem(h, false);
   rc = meta::set_smem(meta::head_kernel, smem, cached);
   if (rc) return rc;
-  meta::head_kernel<<<1, meta::NT, smem, as_stream(stream)>>>(*dims, theta, nullptr, u, y, (int)n, 0, 0.f, grad_out,
-                                                               mse_out);
+  meta::head_kernel<<<1, meta::NT, smem, as_stream(stream)>>>(*dims, h.RC, theta, nullptr, u, y, (int)n, 0, 0.f,
+                                                               grad_out, mse_out);
   note_launches(1);
   return check_launch("kt_head_loss_grad");
 }
@@ -381,12 +408,13 @@ int kt_head_hvp(const kt_dims* dims, const float* theta, const float* u, const f
   KT_REQUIRE(n > 0, KT_E_EMPTY, "kt_head_hvp: empty batch");
   int rc = meta::check_head(*dims);
   if (rc) return rc;
-  const meta::Head h = meta::head_of(*dims);
+  const meta::Head h = meta::fit_rows(*dims, 32, false, true);
   static size_t cached = 0;
   const size_t smem = meta::head_smem(h, true);
   rc = meta::set_smem(meta::head_kernel, smem, cached);
   if (rc) return rc;
-  meta::head_kernel<<<1, meta::NT, smem, as_stream(stream)>>>(*dims, theta, v, u, y, (int)n, 0, 0.f, hvp_out, nullptr);
+  meta::head_kernel<<<1, meta::NT, smem, as_stream(stream)>>>(*dims, h.RC, theta, v, u, y, (int)n, 0, 0.f, hvp_out,
+                                                               nullptr);
   note_launches(1);
   return check_launch("kt_head_hvp");
 }
@@ -398,12 +426,12 @@ int kt_fine_tune(const kt_dims* dims, const float* theta, const float* u, const 
   KT_REQUIRE(n > 0 && steps > 0, KT_E_EMPTY, "kt_fine_tune: nothing to do");
   int rc = meta::check_head(*dims);
   if (rc) return rc;
-  const meta::Head h = meta::head_of(*dims);
+  const meta::Head h = meta::fit_rows(*dims, 32, false, false);
   static size_t cached = 0;
   const size_t smem = meta::head_smem(h, false);
   rc = meta::set_smem(meta::head_kernel, smem, cached);
   if (rc) return rc;
-  meta::head_kernel<<<1, meta::NT, smem, as_stream(stream)>>>(*dims, theta, nullptr, u, y, (int)n, steps, alpha,
+  meta::head_kernel<<<1, meta::NT, smem, as_stream(stream)>>>(*dims, h.RC, theta, nullptr, u, y, (int)n, steps, alpha,
                                                                theta_out, mse_out);
   note_launches(1);
   return check_launch("kt_fine_tune");
@@ -429,8 +457,8 @@ int kt_maml_tasks(const kt_dims* dims, const float* theta, const float* u, const
              "kt_maml_tasks: workspace too small");
   int rc = meta::check_head(*dims);
   if (rc) return rc;
-  const meta::Head h = meta::head_of(*dims);
   const bool so = !first_order;
+  const meta::Head h = meta::fit_rows(*dims, 8, true, so);
   static size_t cached = 0;
   const size_t smem = meta::task_smem(h, so);
   rc = meta::set_smem(meta::maml_task_kernel, smem, cached);
@@ -440,8 +468,8 @@ int kt_maml_tasks(const kt_dims* dims, const float* theta, const float* u, const
   float* thws = losses + 2 * T;
   meta::TaskSet ts{u, y, s_off, s_idx, q_off, q_idx};
   cudaStream_t st = as_stream(stream);
-  meta::maml_task_kernel<<<T, meta::NT, smem, st>>>(*dims, theta, ts, T, alpha, inner_steps, first_order, thws, g,
-                                                    losses);
+  meta::maml_task_kernel<<<T, meta::NT, smem, st>>>(*dims, h.RC, theta, ts, T, alpha, inner_steps, first_order,
+                                                    thws, g, losses);
   meta::task_sum_kernel<<<(h.P + 255) / 256, 256, 0, st>>>(g, T, h.P, g_sum, losses, stats);
   note_launches(2);
   return check_launch("kt_maml_tasks");
