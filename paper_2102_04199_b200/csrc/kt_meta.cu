@@ -90,8 +90,8 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // the Hessian-vector product H(theta) v instead (forward-over-reverse, ReLU masks
 // constant).  Rows are u[ridx[r]] (or u[r]) and labels y[ridx[r]] (or y[r]).
 // out (h.P floats, smem) is overwritten.  Returns the mse.
-__device__ float head_pass(const Head& h, const float* th, const float* v, const float* u, const int64_t* ridx,
-                           const float* y, int n, float* out, const Scratch& S) {
+__device__ float head_pass_scalar(const Head& h, const float* th, const float* v, const float* u,
+                                  const int64_t* ridx, const float* y, int n, float* out, const Scratch& S) {
   const int nh = h.nh, HS = h.HS, RC = h.RC;
   const bool hvp = v != nullptr;
   for (int e = threadIdx.x; e < h.P; e += NT) out[e] = 0.0f;
@@ -234,6 +234,262 @@ __device__ float head_pass(const Head& h, const float* th, const float* v, const
   }
   const float sq = block_sum(sq_local, S.red());
   return sq / static_cast<float>(n);
+}
+
+
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+
+// Register-tiled pass (all hidden widths and the input width multiples of 4,
+// single-output last layer): same arithmetic contract as head_pass_scalar.
+//   forward   2 rows x 4 cols per thread, float4 weight loads
+//   dW        4 x 4 (k, c) tile per thread, float4 row loads, summed over the chunk rows in order
+//   propagate 2 rows x 4 k per thread, float4 loads along c
+__device__ float head_pass_tiled(const Head& h, const float* th, const float* v, const float* u,
+                                 const int64_t* ridx, const float* y, int n, float* out, const Scratch& S) {
+  const int nh = h.nh, HS = h.HS, RC = h.RC;
+  const bool hvp = v != nullptr;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < h.P; e += NT) out[e] = 0.0f;
+  float sq_local = 0.0f;
+  const float two_n = 2.0f / static_cast<float>(n);
+  for (int r0 = 0; r0 < n; r0 += RC) {
+    const int nr = n - r0 < RC ? n - r0 : RC;
+    const int nr2 = (nr + 1) & ~1;  // rows padded to pairs (pad row is zero)
+    __syncthreads();
+    {
+      const int d4 = h.dim[0] >> 2;
+      float* A0 = S.A(0);
+      for (int e = tid; e < nr2 * d4; e += NT) {
+        const int r = e / d4, c = (e - r * d4) * 4;
+        float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r < nr) {
+          const int64_t row = ridx ? ridx[r0 + r] : r0 + r;
+          val = *reinterpret_cast<const float4*>(u + row * h.dim[0] + c);
+        }
+        st4(A0 + r * HS + c, val);
+        if (hvp) st4(S.TA(0) + r * HS + c, make_float4(0.f, 0.f, 0.f, 0.f));
+      }
+    }
+    __syncthreads();
+    // ---- forward
+    for (int i = 0; i < nh; ++i) {
+      const int din = h.dim[i], dout = h.dim[i + 1];
+      const float* __restrict__ W = th + h.ow[i];
+      const float* __restrict__ b = th + h.ob[i];
+      const float* __restrict__ Ai = S.A(i);
+      float* __restrict__ Zi = S.Z(i);
+      float* __restrict__ An = S.A(i + 1);
+      const bool last = i == nh - 1;
+      if (last) {  // dout == 1: one thread per row
+        for (int r = tid; r < nr2; r += NT) {
+          float acc = b[0], t = hvp ? v[h.ob[i]] : 0.0f;
+          for (int k = 0; k < din; ++k) {
+            acc = fmaf(Ai[r * HS + k], W[k], acc);
+            if (hvp) t = fmaf(S.TA(i)[r * HS + k], W[k], fmaf(Ai[r * HS + k], v[h.ow[i] + k], t));
+          }
+          Zi[r * HS] = acc;
+          An[r * HS] = acc;
+          if (hvp) S.TA(i + 1)[r * HS] = t;
+        }
+      } else {
+        const int ncg = dout >> 2;
+        const float* __restrict__ vW = hvp ? v + h.ow[i] : nullptr;
+        const float* __restrict__ TAi = hvp ? S.TA(i) : nullptr;
+        for (int it = tid; it < ncg * (nr2 >> 1); it += NT) {
+          const int c = (it % ncg) * 4, r = (it / ncg) * 2;
+          const float4 bb = ld4(b + c);
+          float4 a0 = bb, a1 = bb;
+          float4 t0 = make_float4(0.f, 0.f, 0.f, 0.f), t1 = t0;
+          if (hvp) t0 = t1 = ld4(v + h.ob[i] + c);
+          const float* x0 = Ai + r * HS;
+          const float* x1 = x0 + HS;
+#pragma unroll 4
+          for (int k = 0; k < din; ++k) {
+            const float4 w = ld4(W + k * dout + c);
+            const float p = x0[k], q = x1[k];
+            a0.x = fmaf(p, w.x, a0.x); a0.y = fmaf(p, w.y, a0.y); a0.z = fmaf(p, w.z, a0.z); a0.w = fmaf(p, w.w, a0.w);
+            a1.x = fmaf(q, w.x, a1.x); a1.y = fmaf(q, w.y, a1.y); a1.z = fmaf(q, w.z, a1.z); a1.w = fmaf(q, w.w, a1.w);
+            if (hvp) {
+              const float4 vw = ld4(vW + k * dout + c);
+              const float tp = TAi[r * HS + k], tq = TAi[(r + 1) * HS + k];
+              t0.x = fmaf(tp, w.x, fmaf(p, vw.x, t0.x)); t0.y = fmaf(tp, w.y, fmaf(p, vw.y, t0.y));
+              t0.z = fmaf(tp, w.z, fmaf(p, vw.z, t0.z)); t0.w = fmaf(tp, w.w, fmaf(p, vw.w, t0.w));
+              t1.x = fmaf(tq, w.x, fmaf(q, vw.x, t1.x)); t1.y = fmaf(tq, w.y, fmaf(q, vw.y, t1.y));
+              t1.z = fmaf(tq, w.z, fmaf(q, vw.z, t1.z)); t1.w = fmaf(tq, w.w, fmaf(q, vw.w, t1.w));
+            }
+          }
+          st4(Zi + r * HS + c, a0);
+          st4(Zi + (r + 1) * HS + c, a1);
+          const float4 z0 = make_float4(fmaxf(a0.x, 0.f), fmaxf(a0.y, 0.f), fmaxf(a0.z, 0.f), fmaxf(a0.w, 0.f));
+          const float4 z1 = make_float4(fmaxf(a1.x, 0.f), fmaxf(a1.y, 0.f), fmaxf(a1.z, 0.f), fmaxf(a1.w, 0.f));
+          st4(An + r * HS + c, z0);
+          st4(An + (r + 1) * HS + c, z1);
+          if (hvp) {
+            float* TAn = S.TA(i + 1);
+            st4(TAn + r * HS + c, make_float4(a0.x > 0.f ? t0.x : 0.f, a0.y > 0.f ? t0.y : 0.f,
+                                              a0.z > 0.f ? t0.z : 0.f, a0.w > 0.f ? t0.w : 0.f));
+            st4(TAn + (r + 1) * HS + c, make_float4(a1.x > 0.f ? t1.x : 0.f, a1.y > 0.f ? t1.y : 0.f,
+                                                    a1.z > 0.f ? t1.z : 0.f, a1.w > 0.f ? t1.w : 0.f));
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // ---- output deltas; the pad row (if any) gets zero deltas
+    {
+      const float* An = S.A(nh);
+      float* D0 = S.D(0);
+      for (int r = tid; r < nr2; r += NT) {
+        float d = 0.0f, td = 0.0f;
+        if (r < nr) {
+          const int64_t row = ridx ? ridx[r0 + r] : r0 + r;
+          const float resid = An[r * HS] - y[row];
+          sq_local += resid * resid;
+          d = two_n * resid;
+          if (hvp) td = two_n * S.TA(nh)[r * HS];
+        }
+        D0[r * HS] = d;
+        if (hvp) S.D(2)[r * HS] = td;
+      }
+    }
+    __syncthreads();
+    // ---- backward
+    int cur = 0;
+    for (int i = nh - 1; i >= 0; --i) {
+      const int din = h.dim[i], dout = h.dim[i + 1];
+      const bool last = i == nh - 1;
+      float* __restrict__ da = S.D(cur);
+      float* __restrict__ dn = S.D(cur ^ 1);
+      float* __restrict__ tda = hvp ? S.D(2 + cur) : nullptr;
+      float* __restrict__ tdn = hvp ? S.D(2 + (cur ^ 1)) : nullptr;
+      const float* __restrict__ Zi = S.Z(i);
+      const float* __restrict__ Ai = S.A(i);
+      const float* __restrict__ TAi = hvp ? S.TA(i) : nullptr;
+      if (!last) {  // dz = da * (z > 0)
+        for (int e = tid; e < nr2 * dout; e += NT) {
+          const int r = e / dout, c = e - r * dout;
+          if (!(Zi[r * HS + c] > 0.0f)) {
+            da[r * HS + c] = 0.0f;
+            if (hvp) tda[r * HS + c] = 0.0f;
+          }
+        }
+        __syncthreads();
+      }
+      float* gw = out + h.ow[i];
+      if (last) {  // dout == 1: gW[k] += sum_r A[r][k] dz[r]
+        for (int k = tid; k < din; k += NT) {
+          float acc = gw[k];
+          for (int r = 0; r < nr; ++r)
+            acc = hvp ? fmaf(TAi[r * HS + k], da[r * HS], fmaf(Ai[r * HS + k], tda[r * HS], acc))
+                      : fmaf(Ai[r * HS + k], da[r * HS], acc);
+          gw[k] = acc;
+        }
+      } else {
+        const int ncg = dout >> 2;
+        for (int it = tid; it < (din >> 2) * ncg; it += NT) {
+          const int c = (it % ncg) * 4, k = (it / ncg) * 4;
+          float4 g[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) g[j] = ld4(gw + (k + j) * dout + c);
+          for (int r = 0; r < nr; ++r) {
+            const float4 a = ld4(Ai + r * HS + k);
+            const float4 d = ld4(da + r * HS + c);
+            const float av[4] = {a.x, a.y, a.z, a.w};
+            if (!hvp) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                g[j].x = fmaf(av[j], d.x, g[j].x); g[j].y = fmaf(av[j], d.y, g[j].y);
+                g[j].z = fmaf(av[j], d.z, g[j].z); g[j].w = fmaf(av[j], d.w, g[j].w);
+              }
+            } else {  // hvp: TA^T dz + A^T tdz
+              const float4 ta = ld4(TAi + r * HS + k);
+              const float4 td = ld4(tda + r * HS + c);
+              const float tv[4] = {ta.x, ta.y, ta.z, ta.w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                g[j].x = fmaf(tv[j], d.x, fmaf(av[j], td.x, g[j].x));
+                g[j].y = fmaf(tv[j], d.y, fmaf(av[j], td.y, g[j].y));
+                g[j].z = fmaf(tv[j], d.z, fmaf(av[j], td.z, g[j].z));
+                g[j].w = fmaf(tv[j], d.w, fmaf(av[j], td.w, g[j].w));
+              }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) st4(gw + (k + j) * dout + c, g[j]);
+        }
+      }
+      for (int c = tid; c < dout; c += NT) {
+        float acc = out[h.ob[i] + c];
+        const float* src = hvp ? tda : da;
+        for (int r = 0; r < nr; ++r) acc += src[r * HS + c];
+        out[h.ob[i] + c] = acc;
+      }
+      if (i > 0) {  // da' = dz W^T ; tda' = tdz W^T + dz vW^T   (2 rows x 4 k per thread)
+        const float* __restrict__ W = th + h.ow[i];
+        const float* __restrict__ vW = hvp ? v + h.ow[i] : nullptr;
+        const int nkg = din >> 2;
+        for (int it = tid; it < nkg * (nr2 >> 1); it += NT) {
+          const int k = (it % nkg) * 4, r = (it / nkg) * 2;
+          float a[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+          float t[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+          if (last) {  // dout == 1
+            const float d0 = da[r * HS], d1 = da[(r + 1) * HS];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              a[0][j] = d0 * W[k + j];
+              a[1][j] = d1 * W[k + j];
+              if (hvp) {
+                t[0][j] = fmaf(tda[r * HS], W[k + j], d0 * vW[k + j]);
+                t[1][j] = fmaf(tda[(r + 1) * HS], W[k + j], d1 * vW[k + j]);
+              }
+            }
+          } else {
+            for (int c = 0; c < dout; c += 4) {
+              const float4 d0 = ld4(da + r * HS + c), d1 = ld4(da + (r + 1) * HS + c);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float4 w = ld4(W + (k + j) * dout + c);
+                a[0][j] += d0.x * w.x + d0.y * w.y + d0.z * w.z + d0.w * w.w;
+                a[1][j] += d1.x * w.x + d1.y * w.y + d1.z * w.z + d1.w * w.w;
+                if (hvp) {
+                  const float4 vw = ld4(vW + (k + j) * dout + c);
+                  const float4 e0 = ld4(tda + r * HS + c), e1 = ld4(tda + (r + 1) * HS + c);
+                  t[0][j] += e0.x * w.x + e0.y * w.y + e0.z * w.z + e0.w * w.w + d0.x * vw.x + d0.y * vw.y +
+                             d0.z * vw.z + d0.w * vw.w;
+                  t[1][j] += e1.x * w.x + e1.y * w.y + e1.z * w.z + e1.w * w.w + d1.x * vw.x + d1.y * vw.y +
+                             d1.z * vw.z + d1.w * vw.w;
+                }
+              }
+            }
+          }
+          st4(dn + r * HS + k, make_float4(a[0][0], a[0][1], a[0][2], a[0][3]));
+          st4(dn + (r + 1) * HS + k, make_float4(a[1][0], a[1][1], a[1][2], a[1][3]));
+          if (hvp) {
+            st4(tdn + r * HS + k, make_float4(t[0][0], t[0][1], t[0][2], t[0][3]));
+            st4(tdn + (r + 1) * HS + k, make_float4(t[1][0], t[1][1], t[1][2], t[1][3]));
+          }
+        }
+      }
+      __syncthreads();
+      cur ^= 1;
+    }
+  }
+  const float sq = block_sum(sq_local, S.red());
+  return sq / static_cast<float>(n);
+}
+
+__device__ __forceinline__ bool tiled_ok(const Head& h) {
+  if (h.dim[h.nh] != 1 || (h.dim[0] & 3) || (h.RC & 1)) return false;
+  for (int i = 1; i < h.nh; ++i)
+    if (h.dim[i] & 3) return false;
+  return true;
+}
+
+__device__ float head_pass(const Head& h, const float* th, const float* v, const float* u, const int64_t* ridx,
+                           const float* y, int n, float* out, const Scratch& S) {
+  return tiled_ok(h) ? head_pass_tiled(h, th, v, u, ridx, y, n, out, S)
+                     : head_pass_scalar(h, th, v, u, ridx, y, n, out, S);
 }
 
 struct TaskSet {
