@@ -117,7 +117,8 @@ int kt_encode_raw_choices(const kt_spec_table* tab, const int64_t* choices, int6
                           double* feats_out, int32_t* err_flag, void* stream);
 
 /* ---- candidate scoring (the predictor of search.py:534-541) ------------------------ */
-/* Fused encode -> GCN(12->32->32) -> weighted-sum+max readout -> head(64->64->64->1)
+/* Fused encode -> GCN(12->32->32) -> weighted-sum+max readout -> head(64->64->64->1),
+ * all four GEMMs on tcgen05 tensor cores in 3xTF32 (fp32-accurate),
  * for graphs on the star layouts batch_layout (graphs.py:278) produces; equals
  * head_forward_batch(embed_batch(encode_batch(...))) (model.py:185-203).
  * Requires the default dims (F=12, gcn (32,32), head (64,64)).  `idx` may be NULL:
@@ -126,6 +127,12 @@ int kt_encode_raw_choices(const kt_spec_table* tab, const int64_t* choices, int6
 int kt_score_indices(const kt_spec_table* tab, const kt_dims* dims, const float* params,
                      const int64_t* idx, int64_t idx_base, int64_t B,
                      float* z_out, float* u_out, int32_t* err_flag, void* stream);
+/* Same contract on the FP32 FMA pipe (FFMA2 register tiles) instead of tcgen05
+ * 3xTF32 tensor cores; kept as the second, independent implementation the parity
+ * tests hold the tensor-core kernel against. */
+int kt_score_indices_fp32(const kt_spec_table* tab, const kt_dims* dims, const float* params,
+                          const int64_t* idx, int64_t idx_base, int64_t B,
+                          float* z_out, float* u_out, int32_t* err_flag, void* stream);
 
 /* ---- general forward (arbitrary adjacency, segmented batches) ------------------------ */
 /* embed_batch (model.py:185-194) generalised to CSR batches.

@@ -85,6 +85,7 @@ _SIGS = {
     "kt_encode_raw": (ctypes.c_int, [vp, vp, i64, vp, vp, vp]),
     "kt_encode_raw_choices": (ctypes.c_int, [vp, vp, i64, vp, vp, vp]),
     "kt_score_indices": (ctypes.c_int, [vp, ctypes.POINTER(Dims), vp, vp, i64, i64, vp, vp, vp, vp]),
+    "kt_score_indices_fp32": (ctypes.c_int, [vp, ctypes.POINTER(Dims), vp, vp, i64, i64, vp, vp, vp, vp]),
     "kt_embed_csr": (ctypes.c_int, [ctypes.POINTER(Dims), vp, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp,
                                     i64, vp, vp, vp]),
     "kt_head_forward": (ctypes.c_int, [ctypes.POINTER(Dims), vp, vp, i64, vp, vp]),

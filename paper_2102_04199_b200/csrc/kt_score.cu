@@ -1,4 +1,5 @@
-// kt_score_indices: fused candidate scorer for star-layout schedule graphs.
+// kt_score_indices_fp32: fused candidate scorer for star-layout schedule graphs on the
+// FP32 FMA pipe (FFMA2).  kt_score_tc.cu holds the tensor-core version (kt_score_indices).
 //
 // Replaces the predictor closure meta_scores (search.py:534-541):
 //   encode_batch (graphs.py:305) -> embed_batch (model.py:185-194)
@@ -421,11 +422,11 @@ static bool default_dims(const kt_dims& d) {
 
 }  // namespace kt
 
-extern "C" int kt_score_indices(const kt_spec_table* tab, const kt_dims* dims, const float* params,
+extern "C" int kt_score_indices_fp32(const kt_spec_table* tab, const kt_dims* dims, const float* params,
                                 const int64_t* idx, int64_t idx_base, int64_t B, float* z_out,
                                 float* u_out, int32_t* err_flag, void* stream) {
   using namespace kt;
-  KT_REQUIRE(tab && dims && params && z_out && err_flag, KT_E_ARG, "kt_score_indices: null pointer");
+  KT_REQUIRE(tab && dims && params && z_out && err_flag, KT_E_ARG, "kt_score_indices_fp32: null pointer");
   KT_REQUIRE(B > 0, KT_E_EMPTY, "kt_score_indices: empty batch");
   KT_REQUIRE(default_dims(*dims), KT_E_UNSUPPORTED,
              "kt_score_indices: fused scorer needs F=12, gcn (32,32), head (64,64)");
@@ -442,5 +443,5 @@ extern "C" int kt_score_indices(const kt_spec_table* tab, const kt_dims* dims, c
   score::score_star_kernel<<<grid, score::NT, smem, as_stream(stream)>>>(tab, *dims, params, idx, idx_base,
                                                                          B, z_out, u_out, err_flag);
   note_launches(1);
-  return check_launch("kt_score_indices");
+  return check_launch("kt_score_indices_fp32");
 }

@@ -30,12 +30,13 @@ def _default_model(m: ModelState) -> bool:
 
 def score_indices(m: ModelState, spec: KernelSpec, space: KnobSpace, layout: BatchLayout, idx=None, *,
                   base: int = 0, count: int | None = None, want_u: bool = False, check: bool = True,
-                  z_out=None, u_out=None, err=None):
+                  z_out=None, u_out=None, err=None, engine: str = "tc"):
     """Scores z (fp32 device, normalised log2 GFLOPS) of config indices.
 
     `idx` is an int64 device tensor (or array-like); with idx=None the candidates
     are the contiguous range [base, base+count).  Equals
     head_forward_batch(embed_batch(m, encode_batch(...), mask, adj), head).
+    engine "tc": tcgen05 3xTF32 kernel (kt_score_indices); "fp32": FFMA2 kernel.
     """
     flat = flat_params(m)
     dev = flat.device
@@ -54,9 +55,9 @@ def score_indices(m: ModelState, spec: KernelSpec, space: KnobSpace, layout: Bat
     e = err if err is not None else torch.zeros(1, dtype=torch.int32, device=dev)
     lib = _lib.load()
     with torch.cuda.device(dev):
-        _lib.check(lib.kt_score_indices(_lib.ptr(tab), dims_of(m), _lib.ptr(flat), _lib.ptr(idx), base, b,
-                                        _lib.ptr(z), _lib.ptr(u), _lib.ptr(e), _lib.stream_handle()),
-                   "score_indices")
+        fn = lib.kt_score_indices if engine == "tc" else lib.kt_score_indices_fp32
+        _lib.check(fn(_lib.ptr(tab), dims_of(m), _lib.ptr(flat), _lib.ptr(idx), base, b, _lib.ptr(z), _lib.ptr(u),
+                      _lib.ptr(e), _lib.stream_handle()), "score_indices")
     if check and int(e.item()):
         raise DomainError("config index out of range for the knob space")
     return (z, u) if want_u else z

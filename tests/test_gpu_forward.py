@@ -69,18 +69,23 @@ def test_encode_rejects_out_of_range(cuda_device, g_encode):
         pg.encode_batch(spec, space, np.array([space.size]), _layout(spec, "super"))
 
 
+ENGINES = ["tc", "fp32"]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("rep", ["raw", "super"])
-def test_fused_scorer_matches_reference(cuda_device, g_encode, g_model, rep):
+def test_fused_scorer_matches_reference(cuda_device, g_encode, g_model, rep, engine):
     m = device_model(g_model)
     spec = spec_of(g_encode, "conv2d")
     space = pk.build_knob_space(spec)
-    z, u = ps.score_indices(m, spec, space, _layout(spec, rep), g_model["score/idx"], want_u=True)
+    z, u = ps.score_indices(m, spec, space, _layout(spec, rep), g_model["score/idx"], want_u=True, engine=engine)
     _assert_gflops_close(z, g_model[f"score/{rep}/z"], m.label_norm.std)
     np.testing.assert_allclose(u.double().cpu().numpy(), g_model[f"score/{rep}/u"], rtol=1e-4, atol=1e-5)
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("op", OPS)
-def test_fused_scorer_all_ops_vs_oracle(cuda_device, g_encode, g_model, op):
+def test_fused_scorer_all_ops_vs_oracle(cuda_device, g_encode, g_model, op, engine):
     p = oracle_params(g_model)
     m = device_model(g_model)
     spec = spec_of(g_encode, op)
@@ -92,22 +97,37 @@ def test_fused_scorer_all_ops_vs_oracle(cuda_device, g_encode, g_model, op):
         adj, rows, mask = ko.layout(op, rep == "super")
         x = ko.encode(op, ext, knobs, g_encode[f"{op}/choices"], adj.shape[0], rows)
         zref = ko.score(p, x, mask, adj)
-        z = ps.score_indices(m, spec, space, _layout(spec, rep), g_encode[f"{op}/idx"])
+        z = ps.score_indices(m, spec, space, _layout(spec, rep), g_encode[f"{op}/idx"], engine=engine)
         _assert_gflops_close(z, zref, m.label_norm.std)
 
 
-def test_scorer_contiguous_range_equals_index_list(cuda_device, g_model):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_scorer_contiguous_range_equals_index_list(cuda_device, g_model, engine):
     m = device_model(g_model)
     spec = pk.KernelSpec("conv2d", 56, 64, 64, 3, 3, 1)
     space = pk.build_knob_space(spec)
     lay = _layout(spec, "super")
     base = 123_456_789
-    a = ps.score_indices(m, spec, space, lay, base=base, count=5000)
-    b = ps.score_indices(m, spec, space, lay, np.arange(base, base + 5000))
+    a = ps.score_indices(m, spec, space, lay, base=base, count=5000, engine=engine)
+    b = ps.score_indices(m, spec, space, lay, np.arange(base, base + 5000), engine=engine)
     assert torch.equal(a, b)
 
 
-def test_scorer_is_batch_position_invariant_and_deterministic(cuda_device, g_model):
+def test_tensor_core_and_fp32_scorers_agree(cuda_device, g_model):
+    """3xTF32 tcgen05 kernel vs the independent FFMA2 kernel on 100k candidates (both vs fp64 elsewhere)."""
+    m = device_model(g_model)
+    spec = pk.KernelSpec("conv2d", 56, 64, 64, 3, 3, 1)
+    space = pk.build_knob_space(spec)
+    lay = _layout(spec, "super")
+    idx = np.random.default_rng(11).integers(0, space.size, 100_000)
+    a = ps.score_indices(m, spec, space, lay, idx, engine="tc").double()
+    b = ps.score_indices(m, spec, space, lay, idx, engine="fp32").double()
+    assert torch.isfinite(a).all()
+    assert (a - b).abs().max().item() <= 2e-5 * max(1.0, b.abs().max().item())
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_scorer_is_batch_position_invariant_and_deterministic(cuda_device, g_model, engine):
     """Per-candidate arithmetic must not depend on the batch (ties stay ties)."""
     m = device_model(g_model)
     spec = pk.KernelSpec("conv2d", 56, 64, 64, 3, 3, 1)
@@ -115,17 +135,18 @@ def test_scorer_is_batch_position_invariant_and_deterministic(cuda_device, g_mod
     lay = _layout(spec, "super")
     rng = np.random.default_rng(7)
     idx = rng.integers(0, space.size, 3001)
-    z_full = ps.score_indices(m, spec, space, lay, idx).cpu().numpy()
+    z_full = ps.score_indices(m, spec, space, lay, idx, engine=engine).cpu().numpy()
     perm = rng.permutation(idx.size)
-    z_perm = ps.score_indices(m, spec, space, lay, idx[perm]).cpu().numpy()
+    z_perm = ps.score_indices(m, spec, space, lay, idx[perm], engine=engine).cpu().numpy()
     assert z_perm.tobytes() == z_full[perm].tobytes()
-    for b in (1, 7, 64, 65):
-        z_small = ps.score_indices(m, spec, space, lay, idx[:b]).cpu().numpy()
+    for b in (1, 7, 64, 65, 121):
+        z_small = ps.score_indices(m, spec, space, lay, idx[:b], engine=engine).cpu().numpy()
         assert z_small.tobytes() == z_full[:b].tobytes()
-    assert ps.score_indices(m, spec, space, lay, idx).cpu().numpy().tobytes() == z_full.tobytes()
+    assert ps.score_indices(m, spec, space, lay, idx, engine=engine).cpu().numpy().tobytes() == z_full.tobytes()
 
 
-def test_scorer_tie_classes_match_reference(cuda_device, g_model):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_scorer_tie_classes_match_reference(cuda_device, g_model, engine):
     """Identical encoded features => bit-identical scores (the reference's exact ties)."""
     m = device_model(g_model)
     spec = pk.KernelSpec("conv2d", 56, 64, 64, 3, 3, 1)
@@ -133,7 +154,7 @@ def test_scorer_tie_classes_match_reference(cuda_device, g_model):
     lay = _layout(spec, "super")
     idx = np.random.default_rng(3).integers(0, space.size, 20000)
     feats = pg.encode_batch(spec, space, idx, lay).cpu().numpy()
-    z = ps.score_indices(m, spec, space, lay, idx).cpu().numpy()
+    z = ps.score_indices(m, spec, space, lay, idx, engine=engine).cpu().numpy()
     keys = {}
     for f, v in zip(feats.reshape(len(idx), -1), z):
         keys.setdefault(f.tobytes(), set()).add(v.tobytes())
