@@ -39,7 +39,20 @@ POOL_SLICES = 24
 SPEC_ARGS = ("conv2d", 56, 64, 64, 3, 3, 1)
 FLOP_PER_GRAPH = 2 * (12 * 12 * 32 + 12 * 32 * 32 + 64 * 64 + 64 * 64 + 64)  # star-factored MACs x 2
 REF_FLOP_PER_GRAPH = 95065  # dense 25-node evaluation
+# tensor FLOPs the 3xTF32 scorer issues per graph: 3 products per GEMM, K padded 12 -> 16
+TC_FLOP_PER_GRAPH = 3 * 2 * (12 * 16 * 32 + 12 * 32 * 32 + 64 * 64 + 64 * 64)
 FP32_PEAK_TFLOPS = 71.4  # measured in-repo, tools/fma_peak.cu (profiles/r01_fp32_peak.md)
+
+
+def tf32_peak():
+    """Dense TF32 tensor peak: the driver-measured bf16 burst (MEASURED_PEAKS.json) / 2
+    (tcgen05 kind::tf32 runs at half the kind::f16 rate; tools/tc_lat2.cu measures both
+    at 128 cycles per 128x256x{8 tf32, 16 f16} MMA)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"]) / 2, "MEASURED_PEAKS.json bf16_tflops / 2 (tf32 = half the bf16 rate)"
+    except (OSError, ValueError, KeyError):
+        return 1590.0 / 2, "fallback 1.59 PFLOP/s bf16 (B200_PROFILING.md) / 2"
 LABEL_NORM = (-5.62, 7.08)  # conftest corpus statistics (SURVEY.md 8(d))
 
 
@@ -129,6 +142,14 @@ class ClockSampler:
         load = [s for s in sm if s > 0.5 * mx] or sm
         return {"sm_mhz": float(np.median(load)), "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm)}
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        return 6650.0
 
 
 def load_traffic():
@@ -467,6 +488,7 @@ def run_ours(args):
                          f"4096-candidate chunks, {procs} processes x 1 BLAS thread), {secs:.1f} s"}
 
     achieved = FLOP_PER_GRAPH * BATCH / (kern_ms / 1e3) / 1e12
+    peak, peak_src = tf32_peak()
     traffic = load_traffic()
     line = {
         "metric": METRIC, "value": value, "unit": "graphs/s", "n_gpus": ws, "steps": args.steps,
@@ -478,11 +500,13 @@ def run_ours(args):
                    "model": "GCN 12->32->32, sum+max readout, FC 64->64->64->1 (random init, bench-model)",
                    "parallelism": f"dp{ws} (candidate shards)",
                    "l2": f"timed steps rotate over a {POOL_SLICES * BATCH * 8 >> 20} MiB index pool (> 126 MB L2)"},
-        "roofline": {"bound": "fp32", "kernel": "score_star_kernel", "achieved": achieved,
-                     "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
-                     "traffic": traffic, "kernel_ms": kern_ms,
-                     "flop_per_graph": FLOP_PER_GRAPH, "ref_formula_flop_per_graph": REF_FLOP_PER_GRAPH,
-                     "peak_source": "measured in-repo FFMA peak (tools/fma_peak.cu); not in MEASURED_PEAKS.json"},
+        "roofline": {"bound": "tensor", "kernel": "score_tc_kernel (kt_score_indices)", "achieved": achieved,
+                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                     "kernel_ms": kern_ms, "flop_per_graph": FLOP_PER_GRAPH,
+                     "tensor_flop_per_graph_issued": TC_FLOP_PER_GRAPH,
+                     "tensor_issued_frac": TC_FLOP_PER_GRAPH * BATCH / (kern_ms / 1e3) / 1e12 / peak,
+                     "ref_formula_flop_per_graph": REF_FLOP_PER_GRAPH, "peak_source": peak_src,
+                     "algorithmic_bytes_per_graph": 12, "hbm_frac": 12 * BATCH / (kern_ms / 1e3) / 1e9 / hbm_peak()},
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
     }
     if cpu:
@@ -514,7 +538,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=1 << 18)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 22)
     ap.add_argument("--ref-sample", type=int, default=0)
     ap.add_argument("--no-extras", action="store_true", help="skip the C2/C3/C4 secondary measurements")
     ap.add_argument("--meta-steps", type=int, default=200)

@@ -1,64 +1,92 @@
 // kt_score_indices (tensor-core path): the fused candidate scorer with all four
 // GEMMs on the 5th-generation tensor cores (tcgen05.mma kind::tf32, accumulators
 // in TMEM) in 3xTF32 split precision (A*B ~= Ah*Bh + Ah*Bl + Al*Bh, fp32-level
-// accuracy).  Same math and contract as the FFMA2 kernel in kt_score.cu
-// (star-layout algebra documented there); replaces meta_scores
+// accuracy).  Same math and contract as the FFMA2 kernel in kt_score.cu (the
+// star-layout algebra is documented there); replaces meta_scores
 // (search.py:534-541) = encode_batch -> embed_batch -> head_forward_batch.
 //
-// Work unit: a tile of 120 graphs = 12 chunks x 10 graphs; a chunk is one
-// 128-row MMA tile (graph g of the chunk owns rows 12g..12g+11, rows 120..127
-// are padding).  Per chunk:
-//   GEMM1  D1[128x32]  = X[128x16] * W1          (A = X in TMEM, 2 K-steps x 3)
-//   GEMM2  D2[128x32]  = ReLU(D1) * W2           (A = R in TMEM, 4 K-steps x 3)
-// then the star readout (sum / max over each graph's 12 rows) into U[120x64].
-// Per tile:
-//   GEMM3  D3[128x64]  = U * H0 + b0 -> ReLU     (A = U in smem, 8 K-steps x 3)
-//   GEMM4  D4[128x64]  = Z1 * H1 + b1 -> ReLU -> . w3 + b3   (A = Z1 in TMEM)
+// Loop-major tiling.  A tile is 128 graphs and TMEM lane g is graph g of the
+// tile for every accumulator.  The tile is processed as n_loops chunks; chunk k
+// holds loop row k of all 128 graphs:
+//   GEMM1  D1[128x32] = X_k[128x16] * W1            (A = X_k in TMEM, 2 K-steps x 3)
+//   GEMM2  D2[128x32] = ReLU(D1) * W2 = s_k          (A = R_k in TMEM, 4 K-steps x 3)
+// so the star readout (sum_k s_k, sum_k ReLU(s_k), max_k s_k per channel) is a
+// per-thread running reduction over chunks -- no cross-lane traffic at all.
+// After the last chunk each epilogue thread owns its graph's readout row u:
+//   GEMM3  D3[128x64] = U * H0 (+b0, ReLU)          (A = U in smem, 8 K-steps x 3)
+//   GEMM4  D4[128x64] = Z1 * H1 (+b1, ReLU) . w3 + b3 (A = Z1 in smem)
 //
-// Warp specialisation (256 threads, 1 CTA / SM, 512 TMEM columns):
-//   warps 4-7 (producer): encode feature rows of chunk q (index decode, fp64
-//     touched/log2/z-norm, host tables for the rest), split hi/lo and tcgen05.st
-//     them into the double-buffered TMEM A operand X[q % 2];  mbarrier x_full.
-//   warps 0-3 (consumer): thread 0 issues the MMAs and tcgen05.commit's
-//     (x_empty releases X buffers, bar_g1/g2/h signal accumulators); all four
-//     warps run the epilogues -- each thread owns one TMEM lane = one row.
-// The encode of chunk q+1 overlaps GEMM1/GEMM2 and the epilogues of chunk q.
+// Warp roles (544 threads = 17 warps, 1 CTA / SM, 512 TMEM columns):
+//   warps 0-3    R: thread = TMEM lane = graph; ReLU(D1) split hi/lo into R (TMEM)
+//   warps 4-7    encode: thread = graph; index decode once per tile, then one
+//                normalised feature row per chunk (fp64 touched / log2 / z-norm,
+//                host tables for the rest), hi/lo split, tcgen05.st into an X slot
+//   warp 8       MMA: a non-blocking scheduler that polls the ring barriers and
+//                issues whichever GEMM is ready (one elected lane issues)
+//   warps 9-16   readout + head: two warps per lane quadrant, 16 channels each;
+//                running sum / ReLU-sum / max over the chunks, then the head
+//                epilogues (U -> smem, ReLU(D3 + b0) -> smem, (D4 + b1) . w3)
+// Rings: X 4 slots, D1 / R / D2 double-buffered; the R warps and the readout
+// warps never wait on each other, and the head of tile t overlaps the GCN
+// chunks of tile t+1 on the tensor pipe.
 #include "kt_encode.cuh"
 #include "kt_tc.cuh"
+
+// Debug timeline (tools/tc_trace.py builds with -DKT_TC_TRACE): clock64 stamps of
+// CTA 0's pipeline events.  Compiled out of the product library.
+#ifdef KT_TC_TRACE
+#define KT_TRACE_N 64
+__device__ long long g_kt_trace[20][KT_TRACE_N];
+#define TRACE(ev, i)                                              \
+  do {                                                            \
+    if (blockIdx.x == 0 && (i) < KT_TRACE_N) g_kt_trace[ev][i] = clock64(); \
+  } while (0)
+extern "C" int kt_debug_trace_read(void* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_kt_trace, sizeof(g_kt_trace)));
+}
+#else
+#define TRACE(ev, i) \
+  do {               \
+  } while (0)
+#endif
 
 namespace kt {
 namespace tcs {
 
 using namespace kt::tc;
 
-constexpr int NT = 256;
-constexpr int GPC = 10;             // graphs per chunk
-constexpr int CPT = 12;             // chunks per tile
-constexpr int GT = GPC * CPT;       // graphs per tile (head M = 128 rows, 120 used)
+constexpr int NT = 544;  // 17 warps
+constexpr int GT = 128;   // graphs per tile (one TMEM lane each)
 constexpr int H = 64;
-constexpr int ULBO = 144;           // padded K-chunk stride of U (bank spread for column writes)
-constexpr int UF = (128 / 8) * (H / 4) * ULBO / 4;  // floats per U plane
-constexpr int SS = 33;              // readout staging row stride
+constexpr int XS = 4;     // X ring slots
 constexpr int TAB = 448;
 
 // TMEM column map (512 allocated)
-constexpr uint32_t T_D1 = 0, T_RH = 32, T_RL = 64, T_D2 = 96, T_D3 = 128, T_ZH = 192, T_ZL = 256, T_D4 = 320,
-                   T_X = 384;  // X[buf]: hi at T_X + 32 buf, lo at T_X + 32 buf + 16
+constexpr uint32_t T_X = 0;     // X[s]: hi at 32 s, lo at 32 s + 16       [0, 128)
+constexpr uint32_t T_D1 = 128;  // D1[b] at 128 + 32 b                    [128, 192)
+constexpr uint32_t T_R = 192;   // R[b]: hi at 192 + 64 b, lo at +32        [192, 320)
+constexpr uint32_t T_D2 = 320;  // D2[b] at 320 + 32 b                    [320, 384)
+constexpr uint32_t T_D3 = 384;  //                                         [384, 448)
+constexpr uint32_t T_D4 = 448;  //                                         [448, 512)
 
-struct __align__(16) Smem {
-  float b1h[32 * 16], b1l[32 * 16];  // W1^T  (N=32, K=16; K 12..15 zero)
+struct __align__(1024) Smem {
+  float b1h[32 * 16], b1l[32 * 16];  // W1^T (N=32, K=16; K 12..15 zero), K-major core matrices
   float b2h[32 * 32], b2l[32 * 32];  // W2^T
   float b3h[H * H], b3l[H * H];      // H0^T
   float b4h[H * H], b4l[H * H];      // H1^T
-  float uh[UF], ul[UF];              // U operand (head A), K-major with LBO 144
-  float s[128 * SS];                 // D2 rows staged for the per-graph readout
+  float ah[GT * H], al[GT * H];      // head A operand: U, then Z1 (K-major)
   float bias0[H], bias1[H], w3[H], agg[32];
+  float part[GT];  // head: half-1 partial dot per graph
   int2 oi[TAB];
   float4 nrm_o[TAB];
   float2 nrm_i[TAB];
+  double2 l2[TAB];  // numpy log2 of (outer, inner) extent
   float nconst[KT_MAX_LOOPS][8];
   int tab_off[KT_MAX_AXES];
-  uint64_t x_full[2], x_empty[2], bar_g1, bar_g2, bar_h;
+  short sel[KT_MAX_AXES][GT];  // per graph: packed table entry of each axis' tile choice
+  uint64_t x_full[XS], x_empty[XS];
+  uint64_t d1_full[2], d1_empty[2], r_full[2], r_empty[2], d2_full[2], d2_empty[2];
+  uint64_t u_full, z_full, d3_full, d4_full;
   uint32_t tmem_base;
 };
 
@@ -66,69 +94,6 @@ __device__ __forceinline__ float relu(float v) { return fmaxf(v, 0.0f); }
 
 __device__ __forceinline__ uint32_t udiv(uint32_t v, uint32_t d, uint64_t magic) {
   return d == 1 ? v : static_cast<uint32_t>(__umul64hi(static_cast<uint64_t>(v), magic));
-}
-
-// Normalised feature row of loop k of the graph with config index v (valid, < 2^32).
-__device__ __forceinline__ void encode_row(const kt_spec_table& T, const Smem& S, uint32_t v, int k, float* x) {
-  const int na = T.n_axes, n_loops = T.n_loops;
-  int ch[KT_MAX_KNOBS];
-#pragma unroll
-  for (int j = KT_MAX_KNOBS - 1; j >= 0; --j) {
-    ch[j] = 0;
-    if (j < T.n_knobs) {
-      const uint32_t d = T.card[j];
-      const uint32_t q = udiv(v, d, T.card_magic[j]);
-      ch[j] = static_cast<int>(v - q * d);
-      v = q;
-    }
-  }
-  const int autov = T.auto_knob >= 0 ? T.auto_vals[ch[T.auto_knob]] : 0;
-  const int expl = T.expl_knob >= 0 ? T.expl_vals[ch[T.expl_knob]] : 0;
-  // chain extents: outer loops of axes 0..na-1, then inner loops; touched = prod over loops > k
-  double t = 1.0;
-  int my_c = 0, my_e = 1, my_unr = 0;
-#pragma unroll
-  for (int lvl = 1; lvl >= 0; --lvl) {
-#pragma unroll
-    for (int a = KT_MAX_AXES - 1; a >= 0; --a) {
-      if (a < na) {
-        const int c = T.axis_knob[a] >= 0 ? ch[T.axis_knob[a]] : 0;
-        const int2 p = S.oi[S.tab_off[a] + c];
-        const int e = lvl ? p.y : p.x;
-        const int j = lvl ? na + a : a;
-        if (j == k) {
-          my_c = S.tab_off[a] + c;
-          my_e = e;
-          my_unr = lvl && expl != 0 && autov > 0 && p.y <= autov;
-        }
-        if (j > k) t *= static_cast<double>(e);
-      }
-    }
-  }
-  (void)my_e;
-  const bool level = k >= na;
-  if (level) {
-    const float2 ni = S.nrm_i[my_c];
-    x[0] = ni.x;
-    x[1] = ni.y;
-    x[5] = S.nconst[k][4];
-  } else {
-    const float4 no = S.nrm_o[my_c];
-    x[0] = no.x;
-    x[1] = no.y;
-    x[5] = no.z;
-  }
-  x[2] = S.nconst[k][0];
-  x[3] = S.nconst[k][1];
-  x[4] = my_unr ? S.nconst[k][3] : S.nconst[k][2];
-  const double ar = 2.0 * t;
-  x[6] = static_cast<float>((t - T.fmean[6]) / T.fstd[6]);
-  x[7] = static_cast<float>((log2(t) - T.fmean[7]) / T.fstd[7]);
-  x[8] = static_cast<float>((ar - T.fmean[8]) / T.fstd[8]);
-  x[9] = static_cast<float>((log2(ar) - T.fmean[9]) / T.fstd[9]);
-  x[10] = S.nconst[k][5];
-  x[11] = S.nconst[k][6];
-  (void)n_loops;
 }
 
 __device__ __forceinline__ void stage_operand(const float* W, int K_src, int N, int K, float* hi, float* lo, int tid) {
@@ -141,6 +106,22 @@ __device__ __forceinline__ void stage_operand(const float* W, int K_src, int N, 
     hi[off] = h;
     lo[off] = v - h;
   }
+}
+
+// thread-owned row `row` of a 128 x 64 K-major A operand: columns 4kq..4kq+3 as hi / lo
+__device__ __forceinline__ void store_head_quad(float* ah, float* al, int row, int kq, float4 v) {
+  float4 h, l;
+  h.x = tf32_trunc(v.x);
+  h.y = tf32_trunc(v.y);
+  h.z = tf32_trunc(v.z);
+  h.w = tf32_trunc(v.w);
+  l.x = v.x - h.x;
+  l.y = v.y - h.y;
+  l.z = v.z - h.z;
+  l.w = v.w - h.w;
+  const int off = kmajor_offset(row, 4 * kq, H) >> 2;
+  *reinterpret_cast<float4*>(ah + off) = h;
+  *reinterpret_cast<float4*>(al + off) = l;
 }
 
 __global__ void __launch_bounds__(NT, 1)
@@ -157,27 +138,35 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
   stage_operand(params + dims.off_gcn[1], 32, 32, 32, S.b2h, S.b2l, tid);
   stage_operand(params + dims.off_hw[0], H, H, H, S.b3h, S.b3l, tid);
   stage_operand(params + dims.off_hw[1], H, H, H, S.b4h, S.b4l, tid);
-  for (int i = tid; i < UF; i += NT) S.uh[i] = S.ul[i] = 0.0f;
   if (tid < H) {
     S.bias0[tid] = params[dims.off_hb[0] + tid];
     S.bias1[tid] = params[dims.off_hb[1] + tid];
     S.w3[tid] = params[dims.off_hw[2] + tid];
   }
   if (tid < 32) S.agg[tid] = params[dims.off_agg + tid];
-  const int na = T.n_axes;
+  const int na = T.n_axes, n_loops = T.n_loops;
   if (tid == 0) {
     int off = 0;
     for (int a = 0; a < na; ++a) {
       S.tab_off[a] = off;
       off += T.axis_knob[a] >= 0 ? static_cast<int>(T.card[T.axis_knob[a]]) : 1;
     }
-    mbar_init(&S.x_full[0], 128);
-    mbar_init(&S.x_full[1], 128);
-    mbar_init(&S.x_empty[0], 1);
-    mbar_init(&S.x_empty[1], 1);
-    mbar_init(&S.bar_g1, 1);
-    mbar_init(&S.bar_g2, 1);
-    mbar_init(&S.bar_h, 1);
+    for (int s = 0; s < XS; ++s) {
+      mbar_init(&S.x_full[s], 4);
+      mbar_init(&S.x_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&S.d1_full[b], 1);
+      mbar_init(&S.d1_empty[b], 4);
+      mbar_init(&S.r_full[b], 4);
+      mbar_init(&S.r_empty[b], 1);
+      mbar_init(&S.d2_full[b], 1);
+      mbar_init(&S.d2_empty[b], 8);
+    }
+    mbar_init(&S.u_full, 8);
+    mbar_init(&S.z_full, 8);
+    mbar_init(&S.d3_full, 1);
+    mbar_init(&S.d4_full, 1);
   }
   if (tid < KT_MAX_LOOPS) {
     const int k = tid;
@@ -190,7 +179,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     S.nconst[k][6] = T.nrm_const[k][11];
     S.nconst[k][7] = 0.f;
   }
-  if (warp == 0) tmem_alloc(&S.tmem_base, 512);
+  if (warp == 8) tmem_alloc(&S.tmem_base, 512);
   __syncthreads();
   for (int a = 0; a < na; ++a) {
     const int n = T.axis_knob[a] >= 0 ? static_cast<int>(T.card[T.axis_knob[a]]) : 1;
@@ -199,6 +188,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       S.oi[e] = make_int2(T.outer[a][c], T.inner[a][c]);
       S.nrm_o[e] = make_float4(T.nrm_ext[a][c], T.nrm_log2ext[a][c], T.nrm_stride[a][c], 0.f);
       S.nrm_i[e] = make_float2(T.nrm_ext[na + a][c], T.nrm_log2ext[na + a][c]);
+      S.l2[e] = make_double2(T.raw_log2[0][a][c], T.raw_log2[1][a][c]);
     }
   }
   fence_async_smem();
@@ -208,223 +198,407 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
   const uint32_t tmem = S.tmem_base;
   const int64_t n_tiles = (B + GT - 1) / GT;
   const int64_t my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int64_t n_chunks = my_tiles * CPT;
+  const int C = n_loops;  // chunks per tile
+  const int64_t n_chunks = my_tiles * C;
   const uint64_t size = T.space_size;
 
-  if (warp >= 4) {
-    // ===================== producer: encode rows into TMEM X[q % 2] =====================
-    const int row = tid - 128;
-    const uint32_t lane_addr = static_cast<uint32_t>((row & ~31) << 16);
-    const int gl = row / 12, k = row - (row / 12) * 12;
-    for (int64_t q = 0; q < n_chunks; ++q) {
-      const int buf = static_cast<int>(q & 1);
-      mbar_wait(&S.x_empty[buf], static_cast<uint32_t>(((q >> 1) & 1) ^ 1));
-      tc_fence_after();
-      const int64_t tile = blockIdx.x + (q / CPT) * gridDim.x;
-      const int c = static_cast<int>(q % CPT);
-      float x[16];
+  if (warp >= 4 && warp < 8) {
+    // ===================== encode: thread = graph; one feature row per chunk ================
+    const int g = tid - 128;
+    const uint32_t lane = static_cast<uint32_t>((g & ~31) << 16);
+    const int n_knobs = T.n_knobs;
+    // touched-derived slots in fp64 with reciprocal scales: within 1 fp64 ulp of the
+    // IEEE (x - mean) / std of model.py:108-112 before the single cast to fp32
+#ifdef KT_DBG_F32
+    using dbl = float;
+#else
+    using dbl = double;
+#endif
+    const double m6 = T.fmean[6], r6 = 1.0 / T.fstd[6], m7 = T.fmean[7], r7 = 1.0 / T.fstd[7];
+    const double m8 = T.fmean[8], r8 = 1.0 / T.fstd[8], m9 = T.fmean[9] - 1.0, r9 = 1.0 / T.fstd[9];
+    int64_t q = 0;
+    for (int64_t ti = 0; ti < my_tiles; ++ti) {
+      const int64_t gi = (blockIdx.x + ti * gridDim.x) * GT + g;
+      bool ok = false;
+      int ch[KT_MAX_KNOBS];
 #pragma unroll
-      for (int f = 0; f < 16; ++f) x[f] = 0.0f;
-      if (row < GT / CPT * 12) {
-        const int64_t gi = tile * GT + c * GPC + gl;
-        if (gi < B) {
-          const int64_t v = idx ? idx[gi] : idx_base + gi;
-          const bool ok = v >= 0 && static_cast<uint64_t>(v) < size;
-          if (!ok) {
-            if (k == 0) atomicOr(err, 1);
-          } else if (k < T.n_loops) {
-            encode_row(T, S, static_cast<uint32_t>(v), k, x);
+      for (int j = 0; j < KT_MAX_KNOBS; ++j) ch[j] = 0;
+      if (gi < B) {
+        const int64_t v = idx ? idx[gi] : idx_base + gi;
+        ok = v >= 0 && static_cast<uint64_t>(v) < size;
+        if (ok && size <= 0xffffffffull) {
+          uint32_t r = static_cast<uint32_t>(v);
+#pragma unroll
+          for (int j = KT_MAX_KNOBS - 1; j >= 0; --j) {
+            if (j < n_knobs) {
+              const uint32_t d = T.card[j];
+              const uint32_t qq = udiv(r, d, T.card_magic[j]);
+              ch[j] = static_cast<int>(r - qq * d);
+              r = qq;
+            }
           }
+        } else if (ok) {
+          uint64_t r = static_cast<uint64_t>(v);
+#pragma unroll
+          for (int j = KT_MAX_KNOBS - 1; j >= 0; --j) {
+            if (j < n_knobs) {
+              const uint64_t d = T.card[j];
+              const uint64_t qq = r / d;
+              ch[j] = static_cast<int>(r - qq * d);
+              r = qq;
+            }
+          }
+        } else {
+          atomicOr(err, 1);
         }
       }
-      float hi[16], lo[16];
+      // per-axis table entries and unroll flags, with ch[] only indexed by unrolled
+      // constants (keeps it in registers)
+      int ca_auto = 0, ca_expl = 0;
 #pragma unroll
-      for (int f = 0; f < 16; ++f) {
-        hi[f] = tf32_hi(x[f]);
-        lo[f] = x[f] - hi[f];
+      for (int j = 0; j < KT_MAX_KNOBS; ++j) {
+        if (j == T.auto_knob) ca_auto = ch[j];
+        if (j == T.expl_knob) ca_expl = ch[j];
       }
-      tmem_st16(tmem + lane_addr + T_X + 32 * buf, hi);
-      tmem_st16(tmem + lane_addr + T_X + 32 * buf + 16, lo);
-      tmem_wait_st();
+      const int autov = T.auto_knob >= 0 ? T.auto_vals[ca_auto] : 0;
+      const int expl = T.expl_knob >= 0 ? T.expl_vals[ca_expl] : 0;
+      unsigned unr_mask = 0;
+#pragma unroll
+      for (int a = 0; a < KT_MAX_AXES; ++a) {
+        if (a < na) {
+          const int kn = T.axis_knob[a];
+          int c = 0;
+#pragma unroll
+          for (int j = 0; j < KT_MAX_KNOBS; ++j)
+            if (j == kn) c = ch[j];
+          const int e = S.tab_off[a] + c;
+          S.sel[a][g] = static_cast<short>(e);
+          if (expl != 0 && autov > 0 && S.oi[e].y <= autov) unr_mask |= 1u << a;
+        }
+      }
+      // loops are emitted innermost first (k = n_loops-1 .. 0), so touched -- the
+      // product of the extents of the loops inside loop k, multiplied innermost
+      // outward as np.cumprod(e[::-1]) does -- accumulates exactly in fp64, and
+      // log2(touched) accumulates as the sum of the numpy log2 of those extents
+      // (log2(arith) = log2(2 touched) = that + 1).  Both are functions of the
+      // extent vector only, so configs with equal features score identically.
+      dbl t = 1.0, lt = 0.0;
+      for (int c = 0; c < C; ++c, ++q) {
+        const int k = C - 1 - c;
+        const int level = k >= na;
+        const int a = level ? k - na : k;
+        const int e = S.sel[a][g];
+        const int2 oi = S.oi[e];
+        float x[16];
+#pragma unroll
+        for (int f = 12; f < 16; ++f) x[f] = 0.0f;
+        if (ok) {
+          if (level) {
+            const float2 ni = S.nrm_i[e];
+            x[0] = ni.x;
+            x[1] = ni.y;
+            x[5] = S.nconst[k][4];
+          } else {
+            const float4 no = S.nrm_o[e];
+            x[0] = no.x;
+            x[1] = no.y;
+            x[5] = no.z;
+          }
+          x[2] = S.nconst[k][0];
+          x[3] = S.nconst[k][1];
+          const bool unr = level && ((unr_mask >> a) & 1u);
+          x[4] = unr ? S.nconst[k][3] : S.nconst[k][2];
+          x[6] = static_cast<float>((t - static_cast<dbl>(m6)) * static_cast<dbl>(r6));
+          x[7] = static_cast<float>((lt - static_cast<dbl>(m7)) * static_cast<dbl>(r7));
+          x[8] = static_cast<float>((static_cast<dbl>(2.0) * t - static_cast<dbl>(m8)) * static_cast<dbl>(r8));
+          x[9] = static_cast<float>((lt - static_cast<dbl>(m9)) * static_cast<dbl>(r9));
+          x[10] = S.nconst[k][5];
+          x[11] = S.nconst[k][6];
+        } else {
+#pragma unroll
+          for (int f = 0; f < 12; ++f) x[f] = 0.0f;
+        }
+        t *= static_cast<dbl>(level ? oi.y : oi.x);
+        const double2 l2 = S.l2[e];
+        lt += static_cast<dbl>(level ? l2.y : l2.x);
+        float hl[32];
+#pragma unroll
+        for (int f = 0; f < 16; ++f) {
+          hl[f] = tf32_trunc(x[f]);
+          hl[16 + f] = x[f] - hl[f];
+        }
+        const int s = static_cast<int>(q % XS);
+        mbar_wait(&S.x_empty[s], static_cast<uint32_t>(((q / XS) & 1) ^ 1));
+        __syncwarp();
+        tc_fence_after();
+#ifndef KT_DBG_NO_XST
+        tmem_st32(tmem + lane + T_X + 32 * s, hl);
+#endif
+        tmem_wait_st();
+        tc_fence_before();
+        warp_arrive(&S.x_full[s]);
+        if (g == 0) TRACE(0, q);
+      }
+    }
+  } else if (warp == 8) {
+    // ===================== MMA: polling scheduler, one elected lane issues =====================
+    const uint32_t id32 = idesc_tf32(128, 32), id64 = idesc_tf32(128, 64);
+    auto ready = [&](uint64_t* bar, uint32_t parity) {
+      return __shfl_sync(0xffffffffu, static_cast<int>(mbar_test(bar, parity)), 0) != 0;
+    };
+    int64_t q1 = 0, q2 = 0, t3 = 0, t4 = 0;
+    int64_t issued = 0, last = -1;
+    while (q2 < n_chunks || t4 < my_tiles) {
+      if (issued == last) __nanosleep(64);  // nothing was ready: back off instead of hogging SMSP 0
+      last = issued;
+      // head GEMM4 of tile t4 once its Z1 operand is in smem
+      if (t4 < t3 && ready(&S.z_full, static_cast<uint32_t>(t4 & 1))) {
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            mma_tf32(tmem + T_D4, kdesc(S.ah, H, kk), kdesc(S.b4h, H, kk), id64, kk > 0);
+            mma_tf32(tmem + T_D4, kdesc(S.ah, H, kk), kdesc(S.b4l, H, kk), id64, 1);
+            mma_tf32(tmem + T_D4, kdesc(S.al, H, kk), kdesc(S.b4h, H, kk), id64, 1);
+          }
+          mma_commit(&S.d4_full);
+          TRACE(4, t4);
+        }
+        __syncwarp();
+        ++t4;
+        ++issued;
+      }
+      // head GEMM3 of tile t3: all its chunks through GEMM2, D3 free (t3 == t4), U in smem
+      if (t3 < my_tiles && t3 == t4 && q2 >= (t3 + 1) * C && ready(&S.u_full, static_cast<uint32_t>(t3 & 1))) {
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            mma_tf32(tmem + T_D3, kdesc(S.ah, H, kk), kdesc(S.b3h, H, kk), id64, kk > 0);
+            mma_tf32(tmem + T_D3, kdesc(S.ah, H, kk), kdesc(S.b3l, H, kk), id64, 1);
+            mma_tf32(tmem + T_D3, kdesc(S.al, H, kk), kdesc(S.b3h, H, kk), id64, 1);
+          }
+          mma_commit(&S.d3_full);
+          TRACE(3, t3);
+        }
+        __syncwarp();
+        ++t3;
+        ++issued;
+      }
+      // GEMM2 of chunk q2: R ready, D2 buffer drained
+      if (q2 < q1) {
+        const int b = static_cast<int>(q2 & 1);
+        const uint32_t ph = static_cast<uint32_t>((q2 >> 1) & 1);
+        if (ready(&S.r_full[b], ph) && ready(&S.d2_empty[b], ph ^ 1)) {
+          tc_fence_after();
+          const uint32_t rh = tmem + T_R + 64 * b, rl = rh + 32, d = tmem + T_D2 + 32 * b;
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              mma_tf32_ts(d, rh + 8 * kk, kdesc(S.b2h, 32, kk), id32, kk > 0);
+              mma_tf32_ts(d, rh + 8 * kk, kdesc(S.b2l, 32, kk), id32, 1);
+              mma_tf32_ts(d, rl + 8 * kk, kdesc(S.b2h, 32, kk), id32, 1);
+            }
+            mma_commit(&S.r_empty[b]);
+            mma_commit(&S.d2_full[b]);
+            TRACE(2, q2);
+          }
+          __syncwarp();
+          ++q2;
+          ++issued;
+        }
+      }
+      // GEMM1 of chunk q1: X slot filled, D1 buffer drained
+      if (q1 < n_chunks) {
+        const int s = static_cast<int>(q1 % XS), b = static_cast<int>(q1 & 1);
+        if (ready(&S.x_full[s], static_cast<uint32_t>((q1 / XS) & 1)) &&
+            ready(&S.d1_empty[b], static_cast<uint32_t>(((q1 >> 1) & 1) ^ 1))) {
+          tc_fence_after();
+          const uint32_t xh = tmem + T_X + 32 * s, xl = xh + 16, d = tmem + T_D1 + 32 * b;
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+              mma_tf32_ts(d, xh + 8 * kk, kdesc(S.b1h, 16, kk), id32, kk > 0);
+              mma_tf32_ts(d, xh + 8 * kk, kdesc(S.b1l, 16, kk), id32, 1);
+              mma_tf32_ts(d, xl + 8 * kk, kdesc(S.b1h, 16, kk), id32, 1);
+            }
+            mma_commit(&S.x_empty[s]);
+            mma_commit(&S.d1_full[b]);
+            TRACE(1, q1);
+          }
+          __syncwarp();
+          ++q1;
+          ++issued;
+        }
+      }
+    }
+  } else if (warp < 4) {
+    // ===================== R: ReLU(D1) -> R (hi, lo) in TMEM; thread = lane = graph ===============
+    const int g = tid;
+    const uint32_t lane = static_cast<uint32_t>((32 * warp) << 16);
+    for (int64_t q = 0; q < n_chunks; ++q) {
+      const int b = static_cast<int>(q & 1);
+      const uint32_t ph = static_cast<uint32_t>((q >> 1) & 1);
+      mbar_wait(&S.d1_full[b], ph);
+      __syncwarp();
+      if (g == 0) TRACE(5, q);
+      tc_fence_after();
+      float v[32];
+      tmem_ld16(tmem + lane + T_D1 + 32 * b, v);
+      tmem_ld16(tmem + lane + T_D1 + 32 * b + 16, v + 16);
+      tmem_wait_ld();
+      if (g == 0) TRACE(13, q);
       tc_fence_before();
-      mbar_arrive(&S.x_full[buf]);
+      warp_arrive(&S.d1_empty[b]);
+      mbar_wait(&S.r_empty[b], ph ^ 1);  // GEMM2 of chunk q-2 has finished reading R[b]
+      __syncwarp();
+      if (g == 0) TRACE(14, q);
+      tc_fence_after();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float hi[16], lo[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float r = relu(v[16 * h + j]);
+          hi[j] = tf32_trunc(r);
+          lo[j] = r - hi[j];
+        }
+        tmem_st16(tmem + lane + T_R + 64 * b + 16 * h, hi);
+        tmem_st16(tmem + lane + T_R + 64 * b + 32 + 16 * h, lo);
+      }
+      if (g == 0) TRACE(15, q);
+      tmem_wait_st();
+      if (g == 0) TRACE(16, q);
+      tc_fence_before();
+      warp_arrive(&S.r_full[b]);
+      if (g == 0) TRACE(6, q);
     }
   } else {
-    // ===================== consumer: MMA issue + epilogues (thread = TMEM lane = row) =====
-    const int t = tid;
-    const uint32_t lane_addr = static_cast<uint32_t>((t & ~31) << 16);
-    const bool issuer = t == 0;
-    const uint32_t id32 = idesc_tf32(128, 32), id64 = idesc_tf32(128, 64);
+    // ===================== readout + head: thread = lane = graph, 16 channels ====================
+    const int quad = warp & 3, eh = (warp - 9) >> 2;
+    const int g = 32 * quad + (tid & 31);
+    const uint32_t lane = static_cast<uint32_t>((32 * quad) << 16);
     const float c_t = static_cast<float>(5.0 / 12.0);
     const float c_ft = static_cast<float>(5.0 / (6.0 * sqrt(6.0)) + 5.0 / 12.0);
     const float c_r = static_cast<float>(1.0 / sqrt(18.0 * (T.n_pairs + 1)));
-    uint32_t ph_g1 = 0, ph_g2 = 0, ph_h = 0;
-
-    auto issue_g1 = [&](int64_t q) {
-      const int buf = static_cast<int>(q & 1);
-      mbar_wait(&S.x_full[buf], static_cast<uint32_t>((q >> 1) & 1));
+    const float b3 = params[dims.off_hb[2]];
+    const bool tr = g == 0 && eh == 0;
+    float2 tot[8], rs[8];
+    float mx[16];
+    int kc = 0;       // chunk index within the current tile (no 64-bit % / on this path)
+    int64_t ti = 0;   // local tile index
+    for (int64_t q = 0; q < n_chunks; ++q) {
+      const int b = static_cast<int>(q & 1);
+      if (kc == 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) tot[j] = rs[j] = make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) mx[j] = 0.0f;  // max_k ReLU(s_k) = max(0, max_k s_k)
+      }
+      mbar_wait(&S.d2_full[b], static_cast<uint32_t>((q >> 1) & 1));
+      __syncwarp();
+      if (tr) TRACE(7, q);
       tc_fence_after();
-      const uint32_t xh = tmem + T_X + 32 * buf, xl = xh + 16;
-#pragma unroll
-      for (int kk = 0; kk < 2; ++kk) {
-        mma_tf32_ts(tmem + T_D1, xh + 8 * kk, kdesc(S.b1h, 16, kk), id32, kk > 0);
-        mma_tf32_ts(tmem + T_D1, xh + 8 * kk, kdesc(S.b1l, 16, kk), id32, 1);
-        mma_tf32_ts(tmem + T_D1, xl + 8 * kk, kdesc(S.b1h, 16, kk), id32, 1);
-      }
-      mma_commit(&S.x_empty[buf]);
-      mma_commit(&S.bar_g1);
-    };
-
-    if (issuer && n_chunks > 0) issue_g1(0);
-    int64_t q = 0;
-    for (int64_t ti = 0; ti < my_tiles; ++ti) {
-      const int64_t tile = blockIdx.x + ti * gridDim.x;
-      for (int c = 0; c < CPT; ++c, ++q) {
-        // ---- epilogue 1: R = ReLU(D1) -> TMEM (hi, lo)
-        mbar_wait(&S.bar_g1, ph_g1);
-        ph_g1 ^= 1;
-        tc_fence_after();
-        {
-          float v[32], lo[32];
-          tmem_ld32(tmem + lane_addr + T_D1, v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float r = relu(v[j]);
-            v[j] = tf32_hi(r);
-            lo[j] = r - v[j];
-          }
-          tmem_st32(tmem + lane_addr + T_RH, v);
-          tmem_st32(tmem + lane_addr + T_RL, lo);
-          tmem_wait_st();
-        }
+      {
+        float v[16];
+        tmem_ld16(tmem + lane + T_D2 + 32 * b + 16 * eh, v);
+        tmem_wait_ld();
         tc_fence_before();
-        named_sync(1, 128);
-        tc_fence_after();
-        if (issuer) {
+        warp_arrive(&S.d2_empty[b]);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            mma_tf32_ts(tmem + T_D2, tmem + T_RH + 8 * kk, kdesc(S.b2h, 32, kk), id32, kk > 0);
-            mma_tf32_ts(tmem + T_D2, tmem + T_RH + 8 * kk, kdesc(S.b2l, 32, kk), id32, 1);
-            mma_tf32_ts(tmem + T_D2, tmem + T_RL + 8 * kk, kdesc(S.b2h, 32, kk), id32, 1);
-          }
-          mma_commit(&S.bar_g2);
-          if (q + 1 < n_chunks) issue_g1(q + 1);
-        }
-        // ---- epilogue 2: D2 rows -> smem, per-graph readout -> U
-        mbar_wait(&S.bar_g2, ph_g2);
-        ph_g2 ^= 1;
-        tc_fence_after();
-        {
-          float v[32];
-          tmem_ld32(tmem + lane_addr + T_D2, v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) S.s[t * SS + j] = v[j];
-        }
-        tc_fence_before();
-        named_sync(1, 128);
-        for (int item = t; item < GPC * 32; item += 128) {
-          const int g = item >> 5, chn = item & 31;
-          const float* col = S.s + (g * 12) * SS + chn;
-          float tot = 0.f, rsum = 0.f, rmax = 0.f;
-#pragma unroll
-          for (int k = 0; k < 12; ++k) {
-            const float sv = col[k * SS];
-            tot += sv;
-            rsum += relu(sv);
-            rmax = fmaxf(rmax, sv);
-          }
-          const float root = relu(c_r * tot);
-          const float us = S.agg[chn] * (root + c_ft * rsum);
-          const float um = fmaxf(root, c_t * rmax);
-          const int ur = c * GPC + g;
-          const int o1 = kmajor_offset_lbo(ur, chn, H, ULBO) >> 2;
-          const int o2 = kmajor_offset_lbo(ur, 32 + chn, H, ULBO) >> 2;
-          const float h1 = tf32_hi(us), h2 = tf32_hi(um);
-          S.uh[o1] = h1;
-          S.ul[o1] = us - h1;
-          S.uh[o2] = h2;
-          S.ul[o2] = um - h2;
-          if (u_out) {
-            const int64_t gi = tile * GT + ur;
-            if (gi < B) {
-              u_out[gi * 64 + chn] = us;
-              u_out[gi * 64 + 32 + chn] = um;
-            }
-          }
+        for (int i = 0; i < 8; ++i) {
+          const float2 s2 = make_float2(v[2 * i], v[2 * i + 1]);
+          tot[i] = fadd2(tot[i], s2);
+          rs[i] = fadd2(rs[i], make_float2(relu(s2.x), relu(s2.y)));
+          mx[2 * i] = fmaxf(mx[2 * i], s2.x);
+          mx[2 * i + 1] = fmaxf(mx[2 * i + 1], s2.y);
         }
       }
-      // ---- head: GEMM3 (U from smem) -> ReLU(+b0) -> Z1 (TMEM) -> GEMM4 -> ReLU(+b1) . w3 + b3
+      if (tr) TRACE(8, q);
+      if (++kc < C) continue;
+      kc = 0;
+      // ---- head of tile ti ------------------------------------------------------------
+      const uint32_t ph = static_cast<uint32_t>(ti & 1);
+      const int64_t gi = (blockIdx.x + ti * gridDim.x) * GT + g;
+      float4* urow = u_out && gi < B ? reinterpret_cast<float4*>(u_out + gi * H) : nullptr;
+#pragma unroll
+      for (int jq = 0; jq < 4; ++jq) {  // channels 16 eh + 4 jq .. +3
+        float us[4], um[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int jl = 4 * jq + i, j = 16 * eh + jl;
+          const float tj = (jl & 1) ? tot[jl >> 1].y : tot[jl >> 1].x;
+          const float rj = (jl & 1) ? rs[jl >> 1].y : rs[jl >> 1].x;
+          const float root = relu(c_r * tj);
+          us[i] = S.agg[j] * (root + c_ft * rj);
+          um[i] = fmaxf(root, c_t * mx[jl]);
+        }
+        const float4 s4 = make_float4(us[0], us[1], us[2], us[3]);
+        const float4 m4 = make_float4(um[0], um[1], um[2], um[3]);
+        store_head_quad(S.ah, S.al, g, 4 * eh + jq, s4);
+        store_head_quad(S.ah, S.al, g, 8 + 4 * eh + jq, m4);
+        if (urow) {
+          urow[4 * eh + jq] = s4;
+          urow[8 + 4 * eh + jq] = m4;
+        }
+      }
+      fence_async_smem();
+      warp_arrive(&S.u_full);
+      if (tr) TRACE(9, ti);
+      mbar_wait(&S.d3_full, ph);
+      __syncwarp();
+      if (tr) TRACE(10, ti);
+      tc_fence_after();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // D3 columns 32 eh + 16 h ..
+        float z[16];
+        tmem_ld16(tmem + lane + T_D3 + 32 * eh + 16 * h, z);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int c0 = 32 * eh + 16 * h + 4 * i;
+          const float4 bb = *reinterpret_cast<const float4*>(S.bias0 + c0);
+          store_head_quad(S.ah, S.al, g, c0 >> 2,
+                          make_float4(relu(z[4 * i] + bb.x), relu(z[4 * i + 1] + bb.y), relu(z[4 * i + 2] + bb.z),
+                                      relu(z[4 * i + 3] + bb.w)));
+        }
+      }
       fence_async_smem();
       tc_fence_before();
-      named_sync(1, 128);
+      warp_arrive(&S.z_full);
+      mbar_wait(&S.d4_full, ph);
+      __syncwarp();
+      if (tr) TRACE(11, ti);
       tc_fence_after();
-      if (issuer) {
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          mma_tf32(tmem + T_D3, kdesc_lbo(S.uh, H, kk, ULBO), kdesc(S.b3h, H, kk), id64, kk > 0);
-          mma_tf32(tmem + T_D3, kdesc_lbo(S.uh, H, kk, ULBO), kdesc(S.b3l, H, kk), id64, 1);
-          mma_tf32(tmem + T_D3, kdesc_lbo(S.ul, H, kk, ULBO), kdesc(S.b3h, H, kk), id64, 1);
-        }
-        mma_commit(&S.bar_h);
-      }
-      mbar_wait(&S.bar_h, ph_h);
-      ph_h ^= 1;
-      tc_fence_after();
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        float v[32], lo[32];
-        tmem_ld32(tmem + lane_addr + T_D3 + 32 * half, v);
-        tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float z = relu(v[j] + S.bias0[32 * half + j]);
-          v[j] = tf32_hi(z);
-          lo[j] = z - v[j];
-        }
-        tmem_st32(tmem + lane_addr + T_ZH + 32 * half, v);
-        tmem_st32(tmem + lane_addr + T_ZL + 32 * half, lo);
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      named_sync(1, 128);
-      tc_fence_after();
-      if (issuer) {
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          mma_tf32_ts(tmem + T_D4, tmem + T_ZH + 8 * kk, kdesc(S.b4h, H, kk), id64, kk > 0);
-          mma_tf32_ts(tmem + T_D4, tmem + T_ZH + 8 * kk, kdesc(S.b4l, H, kk), id64, 1);
-          mma_tf32_ts(tmem + T_D4, tmem + T_ZL + 8 * kk, kdesc(S.b4h, H, kk), id64, 1);
-        }
-        mma_commit(&S.bar_h);
-      }
-      mbar_wait(&S.bar_h, ph_h);
-      ph_h ^= 1;
-      tc_fence_after();
-      float acc = params[dims.off_hb[2]];
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
+      float acc = 0.0f;
+      {
         float v[32];
-        tmem_ld32(tmem + lane_addr + T_D4 + 32 * half, v);
+        tmem_ld16(tmem + lane + T_D4 + 32 * eh, v);
+        tmem_ld16(tmem + lane + T_D4 + 32 * eh + 16, v + 16);
         tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc = fmaf(relu(v[j] + S.bias1[32 * half + j]), S.w3[32 * half + j], acc);
+        for (int j = 0; j < 32; ++j) acc = fmaf(relu(v[j] + S.bias1[32 * eh + j]), S.w3[32 * eh + j], acc);
       }
-      const int64_t gi = tile * GT + t;
-      if (t < GT && gi < B) {
+      tc_fence_before();
+      // combine the two halves' partial dots: half 1 hands its value over through smem
+      if (eh == 1) S.part[g] = acc;
+      named_sync(1 + quad, 64);
+      if (eh == 0 && gi < B) {
         const int64_t v = idx ? idx[gi] : idx_base + gi;
         const bool ok = v >= 0 && static_cast<uint64_t>(v) < size;
-        z_out[gi] = ok ? acc : __int_as_float(0x7fc00000);
+        z_out[gi] = ok ? (b3 + acc) + S.part[g] : __int_as_float(0x7fc00000);
       }
-      tc_fence_before();
-      named_sync(1, 128);  // all D3/D4 reads done before the next tile's head overwrites them
-      tc_fence_after();
+      named_sync(1 + quad, 64);  // S.part consumed before the next tile overwrites it
+      if (tr) TRACE(12, ti);
+      ++ti;
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, 512);
+  if (warp == 8) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
 }
 
 }  // namespace tcs

@@ -46,6 +46,11 @@ __device__ __forceinline__ float tf32_hi(float v) {
   return __uint_as_float(r);
 }
 
+// Truncating split (one LOP3): hi keeps the 10 explicit tf32 mantissa bits, and
+// lo = v - hi is exact in fp32, so hi + lo == v; the tensor core then sees lo to
+// 11 significant bits (split error <= 2^-21 |v|, fp32-level).  For the hot loops.
+__device__ __forceinline__ float tf32_trunc(float v) { return __uint_as_float(__float_as_uint(v) & 0xffffe000u); }
+
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, int accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -78,21 +83,54 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+// Blocking wait with a suspend-time hint: a thread whose phase is not complete is
+// parked by the hardware (woken on completion) instead of spinning through issue
+// slots its SMSP neighbours need.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}\n"
-      :
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}\n"
+      : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(phase)
       : "memory");
+  // not complete yet: back off between probes so a waiting warp does not take the
+  // issue slots its SMSP neighbours on the critical path need
+  while (!ok) {
+    __nanosleep(20);
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+
+// Non-blocking probe: true once the phase with parity `phase` has completed.
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
 }
 
 // generic-proxy smem writes -> visible to the tensor core (async proxy)
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+#ifndef KT_DBG_NO_FENCE
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+#else
+__device__ __forceinline__ void tc_fence_before() { asm volatile("" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("" ::: "memory"); }
+#endif
 
 // Whole warp: allocate ncols (power of 2 >= 32) TMEM columns; base address -> *slot.
 __device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t ncols) {
@@ -122,6 +160,19 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
       : "r"(taddr));
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Warp-collective load of 16 consecutive columns of this thread's TMEM lane.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 // Warp-collective store of 32 consecutive columns of this thread's TMEM lane.
@@ -178,9 +229,25 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" : : "r"(smem_u32(bar)) : "memory");
 }
 
+// One arrive per warp (the barrier counts warps, not threads): 128 per-thread
+// arrives on one mbarrier serialise in the shared-memory atomic unit and stall
+// the tensor core's shared-memory operand reads behind them.
+__device__ __forceinline__ void warp_arrive(uint64_t* bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
+
 // Named barrier over `count` threads (ids 1..15; 0 is __syncthreads).
 __device__ __forceinline__ void named_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" : : "r"(id), "r"(count) : "memory");
+}
+
+// One lane of a converged warp (elect.sync): the single-thread tcgen05.mma / commit
+// issue idiom that keeps the warp's descriptors in uniform registers.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p = 0;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(p));
+  return p != 0;
 }
 
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }

@@ -12,7 +12,7 @@ echo "bench rc=$?" >> gpurun_out/bench.err
 if [ "${SKIP_NCU:-0}" != "1" ]; then
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-extras > gpurun_out/ncu_launches.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:score_star -s 3 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:${NCU_K:-score_tc} -s 3 -c 1 \
   -o gpurun_out/prof_score -f python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-extras > gpurun_out/ncu_full.log 2>&1
 fi
 echo done
