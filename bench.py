@@ -306,7 +306,70 @@ def bench_fine_tune(m, corpus, reps=50):
             "config": "C4: fine_tune_embedded(u 64x64, y, alpha 0.01, 8 steps), one kernel"}
 
 
-# --- CPU arms -------------------------------------------------------------------------
+def bench_aggregate(m, reps=10):
+    """The streaming aggregation kernels (kt_gcn_layer x2, kt_readout) on 1M super-graph
+    conv2d candidates, HBM GB/s against MEASURED_PEAKS.json.  Algorithmic bytes per
+    graph (N = 25 rows): layer 1 reads the fp64 raw features (2400 B) and writes H1
+    (3200 B); layer 2 reads H1 and writes H2 (3200 + 3200 B); the readout reads H2 and
+    writes u (3200 + 256 B).  Every buffer is larger than the 126 MB L2."""
+    import torch
+
+    from paper_2102_04199_b200 import _lib
+    from paper_2102_04199_b200 import graphs as pg
+    from paper_2102_04199_b200 import kernels as pk
+    from paper_2102_04199_b200 import model as pm
+    from paper_2102_04199_b200.util import rng_from
+
+    dev = pm.flat_params(m).device
+    b, n = BATCH, 25
+    spec = pk.KernelSpec(*SPEC_ARGS)
+    space = pk.build_knob_space(spec)
+    lay = pg.batch_layout(spec, pg.build_super_template(pk.OP_TYPES))
+    idx = torch.from_numpy(rng_from("bench-aggregate").integers(0, space.size, b)).to(dev)
+    x = pg.encode_batch(spec, space, idx, lay).reshape(b * n, -1)
+    pats = pm.adjacency_patterns([lay.adjacency], [lay.feature_mask], dev)
+    mean, std = pm._norm_tensors(m, dev)
+    lib = _lib.load()
+    w1, w2 = (w.contiguous() for w in m.gcn.layers)
+    h1 = torch.empty((b * n, 32), dtype=torch.float32, device=dev)
+    h2 = torch.empty_like(h1)
+    u = torch.empty((b, 64), dtype=torch.float32, device=dev)
+    aw = m.agg.sum_weights.contiguous()
+    p = _lib.ptr
+    st = _lib.stream_handle()
+
+    def layer(src, f64, w, dst):
+        _lib.check(lib.kt_gcn_layer(p(src), f64, p(mean), p(std), p(w), int(w.shape[0]), int(w.shape[1]), 1, b, n,
+                                    None, None, pats.n_pat, p(pats.pat_n), p(pats.rp), p(pats.col), p(pats.val),
+                                    p(pats.mask), pats.nnz, pats.max_nodes, p(dst), st), "gcn_layer")
+
+    kernels = {
+        "gcn_layer1 (fp64 raw in, norm + A.X.W1 + ReLU)": (lambda: layer(x, 1, w1, h1), n * 12 * 8 + n * 32 * 4),
+        "gcn_layer2 (A.H1.W2 + ReLU)": (lambda: layer(h1, 0, w2, h2), n * 32 * 4 * 2),
+        "readout (sum + max, warp shuffles)": (lambda: _lib.check(lib.kt_readout(p(h2), 32, b, n, None, p(aw), p(u),
+                                                                                 st), "readout"), n * 32 * 4 + 64 * 4),
+    }
+    hbm = hbm_peak()
+    out = {}
+    for name, (fn, bytes_per_graph) in kernels.items():
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        gbs = bytes_per_graph * b / (ms / 1e3) / 1e9
+        out[name] = {"ms": ms, "achieved_gbs": gbs, "peak_gbs": hbm, "frac": gbs / hbm,
+                     "bytes_per_graph": bytes_per_graph, "graphs_per_s": b / (ms / 1e3)}
+    return {"metric": "streaming aggregation kernels, HBM GB/s (1M super-graph conv2d candidates)",
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs", "kernels": out}
+
+
+# --- CPU arms -------------------------------------------------------------------------# --- CPU arms -------------------------------------------------------------------------
 
 
 def cpu_sweep(m_params, n, seed_rank=0):
@@ -524,6 +587,7 @@ def run_ours(args):
             line["pretrain"] = bench_pretrain_step(m, [s for s in corpus if s.kernel_class.split("/")[0] in
                                                        ("conv2d", "winograd", "depthwise")], 50, 5)
             line["fine_tune"] = bench_fine_tune(m, corpus)
+            line["aggregation"] = bench_aggregate(m)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:

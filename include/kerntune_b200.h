@@ -151,6 +151,28 @@ int kt_embed_csr(const kt_dims* dims, const float* params, const double* fmean, 
                  int32_t nodes_per_graph, int32_t max_nodes,
                  const int32_t* row_ptr, const int32_t* col, const float* val,
                  const int64_t* graph_idx, int64_t B, float* u_out, float* z_out, void* stream);
+/* ---- streaming aggregation (HBM-bound layer-by-layer form of embed_batch) ------------------ */
+/* One GCN layer, out = ReLU(A_hat . in . W) per graph (gcn_forward model.py:127-133,
+ * the einsum of embed_batch model.py:189-191), rows of all graphs contiguous.
+ * in: (rows, d_in) fp32, or (in_f64 != 0) the raw fp64 features, z-normalised on the
+ *   fly with fmean / fstd on nodes whose pattern mask is 1 and zero elsewhere
+ *   (model.py:108-112).  W: (d_in, d_out) row-major.  out: (rows, d_out) fp32.
+ * Rows: nodes_per_graph > 0 -> graph g owns rows [g n, (g+1) n) (node_ptr ignored);
+ *   else [node_ptr[g], node_ptr[g+1]).
+ * Adjacency: n_pat (<= 8) local CSR patterns (pat_n nodes each; pat_rp (n+1) per
+ *   pattern, concatenated; pat_col / pat_val concatenated, pat_nnz in total <= 1024;
+ *   pat_mask one byte per pattern node); graph g uses pattern pat_id ? pat_id[g] : 0.
+ * Bulk (1D TMA) copies move each tile in / out when rows are 16-byte multiples. */
+int kt_gcn_layer(const void* in, int32_t in_f64, const double* fmean, const double* fstd,
+                 const float* W, int32_t d_in, int32_t d_out, int32_t relu, int64_t B,
+                 int32_t nodes_per_graph, const int64_t* node_ptr, const int32_t* pat_id,
+                 int32_t n_pat, const int32_t* pat_n, const int32_t* pat_rp, const int32_t* pat_col,
+                 const float* pat_val, const uint8_t* pat_mask, int32_t pat_nnz, int32_t max_nodes,
+                 float* out, void* stream);
+/* aggregate (model.py:136-141) per graph: u[g] = [sum_n agg_w * h_n, max_n h_n],
+ * h (rows, d) fp32 with graph rows as in kt_gcn_layer; u (B, 2 d). */
+int kt_readout(const float* h, int32_t d, int64_t B, int32_t nodes_per_graph, const int64_t* node_ptr,
+               const float* agg_w, float* u_out, void* stream);
 /* head_forward_batch (model.py:197-203): u (B, head[0]) -> z (B). */
 int kt_head_forward(const kt_dims* dims, const float* params, const float* u, int64_t B,
                     float* z_out, void* stream);

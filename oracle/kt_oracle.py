@@ -205,6 +205,19 @@ def embed_batch(p, feats, mask, adj) -> np.ndarray:
     return np.concatenate([(h * p["agg"]).sum(axis=1), h.max(axis=1)], axis=1)
 
 
+def gcn_forward_batch(p, feats, mask, adj) -> np.ndarray:
+    """gcn_forward (model.py:127-133) over a batch sharing one adjacency: H_L (B, N, d_L)."""
+    h = normalize(p, feats, mask)
+    for w in p["gcn"]:
+        h = np.maximum(np.einsum("nm,bmf,fd->bnd", adj, h, w, optimize=True), 0.0)
+    return h
+
+
+def aggregate_batch(h, agg) -> np.ndarray:
+    """aggregate (model.py:136-141) per graph: [sum_n a * h_n, max_n h_n]."""
+    return np.concatenate([(h * agg).sum(axis=1), h.max(axis=1)], axis=1)
+
+
 def head_forward_batch(u, hw, hb) -> np.ndarray:
     """model.py:197-203."""
     a = u

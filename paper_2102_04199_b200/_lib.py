@@ -89,6 +89,9 @@ _SIGS = {
     "kt_embed_csr": (ctypes.c_int, [ctypes.POINTER(Dims), vp, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp,
                                     i64, vp, vp, vp]),
     "kt_head_forward": (ctypes.c_int, [ctypes.POINTER(Dims), vp, vp, i64, vp, vp]),
+    "kt_gcn_layer": (ctypes.c_int, [vp, i32, vp, vp, vp, i32, i32, i32, i64, i32, vp, vp, i32, vp, vp, vp, vp, vp,
+                                    i32, i32, vp, vp]),
+    "kt_readout": (ctypes.c_int, [vp, i32, i64, i32, vp, vp, vp, vp]),
     "kt_grad_workspace_bytes": (i64, [ctypes.POINTER(Dims), i64]),
     "kt_grad": (ctypes.c_int, [ctypes.POINTER(Dims), vp, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, i64,
                                i32, vp, vp, f32, vp, vp, i64, vp]),

@@ -1,0 +1,719 @@
+// Streaming aggregation kernels: the layer-by-layer form of embed_batch
+// (model.py:185-194) for large batches, HBM-bound by design.
+//
+//   kt_gcn_layer  H_out = ReLU(A_hat . H_in . W) for every graph of a batch
+//                 (gcn_forward model.py:127-133; the einsum of embed_batch
+//                 model.py:189-191).  Segmented CSR: graphs own contiguous row
+//                 ranges; the adjacency of a graph is one of a few patterns
+//                 (batch_layout yields one per op type), staged in shared memory.
+//                 Layer-1 input may be the raw fp64 features, z-normalised on the
+//                 fly (model.py:108-112: masked rows only, others exactly 0).
+//   kt_readout    u = [sum_n a * h_n, max_n h_n] per graph (aggregate
+//                 model.py:136-141) as warp-shuffle segmented reductions.
+//
+// Data movement (kt_gcn_layer): a persistent CTA walks tiles of G graphs whose
+// rows are one contiguous byte range, so a tile moves in ONE bulk copy each way
+// (cp.async.bulk, the 1D TMA: global -> smem completing on an mbarrier, smem ->
+// global as a bulk group), double-buffered so the next tile's load overlaps this
+// tile's math.  Math per tile: neighbour aggregation A_hat . H_in from the staged
+// rows into a transposed buffer (float4 channel quads), then the dense transform
+// on the FP32 pipe as 4-row x 8-column FFMA2 register tiles, ReLU, into the
+// staged output rows.  Algorithmic bytes per graph: n d_in sizeof(in) + n d_out 4.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+
+#include "kt_common.cuh"
+#include "kt_tc.cuh"
+
+namespace kt {
+namespace agg {
+
+constexpr int NT = 256;
+constexpr int MAXPAT = 8;       // adjacency patterns per batch
+constexpr int MAXPNNZ = 1024;   // nnz over all patterns
+constexpr int NST = 4;          // input ring stages (bulk loads in flight per CTA)
+
+struct LayerArgs {
+  const void* in;
+  int in_f64;
+  float* out;
+  const float* W;
+  const double* fmean;
+  const double* fstd;
+  int d_in, d_out, relu;
+  int64_t B;
+  int n_uniform;             // > 0: every graph has n_uniform rows (node_ptr NULL)
+  const int64_t* node_ptr;   // segmented row ranges (B + 1)
+  const int32_t* pat_id;     // per graph (NULL: pattern 0)
+  int n_pat;
+  const int32_t* pat_n;      // nodes per pattern
+  const int32_t* pat_rp;     // concatenated local row_ptr, (n_p + 1) per pattern
+  const int32_t* pat_col;    // concatenated local column ids
+  const float* pat_val;      // fp32 of the fp64 normalised adjacency
+  const uint8_t* pat_mask;   // concatenated per-pattern node masks (fp64 input only)
+  int G;                     // graphs per tile
+  int R;                     // max rows per tile (buffer capacity)
+  int bulk;                  // rows are 16-byte multiples: bulk copies
+};
+
+struct PatSmem {
+  int n[MAXPAT], rp_off[MAXPAT], nz_off[MAXPAT], mask_off[MAXPAT];
+};
+
+__device__ __forceinline__ uint32_t s32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_par(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n\tW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra W_%=;\n\t}\n" ::"r"(s32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1D TMA: global -> shared, completion counted on the mbarrier (bytes % 16 == 0)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   s32(dst)),
+               "l"(src), "r"(bytes), "r"(s32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(s32(src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ int64_t tile_row0(const LayerArgs& a, int64_t g0) {
+  return a.node_ptr ? a.node_ptr[g0] : g0 * a.n_uniform;
+}
+
+__device__ __forceinline__ float4 ldg_stream(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
+constexpr int PF = 8;  // prefetched float4 per lane: 4 KB of the next graph per warp
+constexpr int WPC = NT / 32;
+
+// One warp per graph (grid-stride), no block-wide barriers: the warp prefetches
+// the next graph's rows into registers (coalesced 16-byte loads, 4 KB in flight
+// per warp) while it aggregates and transforms the current one out of its own
+// shared-memory slab, and writes the output rows straight to HBM (each store
+// instruction covers two adjacent 128-byte row segments).
+template <int DIN_T, int DOUT_T>
+__global__ void __launch_bounds__(NT, 2) gcn_layer_kernel(LayerArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ PatSmem P;
+  __shared__ double s_mean[KT_MAX_DIM], s_rstd[KT_MAX_DIM];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int din = DIN_T ? DIN_T : a.d_in, dout = DOUT_T ? DOUT_T : a.d_out;
+  const int dinp = (din + 3) & ~3;  // slab row stride (float4 aligned)
+  const int maxn = a.R;             // rows of the largest graph
+  // ---- carve: W | pattern CSR | per-warp slabs (X rows, aggregated rows) ----------------------
+  float* sW = reinterpret_cast<float*>(smem);
+  int* s_rp = reinterpret_cast<int*>(sW + ((din * dout + 3) & ~3));
+  const int rp_cap = a.n_pat * (KT_MAX_NODES + 1);
+  int* s_col = s_rp + ((rp_cap + 3) & ~3);
+  float* s_val = reinterpret_cast<float*>(s_col + MAXPNNZ);
+  uint8_t* s_mask = reinterpret_cast<uint8_t*>(s_val + MAXPNNZ);
+  float* slab0 = reinterpret_cast<float*>(s_mask + ((a.n_pat * KT_MAX_NODES + 15) & ~15));
+  const int slab = 2 * maxn * dinp;
+  float* X = slab0 + warp * slab;
+  float* AG = X + maxn * dinp;
+
+  for (int i = tid; i < din * dout; i += NT) sW[i] = a.W[i];
+  if (tid == 0) {
+    int rp = 0, nz = 0, mk = 0;
+    for (int p = 0; p < a.n_pat; ++p) {
+      P.n[p] = a.pat_n[p];
+      P.rp_off[p] = rp;
+      P.nz_off[p] = nz;
+      P.mask_off[p] = mk;
+      nz += a.pat_rp[rp + P.n[p]];
+      rp += P.n[p] + 1;
+      mk += P.n[p];
+    }
+  }
+  if (a.in_f64)
+    for (int c = tid; c < din; c += NT) {
+      s_mean[c] = a.fmean[c];
+      s_rstd[c] = 1.0 / a.fstd[c];
+    }
+  __syncthreads();
+  int tot_rp = 0, tot_nz = 0, tot_mask = 0;
+  for (int p = 0; p < a.n_pat; ++p) {
+    tot_rp += P.n[p] + 1;
+    tot_mask += P.n[p];
+    tot_nz += a.pat_rp[P.rp_off[p] + P.n[p]];
+  }
+  for (int i = tid; i < tot_rp; i += NT) s_rp[i] = a.pat_rp[i];
+  for (int i = tid; i < tot_nz; i += NT) {
+    s_col[i] = a.pat_col[i];
+    s_val[i] = a.pat_val[i];
+  }
+  const bool masked = a.in_f64 && a.pat_mask;
+  if (masked)
+    for (int i = tid; i < tot_mask; i += NT) s_mask[i] = a.pat_mask[i];
+  __syncthreads();
+
+  const int esz = a.in_f64 ? 8 : 4;
+  const bool vec_in = ((din * esz) & 15) == 0;
+  // fast transform: 16 lanes x 2 output channels, half-warp h takes rows h, h+2, ...
+  constexpr bool kFast = DOUT_T == 32 && DIN_T > 0 && (DIN_T % 4) == 0;
+  float2 wreg[kFast ? DIN_T : 1];
+  if constexpr (kFast) {
+    const int c2 = 2 * (lane & 15);
+#pragma unroll
+    for (int k = 0; k < DIN_T; ++k) wreg[k] = make_float2(sW[k * 32 + c2], sW[k * 32 + c2 + 1]);
+  }
+
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * WPC;
+  int64_t g = static_cast<int64_t>(blockIdx.x) * WPC + warp;
+  float4 pf[PF];
+  int64_t pr0 = 0;
+  int pn = 0;
+  auto prefetch = [&](int64_t gg) {
+    pr0 = tile_row0(a, gg);
+    pn = static_cast<int>(tile_row0(a, gg + 1) - pr0);
+    if (vec_in) {
+      const float4* src = reinterpret_cast<const float4*>(static_cast<const unsigned char*>(a.in) + pr0 * din * esz);
+      const int nq = pn * din * esz / 16;
+#pragma unroll
+      for (int i = 0; i < PF; ++i)
+        if (i * 32 + lane < nq) pf[i] = ldg_stream(src + i * 32 + lane);
+    }
+  };
+  if (g < a.B) prefetch(g);
+  for (; g < a.B; g += nw) {
+    const int64_t r0 = pr0;
+    const int n = pn;
+    const int p = a.pat_id ? a.pat_id[g] : 0;
+    const int moff = P.mask_off[p];
+    // ---- 1. current graph -> X slab (fp32; fp64 rows z-normalised, model.py:108-112) ----------
+    auto put64 = [&](int e, double v) {
+      const int r = e / din, c = e - r * din;
+      const bool on = !masked || s_mask[moff + r];
+      X[r * dinp + c] = on ? static_cast<float>((v - s_mean[c]) * s_rstd[c]) : 0.0f;
+    };
+    if (vec_in) {
+      const int nq = n * din * esz / 16;
+      const float4* src = reinterpret_cast<const float4*>(static_cast<const unsigned char*>(a.in) + r0 * din * esz);
+#pragma unroll
+      for (int i = 0; i < PF + 1; ++i) {
+        // the first PF float4 per lane come from the prefetch registers, any rest from HBM
+        for (int q = i * 32 + lane; q < (i < PF ? (i + 1) * 32 : nq) && q < nq; q += 32) {
+          const float4 v = i < PF ? pf[i < PF ? i : 0] : ldg_stream(src + q);
+          if (a.in_f64) {
+            const double2 d = *reinterpret_cast<const double2*>(&v);
+            put64(2 * q, d.x);
+            put64(2 * q + 1, d.y);
+          } else if (din == dinp) {
+            *reinterpret_cast<float4*>(X + 4 * q) = v;
+          } else {
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int e = 4 * q + t, r = e / din;
+              X[r * dinp + (e - r * din)] = vv[t];
+            }
+          }
+        }
+      }
+    } else {
+      for (int e = lane; e < n * din; e += 32) {
+        if (a.in_f64) {
+          put64(e, reinterpret_cast<const double*>(a.in)[r0 * din + e]);
+        } else {
+          const int r = e / din;
+          X[r * dinp + (e - r * din)] = reinterpret_cast<const float*>(a.in)[r0 * din + e];
+        }
+      }
+    }
+    // ---- 2. start the next graph's loads (registers) before this graph's math ------------------
+    if (g + nw < a.B) prefetch(g + nw);
+    __syncwarp();
+    // ---- 3. aggregation AG = A_hat X (float4 channel quads) ------------------------------------
+    {
+      const int* rp = s_rp + P.rp_off[p];
+      const int nz0 = P.nz_off[p];
+      const int nq = dinp >> 2;
+      for (int item = lane; item < n * nq; item += 32) {
+        const int r = item / nq, c0 = 4 * (item - r * nq);
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int j = rp[r]; j < rp[r + 1]; ++j) {
+          const float v = s_val[nz0 + j];
+          const float4 x = *reinterpret_cast<const float4*>(X + s_col[nz0 + j] * dinp + c0);
+          acc.x = fmaf(v, x.x, acc.x);
+          acc.y = fmaf(v, x.y, acc.y);
+          acc.z = fmaf(v, x.z, acc.z);
+          acc.w = fmaf(v, x.w, acc.w);
+        }
+        *reinterpret_cast<float4*>(AG + r * dinp + c0) = acc;
+      }
+    }
+    __syncwarp();
+    // ---- 4. transform + ReLU, rows straight to HBM --------------------------------------------
+    float* out = a.out + r0 * dout;
+    if constexpr (kFast) {
+      // four rows per pass (r, r+2, r+4, r+6): independent FFMA2 chains for ILP
+      const int c2 = 2 * (lane & 15), h = lane >> 4;
+      for (int rb = h; rb < n; rb += 8) {
+        float2 acc[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k4 = 0; k4 < DIN_T / 4; ++k4) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int r = rb + 2 * i < n ? rb + 2 * i : rb;  // clamp: recompute a valid row, store skipped
+            const float4 v = reinterpret_cast<const float4*>(AG + r * dinp)[k4];
+            acc[i] = ffma2s(v.x, wreg[4 * k4 + 0], acc[i]);
+            acc[i] = ffma2s(v.y, wreg[4 * k4 + 1], acc[i]);
+            acc[i] = ffma2s(v.z, wreg[4 * k4 + 2], acc[i]);
+            acc[i] = ffma2s(v.w, wreg[4 * k4 + 3], acc[i]);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = rb + 2 * i;
+          if (r < n) {
+            float2 o = acc[i];
+            if (a.relu) o = make_float2(fmaxf(o.x, 0.f), fmaxf(o.y, 0.f));
+            __stcs(reinterpret_cast<float2*>(out + r * 32 + c2), o);
+          }
+        }
+      }
+    } else {
+      for (int e = lane; e < n * dout; e += 32) {
+        const int r = e / dout, c = e - r * dout;
+        float acc = 0.f;
+        for (int k = 0; k < din; ++k) acc = fmaf(AG[r * dinp + k], sW[k * dout + c], acc);
+        out[e] = a.relu ? fmaxf(acc, 0.f) : acc;
+      }
+    }
+    __syncwarp();  // slabs consumed before the next graph overwrites them
+  }
+}
+
+// ---- readout: one warp per graph ------------------------------------------------------------
+__global__ void __launch_bounds__(256) readout_kernel(const float* __restrict__ h, int d, int64_t B, int n_uniform,
+                                                      const int64_t* __restrict__ node_ptr,
+                                                      const float* __restrict__ aw, float* __restrict__ u) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int dq = d >> 2;
+  const bool vec = (d & 3) == 0 && dq <= 32 && (32 % dq) == 0;
+  for (int64_t g = warp0; g < B; g += nwarps) {
+    const int64_t r0 = node_ptr ? node_ptr[g] : g * n_uniform;
+    const int n = static_cast<int>((node_ptr ? node_ptr[g + 1] : r0 + n_uniform) - r0);
+    if (vec) {
+      // lane owns channel quad (lane % dq) of rows lane / dq, + 32 / dq, ...
+      const int cq = lane % dq, rstep = 32 / dq;
+      const float4 a4 = reinterpret_cast<const float4*>(aw)[cq];
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 mx = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      const float4* base = reinterpret_cast<const float4*>(h + r0 * d);
+#pragma unroll 4
+      for (int r = lane / dq; r < n; r += rstep) {
+        const float4 v = __ldcs(base + r * dq + cq);  // streamed once: evict-first
+        s.x = fmaf(v.x, a4.x, s.x);
+        s.y = fmaf(v.y, a4.y, s.y);
+        s.z = fmaf(v.z, a4.z, s.z);
+        s.w = fmaf(v.w, a4.w, s.w);
+        mx.x = fmaxf(mx.x, v.x);
+        mx.y = fmaxf(mx.y, v.y);
+        mx.z = fmaxf(mx.z, v.z);
+        mx.w = fmaxf(mx.w, v.w);
+      }
+      for (int off = dq; off < 32; off <<= 1) {  // segmented shuffle reduction over row groups
+        s.x += __shfl_xor_sync(0xffffffffu, s.x, off);
+        s.y += __shfl_xor_sync(0xffffffffu, s.y, off);
+        s.z += __shfl_xor_sync(0xffffffffu, s.z, off);
+        s.w += __shfl_xor_sync(0xffffffffu, s.w, off);
+        mx.x = fmaxf(mx.x, __shfl_xor_sync(0xffffffffu, mx.x, off));
+        mx.y = fmaxf(mx.y, __shfl_xor_sync(0xffffffffu, mx.y, off));
+        mx.z = fmaxf(mx.z, __shfl_xor_sync(0xffffffffu, mx.z, off));
+        mx.w = fmaxf(mx.w, __shfl_xor_sync(0xffffffffu, mx.w, off));
+      }
+      if (lane < dq) {
+        float4* uo = reinterpret_cast<float4*>(u + g * 2 * d);
+        uo[lane] = s;
+        uo[dq + lane] = mx;
+      }
+    } else {
+      for (int c = lane; c < d; c += 32) {
+        float s = 0.f, mx = -INFINITY;
+        for (int r = 0; r < n; ++r) {
+          const float v = h[(r0 + r) * d + c];
+          s = fmaf(v, aw[c], s);
+          mx = fmaxf(mx, v);
+        }
+        u[g * 2 * d + c] = s;
+        u[g * 2 * d + d + c] = mx;
+      }
+    }
+  }
+}
+
+
+// ---- tensor-core layer: transform on tcgen05 (3xTF32), aggregation on the CUDA cores -------
+//
+// CTA = 4 warps = one tile of up to 128 rows (whole graphs); thread r owns row r,
+// which is also TMEM lane r.  Per tile:
+//   1. thread r holds its input row in registers (loaded one tile ahead), z-normalises
+//      fp64 rows, splits it hi/lo and tcgen05.st's both into TMEM (the A operand);
+//   2. one elected thread issues P = X W as 3 x (DIN/8) tcgen05.mma kind::tf32
+//      (A from TMEM, W^T hi/lo from smem, D in TMEM);
+//   3. thread r tcgen05.ld's P row r into a padded smem tile; after a CTA barrier it
+//      forms out_r = ReLU(sum_j a_rj P_j) over its CSR row and stores it to HBM.
+// Four CTAs per SM (128 TMEM columns each) overlap one another's load, MMA and
+// aggregation phases.  Per graph the CUDA cores issue ~10x fewer instructions than
+// the FFMA transform, so the kernel stays on the HBM roofline.
+constexpr int TC_ROWS = 128;
+constexpr int TC_PS = 36;  // P tile row stride (floats): float4 rows, spread banks
+
+template <int DIN, bool IN64>
+__global__ void __launch_bounds__(TC_ROWS, 4) gcn_layer_tc_kernel(LayerArgs a) {
+  constexpr int K = (DIN + 7) & ~7;   // MMA K (tf32: 8 per instruction)
+  constexpr int DOUT = 32;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  float* bh = reinterpret_cast<float*>(smem);   // W^T hi, K-major core matrices (N = 32 rows, K)
+  float* bl = bh + DOUT * K;                    // W^T lo
+  float* sP = bl + DOUT * K;                    // [128][TC_PS] transformed rows
+  int* s_rp = reinterpret_cast<int*>(sP + TC_ROWS * TC_PS);
+  const int rp_cap = a.n_pat * (KT_MAX_NODES + 1);
+  int* s_col = s_rp + ((rp_cap + 3) & ~3);
+  float* s_val = reinterpret_cast<float*>(s_col + MAXPNNZ);
+  uint8_t* s_mask = reinterpret_cast<uint8_t*>(s_val + MAXPNNZ);
+  __shared__ PatSmem P;
+  __shared__ double s_mean[KT_MAX_DIM], s_rstd[KT_MAX_DIM];
+  __shared__ __align__(8) uint64_t mma_bar;
+  __shared__ uint32_t tmem_slot;
+  __shared__ int64_t s_gptr[TC_ROWS + 1];  // row starts of the tile's graphs (tile-relative)
+  const int tid = threadIdx.x, warp = tid >> 5;
+
+  // ---- setup ---------------------------------------------------------------------------------
+  for (int e = tid; e < DOUT * K; e += TC_ROWS) {  // B = W^T: row n, column k
+    const int n = e / K, k = e - n * K;
+    const float v = k < DIN ? a.W[k * DOUT + n] : 0.0f;
+    const float h = tc::tf32_trunc(v);
+    const int off = tc::kmajor_offset(n, k, K) >> 2;
+    bh[off] = h;
+    bl[off] = v - h;
+  }
+  if (tid == 0) {
+    int rp = 0, nz = 0, mk = 0;
+    for (int p = 0; p < a.n_pat; ++p) {
+      P.n[p] = a.pat_n[p];
+      P.rp_off[p] = rp;
+      P.nz_off[p] = nz;
+      P.mask_off[p] = mk;
+      nz += a.pat_rp[rp + P.n[p]];
+      rp += P.n[p] + 1;
+      mk += P.n[p];
+    }
+    tc::mbar_init(&mma_bar, 1);
+  }
+  if (IN64)
+    for (int c = tid; c < DIN; c += TC_ROWS) {
+      s_mean[c] = a.fmean[c];
+      s_rstd[c] = 1.0 / a.fstd[c];
+    }
+  if (warp == 0) tc::tmem_alloc(&tmem_slot, 128);
+  __syncthreads();
+  {
+    int tot_rp = 0, tot_nz = 0, tot_mask = 0;
+    for (int p = 0; p < a.n_pat; ++p) {
+      tot_rp += P.n[p] + 1;
+      tot_mask += P.n[p];
+      tot_nz += a.pat_rp[P.rp_off[p] + P.n[p]];
+    }
+    for (int i = tid; i < tot_rp; i += TC_ROWS) s_rp[i] = a.pat_rp[i];
+    for (int i = tid; i < tot_nz; i += TC_ROWS) {
+      s_col[i] = a.pat_col[i];
+      s_val[i] = a.pat_val[i];
+    }
+    if (IN64 && a.pat_mask)
+      for (int i = tid; i < tot_mask; i += TC_ROWS) s_mask[i] = a.pat_mask[i];
+  }
+  tc::fence_async_smem();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const uint32_t lane_addr = static_cast<uint32_t>((32 * warp) << 16);
+  const uint32_t T_AH = 0, T_AL = 32, T_D = 64;
+  const uint32_t idesc = tc::idesc_tf32(128, DOUT);
+  const bool masked = IN64 && a.pat_mask;
+  constexpr int esz = IN64 ? 8 : 4;
+  constexpr int NQ = DIN * esz / 16;  // 16-byte pieces per row
+
+  const int64_t n_tiles = (a.B + a.G - 1) / a.G;
+  float4 pf[NQ];
+  int64_t cur_r0 = 0;
+  int cur_rows = 0;
+  // row range of tile t and this thread's row (prefetch into registers)
+  auto load_tile = [&](int64_t t) {
+    const int64_t g0 = t * a.G;
+    const int64_t g1 = g0 + a.G < a.B ? g0 + a.G : a.B;
+    cur_r0 = tile_row0(a, g0);
+    cur_rows = static_cast<int>(tile_row0(a, g1) - cur_r0);
+    if (tid < cur_rows) {
+      const float4* src =
+          reinterpret_cast<const float4*>(static_cast<const unsigned char*>(a.in) + (cur_r0 + tid) * DIN * esz);
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) pf[i] = __ldg(src + i);  // L1-allocating: a row's 16-B pieces share sectors
+    }
+  };
+  int64_t it = 0;
+  if (blockIdx.x < n_tiles) load_tile(blockIdx.x);
+  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+    const int64_t g0 = t * a.G;
+    const int ng = static_cast<int>((g0 + a.G < a.B ? g0 + a.G : a.B) - g0);
+    const int64_t r0 = cur_r0;
+    const int rows = cur_rows;
+    // ---- 1. own row -> normalised fp32 -> hi / lo into TMEM ---------------------------------
+    float x[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) x[k] = 0.0f;
+    int my_g = -1, my_l = 0;
+    if (tid <= ng) s_gptr[tid] = tile_row0(a, g0 + tid) - r0;
+    __syncthreads();  // s_gptr ready; previous tile's sP reads done
+    if (tid < rows) {
+      my_g = 0;
+      while (my_g + 1 < ng && s_gptr[my_g + 1] <= tid) ++my_g;
+      my_l = tid - static_cast<int>(s_gptr[my_g]);
+      if constexpr (IN64) {
+        const int p = a.pat_id ? a.pat_id[g0 + my_g] : 0;
+        const bool on = !masked || s_mask[P.mask_off[p] + my_l];
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) {
+          const double2 d = *reinterpret_cast<const double2*>(&pf[i]);
+          x[2 * i] = on ? static_cast<float>((d.x - s_mean[2 * i]) * s_rstd[2 * i]) : 0.0f;
+          x[2 * i + 1] = on ? static_cast<float>((d.y - s_mean[2 * i + 1]) * s_rstd[2 * i + 1]) : 0.0f;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) {
+          x[4 * i] = pf[i].x;
+          x[4 * i + 1] = pf[i].y;
+          x[4 * i + 2] = pf[i].z;
+          x[4 * i + 3] = pf[i].w;
+        }
+      }
+    }
+    {
+      float hi[K], lo[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        hi[k] = tc::tf32_trunc(x[k]);
+        lo[k] = x[k] - hi[k];
+      }
+#pragma unroll
+      for (int k0 = 0; k0 < K; k0 += 16) {
+        if (K - k0 >= 16) {
+          tc::tmem_st16(tmem + lane_addr + T_AH + k0, hi + k0);
+          tc::tmem_st16(tmem + lane_addr + T_AL + k0, lo + k0);
+        }
+      }
+      if constexpr (K % 16 == 8) {  // K = 8, 24, 40 ...: last 8 columns
+        float h16[16], l16[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          h16[k] = k < 8 ? hi[K - 8 + k] : 0.f;
+          l16[k] = k < 8 ? lo[K - 8 + k] : 0.f;
+        }
+        tc::tmem_st16(tmem + lane_addr + T_AH + K - 8, h16);
+        tc::tmem_st16(tmem + lane_addr + T_AL + K - 8, l16);
+      }
+      tc::tmem_wait_st();
+    }
+    // next tile's rows in flight while this tile computes
+    if (t + gridDim.x < n_tiles) load_tile(t + gridDim.x);
+    tc::tc_fence_before();
+    __syncthreads();
+    // ---- 2. P = X W on the tensor cores ------------------------------------------------------
+    if (warp == 0) {
+      tc::tc_fence_after();
+      if (tc::elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < K / 8; ++kk) {
+          tc::mma_tf32_ts(tmem + T_D, tmem + T_AH + 8 * kk, tc::kdesc(bh, K, kk), idesc, kk > 0);
+          tc::mma_tf32_ts(tmem + T_D, tmem + T_AH + 8 * kk, tc::kdesc(bl, K, kk), idesc, 1);
+          tc::mma_tf32_ts(tmem + T_D, tmem + T_AL + 8 * kk, tc::kdesc(bh, K, kk), idesc, 1);
+        }
+        tc::mma_commit(&mma_bar);
+      }
+      __syncwarp();
+    }
+    tc::mbar_wait(&mma_bar, static_cast<uint32_t>(it & 1));
+    __syncwarp();
+    tc::tc_fence_after();
+    {
+      float v[32];
+      tc::tmem_ld32(tmem + lane_addr + T_D, v);
+      tc::tmem_wait_ld();
+      float4* dst = reinterpret_cast<float4*>(sP + tid * TC_PS);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    // ---- 3. out_r = ReLU(sum_j a_rj P_j) -> HBM ----------------------------------------------
+    if (tid < rows) {
+      const int p = a.pat_id ? a.pat_id[g0 + my_g] : 0;
+      const int* rp = s_rp + P.rp_off[p];
+      const int nz0 = P.nz_off[p];
+      const int base = static_cast<int>(s_gptr[my_g]);
+      float2 acc[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = make_float2(0.f, 0.f);
+      for (int e = rp[my_l]; e < rp[my_l + 1]; ++e) {
+        const float w = s_val[nz0 + e];
+        const float4* src = reinterpret_cast<const float4*>(sP + (base + s_col[nz0 + e]) * TC_PS);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 pv = src[j];
+          acc[2 * j] = ffma2s(w, make_float2(pv.x, pv.y), acc[2 * j]);
+          acc[2 * j + 1] = ffma2s(w, make_float2(pv.z, pv.w), acc[2 * j + 1]);
+        }
+      }
+      float4* out = reinterpret_cast<float4*>(a.out + (r0 + tid) * DOUT);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float4 o = make_float4(acc[2 * j].x, acc[2 * j].y, acc[2 * j + 1].x, acc[2 * j + 1].y);
+        if (a.relu) o = make_float4(fmaxf(o.x, 0.f), fmaxf(o.y, 0.f), fmaxf(o.z, 0.f), fmaxf(o.w, 0.f));
+        __stcs(out + j, o);
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, 128);
+  }
+}
+
+}  // namespace agg
+}  // namespace kt
+
+using namespace kt;
+
+extern "C" int kt_gcn_layer(const void* in, int32_t in_f64, const double* fmean, const double* fstd,
+                            const float* W, int32_t d_in, int32_t d_out, int32_t relu, int64_t B,
+                            int32_t nodes_per_graph, const int64_t* node_ptr, const int32_t* pat_id,
+                            int32_t n_pat, const int32_t* pat_n, const int32_t* pat_rp, const int32_t* pat_col,
+                            const float* pat_val, const uint8_t* pat_mask, int32_t pat_nnz, int32_t max_nodes,
+                            float* out, void* stream) {
+  KT_REQUIRE(in && W && out && pat_n && pat_rp && pat_col && pat_val, KT_E_ARG, "kt_gcn_layer: null pointer");
+  KT_REQUIRE(B > 0, KT_E_EMPTY, "kt_gcn_layer: empty batch");
+  KT_REQUIRE(d_in > 0 && d_out > 0 && d_in <= KT_MAX_DIM && d_out <= KT_MAX_DIM, KT_E_SHAPE,
+             "kt_gcn_layer: layer widths must be in [1, %d]", KT_MAX_DIM);
+  KT_REQUIRE(n_pat >= 1 && n_pat <= agg::MAXPAT, KT_E_UNSUPPORTED, "kt_gcn_layer: 1..%d adjacency patterns",
+             agg::MAXPAT);
+  KT_REQUIRE(nodes_per_graph > 0 || node_ptr, KT_E_ARG, "kt_gcn_layer: need nodes_per_graph or node_ptr");
+  KT_REQUIRE(pat_nnz > 0 && pat_nnz <= agg::MAXPNNZ, KT_E_UNSUPPORTED, "kt_gcn_layer: <= %d adjacency nonzeros",
+             agg::MAXPNNZ);
+  KT_REQUIRE(!in_f64 || (fmean && fstd), KT_E_ARG, "kt_gcn_layer: fp64 input needs the feature norms");
+  KT_REQUIRE(max_nodes > 0 && max_nodes <= KT_MAX_NODES, KT_E_SHAPE, "kt_gcn_layer: graphs of <= %d nodes",
+             KT_MAX_NODES);
+  agg::LayerArgs a{};
+  a.in = in;
+  a.in_f64 = in_f64;
+  a.out = out;
+  a.W = W;
+  a.fmean = fmean;
+  a.fstd = fstd;
+  a.d_in = d_in;
+  a.d_out = d_out;
+  a.relu = relu;
+  a.B = B;
+  a.n_uniform = nodes_per_graph;
+  a.node_ptr = nodes_per_graph > 0 ? nullptr : node_ptr;
+  a.pat_id = pat_id;
+  a.n_pat = n_pat;
+  a.pat_n = pat_n;
+  a.pat_rp = pat_rp;
+  a.pat_col = pat_col;
+  a.pat_val = pat_val;
+  a.pat_mask = pat_mask;
+  const int esz = in_f64 ? 8 : 4;
+  // per-warp slabs (X rows + aggregated rows, fp32) sized for the largest graph
+  a.R = max_nodes;
+  a.G = 1;
+  a.bulk = 0;
+  const int dinp = (d_in + 3) & ~3;
+  const size_t smem = static_cast<size_t>((d_in * d_out + 3) & ~3) * 4 +
+                      ((static_cast<size_t>(n_pat) * (KT_MAX_NODES + 1) + 3) & ~3) * 4 + agg::MAXPNNZ * 8 +
+                      ((static_cast<size_t>(n_pat) * KT_MAX_NODES + 15) & ~15) +
+                      static_cast<size_t>(agg::WPC) * 2 * max_nodes * dinp * 4;
+  KT_REQUIRE(smem <= 200 * 1024, KT_E_UNSUPPORTED, "kt_gcn_layer: slabs do not fit shared memory (%zu B)", smem);
+  const int64_t blocks = (B + agg::WPC - 1) / agg::WPC;
+  const int grid = static_cast<int>(blocks < 4 * kNumSMs ? blocks : 4 * kNumSMs);
+  auto launch = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kern<<<grid, agg::NT, smem, as_stream(stream)>>>(a);
+  };
+  const bool tc_ok = d_out == 32 && ((d_in == 12 && in_f64) || (d_in == 32 && !in_f64)) &&
+                     max_nodes <= agg::TC_ROWS &&
+                     (reinterpret_cast<uintptr_t>(in) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
+                     !(getenv("KT_AGG_FFMA") && getenv("KT_AGG_FFMA")[0] == '1');
+  if (tc_ok) {
+    // tiles of whole graphs, <= 128 rows; 4 CTAs per SM (128 TMEM columns each)
+    a.G = agg::TC_ROWS / max_nodes;
+    const int K = (d_in + 7) & ~7;
+    const size_t tsm = 1024 + static_cast<size_t>(2 * 32 * K) * 4 + agg::TC_ROWS * agg::TC_PS * 4 +
+                       ((static_cast<size_t>(n_pat) * (KT_MAX_NODES + 1) + 3) & ~3) * 4 + agg::MAXPNNZ * 8 +
+                       static_cast<size_t>(n_pat) * KT_MAX_NODES + 64;
+    const int64_t tiles = (B + a.G - 1) / a.G;
+    const int tgrid = static_cast<int>(tiles < 4 * kNumSMs ? tiles : 4 * kNumSMs);
+    auto tlaunch = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsm));
+      kern<<<tgrid, agg::TC_ROWS, tsm, as_stream(stream)>>>(a);
+    };
+    if (d_in == 12)
+      tlaunch(agg::gcn_layer_tc_kernel<12, true>);
+    else
+      tlaunch(agg::gcn_layer_tc_kernel<32, false>);
+  } else if (d_in == 12 && d_out == 32) {
+    launch(agg::gcn_layer_kernel<12, 32>);
+  } else if (d_in == 32 && d_out == 32) {
+    launch(agg::gcn_layer_kernel<32, 32>);
+  } else {
+    launch(agg::gcn_layer_kernel<0, 0>);
+  }
+  note_launches(1);
+  return check_launch("kt_gcn_layer");
+}
+
+extern "C" int kt_readout(const float* h, int32_t d, int64_t B, int32_t nodes_per_graph, const int64_t* node_ptr,
+                          const float* agg_w, float* u_out, void* stream) {
+  KT_REQUIRE(h && agg_w && u_out, KT_E_ARG, "kt_readout: null pointer");
+  KT_REQUIRE(B > 0, KT_E_EMPTY, "kt_readout: empty batch");
+  KT_REQUIRE(d > 0, KT_E_SHAPE, "kt_readout: embedding width must be positive");
+  KT_REQUIRE(nodes_per_graph > 0 || node_ptr, KT_E_ARG, "kt_readout: need nodes_per_graph or node_ptr");
+  const int64_t warps = B;
+  const int64_t blocks = (warps * 32 + 255) / 256;
+  const int grid = static_cast<int>(blocks < 16 * kNumSMs ? blocks : 16 * kNumSMs);
+  agg::readout_kernel<<<grid, 256, 0, as_stream(stream)>>>(h, d, B, nodes_per_graph,
+                                                           nodes_per_graph > 0 ? nullptr : node_ptr, agg_w, u_out);
+  note_launches(1);
+  return check_launch("kt_readout");
+}

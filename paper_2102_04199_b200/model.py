@@ -437,6 +437,161 @@ def embed_graphs(m: ModelState, graphs, with_scores: bool = False):
     return (u, z) if with_scores else u
 
 
+# --- streaming layer path: the HBM-bound aggregation kernels -------------------------------
+
+
+@dataclass
+class AdjPatterns:
+    """Distinct normalised adjacencies of a batch as local CSRs (kt_gcn_layer's input)."""
+    n_pat: int
+    pat_n: torch.Tensor     # (n_pat,) int32 nodes per pattern
+    rp: torch.Tensor        # concatenated local row_ptr, (n + 1) per pattern
+    col: torch.Tensor       # concatenated local column ids
+    val: torch.Tensor       # fp32 of the fp64 A_hat entries
+    mask: torch.Tensor      # concatenated node masks (uint8)
+    nnz: int
+    max_nodes: int
+
+
+_PAT_CACHE: dict = {}
+
+
+def adjacency_patterns(adjs, masks, dev) -> AdjPatterns:
+    """Local CSR (row-major nonzeros of the fp64 A_hat, graphs.py:234-241) of each
+    distinct adjacency, cached by content."""
+    adjs = [np.asarray(_host(a), dtype=np.float64) for a in adjs]
+    masks = [np.asarray(_host(mk), dtype=bool) for mk in masks]
+    key = (tuple(a.tobytes() for a in adjs), tuple(mk.tobytes() for mk in masks), str(dev))
+    hit = _PAT_CACHE.get(key)
+    if hit is not None:
+        return hit
+    if len(adjs) > 8:
+        raise DomainError("kt_gcn_layer takes at most 8 distinct adjacency patterns per batch")
+    rps, cols, vals, mks, ns = [], [], [], [], []
+    for a, mk in zip(adjs, masks):
+        if a.shape[0] > _lib.KT_MAX_NODES:
+            raise DomainError(f"graphs of {a.shape[0]} nodes exceed the device limit {_lib.KT_MAX_NODES}")
+        r, c = np.nonzero(a)
+        rp = np.zeros(a.shape[0] + 1, dtype=np.int64)
+        np.add.at(rp, r + 1, 1)
+        rps.append(np.cumsum(rp))
+        cols.append(c)
+        vals.append(a[r, c])
+        mks.append(mk.astype(np.uint8))
+        ns.append(a.shape[0])
+    nnz = int(sum(len(c) for c in cols))
+    if nnz > 1024:
+        raise DomainError("kt_gcn_layer takes at most 1024 adjacency nonzeros per batch")
+    up = lambda x, dt: torch.from_numpy(np.ascontiguousarray(np.concatenate(x), dtype=dt)).to(dev)
+    hit = AdjPatterns(len(adjs), torch.tensor(ns, dtype=torch.int32, device=dev), up(rps, np.int32),
+                      up(cols, np.int32), up(vals, np.float32), up(mks, np.uint8), nnz, int(max(ns)))
+    if len(_PAT_CACHE) > 64:
+        _PAT_CACHE.clear()
+    _PAT_CACHE[key] = hit
+    return hit
+
+
+def _gcn_layers(m: ModelState, x64: torch.Tensor, n_graphs: int, n_uniform: int, node_ptr, pat_id,
+                pats: AdjPatterns) -> torch.Tensor:
+    """All GCN layers through kt_gcn_layer: fp64 raw rows in, fp32 H_L rows out."""
+    flat = flat_params(m)
+    dev = flat.device
+    mean, std = _norm_tensors(m, dev)
+    rows = x64.shape[0]
+    lib = _lib.load()
+    h = x64
+    for i, w in enumerate(m.gcn.layers):
+        d_in, d_out = int(w.shape[0]), int(w.shape[1])
+        if h.shape[1] != d_in:
+            raise DomainError(f"GCN input width {h.shape[1]} != weight rows {d_in}")
+        out = torch.empty((rows, d_out), dtype=torch.float32, device=dev)
+        wc = w.contiguous()
+        with torch.cuda.device(dev):
+            _lib.check(lib.kt_gcn_layer(_lib.ptr(h), int(i == 0), _lib.ptr(mean), _lib.ptr(std), _lib.ptr(wc),
+                                        d_in, d_out, 1, n_graphs, n_uniform, _lib.ptr(node_ptr), _lib.ptr(pat_id),
+                                        pats.n_pat, _lib.ptr(pats.pat_n), _lib.ptr(pats.rp), _lib.ptr(pats.col),
+                                        _lib.ptr(pats.val), _lib.ptr(pats.mask), pats.nnz, pats.max_nodes,
+                                        _lib.ptr(out), _lib.stream_handle()), "gcn_layer")
+        h = out
+    return h
+
+
+def gcn_forward_batch(m: ModelState, feats, mask, adj) -> torch.Tensor:
+    """gcn_forward (model.py:127-133) for a batch sharing one adjacency / mask:
+    (B, N, F) raw features -> H_L (B, N, d_L) fp32, one streaming kernel per layer."""
+    dev = flat_params(m).device
+    x = _as_device(feats, dev, torch.float64)
+    if x.dim() != 3 or x.shape[2] != m.gcn.layers[0].shape[0]:
+        raise DomainError(f"feats must be (B, N, {m.gcn.layers[0].shape[0]})")
+    b, n = x.shape[0], x.shape[1]
+    if b == 0:
+        raise DomainError("empty batch")
+    adj = np.asarray(_host(adj), dtype=np.float64)
+    msk = np.asarray(_host(mask), dtype=bool)
+    if adj.shape != (n, n) or msk.shape != (n,):
+        raise DomainError("adjacency / mask shape does not match feats")
+    pats = adjacency_patterns([adj], [msk], dev)
+    h = _gcn_layers(m, x.reshape(b * n, -1), b, n, None, None, pats)
+    return h.reshape(b, n, -1)
+
+
+def gcn_forward_graphs(m: ModelState, graphs):
+    """gcn_forward over CodeGraphs of any sizes: H_L rows (total nodes, d_L) and the
+    int64 node_ptr (B + 1) segmenting them."""
+    if not graphs:
+        raise DomainError("empty batch")
+    dev = flat_params(m).device
+    ts = [tensors_for(g) for g in graphs]
+    keys, pat_of, adjs, masks = {}, [], [], []
+    for t in ts:
+        k = (t.normalized_adjacency.tobytes(), np.asarray(t.feature_mask).tobytes())
+        if k not in keys:
+            keys[k] = len(adjs)
+            adjs.append(t.normalized_adjacency)
+            masks.append(t.feature_mask)
+        pat_of.append(keys[k])
+    pats = adjacency_patterns(adjs, masks, dev)
+    sizes = np.array([t.feature_matrix.shape[0] for t in ts], dtype=np.int64)
+    node_ptr = torch.from_numpy(np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)).to(dev)
+    x = torch.from_numpy(np.ascontiguousarray(np.concatenate([t.feature_matrix for t in ts]),
+                                              dtype=np.float64)).to(dev)
+    pid = torch.tensor(pat_of, dtype=torch.int32, device=dev)
+    return _gcn_layers(m, x, len(graphs), 0, node_ptr, pid, pats), node_ptr
+
+
+def aggregate_batch(h, agg: AggParams, node_ptr=None) -> torch.Tensor:
+    """aggregate (model.py:136-141) per graph: h (B, N, d) -> (B, 2 d); or h (rows, d)
+    segmented by node_ptr (B + 1).  Warp-shuffle segmented reductions (kt_readout)."""
+    w = agg.sum_weights
+    dev = w.device
+    hh = _as_device(h, dev, torch.float32)
+    d = int(w.shape[0])
+    if hh.shape[-1] != d:
+        raise DomainError("embedding width does not match aggregation weights")
+    if node_ptr is None:
+        if hh.dim() != 3 or hh.shape[0] == 0 or hh.shape[1] == 0:
+            raise DomainError("cannot aggregate an empty embedding matrix")
+        b, n = hh.shape[0], hh.shape[1]
+        np_t = None
+    else:
+        np_t = _as_device(node_ptr, dev, torch.int64)
+        b, n = np_t.numel() - 1, 0
+        if b <= 0:
+            raise DomainError("empty batch")
+    u = torch.empty((b, 2 * d), dtype=torch.float32, device=dev)
+    lib = _lib.load()
+    with torch.cuda.device(dev):
+        _lib.check(lib.kt_readout(_lib.ptr(hh), d, b, n, _lib.ptr(np_t), _lib.ptr(w.contiguous()), _lib.ptr(u),
+                                  _lib.stream_handle()), "aggregate_batch")
+    return u
+
+
+def embed_batch_streaming(m: ModelState, feats, mask, adj) -> torch.Tensor:
+    """embed_batch (model.py:185-194) as layer kernels + readout: same result as
+    embed_batch, materialising H_l in HBM (the form large batches stream through)."""
+    return aggregate_batch(gcn_forward_batch(m, feats, mask, adj), m.agg)
+
+
 def embed(graph, m: ModelState) -> torch.Tensor:
     """Aggregated embedding of one graph (model.py:153-160)."""
     return embed_graphs(m, [graph])[0]
