@@ -36,7 +36,7 @@
 // CTA 0's pipeline events.  Compiled out of the product library.
 #ifdef KT_TC_TRACE
 #define KT_TRACE_N 64
-__device__ long long g_kt_trace[20][KT_TRACE_N];
+__device__ long long g_kt_trace[24][KT_TRACE_N];
 #define TRACE(ev, i)                                              \
   do {                                                            \
     if (blockIdx.x == 0 && (i) < KT_TRACE_N) g_kt_trace[ev][i] = clock64(); \
@@ -335,103 +335,118 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         tmem_st32(tmem + lane + T_X + 32 * s, hl);
 #endif
         tmem_wait_st();
+        // fold GEMM1's second dependency in here: D1[q & 1] drained by the R warps
+        // (chunk q - 2), so the MMA warp waits on x_full alone
+        mbar_wait(&S.d1_empty[q & 1], static_cast<uint32_t>(((q >> 1) & 1) ^ 1));
+        __syncwarp();
         tc_fence_before();
         warp_arrive(&S.x_full[s]);
         if (g == 0) TRACE(0, q);
       }
     }
   } else if (warp == 8) {
-    // ===================== MMA: polling scheduler, one elected lane issues =====================
+    // ===================== MMA: fixed issue order, blocking waits, one elected lane issues =====
+    // Order per chunk q: GEMM1(q + 2), GEMM2(q); the head of tile t is issued two
+    // (GEMM3) and three (GEMM4) chunks into tile t + 1, so its epilogue overlaps the
+    // next tile's GCN chunks.  Each wait parks the warp in hardware until the phase
+    // completes (no polling: a polling warp costs its SMSP neighbours issue slots).
     const uint32_t id32 = idesc_tf32(128, 32), id64 = idesc_tf32(128, 64);
-    auto ready = [&](uint64_t* bar, uint32_t parity) {
-      return __shfl_sync(0xffffffffu, static_cast<int>(mbar_test(bar, parity)), 0) != 0;
+    auto wait_bar = [&](uint64_t* bar, uint32_t parity) {
+      mbar_wait(bar, parity);
+      __syncwarp();
+      tc_fence_after();
     };
-    int64_t q1 = 0, q2 = 0, t3 = 0, t4 = 0;
-    int64_t issued = 0, last = -1;
-    while (q2 < n_chunks || t4 < my_tiles) {
-      if (issued == last) __nanosleep(64);  // nothing was ready: back off instead of hogging SMSP 0
-      last = issued;
-      // head GEMM4 of tile t4 once its Z1 operand is in smem
-      if (t4 < t3 && ready(&S.z_full, static_cast<uint32_t>(t4 & 1))) {
-        tc_fence_after();
-        if (elect_one()) {
+    auto g1 = [&](int64_t q) {
+      const int s = static_cast<int>(q % XS), b = static_cast<int>(q & 1);
+      if ((tid & 31) == 0) TRACE(22, q);
+      wait_bar(&S.x_full[s], static_cast<uint32_t>((q / XS) & 1));  // implies D1[b] drained
+      if ((tid & 31) == 0) TRACE(23, q);
+      const uint32_t xh = tmem + T_X + 32 * s, xl = xh + 16, d = tmem + T_D1 + 32 * b;
+      if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            mma_tf32(tmem + T_D4, kdesc(S.ah, H, kk), kdesc(S.b4h, H, kk), id64, kk > 0);
-            mma_tf32(tmem + T_D4, kdesc(S.ah, H, kk), kdesc(S.b4l, H, kk), id64, 1);
-            mma_tf32(tmem + T_D4, kdesc(S.al, H, kk), kdesc(S.b4h, H, kk), id64, 1);
-          }
-          mma_commit(&S.d4_full);
-          TRACE(4, t4);
+        for (int kk = 0; kk < 2; ++kk) {
+          mma_tf32_ts(d, xh + 8 * kk, kdesc(S.b1h, 16, kk), id32, kk > 0);
+          mma_tf32_ts(d, xh + 8 * kk, kdesc(S.b1l, 16, kk), id32, 1);
+          mma_tf32_ts(d, xl + 8 * kk, kdesc(S.b1h, 16, kk), id32, 1);
         }
-        __syncwarp();
-        ++t4;
-        ++issued;
+        mma_commit(&S.x_empty[s]);
+        mma_commit(&S.d1_full[b]);
+        TRACE(1, q);
       }
-      // head GEMM3 of tile t3: all its chunks through GEMM2, D3 free (t3 == t4), U in smem
-      if (t3 < my_tiles && t3 == t4 && q2 >= (t3 + 1) * C && ready(&S.u_full, static_cast<uint32_t>(t3 & 1))) {
-        tc_fence_after();
-        if (elect_one()) {
+      __syncwarp();
+    };
+    auto g2 = [&](int64_t q) {
+      const int b = static_cast<int>(q & 1);
+      const uint32_t ph = static_cast<uint32_t>((q >> 1) & 1);
+      if ((tid & 31) == 0) TRACE(17, q);
+      wait_bar(&S.r_full[b], ph);  // implies D2[b] drained
+      if ((tid & 31) == 0) TRACE(18, q);
+      const uint32_t rh = tmem + T_R + 64 * b, rl = rh + 32, d = tmem + T_D2 + 32 * b;
+      if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            mma_tf32(tmem + T_D3, kdesc(S.ah, H, kk), kdesc(S.b3h, H, kk), id64, kk > 0);
-            mma_tf32(tmem + T_D3, kdesc(S.ah, H, kk), kdesc(S.b3l, H, kk), id64, 1);
-            mma_tf32(tmem + T_D3, kdesc(S.al, H, kk), kdesc(S.b3h, H, kk), id64, 1);
-          }
-          mma_commit(&S.d3_full);
-          TRACE(3, t3);
+        for (int kk = 0; kk < 4; ++kk) {
+          mma_tf32_ts(d, rh + 8 * kk, kdesc(S.b2h, 32, kk), id32, kk > 0);
+          mma_tf32_ts(d, rh + 8 * kk, kdesc(S.b2l, 32, kk), id32, 1);
+          mma_tf32_ts(d, rl + 8 * kk, kdesc(S.b2h, 32, kk), id32, 1);
         }
-        __syncwarp();
-        ++t3;
-        ++issued;
+        mma_commit(&S.r_empty[b]);
+        mma_commit(&S.d2_full[b]);
+        TRACE(2, q);
       }
-      // GEMM2 of chunk q2: R ready, D2 buffer drained
-      if (q2 < q1) {
-        const int b = static_cast<int>(q2 & 1);
-        const uint32_t ph = static_cast<uint32_t>((q2 >> 1) & 1);
-        if (ready(&S.r_full[b], ph) && ready(&S.d2_empty[b], ph ^ 1)) {
-          tc_fence_after();
-          const uint32_t rh = tmem + T_R + 64 * b, rl = rh + 32, d = tmem + T_D2 + 32 * b;
-          if (elect_one()) {
+      __syncwarp();
+    };
+    auto g3 = [&](int64_t t) {
+      wait_bar(&S.u_full, static_cast<uint32_t>(t & 1));
+      if (elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              mma_tf32_ts(d, rh + 8 * kk, kdesc(S.b2h, 32, kk), id32, kk > 0);
-              mma_tf32_ts(d, rh + 8 * kk, kdesc(S.b2l, 32, kk), id32, 1);
-              mma_tf32_ts(d, rl + 8 * kk, kdesc(S.b2h, 32, kk), id32, 1);
-            }
-            mma_commit(&S.r_empty[b]);
-            mma_commit(&S.d2_full[b]);
-            TRACE(2, q2);
-          }
-          __syncwarp();
-          ++q2;
-          ++issued;
+        for (int kk = 0; kk < 8; ++kk) {
+          mma_tf32(tmem + T_D3, kdesc(S.ah, H, kk), kdesc(S.b3h, H, kk), id64, kk > 0);
+          mma_tf32(tmem + T_D3, kdesc(S.ah, H, kk), kdesc(S.b3l, H, kk), id64, 1);
+          mma_tf32(tmem + T_D3, kdesc(S.al, H, kk), kdesc(S.b3h, H, kk), id64, 1);
         }
+        mma_commit(&S.d3_full);
+        TRACE(3, t);
       }
-      // GEMM1 of chunk q1: X slot filled, D1 buffer drained
-      if (q1 < n_chunks) {
-        const int s = static_cast<int>(q1 % XS), b = static_cast<int>(q1 & 1);
-        if (ready(&S.x_full[s], static_cast<uint32_t>((q1 / XS) & 1)) &&
-            ready(&S.d1_empty[b], static_cast<uint32_t>(((q1 >> 1) & 1) ^ 1))) {
-          tc_fence_after();
-          const uint32_t xh = tmem + T_X + 32 * s, xl = xh + 16, d = tmem + T_D1 + 32 * b;
-          if (elect_one()) {
+      __syncwarp();
+    };
+    auto g4 = [&](int64_t t) {
+      wait_bar(&S.z_full, static_cast<uint32_t>(t & 1));
+      if (elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < 2; ++kk) {
-              mma_tf32_ts(d, xh + 8 * kk, kdesc(S.b1h, 16, kk), id32, kk > 0);
-              mma_tf32_ts(d, xh + 8 * kk, kdesc(S.b1l, 16, kk), id32, 1);
-              mma_tf32_ts(d, xl + 8 * kk, kdesc(S.b1h, 16, kk), id32, 1);
-            }
-            mma_commit(&S.x_empty[s]);
-            mma_commit(&S.d1_full[b]);
-            TRACE(1, q1);
-          }
-          __syncwarp();
-          ++q1;
-          ++issued;
+        for (int kk = 0; kk < 8; ++kk) {
+          mma_tf32(tmem + T_D4, kdesc(S.ah, H, kk), kdesc(S.b4h, H, kk), id64, kk > 0);
+          mma_tf32(tmem + T_D4, kdesc(S.ah, H, kk), kdesc(S.b4l, H, kk), id64, 1);
+          mma_tf32(tmem + T_D4, kdesc(S.al, H, kk), kdesc(S.b4h, H, kk), id64, 1);
         }
+        mma_commit(&S.d4_full);
+        TRACE(4, t);
+      }
+      __syncwarp();
+    };
+    constexpr int LA = 2;  // GEMM1 runs this many chunks ahead of GEMM2
+    for (int64_t q = 0; q < LA && q < n_chunks; ++q) g1(q);
+    // The head of tile t must be issued no later than right after GEMM2 of chunk
+    // last(t) + 2: GEMM2 of last(t) + 3 needs the D2 buffer the readout warps free only
+    // after finishing the head of tile t (GEMM4's result).
+    int64_t head_t = -1, head_at = 0;
+    auto head = [&]() {
+      g3(head_t);
+      g4(head_t);
+      head_t = -1;
+    };
+    int kc = 0;
+    for (int64_t q = 0; q < n_chunks; ++q) {
+      if (q + LA < n_chunks) g1(q + LA);
+      g2(q);
+      if (head_t >= 0 && q >= head_at) head();
+      if (++kc == C) {  // tile q / C complete: schedule its head (flush one still pending)
+        kc = 0;
+        if (head_t >= 0) head();
+        head_t = q / C;
+        head_at = q + 2;
       }
     }
+    if (head_t >= 0) head();
   } else if (warp < 4) {
     // ===================== R: ReLU(D1) -> R (hi, lo) in TMEM; thread = lane = graph ===============
     const int g = tid;
@@ -469,6 +484,10 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       if (g == 0) TRACE(15, q);
       tmem_wait_st();
       if (g == 0) TRACE(16, q);
+      // fold GEMM2's second dependency in here: D2[b] drained by the readout warps
+      // (chunk q - 2), so the MMA warp waits on r_full alone
+      mbar_wait(&S.d2_empty[b], ph ^ 1);
+      __syncwarp();
       tc_fence_before();
       warp_arrive(&S.r_full[b]);
       if (g == 0) TRACE(6, q);
