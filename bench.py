@@ -369,6 +369,33 @@ def bench_aggregate(m, reps=10):
             "peak_source": "MEASURED_PEAKS.json hbm_gbs", "kernels": out}
 
 
+def bench_sa(m, reps=20):
+    """sa_explore (search.py:202-254) with the SaSchedule defaults (16 chains x 128 steps)
+    through the device annealer: host draws + one CUDA-graph replay + history dict."""
+    import torch
+
+    from paper_2102_04199_b200 import graphs as pg
+    from paper_2102_04199_b200 import kernels as pk
+    from paper_2102_04199_b200 import search as ps
+    from paper_2102_04199_b200.util import rng_from
+
+    spec = pk.KernelSpec(*SPEC_ARGS)
+    space = pk.build_knob_space(spec)
+    pred = ps.CostModelPredictor(m, spec, space, pg.batch_layout(spec, pg.build_super_template(pk.OP_TYPES)))
+    sched = ps.SaSchedule()
+    for i in range(3):
+        ps.sa_explore(pred, space, sched, set(), rng_from("bench-sa-warm", i))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(reps):
+        ps.sa_explore(pred, space, sched, set(), rng_from("bench-sa", i))
+    torch.cuda.synchronize()
+    ms = 1e3 * (time.perf_counter() - t0) / reps
+    return {"metric": "sa_explore call (16 chains x 128 steps)", "value": ms, "unit": "ms/call",
+            "higher_is_better": False, "graphs_per_s": 16 * 129 / (ms / 1e3),
+            "config": "SaSchedule defaults, conv2d bench spec, super layout; wall clock incl. host RNG draws"}
+
+
 # --- CPU arms -------------------------------------------------------------------------# --- CPU arms -------------------------------------------------------------------------
 
 
@@ -590,6 +617,7 @@ def run_ours(args):
                                                        ("conv2d", "winograd", "depthwise")], 50, 5)
             line["fine_tune"] = bench_fine_tune(m, corpus)
             line["aggregation"] = bench_aggregate(m)
+            line["sa_explore"] = bench_sa(m)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:

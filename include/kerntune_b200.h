@@ -177,6 +177,21 @@ int kt_readout(const float* h, int32_t d, int64_t B, int32_t nodes_per_graph, co
 int kt_head_forward(const kt_dims* dims, const float* params, const float* u, int64_t B,
                     float* z_out, void* stream);
 
+/* ---- simulated-annealing exploration (sa_explore, search.py:202-254) ----------------------- */
+/* One proposal step for n_chains chains from pre-drawn randoms (the host draws them
+ * from the caller's numpy Generator in the reference's order): the chosen knob of
+ * chain c is nudged by delta[c] (clipped to [0, card-1]) if nudge[c], else set to
+ * resample[c] (search.py:232-241).  cur / nxt: (n_chains, n_knobs) int32 choices;
+ * nxt_idx: the neighbours' config indices, sum_j nxt[c][j] mult[j]. */
+int kt_sa_propose(const int32_t* cur, int32_t n_chains, int32_t n_knobs, const int32_t* cards,
+                  const int64_t* mult, const int32_t* knob, const uint8_t* nudge, const int32_t* delta,
+                  const int32_t* resample, int32_t* nxt, int64_t* nxt_idx, void* stream);
+/* Metropolis acceptance (search.py:246-251) in fp64: accept if e_new >= energy or
+ * u < exp(min((e_new - energy) / temp, 0)); accepted chains copy nxt into cur and
+ * e_new into energy. */
+int kt_sa_accept(int32_t n_chains, int32_t n_knobs, const float* e_new, const double* u, double temp,
+                 const int32_t* nxt, int32_t* cur, double* energy, void* stream);
+
 /* ---- training (model.py:218-310, meta.py:104-123) ----------------------------------------- */
 /* grad(m, batch, scope) (model.py:218-285) over a CSR batch laid out as for
  * kt_embed_csr.  graph_idx (optional, B entries) gathers graphs of a resident

@@ -449,3 +449,92 @@ def rank_history(indices, scores, visited, count) -> list:
     ranked = sorted(((int(i), float(e)) for i, e in zip(indices, scores) if int(i) not in visited),
                     key=lambda t: (-t[1], t[0]))
     return [i for i, _ in ranked[:count]]
+
+
+# --- simulated-annealing exploration (search.py:177-281) ------------------------------------
+
+
+def space_multipliers(cards) -> np.ndarray:
+    """_space_multipliers (search.py:177-182): knob 0 most significant."""
+    mult = np.ones(len(cards), dtype=np.int64)
+    for j in range(len(cards) - 2, -1, -1):
+        mult[j] = mult[j + 1] * cards[j + 1]
+    return mult
+
+
+def draw_unvisited(size: int, visited: set, count: int, rng) -> list:
+    """draw_unvisited (search.py:185-211): distinct unvisited indices, same RNG draws."""
+    remaining = size - len(visited)
+    count = min(count, max(remaining, 0))
+    if count <= 0:
+        return []
+    if size <= 65536:
+        unvisited = np.array([i for i in range(size) if i not in visited], dtype=np.int64)
+        pick = rng.choice(len(unvisited), size=count, replace=False)
+        return [int(unvisited[i]) for i in pick]
+    out, chosen = [], set()
+    while len(out) < count:
+        need = count - len(out)
+        for v in rng.integers(0, size, size=need + 8):
+            i = int(v)
+            if i not in visited and i not in chosen:
+                chosen.add(i)
+                out.append(i)
+                if len(out) == count:
+                    break
+    return out
+
+
+def sa_draws(rng, cards, n_chains, steps):
+    """The per-step random draws of sa_explore (search.py:233-237), in the reference's order."""
+    cards = np.asarray(cards, dtype=np.int64)
+    out = []
+    for _ in range(steps):
+        knob = rng.integers(0, len(cards), size=n_chains)
+        nudge = rng.random(n_chains) < 0.5
+        delta = rng.integers(0, 2, size=n_chains) * 2 - 1
+        resample = rng.integers(0, cards[knob])
+        u = rng.random(n_chains)
+        out.append((knob, nudge, delta, resample, u))
+    return out
+
+
+def sa_explore(predict_idx, cards, size, sched, visited, rng) -> dict:
+    """sa_explore (search.py:202-254); predict_idx maps int64 config indices -> float64 scores.
+    sched = (initial_temp, cooling, steps_per_round, parallel_chains)."""
+    t0, cooling, steps, chains = sched
+    starts = draw_unvisited(size, visited, chains, rng)
+    if not starts:
+        return {}
+    cards = np.asarray(cards, dtype=np.int64)
+    mult = space_multipliers(cards)
+    cur = decode(cards, np.array(starts, dtype=np.int64))
+    n = cur.shape[0]
+    energy = np.asarray(predict_idx((cur * mult).sum(axis=1)), dtype=np.float64)
+    history = {int(i): float(e) for i, e in zip((cur * mult).sum(axis=1), energy)}
+    temp = t0
+    rows = np.arange(n)
+    for knob, nudge, delta, resample, u in sa_draws(rng, cards, n, steps):
+        nxt = cur.copy()
+        stepped = np.clip(cur[rows, knob] + delta, 0, cards[knob] - 1)
+        nxt[rows, knob] = np.where(nudge, stepped, resample)
+        idx = (nxt * mult).sum(axis=1)
+        e_new = np.asarray(predict_idx(idx), dtype=np.float64)
+        for i, e in zip(idx, e_new):
+            history[int(i)] = float(e)
+        downhill_p = np.exp(np.minimum((e_new - energy) / temp, 0.0))
+        accept = (e_new >= energy) | (u < downhill_p)
+        cur = np.where(accept[:, None], nxt, cur)
+        energy = np.where(accept, e_new, energy)
+        temp = max(temp * cooling, 1e-9)
+    return history
+
+
+def sa_propose(predict_idx, cards, size, sched, visited, rng, batch) -> list:
+    """sa_propose (search.py:266-281): explore, rank, top up with unvisited draws."""
+    history = sa_explore(predict_idx, cards, size, sched, visited, rng)
+    picks = rank_history(np.array(list(history.keys()), dtype=np.int64),
+                         np.array(list(history.values())), visited, batch)
+    if len(picks) < batch:
+        picks += draw_unvisited(size, visited | set(picks), batch - len(picks), rng)
+    return picks

@@ -1,0 +1,79 @@
+// Simulated-annealing exploration (sa_explore, search.py:202-254) on the device.
+//
+// The chains' random draws (knob, nudge, delta, resample, u per step and chain)
+// do not depend on the predictions, so the host draws them from the caller's
+// numpy Generator in the reference's order and uploads them once; the device then
+// runs every step:  kt_sa_propose (the nudged / resampled neighbour and its config
+// index, search.py:232-241), the fused scorer on the n_chains neighbours, and
+// kt_sa_accept (Metropolis test in fp64, search.py:246-251).  With the same draws
+// and the same predictor values the trajectory -- and so the exploration history
+// -- is identical to the reference loop's.
+#include "kt_common.cuh"
+
+namespace kt {
+namespace sa {
+
+__global__ void propose_kernel(const int32_t* __restrict__ cur, int n_chains, int n_knobs,
+                               const int32_t* __restrict__ cards, const int64_t* __restrict__ mult,
+                               const int32_t* __restrict__ knob, const uint8_t* __restrict__ nudge,
+                               const int32_t* __restrict__ delta, const int32_t* __restrict__ resample,
+                               int32_t* __restrict__ nxt, int64_t* __restrict__ nxt_idx) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_chains) return;
+  const int kn = knob[c];
+  int64_t id = 0;
+  for (int j = 0; j < n_knobs; ++j) {
+    int v = cur[c * n_knobs + j];
+    if (j == kn) {
+      // np.clip(cur + delta, 0, card - 1) if nudge else resample (search.py:239-241)
+      const int stepped = min(max(v + delta[c], 0), cards[j] - 1);
+      v = nudge[c] ? stepped : resample[c];
+    }
+    nxt[c * n_knobs + j] = v;
+    id += static_cast<int64_t>(v) * mult[j];  // (mat * mult).sum(axis=1), search.py:220-221
+  }
+  nxt_idx[c] = id;
+}
+
+__global__ void accept_kernel(int n_chains, int n_knobs, const float* __restrict__ e_new,
+                              const double* __restrict__ u, double temp, const int32_t* __restrict__ nxt,
+                              int32_t* __restrict__ cur, double* __restrict__ energy) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_chains) return;
+  const double en = static_cast<double>(e_new[c]);
+  const double eo = energy[c];
+  // downhill_p = exp(min((e_new - energy) / temp, 0)); uphill always accepted (search.py:246-248)
+  const double p = exp(fmin((en - eo) / temp, 0.0));
+  const bool acc = (en >= eo) || (u[c] < p);
+  if (acc) {
+    for (int j = 0; j < n_knobs; ++j) cur[c * n_knobs + j] = nxt[c * n_knobs + j];
+    energy[c] = en;
+  }
+}
+
+}  // namespace sa
+}  // namespace kt
+
+extern "C" int kt_sa_propose(const int32_t* cur, int32_t n_chains, int32_t n_knobs, const int32_t* cards,
+                             const int64_t* mult, const int32_t* knob, const uint8_t* nudge, const int32_t* delta,
+                             const int32_t* resample, int32_t* nxt, int64_t* nxt_idx, void* stream) {
+  KT_REQUIRE(cur && cards && mult && knob && nudge && delta && resample && nxt && nxt_idx, KT_E_ARG,
+             "kt_sa_propose: null pointer");
+  KT_REQUIRE(n_chains > 0, KT_E_EMPTY, "kt_sa_propose: no chains");
+  KT_REQUIRE(n_knobs > 0 && n_knobs <= KT_MAX_KNOBS, KT_E_SHAPE, "kt_sa_propose: 1..%d knobs", KT_MAX_KNOBS);
+  kt::sa::propose_kernel<<<(n_chains + 127) / 128, 128, 0, kt::as_stream(stream)>>>(
+      cur, n_chains, n_knobs, cards, mult, knob, nudge, delta, resample, nxt, nxt_idx);
+  kt::note_launches(1);
+  return kt::check_launch("kt_sa_propose");
+}
+
+extern "C" int kt_sa_accept(int32_t n_chains, int32_t n_knobs, const float* e_new, const double* u, double temp,
+                            const int32_t* nxt, int32_t* cur, double* energy, void* stream) {
+  KT_REQUIRE(e_new && u && nxt && cur && energy, KT_E_ARG, "kt_sa_accept: null pointer");
+  KT_REQUIRE(n_chains > 0, KT_E_EMPTY, "kt_sa_accept: no chains");
+  KT_REQUIRE(temp > 0.0, KT_E_RANGE, "kt_sa_accept: temperature must be positive");
+  kt::sa::accept_kernel<<<(n_chains + 127) / 128, 128, 0, kt::as_stream(stream)>>>(n_chains, n_knobs, e_new, u,
+                                                                                   temp, nxt, cur, energy);
+  kt::note_launches(1);
+  return kt::check_launch("kt_sa_accept");
+}

@@ -11,11 +11,13 @@ candidate sets `score_indices` + `topk` stay on the device end to end.
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
 import torch
 
 from . import _lib
-from .errors import DomainError
+from .errors import DomainError, NumericError
 from .graphs import BatchLayout, batch_layout, configs_to_indices, device_spec_table
 from .kernels import KernelSpec, KnobSpace
 from .model import ModelState, dims_of, flat_params
@@ -240,3 +242,198 @@ class Sweeper:
         if check and int(self.err.item()):
             raise DomainError("config index out of range for the knob space")
         return self.h_z[:n], self.h_top_idx, self.h_top_score
+
+
+# --- simulated-annealing exploration (search.py:177-281), the tuner's caller of the model ------
+
+
+@dataclass
+class SaSchedule:
+    """search.py:48-59, same defaults and validation."""
+    initial_temp: float = 1.0
+    cooling: float = 0.95
+    steps_per_round: int = 128
+    parallel_chains: int = 16
+
+    def __post_init__(self):
+        if not 0.0 < self.cooling < 1.0:
+            raise DomainError("cooling must be in (0, 1)")
+        if self.initial_temp <= 0:
+            raise DomainError("initial_temp must be positive")
+
+
+def _space_multipliers(space: KnobSpace) -> np.ndarray:
+    cards = [len(k.values) for k in space.knobs]
+    mult = np.ones(len(cards), dtype=np.int64)
+    for j in range(len(cards) - 2, -1, -1):
+        mult[j] = mult[j + 1] * cards[j + 1]
+    return mult
+
+
+def draw_unvisited(space: KnobSpace, visited: set, count: int, rng) -> list:
+    """Distinct config indices outside `visited`, uniform (search.py:185-211): the same
+    numpy Generator calls as the reference, so a shared seed gives the same indices."""
+    size = space.size
+    remaining = size - len(visited)
+    count = min(count, max(remaining, 0))
+    if count <= 0:
+        return []
+    if size <= 65536:
+        unvisited = np.array([i for i in range(size) if i not in visited], dtype=np.int64)
+        pick = rng.choice(len(unvisited), size=count, replace=False)
+        return [int(unvisited[i]) for i in pick]
+    out: list = []
+    chosen: set = set()
+    guard = 0
+    while len(out) < count:
+        need = count - len(out)
+        for v in rng.integers(0, size, size=need + 8):
+            i = int(v)
+            if i not in visited and i not in chosen:
+                chosen.add(i)
+                out.append(i)
+                if len(out) == count:
+                    break
+        guard += 1
+        if guard > 10000:
+            raise NumericError("unvisited sampling failed to converge")
+    return out
+
+
+class DeviceAnnealer:
+    """sa_explore's chains on the GPU for one CostModelPredictor.
+
+    Every step is kt_sa_propose -> fused scorer -> kt_sa_accept on device-resident
+    chain state; the per-step random draws come from the caller's Generator in the
+    reference's order (they never depend on the predictions), and the whole
+    step sequence is captured once into a CUDA graph and replayed."""
+
+    def __init__(self, predictor: CostModelPredictor, sched: SaSchedule, n_chains: int):
+        m, space = predictor.m, predictor.space
+        if not _default_model(m) or space.size >= 2**32:
+            raise DomainError("device annealing needs the default model dims and a space < 2^32")
+        self.pred, self.sched, self.n = predictor, sched, n_chains
+        self.lib = _lib.load()
+        self.flat = flat_params(m)
+        dev = self.dev = self.flat.device
+        self.dims = dims_of(m)
+        self.tab = device_spec_table(predictor.spec, space, predictor.layout, m.feature_norm.mean,
+                                     m.feature_norm.std, device=dev)
+        self.cards_np = np.array([len(k.values) for k in space.knobs], dtype=np.int64)
+        self.nk = len(self.cards_np)
+        self.cards = torch.from_numpy(self.cards_np.astype(np.int32)).to(dev)
+        self.mult = torch.from_numpy(_space_multipliers(space)).to(dev)
+        steps, n, nk = sched.steps_per_round, n_chains, self.nk
+        self.knob = torch.empty((steps, n), dtype=torch.int32, device=dev)
+        self.nudge = torch.empty((steps, n), dtype=torch.uint8, device=dev)
+        self.delta = torch.empty((steps, n), dtype=torch.int32, device=dev)
+        self.resample = torch.empty((steps, n), dtype=torch.int32, device=dev)
+        self.u = torch.empty((steps, n), dtype=torch.float64, device=dev)
+        self.cur = torch.empty((n, nk), dtype=torch.int32, device=dev)
+        self.nxt = torch.empty((n, nk), dtype=torch.int32, device=dev)
+        self.energy = torch.empty(n, dtype=torch.float64, device=dev)
+        self.hist_idx = torch.empty((steps + 1, n), dtype=torch.int64, device=dev)
+        self.hist_z = torch.empty((steps + 1, n), dtype=torch.float32, device=dev)
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.temps = []
+        t = sched.initial_temp
+        for _ in range(steps):
+            self.temps.append(t)
+            t = max(t * sched.cooling, 1e-9)
+        self.graph = None
+
+    def _score(self, i, st):
+        p = _lib.ptr
+        _lib.check(self.lib.kt_score_indices(p(self.tab), self.dims, p(self.flat), p(self.hist_idx[i]), 0, self.n,
+                                             p(self.hist_z[i]), None, p(self.err), st), "sa score")
+
+    def _steps(self):
+        p = _lib.ptr
+        st = _lib.stream_handle(self.dev)
+        self._score(0, st)
+        self.energy.copy_(self.hist_z[0].double())
+        for s in range(self.sched.steps_per_round):
+            _lib.check(self.lib.kt_sa_propose(p(self.cur), self.n, self.nk, p(self.cards), p(self.mult),
+                                              p(self.knob[s]), p(self.nudge[s]), p(self.delta[s]),
+                                              p(self.resample[s]), p(self.nxt), p(self.hist_idx[s + 1]), st),
+                       "sa propose")
+            self._score(s + 1, st)
+            _lib.check(self.lib.kt_sa_accept(self.n, self.nk, p(self.hist_z[s + 1]), p(self.u[s]), self.temps[s],
+                                             p(self.nxt), p(self.cur), p(self.energy), st), "sa accept")
+
+    def explore(self, starts: list, rng) -> dict:
+        steps, n = self.sched.steps_per_round, self.n
+        knob = np.empty((steps, n), dtype=np.int32)
+        nudge = np.empty((steps, n), dtype=np.uint8)
+        delta = np.empty((steps, n), dtype=np.int32)
+        resample = np.empty((steps, n), dtype=np.int32)
+        u = np.empty((steps, n), dtype=np.float64)
+        for s in range(steps):  # search.py:233-237, same calls in the same order
+            k = rng.integers(0, self.nk, size=n)
+            knob[s] = k
+            nudge[s] = rng.random(n) < 0.5
+            delta[s] = rng.integers(0, 2, size=n) * 2 - 1
+            resample[s] = rng.integers(0, self.cards_np[k])
+            u[s] = rng.random(n)
+        with torch.cuda.device(self.dev):
+            for dst, src in ((self.knob, knob), (self.nudge, nudge), (self.delta, delta),
+                             (self.resample, resample), (self.u, u)):
+                dst.copy_(torch.from_numpy(src), non_blocking=False)
+            start_idx = np.array(starts, dtype=np.int64)
+            self.hist_idx[0].copy_(torch.from_numpy(start_idx))
+            choices = np.zeros((n, self.nk), dtype=np.int64)
+            rest = start_idx.copy()
+            for j in range(self.nk - 1, -1, -1):
+                choices[:, j] = rest % self.cards_np[j]
+                rest //= self.cards_np[j]
+            self.cur.copy_(torch.from_numpy(choices.astype(np.int32)))
+            if self.graph is None:
+                self._steps()  # eager first run (kernel attributes set outside capture)
+                torch.cuda.synchronize(self.dev)
+                self.hist_idx[0].copy_(torch.from_numpy(start_idx))
+                self.cur.copy_(torch.from_numpy(choices.astype(np.int32)))
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._steps()
+                self.graph = g
+            self.graph.replay()
+            hi = self.hist_idx.cpu().numpy().reshape(-1)
+            hz = self.hist_z.double().cpu().numpy().reshape(-1)
+        history: dict = {}
+        for i, e in zip(hi, hz):  # insertion order: starts, then each step's chains
+            history[int(i)] = float(e)
+        return history
+
+
+_ANNEALERS: dict = {}
+
+
+def sa_explore(predict, space: KnobSpace, sched: SaSchedule, visited: set, rng) -> dict:
+    """Parallel annealing chains maximizing the cost model (search.py:202-254); returns
+    {config_index: score} over everything any chain evaluated, in the reference's
+    insertion order.  `predict` must be a CostModelPredictor: the chains run on the
+    device (there is no host loop)."""
+    if not isinstance(predict, CostModelPredictor):
+        raise DomainError("sa_explore runs on the device and needs a CostModelPredictor as `predict`")
+    starts = draw_unvisited(space, visited, sched.parallel_chains, rng)
+    if not starts:
+        return {}
+    key = (id(predict), sched.initial_temp, sched.cooling, sched.steps_per_round, len(starts))
+    ann = _ANNEALERS.get(key)
+    if ann is None or ann.pred is not predict:
+        if len(_ANNEALERS) > 16:
+            _ANNEALERS.clear()
+        ann = _ANNEALERS[key] = DeviceAnnealer(predict, sched, len(starts))
+    return ann.explore(starts, rng)
+
+
+def sa_propose(predict, space: KnobSpace, sched: SaSchedule, visited: set, rng, batch: int) -> list:
+    """Annealing proposal (search.py:266-281): explore, take the best unvisited configs
+    seen, top up with uniform unvisited draws."""
+    from .kernels import index_config
+
+    history = sa_explore(predict, space, sched, visited, rng)
+    picks = rank_history(history, visited, batch)
+    if len(picks) < batch:
+        picks += draw_unvisited(space, visited | set(picks), batch - len(picks), rng)
+    return [index_config(space, i) for i in picks]

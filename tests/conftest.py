@@ -59,6 +59,11 @@ def g_meta():
 
 
 @pytest.fixture(scope="session")
+def g_sa():
+    return load_golden("sa")
+
+
+@pytest.fixture(scope="session")
 def g_rank():
     return load_golden("rank")
 

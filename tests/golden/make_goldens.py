@@ -17,6 +17,8 @@ Everything is keyed by `rng_from` so reruns are byte-identical.  Outputs:
   meta.npz       meta_step FO + SO (meta.py:223), fine_tune_embedded (meta.py:274),
                  sample_meta_tasks draws (meta.py:136) as dataset positions
   rank.npz       rank_history orderings (search.py:257) on tie-heavy scores
+  sa.npz         sa_explore histories (search.py:202-254) and sa_propose picks
+                 (search.py:266-281) driven by a synthetic, index-keyed predictor
 """
 
 from __future__ import annotations
@@ -236,7 +238,37 @@ def rank_goldens():
     np.savez_compressed(os.path.join(OUT, "rank.npz"), **out)
 
 
+def sa_synthetic(space, configs):
+    """Deterministic stand-in predictor: a scrambled function of the config index."""
+    idx = np.array([rk.config_index(space, c) for c in configs], dtype=np.int64)
+    return ((idx * 2654435761) % 1000003).astype(np.float64) / 1000003.0
+
+
+SA_CASES = ((16, 40, 0), (5, 17, 300), (16, 128, 40))  # (chains, steps, visited)
+
+
+def sa_goldens():
+    space = rk.build_knob_space(BENCH_SPEC)
+    out = {}
+    for case, (chains, steps, n_vis) in enumerate(SA_CASES):
+        visited = set(int(v) for v in rng_from("golden-sa-visited", case).integers(0, space.size, n_vis))
+        sched = rs.SaSchedule(initial_temp=1.0, cooling=0.95, steps_per_round=steps, parallel_chains=chains)
+        hist = rs.sa_explore(lambda cfgs: sa_synthetic(space, cfgs), space, sched, visited,
+                             rng_from("golden-sa", case))
+        out[f"c{case}/idx"] = np.array(list(hist.keys()), dtype=np.int64)
+        out[f"c{case}/score"] = np.array(list(hist.values()), dtype=np.float64)
+        out[f"c{case}/visited"] = np.array(sorted(visited), dtype=np.int64)
+        picks = rs.sa_propose(lambda cfgs: sa_synthetic(space, cfgs), space, sched, visited,
+                              rng_from("golden-sa-propose", case), 24)
+        out[f"c{case}/propose"] = np.array([rk.config_index(space, c) for c in picks], dtype=np.int64)
+    out["cases"] = np.array(SA_CASES, dtype=np.int64)
+    np.savez_compressed(os.path.join(OUT, "sa.npz"), **out)
+
+
 def main():
+    if sys.argv[1:] == ["sa"]:
+        sa_goldens()
+        return
     golden_graph_text()
     encode_goldens()
     items = corpus()
@@ -245,6 +277,7 @@ def main():
     head_goldens(m)
     meta_goldens(items, m)
     rank_goldens()
+    sa_goldens()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))
 
