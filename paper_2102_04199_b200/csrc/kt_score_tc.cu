@@ -16,19 +16,22 @@
 //   GEMM3  D3[128x64] = U * H0 (+b0, ReLU)          (A = U in smem, 8 K-steps x 3)
 //   GEMM4  D4[128x64] = Z1 * H1 (+b1, ReLU) . w3 + b3 (A = Z1 in smem)
 //
-// Warp roles (544 threads = 17 warps, 1 CTA / SM, 512 TMEM columns):
+// Warp roles (608 threads = 19 warps, 1 CTA / SM, 512 TMEM columns):
 //   warps 0-3    R: thread = TMEM lane = graph; ReLU(D1) split hi/lo into R (TMEM)
 //   warps 4-7    encode: thread = graph; index decode once per tile, then one
 //                normalised feature row per chunk (fp64 touched / log2 / z-norm,
 //                host tables for the rest), hi/lo split, tcgen05.st into an X slot
-//   warp 8       MMA: a non-blocking scheduler that polls the ring barriers and
-//                issues whichever GEMM is ready (one elected lane issues)
+//   warps 8, 17, 18  MMA issue, one stream each: GEMM1s, GEMM2s, head GEMMs (one
+//                elected lane issues; each waits only on its own operand barrier)
 //   warps 9-16   readout + head: two warps per lane quadrant, 16 channels each;
 //                running sum / ReLU-sum / max over the chunks, then the head
 //                epilogues (U -> smem, ReLU(D3 + b0) -> smem, (D4 + b1) . w3)
 // Rings: X 4 slots, D1 / R / D2 double-buffered; the R warps and the readout
 // warps never wait on each other, and the head of tile t overlaps the GCN
-// chunks of tile t+1 on the tensor pipe.
+// chunks of tile t+1 on the tensor pipe.  A stage's second dependency is folded
+// into the stage that feeds it (the encode warps wait for D1 to drain before
+// publishing X, the R warps for D2 before publishing R), so every issue stream
+// waits on a single barrier per GEMM.
 #include "kt_encode.cuh"
 #include "kt_tc.cuh"
 
@@ -55,7 +58,7 @@ namespace tcs {
 
 using namespace kt::tc;
 
-constexpr int NT = 544;  // 17 warps
+constexpr int NT = 608;  // 19 warps
 constexpr int GT = 128;   // graphs per tile (one TMEM lane each)
 constexpr int H = 64;
 constexpr int XS = 4;     // X ring slots
@@ -344,7 +347,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         if (g == 0) TRACE(0, q);
       }
     }
-  } else if (warp == 8) {
+  } else if (warp == 8 || warp >= 17) {
     // ===================== MMA: fixed issue order, blocking waits, one elected lane issues =====
     // Order per chunk q: GEMM1(q + 2), GEMM2(q); the head of tile t is issued two
     // (GEMM3) and three (GEMM4) chunks into tile t + 1, so its epilogue overlaps the
@@ -423,30 +426,19 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       }
       __syncwarp();
     };
-    constexpr int LA = 2;  // GEMM1 runs this many chunks ahead of GEMM2
-    for (int64_t q = 0; q < LA && q < n_chunks; ++q) g1(q);
-    // The head of tile t must be issued no later than right after GEMM2 of chunk
-    // last(t) + 2: GEMM2 of last(t) + 3 needs the D2 buffer the readout warps free only
-    // after finishing the head of tile t (GEMM4's result).
-    int64_t head_t = -1, head_at = 0;
-    auto head = [&]() {
-      g3(head_t);
-      g4(head_t);
-      head_t = -1;
-    };
-    int kc = 0;
-    for (int64_t q = 0; q < n_chunks; ++q) {
-      if (q + LA < n_chunks) g1(q + LA);
-      g2(q);
-      if (head_t >= 0 && q >= head_at) head();
-      if (++kc == C) {  // tile q / C complete: schedule its head (flush one still pending)
-        kc = 0;
-        if (head_t >= 0) head();
-        head_t = q / C;
-        head_at = q + 2;
+    // Three independent issue streams, one warp each: tcgen05.commit tracks the MMAs of
+    // the issuing thread only, so GEMM1s, GEMM2s and the head GEMMs need no common
+    // program order -- their data dependencies all go through the ring barriers.
+    if (warp == 8) {
+      for (int64_t q = 0; q < n_chunks; ++q) g1(q);
+    } else if (warp == 17) {
+      for (int64_t q = 0; q < n_chunks; ++q) g2(q);
+    } else {
+      for (int64_t t = 0; t < my_tiles; ++t) {
+        g3(t);
+        g4(t);
       }
     }
-    if (head_t >= 0) head();
   } else if (warp < 4) {
     // ===================== R: ReLU(D1) -> R (hi, lo) in TMEM; thread = lane = graph ===============
     const int g = tid;
