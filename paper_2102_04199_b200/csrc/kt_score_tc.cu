@@ -16,9 +16,11 @@
 //   GEMM3  D3[128x64] = U * H0 (+b0, ReLU)          (A = U in smem, 8 K-steps x 3)
 //   GEMM4  D4[128x64] = Z1 * H1 (+b1, ReLU) . w3 + b3 (A = Z1 in smem)
 //
-// Warp roles (608 threads = 19 warps, 1 CTA / SM, 512 TMEM columns):
+// Warp roles (640 threads = 20 warps, 1 CTA / SM, 512 TMEM columns):
 //   warps 0-3    R: thread = TMEM lane = graph; ReLU(D1) split hi/lo into R (TMEM)
-//   warps 4-7    encode: thread = graph; index decode once per tile, then one
+//   warp 19      decode: config index -> per-axis table entries and unroll flags for
+//                the next tile, into a double-buffered smem slot
+//   warps 4-7    encode: thread = graph; one
 //                normalised feature row per chunk (fp64 touched / log2 / z-norm,
 //                host tables for the rest), hi/lo split, tcgen05.st into an X slot
 //   warps 8, 17, 18  MMA issue, one stream each: GEMM1s, GEMM2s, head GEMMs (one
@@ -28,10 +30,8 @@
 //                epilogues (U -> smem, ReLU(D3 + b0) -> smem, (D4 + b1) . w3)
 // Rings: X 4 slots, D1 / R / D2 double-buffered; the R warps and the readout
 // warps never wait on each other, and the head of tile t overlaps the GCN
-// chunks of tile t+1 on the tensor pipe.  A stage's second dependency is folded
-// into the stage that feeds it (the encode warps wait for D1 to drain before
-// publishing X, the R warps for D2 before publishing R), so every issue stream
-// waits on a single barrier per GEMM.
+// chunks of tile t+1 on the tensor pipe.  The issue warps carry the waits
+// (operand full + accumulator drained), keeping them off the CUDA-core stages.
 #include "kt_encode.cuh"
 #include "kt_tc.cuh"
 
@@ -39,7 +39,7 @@
 // CTA 0's pipeline events.  Compiled out of the product library.
 #ifdef KT_TC_TRACE
 #define KT_TRACE_N 64
-__device__ long long g_kt_trace[24][KT_TRACE_N];
+__device__ long long g_kt_trace[32][KT_TRACE_N];
 #define TRACE(ev, i)                                              \
   do {                                                            \
     if (blockIdx.x == 0 && (i) < KT_TRACE_N) g_kt_trace[ev][i] = clock64(); \
@@ -58,7 +58,7 @@ namespace tcs {
 
 using namespace kt::tc;
 
-constexpr int NT = 608;  // 19 warps
+constexpr int NT = 640;  // 20 warps
 constexpr int GT = 128;   // graphs per tile (one TMEM lane each)
 constexpr int H = 64;
 constexpr int XS = 4;     // X ring slots
@@ -86,7 +86,15 @@ struct __align__(1024) Smem {
   double2 l2[TAB];  // numpy log2 of (outer, inner) extent
   float nconst[KT_MAX_LOOPS][8];
   int tab_off[KT_MAX_AXES];
-  short sel[KT_MAX_AXES][GT];  // per graph: packed table entry of each axis' tile choice
+  short sel[2][KT_MAX_AXES][GT];  // per tile buffer, graph: packed table entry of each axis' tile choice
+  unsigned char unr[2][GT];       // per graph: bit a = inner loop of axis a unrolled
+  unsigned char okf[2][GT];       // per graph: valid config index
+  uint64_t dec_full[2], dec_free[2];
+  unsigned long long magic[KT_MAX_KNOBS];
+  uint32_t card[KT_MAX_KNOBS];
+  int axis_knob[KT_MAX_AXES];
+  int auto_vals[4], expl_vals[2];
+  int auto_knob, expl_knob;
   uint64_t x_full[XS], x_empty[XS];
   uint64_t d1_full[2], d1_empty[2], r_full[2], r_empty[2], d2_full[2], d2_empty[2];
   uint64_t u_full, z_full, d3_full, d4_full;
@@ -148,7 +156,16 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
   }
   if (tid < 32) S.agg[tid] = params[dims.off_agg + tid];
   const int na = T.n_axes, n_loops = T.n_loops;
+  if (tid < KT_MAX_KNOBS) {
+    S.card[tid] = T.card[tid];
+    S.magic[tid] = T.card_magic[tid];
+  }
+  if (tid < KT_MAX_AXES) S.axis_knob[tid] = T.axis_knob[tid];
+  if (tid < 4) S.auto_vals[tid] = T.auto_vals[tid];
+  if (tid < 2) S.expl_vals[tid] = T.expl_vals[tid];
   if (tid == 0) {
+    S.auto_knob = T.auto_knob;
+    S.expl_knob = T.expl_knob;
     int off = 0;
     for (int a = 0; a < na; ++a) {
       S.tab_off[a] = off;
@@ -167,6 +184,10 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       mbar_init(&S.d2_empty[b], 8);
     }
     mbar_init(&S.u_full, 8);
+    mbar_init(&S.dec_full[0], 1);
+    mbar_init(&S.dec_full[1], 1);
+    mbar_init(&S.dec_free[0], 4);
+    mbar_init(&S.dec_free[1], 4);
     mbar_init(&S.z_full, 8);
     mbar_init(&S.d3_full, 1);
     mbar_init(&S.d4_full, 1);
@@ -221,64 +242,10 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     const double m8 = T.fmean[8], r8 = 1.0 / T.fstd[8], m9 = T.fmean[9] - 1.0, r9 = 1.0 / T.fstd[9];
     int64_t q = 0;
     for (int64_t ti = 0; ti < my_tiles; ++ti) {
-      const int64_t gi = (blockIdx.x + ti * gridDim.x) * GT + g;
-      bool ok = false;
-      int ch[KT_MAX_KNOBS];
-#pragma unroll
-      for (int j = 0; j < KT_MAX_KNOBS; ++j) ch[j] = 0;
-      if (gi < B) {
-        const int64_t v = idx ? idx[gi] : idx_base + gi;
-        ok = v >= 0 && static_cast<uint64_t>(v) < size;
-        if (ok && size <= 0xffffffffull) {
-          uint32_t r = static_cast<uint32_t>(v);
-#pragma unroll
-          for (int j = KT_MAX_KNOBS - 1; j >= 0; --j) {
-            if (j < n_knobs) {
-              const uint32_t d = T.card[j];
-              const uint32_t qq = udiv(r, d, T.card_magic[j]);
-              ch[j] = static_cast<int>(r - qq * d);
-              r = qq;
-            }
-          }
-        } else if (ok) {
-          uint64_t r = static_cast<uint64_t>(v);
-#pragma unroll
-          for (int j = KT_MAX_KNOBS - 1; j >= 0; --j) {
-            if (j < n_knobs) {
-              const uint64_t d = T.card[j];
-              const uint64_t qq = r / d;
-              ch[j] = static_cast<int>(r - qq * d);
-              r = qq;
-            }
-          }
-        } else {
-          atomicOr(err, 1);
-        }
-      }
-      // per-axis table entries and unroll flags, with ch[] only indexed by unrolled
-      // constants (keeps it in registers)
-      int ca_auto = 0, ca_expl = 0;
-#pragma unroll
-      for (int j = 0; j < KT_MAX_KNOBS; ++j) {
-        if (j == T.auto_knob) ca_auto = ch[j];
-        if (j == T.expl_knob) ca_expl = ch[j];
-      }
-      const int autov = T.auto_knob >= 0 ? T.auto_vals[ca_auto] : 0;
-      const int expl = T.expl_knob >= 0 ? T.expl_vals[ca_expl] : 0;
-      unsigned unr_mask = 0;
-#pragma unroll
-      for (int a = 0; a < KT_MAX_AXES; ++a) {
-        if (a < na) {
-          const int kn = T.axis_knob[a];
-          int c = 0;
-#pragma unroll
-          for (int j = 0; j < KT_MAX_KNOBS; ++j)
-            if (j == kn) c = ch[j];
-          const int e = S.tab_off[a] + c;
-          S.sel[a][g] = static_cast<short>(e);
-          if (expl != 0 && autov > 0 && S.oi[e].y <= autov) unr_mask |= 1u << a;
-        }
-      }
+      const int db = static_cast<int>(ti & 1);
+      mbar_wait(&S.dec_full[db], static_cast<uint32_t>((ti >> 1) & 1));  // decoder warp done
+      const bool ok = S.okf[db][g] != 0;
+      const unsigned unr_mask = S.unr[db][g];
       // loops are emitted innermost first (k = n_loops-1 .. 0), so touched -- the
       // product of the extents of the loops inside loop k, multiplied innermost
       // outward as np.cumprod(e[::-1]) does -- accumulates exactly in fp64, and
@@ -290,8 +257,9 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         const int k = C - 1 - c;
         const int level = k >= na;
         const int a = level ? k - na : k;
-        const int e = S.sel[a][g];
+        const int e = S.sel[db][a][g];
         const int2 oi = S.oi[e];
+        if (g == 0) TRACE(19, q);
         float x[16];
 #pragma unroll
         for (int f = 12; f < 16; ++f) x[f] = 0.0f;
@@ -331,23 +299,112 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
           hl[16 + f] = x[f] - hl[f];
         }
         const int s = static_cast<int>(q % XS);
+        if (g == 0) TRACE(20, q);
         mbar_wait(&S.x_empty[s], static_cast<uint32_t>(((q / XS) & 1) ^ 1));
         __syncwarp();
+        if (g == 0) TRACE(21, q);
         tc_fence_after();
 #ifndef KT_DBG_NO_XST
         tmem_st32(tmem + lane + T_X + 32 * s, hl);
 #endif
         tmem_wait_st();
-        // fold GEMM1's second dependency in here: D1[q & 1] drained by the R warps
-        // (chunk q - 2), so the MMA warp waits on x_full alone
-        mbar_wait(&S.d1_empty[q & 1], static_cast<uint32_t>(((q >> 1) & 1) ^ 1));
-        __syncwarp();
         tc_fence_before();
         warp_arrive(&S.x_full[s]);
         if (g == 0) TRACE(0, q);
       }
+      warp_arrive(&S.dec_free[db]);  // this tile's decode buffer can be refilled
     }
-  } else if (warp == 8 || warp >= 17) {
+  } else if (warp == 19) {
+    // ===================== decoder: config index -> per-axis table entries, one tile ahead ======
+    const int lane32 = tid & 31;
+    const int n_knobs = T.n_knobs;
+    const int auto_knob = S.auto_knob, expl_knob = S.expl_knob;
+    // loop-invariant tables in registers (the decoder warp has registers to spare)
+    uint32_t cardr[KT_MAX_KNOBS];
+    uint64_t magicr[KT_MAX_KNOBS];
+#pragma unroll
+    for (int j = 0; j < KT_MAX_KNOBS; ++j) {
+      cardr[j] = S.card[j];
+      magicr[j] = S.magic[j];
+    }
+    int aknob[KT_MAX_AXES], aoff[KT_MAX_AXES];
+#pragma unroll
+    for (int a = 0; a < KT_MAX_AXES; ++a) {
+      aknob[a] = S.axis_knob[a];
+      aoff[a] = S.tab_off[a];
+    }
+    for (int64_t ti = 0; ti < my_tiles; ++ti) {
+      const int db = static_cast<int>(ti & 1);
+      mbar_wait(&S.dec_free[db], static_cast<uint32_t>(((ti >> 1) & 1) ^ 1));  // tile ti-2 consumed
+      __syncwarp();
+      if (lane32 == 0) TRACE(24, ti);
+      int64_t vv[GT / 32];  // all four index loads in flight before any decode
+#pragma unroll
+      for (int i = 0; i < GT / 32; ++i) {
+        const int64_t gi = (blockIdx.x + ti * gridDim.x) * GT + lane32 + 32 * i;
+        vv[i] = gi >= B ? 0 : (idx ? __ldcs(idx + gi) : idx_base + gi);
+      }
+#pragma unroll
+      for (int i = 0; i < GT / 32; ++i) {
+        const int g = lane32 + 32 * i;
+        const int64_t gi = (blockIdx.x + ti * gridDim.x) * GT + g;
+        const bool pad = gi >= B;
+        const int64_t v = vv[i];
+        const bool ok = !pad && v >= 0 && static_cast<uint64_t>(v) < size;
+        if (!pad && !ok) atomicOr(err, 1);
+        // mixed-radix decode, knob 0 most significant (kernels.py:278-286)
+        int ch[KT_MAX_KNOBS];
+#pragma unroll
+        for (int j = 0; j < KT_MAX_KNOBS; ++j) ch[j] = 0;
+        if (ok && size <= 0xffffffffull) {
+          uint32_t r = static_cast<uint32_t>(v);
+#pragma unroll
+          for (int j = KT_MAX_KNOBS - 1; j >= 0; --j) {
+            if (j < n_knobs) {
+              const uint32_t qq = udiv(r, cardr[j], magicr[j]);
+              ch[j] = static_cast<int>(r - qq * cardr[j]);
+              r = qq;
+            }
+          }
+        } else if (ok) {
+          uint64_t r = static_cast<uint64_t>(v);
+#pragma unroll
+          for (int j = KT_MAX_KNOBS - 1; j >= 0; --j) {
+            if (j < n_knobs) {
+              const uint64_t qq = r / cardr[j];
+              ch[j] = static_cast<int>(r - qq * cardr[j]);
+              r = qq;
+            }
+          }
+        }
+        int ca = 0, ce = 0;
+#pragma unroll
+        for (int j = 0; j < KT_MAX_KNOBS; ++j) {
+          if (j == auto_knob) ca = ch[j];
+          if (j == expl_knob) ce = ch[j];
+        }
+        const int autov = auto_knob >= 0 ? S.auto_vals[ca] : 0;
+        const int expl = expl_knob >= 0 ? S.expl_vals[ce] : 0;
+        unsigned unr = 0;
+#pragma unroll
+        for (int a = 0; a < KT_MAX_AXES; ++a) {
+          if (a < na) {
+            int c = 0;
+#pragma unroll
+            for (int j = 0; j < KT_MAX_KNOBS; ++j)
+              if (j == aknob[a]) c = ch[j];
+            const int e = aoff[a] + c;
+            S.sel[db][a][g] = static_cast<short>(e);
+            if (expl != 0 && autov > 0 && S.oi[e].y <= autov) unr |= 1u << a;
+          }
+        }
+        S.unr[db][g] = static_cast<unsigned char>(unr);
+        S.okf[db][g] = ok ? 1 : 0;
+      }
+      if (lane32 == 0) TRACE(25, ti);
+      warp_arrive(&S.dec_full[db]);
+    }
+  } else if (warp == 8 || warp == 17 || warp == 18) {
     // ===================== MMA: fixed issue order, blocking waits, one elected lane issues =====
     // Order per chunk q: GEMM1(q + 2), GEMM2(q); the head of tile t is issued two
     // (GEMM3) and three (GEMM4) chunks into tile t + 1, so its epilogue overlaps the
@@ -362,7 +419,8 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     auto g1 = [&](int64_t q) {
       const int s = static_cast<int>(q % XS), b = static_cast<int>(q & 1);
       if ((tid & 31) == 0) TRACE(22, q);
-      wait_bar(&S.x_full[s], static_cast<uint32_t>((q / XS) & 1));  // implies D1[b] drained
+      wait_bar(&S.x_full[s], static_cast<uint32_t>((q / XS) & 1));
+      wait_bar(&S.d1_empty[b], static_cast<uint32_t>(((q >> 1) & 1) ^ 1));
       if ((tid & 31) == 0) TRACE(23, q);
       const uint32_t xh = tmem + T_X + 32 * s, xl = xh + 16, d = tmem + T_D1 + 32 * b;
       if (elect_one()) {
@@ -382,7 +440,8 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       const int b = static_cast<int>(q & 1);
       const uint32_t ph = static_cast<uint32_t>((q >> 1) & 1);
       if ((tid & 31) == 0) TRACE(17, q);
-      wait_bar(&S.r_full[b], ph);  // implies D2[b] drained
+      wait_bar(&S.r_full[b], ph);
+      wait_bar(&S.d2_empty[b], ph ^ 1);
       if ((tid & 31) == 0) TRACE(18, q);
       const uint32_t rh = tmem + T_R + 64 * b, rl = rh + 32, d = tmem + T_D2 + 32 * b;
       if (elect_one()) {
@@ -476,10 +535,6 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       if (g == 0) TRACE(15, q);
       tmem_wait_st();
       if (g == 0) TRACE(16, q);
-      // fold GEMM2's second dependency in here: D2[b] drained by the readout warps
-      // (chunk q - 2), so the MMA warp waits on r_full alone
-      mbar_wait(&S.d2_empty[b], ph ^ 1);
-      __syncwarp();
       tc_fence_before();
       warp_arrive(&S.r_full[b]);
       if (g == 0) TRACE(6, q);

@@ -47,7 +47,7 @@ idx = torch.randint(0, space.size, (1 << 20,), device=dev)
 for _ in range(3):
     ps.score_indices(m, spec, space, lay, idx)
 torch.cuda.synchronize()
-buf = np.zeros((24, 64), dtype=np.int64)
+buf = np.zeros((32, 64), dtype=np.int64)
 L.kt_debug_trace_read(buf.ctypes.data)
 names = ["P_arrive", "G1_issued", "G2_issued", "G3_issued", "G4_issued", "E1_go", "E1_done", "E2_go", "E2_done",
          "H_u_done", "H_d3_go", "H_d4_go", "H_done"]
@@ -55,9 +55,12 @@ t0 = buf[0, 0]
 print("chunk " + " ".join(f"{n:>9s}" for n in ["P_arrive", "G1_issued", "G2_issued", "E1_go", "E1_ld", "E1_rfree", "E1_st", "E1_stw", "E1_done", "E2_go", "E2_done"]))
 for q in range(40):
     print(f"{q:5d} " + " ".join(f"{buf[e, q] - t0:9d}" for e in (0, 1, 2, 5, 13, 14, 15, 16, 6, 7, 8)))
-print("q: g1start g1waited g1commit | g2start g2_rfull g2_d2empty g2commit")
+print("producer tile: prologue_start decoded axes_done")
+for ti in range(5):
+    print(ti, buf[24, ti] - t0, buf[25, ti] - t0, buf[26, ti] - t0)
+print("producer q: row_start computed x_empty_ok arrive | g1start g1commit")
 for q in range(16, 40):
-    print(q, buf[22, q] - t0, buf[23, q] - t0, buf[1, q] - t0, "|", buf[17, q] - t0, buf[18, q] - t0, buf[19, q] - t0, buf[2, q] - t0)
+    print(q, buf[19, q] - t0, buf[20, q] - t0, buf[21, q] - t0, buf[0, q] - t0, "|", buf[22, q] - t0, buf[1, q] - t0)
 print("G2 q: ready-seen -> last MMA issued -> committed")
 for q in range(16, 40):
     print(q, buf[22, q] - t0, buf[23, q] - buf[22, q], buf[2, q] - buf[23, q])
