@@ -118,6 +118,7 @@ int kt_encode_raw_choices(const kt_spec_table* tab, const int64_t* choices, int6
 
 /* ---- candidate scoring (the predictor of search.py:534-541) ------------------------ */
 /* Fused encode -> GCN(12->32->32) -> weighted-sum+max readout -> head(64->64->64->1),
+ * for knob spaces below 2^32 configs (larger spaces set *err_flag = 2 and score nothing),
  * all four GEMMs on tcgen05 tensor cores in 3xTF32 (fp32-accurate),
  * for graphs on the star layouts batch_layout (graphs.py:278) produces; equals
  * head_forward_batch(embed_batch(encode_batch(...))) (model.py:185-203).

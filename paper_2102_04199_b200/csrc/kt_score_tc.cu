@@ -16,11 +16,10 @@
 //   GEMM3  D3[128x64] = U * H0 (+b0, ReLU)          (A = U in smem, 8 K-steps x 3)
 //   GEMM4  D4[128x64] = Z1 * H1 (+b1, ReLU) . w3 + b3 (A = Z1 in smem)
 //
-// Warp roles (640 threads = 20 warps, 1 CTA / SM, 512 TMEM columns):
+// Warp roles (608 threads = 19 warps, 1 CTA / SM, 512 TMEM columns):
 //   warps 0-3    R: thread = TMEM lane = graph; ReLU(D1) split hi/lo into R (TMEM)
-//   warp 19      decode: config index -> per-axis table entries and unroll flags for
-//                the next tile, into a double-buffered smem slot
-//   warps 4-7    encode: thread = graph; one
+//   warps 4-7    encode: thread = graph; per row the axis' knob digit straight from
+//                the index (two magic-number divisions), then one
 //                normalised feature row per chunk (fp64 touched / log2 / z-norm,
 //                host tables for the rest), hi/lo split, tcgen05.st into an X slot
 //   warps 8, 17, 18  MMA issue, one stream each: GEMM1s, GEMM2s, head GEMMs (one
@@ -58,7 +57,7 @@ namespace tcs {
 
 using namespace kt::tc;
 
-constexpr int NT = 640;  // 20 warps
+constexpr int NT = 608;  // 19 warps
 constexpr int GT = 128;   // graphs per tile (one TMEM lane each)
 constexpr int H = 64;
 constexpr int XS = 4;     // X ring slots
@@ -90,6 +89,10 @@ struct __align__(1024) Smem {
   unsigned char unr[2][GT];       // per graph: bit a = inner loop of axis a unrolled
   unsigned char okf[2][GT];       // per graph: valid config index
   uint64_t dec_full[2], dec_free[2];
+  // digit extraction for slot d (axes 0..5, 6 = auto_unroll knob, 7 = explicit knob):
+  // choice = (v / dmult[d]) % dcard[d], both divisions by magic multiply
+  unsigned long long dm_magic[8], dc_magic[8];
+  uint32_t dmult[8], dcard[8];
   unsigned long long magic[KT_MAX_KNOBS];
   uint32_t card[KT_MAX_KNOBS];
   int axis_knob[KT_MAX_AXES];
@@ -143,6 +146,10 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const kt_spec_table& T = *tab;
   const int tid = threadIdx.x, warp = tid >> 5;
+  if (T.space_size > 0xffffffffull) {  // 32-bit digit arithmetic below; larger spaces use kt_embed_csr
+    if (blockIdx.x == 0 && tid == 0) atomicOr(err, 2);
+    return;
+  }
 
   // ---- setup: operands, tables, barriers, TMEM ------------------------------------------
   stage_operand(params + dims.off_gcn[0], KT_F, 32, 16, S.b1h, S.b1l, tid);
@@ -166,6 +173,19 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
   if (tid == 0) {
     S.auto_knob = T.auto_knob;
     S.expl_knob = T.expl_knob;
+    for (int d = 0; d < 8; ++d) {
+      const int kn = d < KT_MAX_AXES ? (d < T.n_axes ? T.axis_knob[d] : -1) : (d == 6 ? T.auto_knob : T.expl_knob);
+      uint64_t mult = 1;
+      uint32_t card = 1;
+      if (kn >= 0) {
+        for (int j = kn + 1; j < T.n_knobs; ++j) mult *= T.card[j];
+        card = T.card[kn];
+      }
+      S.dmult[d] = static_cast<uint32_t>(mult);
+      S.dcard[d] = card;
+      S.dm_magic[d] = mult > 1 ? ~0ull / mult + 1 : 0ull;
+      S.dc_magic[d] = card > 1 ? ~0ull / card + 1 : 0ull;
+    }
     int off = 0;
     for (int a = 0; a < na; ++a) {
       S.tab_off[a] = off;
@@ -241,11 +261,27 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     const double m6 = T.fmean[6], r6 = 1.0 / T.fstd[6], m7 = T.fmean[7], r7 = 1.0 / T.fstd[7];
     const double m8 = T.fmean[8], r8 = 1.0 / T.fstd[8], m9 = T.fmean[9] - 1.0, r9 = 1.0 / T.fstd[9];
     int64_t q = 0;
+    auto index_of = [&](int64_t ti) -> int64_t {  // this thread's config index in tile ti
+      const int64_t gi = (blockIdx.x + ti * gridDim.x) * GT + g;
+      if (ti >= my_tiles || gi >= B) return INT64_MIN;  // padding row
+      return idx ? __ldcs(idx + gi) : idx_base + gi;
+    };
+    // knob digit d of the (32-bit) index: (v / dmult[d]) % dcard[d] (kernels.py:278-286)
+    auto digit = [&](uint32_t v, int d) -> int {
+      const uint32_t qd = udiv(v, S.dmult[d], S.dm_magic[d]);
+      const uint32_t c = S.dcard[d];
+      return static_cast<int>(qd - udiv(qd, c, S.dc_magic[d]) * c);
+    };
+    int64_t v_next = index_of(0);
     for (int64_t ti = 0; ti < my_tiles; ++ti) {
-      const int db = static_cast<int>(ti & 1);
-      mbar_wait(&S.dec_full[db], static_cast<uint32_t>((ti >> 1) & 1));  // decoder warp done
-      const bool ok = S.okf[db][g] != 0;
-      const unsigned unr_mask = S.unr[db][g];
+      const int64_t v64 = v_next;
+      v_next = index_of(ti + 1);  // next tile's index load in flight during this tile
+      const bool ok = v64 >= 0 && static_cast<uint64_t>(v64) < size;
+      if (v64 != INT64_MIN && !ok) atomicOr(err, 1);
+      const uint32_t v = ok ? static_cast<uint32_t>(v64) : 0u;
+      const int autov = S.auto_knob >= 0 ? S.auto_vals[digit(v, 6)] : 0;
+      const int expl = S.expl_knob >= 0 ? S.expl_vals[digit(v, 7)] : 0;
+      const bool unr_on = expl != 0 && autov > 0;
       // loops are emitted innermost first (k = n_loops-1 .. 0), so touched -- the
       // product of the extents of the loops inside loop k, multiplied innermost
       // outward as np.cumprod(e[::-1]) does -- accumulates exactly in fp64, and
@@ -257,7 +293,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         const int k = C - 1 - c;
         const int level = k >= na;
         const int a = level ? k - na : k;
-        const int e = S.sel[db][a][g];
+        const int e = S.tab_off[a] + (S.axis_knob[a] >= 0 ? digit(v, a) : 0);
         const int2 oi = S.oi[e];
         if (g == 0) TRACE(19, q);
         float x[16];
@@ -277,7 +313,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
           }
           x[2] = S.nconst[k][0];
           x[3] = S.nconst[k][1];
-          const bool unr = level && ((unr_mask >> a) & 1u);
+          const bool unr = level && unr_on && oi.y <= autov;
           x[4] = unr ? S.nconst[k][3] : S.nconst[k][2];
           x[6] = static_cast<float>((t - static_cast<dbl>(m6)) * static_cast<dbl>(r6));
           x[7] = static_cast<float>((lt - static_cast<dbl>(m7)) * static_cast<dbl>(r7));
@@ -312,97 +348,6 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         warp_arrive(&S.x_full[s]);
         if (g == 0) TRACE(0, q);
       }
-      warp_arrive(&S.dec_free[db]);  // this tile's decode buffer can be refilled
-    }
-  } else if (warp == 19) {
-    // ===================== decoder: config index -> per-axis table entries, one tile ahead ======
-    const int lane32 = tid & 31;
-    const int n_knobs = T.n_knobs;
-    const int auto_knob = S.auto_knob, expl_knob = S.expl_knob;
-    // loop-invariant tables in registers (the decoder warp has registers to spare)
-    uint32_t cardr[KT_MAX_KNOBS];
-    uint64_t magicr[KT_MAX_KNOBS];
-#pragma unroll
-    for (int j = 0; j < KT_MAX_KNOBS; ++j) {
-      cardr[j] = S.card[j];
-      magicr[j] = S.magic[j];
-    }
-    int aknob[KT_MAX_AXES], aoff[KT_MAX_AXES];
-#pragma unroll
-    for (int a = 0; a < KT_MAX_AXES; ++a) {
-      aknob[a] = S.axis_knob[a];
-      aoff[a] = S.tab_off[a];
-    }
-    for (int64_t ti = 0; ti < my_tiles; ++ti) {
-      const int db = static_cast<int>(ti & 1);
-      mbar_wait(&S.dec_free[db], static_cast<uint32_t>(((ti >> 1) & 1) ^ 1));  // tile ti-2 consumed
-      __syncwarp();
-      if (lane32 == 0) TRACE(24, ti);
-      int64_t vv[GT / 32];  // all four index loads in flight before any decode
-#pragma unroll
-      for (int i = 0; i < GT / 32; ++i) {
-        const int64_t gi = (blockIdx.x + ti * gridDim.x) * GT + lane32 + 32 * i;
-        vv[i] = gi >= B ? 0 : (idx ? __ldcs(idx + gi) : idx_base + gi);
-      }
-#pragma unroll
-      for (int i = 0; i < GT / 32; ++i) {
-        const int g = lane32 + 32 * i;
-        const int64_t gi = (blockIdx.x + ti * gridDim.x) * GT + g;
-        const bool pad = gi >= B;
-        const int64_t v = vv[i];
-        const bool ok = !pad && v >= 0 && static_cast<uint64_t>(v) < size;
-        if (!pad && !ok) atomicOr(err, 1);
-        // mixed-radix decode, knob 0 most significant (kernels.py:278-286)
-        int ch[KT_MAX_KNOBS];
-#pragma unroll
-        for (int j = 0; j < KT_MAX_KNOBS; ++j) ch[j] = 0;
-        if (ok && size <= 0xffffffffull) {
-          uint32_t r = static_cast<uint32_t>(v);
-#pragma unroll
-          for (int j = KT_MAX_KNOBS - 1; j >= 0; --j) {
-            if (j < n_knobs) {
-              const uint32_t qq = udiv(r, cardr[j], magicr[j]);
-              ch[j] = static_cast<int>(r - qq * cardr[j]);
-              r = qq;
-            }
-          }
-        } else if (ok) {
-          uint64_t r = static_cast<uint64_t>(v);
-#pragma unroll
-          for (int j = KT_MAX_KNOBS - 1; j >= 0; --j) {
-            if (j < n_knobs) {
-              const uint64_t qq = r / cardr[j];
-              ch[j] = static_cast<int>(r - qq * cardr[j]);
-              r = qq;
-            }
-          }
-        }
-        int ca = 0, ce = 0;
-#pragma unroll
-        for (int j = 0; j < KT_MAX_KNOBS; ++j) {
-          if (j == auto_knob) ca = ch[j];
-          if (j == expl_knob) ce = ch[j];
-        }
-        const int autov = auto_knob >= 0 ? S.auto_vals[ca] : 0;
-        const int expl = expl_knob >= 0 ? S.expl_vals[ce] : 0;
-        unsigned unr = 0;
-#pragma unroll
-        for (int a = 0; a < KT_MAX_AXES; ++a) {
-          if (a < na) {
-            int c = 0;
-#pragma unroll
-            for (int j = 0; j < KT_MAX_KNOBS; ++j)
-              if (j == aknob[a]) c = ch[j];
-            const int e = aoff[a] + c;
-            S.sel[db][a][g] = static_cast<short>(e);
-            if (expl != 0 && autov > 0 && S.oi[e].y <= autov) unr |= 1u << a;
-          }
-        }
-        S.unr[db][g] = static_cast<unsigned char>(unr);
-        S.okf[db][g] = ok ? 1 : 0;
-      }
-      if (lane32 == 0) TRACE(25, ti);
-      warp_arrive(&S.dec_full[db]);
     }
   } else if (warp == 8 || warp == 17 || warp == 18) {
     // ===================== MMA: fixed issue order, blocking waits, one elected lane issues =====
