@@ -12,6 +12,13 @@
 // accumulated in fp32 in TMEM -- fp32-level accuracy on the tensor pipe.
 #pragma once
 
+#ifndef KT_WAIT_SLEEP
+#define KT_WAIT_SLEEP 20
+#endif
+#if !defined(KT_WAIT_HINT) && !defined(KT_WAIT_SPIN)
+#define KT_WAIT_HINT 1000000  // ns: waiting threads are parked by the hardware
+#endif
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -87,6 +94,17 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
 // parked by the hardware (woken on completion) instead of spinning through issue
 // slots its SMSP neighbours need.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+#if defined(KT_WAIT_HINT)
+  // hardware-suspended wait: the thread parks until the phase completes (or the hint expires)
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n"
+      :
+      : "r"(smem_u32(bar)), "r"(phase), "r"(KT_WAIT_HINT)
+      : "memory");
+#else
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
@@ -98,7 +116,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   // not complete yet: back off between probes so a waiting warp does not take the
   // issue slots its SMSP neighbours on the critical path need
   while (!ok) {
-    __nanosleep(20);
+    __nanosleep(KT_WAIT_SLEEP);
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
@@ -107,6 +125,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         : "r"(smem_u32(bar)), "r"(phase)
         : "memory");
   }
+#endif
 }
 
 // Non-blocking probe: true once the phase with parity `phase` has completed.
