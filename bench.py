@@ -434,9 +434,9 @@ def run_reference(args):
     p["fmean"], p["fstd"] = st.mean(axis=0), np.where(st.std(axis=0) < 1e-12, 1.0, st.std(axis=0))
     p["lmean"], p["lstd"] = LABEL_NORM
     # bounded per-step sample so W + K steps stay within ~2 minutes of CPU time at the
-    # ~4e5 graphs/s the port reaches on 16 host cores; a power of two >= 16 x 4096
+    # ~4e5 graphs/s the port reaches on 16 host cores; a power of two >= 8 x 4096
     budget = int(120 * 4e5 / max(1, args.steps + args.warmup))
-    n = args.ref_sample or max(1 << 16, min(1 << 19, 1 << max(16, budget.bit_length() - 1)))
+    n = args.ref_sample or max(1 << 15, min(1 << 19, 1 << max(15, budget.bit_length() - 1)))
     sp = cpu_baseline.SweepPool(p, op, sargs, True)
     procs = sp.procs
     gen = rng_from("sweep", 0)
