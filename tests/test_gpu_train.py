@@ -218,7 +218,8 @@ def test_pretrain_matches_oracle_sgd_loop(cuda_device, g_encode, g_meta):
 
 
 def test_meta_trainer_equals_meta_train(cuda_device, g_model, super_samples):
-    """Device-resident MetaTrainer (pre-drawn tasks, 3 launches/step) == meta_train."""
+    """Device-resident MetaTrainer (cached frozen-GCN embeddings, pre-drawn tasks,
+    2 launches/step) == meta_train (which re-embeds every step, like the reference)."""
     from paper_2102_04199_b200.util import rng_from
 
     m = device_model(g_model)
@@ -230,3 +231,25 @@ def test_meta_trainer_equals_meta_train(cuda_device, g_model, super_samples):
     got = tr.model()
     assert_params_close(pm.flat_params(got).cpu().numpy(), pm.flat_params(want).cpu().numpy(), rtol=1e-6)
     assert np.isfinite(tr.stats(plan, bufs)).all()
+
+
+def test_meta_trainer_graph_replay_equals_eager(cuda_device, g_model, super_samples):
+    """A captured CUDA graph of the outer steps gives the eager loop's parameters bit for bit."""
+    from paper_2102_04199_b200.util import rng_from
+
+    m = device_model(g_model)
+    cfg = pmeta.MetaConfig(n_way=3, k_shot=2, meta_batch=8, outer_steps=10)
+    eager = pmeta.MetaTrainer(m, super_samples, cfg)
+    plan = eager.plan(rng_from("mt-graph"), cfg.outer_steps)
+    bufs = eager.run(plan)
+    rep = pmeta.MetaTrainer(m, super_samples, cfg)
+    plan2 = rep.plan(rng_from("mt-graph"), cfg.outer_steps)
+    bufs2 = rep._buffers(plan2)
+    for s in range(3):
+        rep.step(plan2, bufs2, s)
+    g = rep.capture(plan2, bufs2, 3, cfg.outer_steps)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(pm.flat_params(rep.model()), pm.flat_params(eager.model()))
+    assert torch.equal(bufs2["stats"], bufs["stats"])
+
