@@ -131,6 +131,13 @@ int kt_score_indices(const kt_spec_table* tab, const kt_dims* dims, const float*
 /* Same contract on the FP32 FMA pipe (FFMA2 register tiles) instead of tcgen05
  * 3xTF32 tensor cores; kept as the second, independent implementation the parity
  * tests hold the tensor-core kernel against. */
+/* kt_score_indices with more inputs / outputs: indices as int64 (idx), as uint32
+ * (idx32, may point at pinned host memory: zero-copy) or idx_base + i; optional
+ * keys_out (B x uint64) receives rank_history keys, (descending-order score code) << 32
+ * | index, EMPTY (all ones) for invalid indices, for kt_topk_keys. */
+int kt_score_indices_ex(const kt_spec_table* tab, const kt_dims* dims, const float* params,
+                        const int64_t* idx, const uint32_t* idx32, int64_t idx_base, int64_t B,
+                        float* z_out, float* u_out, uint64_t* keys_out, int32_t* err_flag, void* stream);
 int kt_score_indices_fp32(const kt_spec_table* tab, const kt_dims* dims, const float* params,
                           const int64_t* idx, int64_t idx_base, int64_t B,
                           float* z_out, float* u_out, int32_t* err_flag, void* stream);
@@ -177,6 +184,19 @@ int kt_readout(const float* h, int32_t d, int64_t B, int32_t nodes_per_graph, co
 /* head_forward_batch (model.py:197-203): u (B, head[0]) -> z (B). */
 int kt_head_forward(const kt_dims* dims, const float* params, const float* u, int64_t B,
                     float* z_out, void* stream);
+
+/* ---- end-to-end sweep step from host memory (the predictor seam, search.py:9-10) ---------- */
+/* Pinned host indices (int64 or uint32: idx_bytes 8 / 4) are read in place by the
+ * scorer (zero-copy: the host-to-device transfer happens inside the kernel), which
+ * writes the scores and the (score, index) keys; the scores return D2H on stream_d2h
+ * while kt_topk_keys ranks the keys; the top-k returns on stream_compute.
+ * Asynchronous: on return stream_compute orders the whole step (synchronise it before
+ * reading z_host / top_*_host).  keys_dev, z_dev: B entries. */
+int kt_sweep_host(const kt_spec_table* tab, const kt_dims* dims, const float* params,
+                  const void* idx_host, int32_t idx_bytes, int64_t B, uint64_t* keys_dev, float* z_dev,
+                  float* z_host, int32_t k, int64_t* top_idx_dev, float* top_score_dev,
+                  int64_t* top_idx_host, float* top_score_host, void* topk_ws, int64_t topk_ws_bytes,
+                  int32_t* err_dev, void* stream_compute, void* stream_d2h);
 
 /* ---- simulated-annealing exploration (sa_explore, search.py:202-254) ----------------------- */
 /* One proposal step for n_chains chains from pre-drawn randoms (the host draws them
@@ -258,6 +278,9 @@ int kt_topk(const float* scores, const int64_t* idx, int64_t idx_base, int64_t B
             const int64_t* visited, int64_t n_visited, int32_t k,
             int64_t* top_idx, float* top_score, void* workspace, int64_t workspace_bytes,
             void* stream);
+/* Top-k of precomputed keys (kt_score_indices_ex keys_out): ascending key order. */
+int kt_topk_keys(const uint64_t* keys, int64_t B, int32_t k, int64_t* top_idx, float* top_score,
+                 void* workspace, int64_t workspace_bytes, void* stream);
 /* Merge world x k (score, index) candidate lists (the all-gathered per-rank top-k). */
 int kt_topk_merge(const float* scores, const int64_t* idx, int64_t n, int32_t k,
                   int64_t* top_idx, float* top_score, void* workspace, int64_t workspace_bytes,

@@ -85,6 +85,7 @@ struct __align__(1024) Smem {
   double2 l2[TAB];  // numpy log2 of (outer, inner) extent
   float nconst[KT_MAX_LOOPS][8];
   int tab_off[KT_MAX_AXES];
+  int64_t vtile[2][GT];           // per tile parity: the graphs' config indices (INT64_MIN: padding)
   short sel[2][KT_MAX_AXES][GT];  // per tile buffer, graph: packed table entry of each axis' tile choice
   unsigned char unr[2][GT];       // per graph: bit a = inner loop of axis a unrolled
   unsigned char okf[2][GT];       // per graph: valid config index
@@ -140,8 +141,9 @@ __device__ __forceinline__ void store_head_quad(float* ah, float* al, int row, i
 
 __global__ void __launch_bounds__(NT, 1)
 score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float* __restrict__ params,
-                const int64_t* __restrict__ idx, int64_t idx_base, int64_t B, float* __restrict__ z_out,
-                float* __restrict__ u_out, int32_t* __restrict__ err) {
+                const int64_t* __restrict__ idx, const uint32_t* __restrict__ idx32, int64_t idx_base, int64_t B,
+                float* __restrict__ z_out, float* __restrict__ u_out, unsigned long long* __restrict__ keys_out,
+                int32_t* __restrict__ err) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const kt_spec_table& T = *tab;
@@ -264,7 +266,8 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     auto index_of = [&](int64_t ti) -> int64_t {  // this thread's config index in tile ti
       const int64_t gi = (blockIdx.x + ti * gridDim.x) * GT + g;
       if (ti >= my_tiles || gi >= B) return INT64_MIN;  // padding row
-      return idx ? __ldcs(idx + gi) : idx_base + gi;
+      // idx32 may point at pinned host memory (zero-copy: the kernel's reads are the H2D transfer)
+      return idx32 ? static_cast<int64_t>(idx32[gi]) : idx ? __ldcs(idx + gi) : idx_base + gi;
     };
     // knob digit d of the (32-bit) index: (v / dmult[d]) % dcard[d] (kernels.py:278-286)
     auto digit = [&](uint32_t v, int d) -> int {
@@ -276,6 +279,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     for (int64_t ti = 0; ti < my_tiles; ++ti) {
       const int64_t v64 = v_next;
       v_next = index_of(ti + 1);  // next tile's index load in flight during this tile
+      S.vtile[ti & 1][g] = v64;   // for the head epilogue (score validity, top-k key)
       const bool ok = v64 >= 0 && static_cast<uint64_t>(v64) < size;
       if (v64 != INT64_MIN && !ok) atomicOr(err, 1);
       const uint32_t v = ok ? static_cast<uint32_t>(v64) : 0u;
@@ -595,9 +599,16 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       if (eh == 1) S.part[g] = acc;
       named_sync(1 + quad, 64);
       if (eh == 0 && gi < B) {
-        const int64_t v = idx ? idx[gi] : idx_base + gi;
+        const int64_t v = S.vtile[ti & 1][g];
         const bool ok = v >= 0 && static_cast<uint64_t>(v) < size;
-        z_out[gi] = ok ? (b3 + acc) + S.part[g] : __int_as_float(0x7fc00000);
+        const float zv = (b3 + acc) + S.part[g];
+        z_out[gi] = ok ? zv : __int_as_float(0x7fc00000);
+        if (keys_out) {  // rank_history key for kt_topk_keys: (descending score code, index)
+          const uint32_t b = __float_as_uint(zv);
+          const uint32_t asc = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+          keys_out[gi] = ok && zv == zv ? (static_cast<unsigned long long>(~asc) << 32) | static_cast<uint32_t>(v)
+                                        : ~0ull;
+        }
       }
       named_sync(1 + quad, 64);  // S.part consumed before the next tile overwrites it
       if (tr) TRACE(12, ti);
@@ -621,9 +632,9 @@ static bool default_dims_tc(const kt_dims& d) {
 
 }  // namespace kt
 
-extern "C" int kt_score_indices(const kt_spec_table* tab, const kt_dims* dims, const float* params,
-                                const int64_t* idx, int64_t idx_base, int64_t B, float* z_out,
-                                float* u_out, int32_t* err_flag, void* stream) {
+extern "C" int kt_score_indices_ex(const kt_spec_table* tab, const kt_dims* dims, const float* params,
+                                   const int64_t* idx, const uint32_t* idx32, int64_t idx_base, int64_t B,
+                                   float* z_out, float* u_out, uint64_t* keys_out, int32_t* err_flag, void* stream) {
   using namespace kt;
   KT_REQUIRE(tab && dims && params && z_out && err_flag, KT_E_ARG, "kt_score_indices: null pointer");
   KT_REQUIRE(B > 0, KT_E_EMPTY, "kt_score_indices: empty batch");
@@ -637,8 +648,15 @@ extern "C" int kt_score_indices(const kt_spec_table* tab, const kt_dims* dims, c
   }
   const int64_t n_tiles = (B + tcs::GT - 1) / tcs::GT;
   const int grid = static_cast<int>(n_tiles < kNumSMs ? n_tiles : kNumSMs);
-  tcs::score_tc_kernel<<<grid, tcs::NT, smem, as_stream(stream)>>>(tab, *dims, params, idx, idx_base, B, z_out,
-                                                                    u_out, err_flag);
+  tcs::score_tc_kernel<<<grid, tcs::NT, smem, as_stream(stream)>>>(
+      tab, *dims, params, idx, idx32, idx_base, B, z_out, u_out, reinterpret_cast<unsigned long long*>(keys_out),
+      err_flag);
   note_launches(1);
   return check_launch("kt_score_indices");
+}
+
+extern "C" int kt_score_indices(const kt_spec_table* tab, const kt_dims* dims, const float* params,
+                                const int64_t* idx, int64_t idx_base, int64_t B, float* z_out,
+                                float* u_out, int32_t* err_flag, void* stream) {
+  return kt_score_indices_ex(tab, dims, params, idx, nullptr, idx_base, B, z_out, u_out, nullptr, err_flag, stream);
 }

@@ -75,6 +75,7 @@ struct Src {
 };
 
 __device__ __forceinline__ unsigned long long key_at(const Src& s, int64_t i) {
+  if (s.keys) return s.keys[i];  // keys built by the scorer's epilogue (kt_score_indices_ex)
   const int64_t id = s.idx ? s.idx[i] : s.base + i;
   if (s.n_visited > 0 && is_visited(s.visited, s.n_visited, id)) return EMPTY;
   return (static_cast<unsigned long long>(desc_code(s.scores[i])) << 32) | static_cast<uint32_t>(id);
@@ -240,15 +241,15 @@ __global__ void __launch_bounds__(NT) sort_unpack(const unsigned long long* __re
 
 static int run(const float* scores, const int64_t* idx, int64_t base, int64_t B, const int64_t* visited,
                int64_t n_visited, int k, int64_t* top_idx, float* top_score, void* ws, int64_t ws_bytes,
-               cudaStream_t stream) {
-  KT_REQUIRE(scores && top_idx && top_score && ws, KT_E_ARG, "kt_topk: null pointer");
+               cudaStream_t stream, const unsigned long long* keys = nullptr) {
+  KT_REQUIRE((scores || keys) && top_idx && top_score && ws, KT_E_ARG, "kt_topk: null pointer");
   KT_REQUIRE(B > 0, KT_E_EMPTY, "kt_topk: empty candidate set");
   KT_REQUIRE(k >= 1 && k <= MAXK, KT_E_UNSUPPORTED, "kt_topk: k must be in [1, %d]", MAXK);
   KT_REQUIRE(ws_bytes >= kt_topk_workspace_bytes(B, k), KT_E_ARG, "kt_topk: workspace too small");
   State* st = static_cast<State*>(ws);
   unsigned int* hist = reinterpret_cast<unsigned int*>(static_cast<char*>(ws) + 64);
   unsigned long long* buf = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 64 + NB * 4);
-  Src src{scores, idx, base, B, visited, n_visited, nullptr};
+  Src src{scores, idx, base, B, visited, n_visited, keys};
   const int64_t want = (B + NT - 1) / NT;
   const int grid = static_cast<int>(want < 2 * kNumSMs ? want : 2 * kNumSMs);
   init_state<<<1, 256, 0, stream>>>(st, hist, k, B <= k ? 1 : 0);
@@ -274,6 +275,12 @@ int kt_topk(const float* scores, const int64_t* idx, int64_t idx_base, int64_t B
             int64_t workspace_bytes, void* stream) {
   return kt::topk::run(scores, idx, idx_base, B, visited, n_visited, k, top_idx, top_score, workspace,
                        workspace_bytes, kt::as_stream(stream));
+}
+
+int kt_topk_keys(const uint64_t* keys, int64_t B, int32_t k, int64_t* top_idx, float* top_score, void* workspace,
+                 int64_t workspace_bytes, void* stream) {
+  return kt::topk::run(nullptr, nullptr, 0, B, nullptr, 0, k, top_idx, top_score, workspace, workspace_bytes,
+                       kt::as_stream(stream), reinterpret_cast<const unsigned long long*>(keys));
 }
 
 int kt_topk_merge(const float* scores, const int64_t* idx, int64_t n, int32_t k, int64_t* top_idx,

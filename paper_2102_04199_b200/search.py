@@ -154,14 +154,15 @@ class Sweeper:
     top-k by (score desc, index asc) -- rank_history over the whole shard.
 
     Everything per call is pre-resolved (spec table, dims, flat params, device
-    buffers, streams, events), so a step is a handful of C-ABI calls.
-    `run_device` takes device-resident indices; `run_host` is the end-to-end
-    form: pinned host indices in, host scores + top-k out, with the H2D copy,
-    the scoring and the D2H copy of `chunks` slices overlapped on three streams.
+    buffers, streams), so a step is one or two C-ABI calls.  The scorer writes the
+    64-bit (score, index) keys the radix top-k ranks, so the top-k never re-reads
+    scores or indices.  `run_device` takes device-resident indices; `run_host` is
+    the end-to-end form: pinned host indices in (read in place by the scorer),
+    host scores + top-k out.
     """
 
     def __init__(self, m: ModelState, spec: KernelSpec, space: KnobSpace, layout: BatchLayout,
-                 max_batch: int, k: int = 512, chunks: int = 4):
+                 max_batch: int, k: int = 512):
         if not _default_model(m) or space.size >= 2**32:
             raise DomainError("Sweeper needs the default model dims and a space < 2^32 (use score_indices)")
         self.lib = _lib.load()
@@ -171,10 +172,10 @@ class Sweeper:
         self.tab = device_spec_table(spec, space, layout, m.feature_norm.mean, m.feature_norm.std,
                                      device=self.dev)
         self.space_size = space.size
-        self.max_batch, self.k, self.chunks = max_batch, k, chunks
+        self.max_batch, self.k = max_batch, k
         dev = self.dev
         self.z = torch.empty(max_batch, dtype=torch.float32, device=dev)
-        self.idx = torch.empty(max_batch, dtype=torch.int64, device=dev)
+        self.keys = torch.empty(max_batch, dtype=torch.int64, device=dev)
         self.err = torch.zeros(1, dtype=torch.int32, device=dev)
         self.ws_bytes = int(self.lib.kt_topk_workspace_bytes(max_batch, k))
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
@@ -183,60 +184,69 @@ class Sweeper:
         self.h_z = torch.empty(max_batch, dtype=torch.float32, pin_memory=True)
         self.h_top_idx = torch.empty(k, dtype=torch.int64, pin_memory=True)
         self.h_top_score = torch.empty(k, dtype=torch.float32, pin_memory=True)
-        self.s_h2d = torch.cuda.Stream(dev)
         self.s_d2h = torch.cuda.Stream(dev)
-        self.ev_in = [torch.cuda.Event() for _ in range(chunks)]
-        self.ev_out = [torch.cuda.Event() for _ in range(chunks)]
         self.ev_done = torch.cuda.Event()
         self._p = dict(tab=self.tab.data_ptr(), flat=self.flat.data_ptr(), err=self.err.data_ptr(),
-                       ws=self.ws.data_ptr(), ti=self.top_idx.data_ptr(), ts=self.top_score.data_ptr())
+                       ws=self.ws.data_ptr(), ti=self.top_idx.data_ptr(), ts=self.top_score.data_ptr(),
+                       z=self.z.data_ptr(), keys=self.keys.data_ptr())
 
-    def _score(self, idx_ptr, base, n, z_ptr, stream):
-        _lib.check(self.lib.kt_score_indices(self._p["tab"], self.dims, self._p["flat"], idx_ptr, base, n, z_ptr,
-                                             None, self._p["err"], stream), "sweep score")
+    def score(self, idx64_ptr, idx32_ptr, base: int, n: int, stream) -> None:
+        """The scorer launch alone: z[:n] and keys[:n] (raw pointers; bench timing hook)."""
+        p = self._p
+        _lib.check(self.lib.kt_score_indices_ex(p["tab"], self.dims, p["flat"], idx64_ptr, idx32_ptr, base, n,
+                                                p["z"], None, p["keys"], p["err"], stream), "sweep score")
 
-    def _topk(self, idx_ptr, base, n, stream, visited=None):
-        vp = None if visited is None else visited.data_ptr()
-        nv = 0 if visited is None else visited.numel()
-        _lib.check(self.lib.kt_topk(self.z.data_ptr(), idx_ptr, base, n, vp, nv, self.k, self._p["ti"],
-                                    self._p["ts"], self._p["ws"], self.ws_bytes, stream), "sweep topk")
+    def rank(self, n: int, stream) -> None:
+        """Top-k of keys[:n] into top_idx / top_score."""
+        p = self._p
+        _lib.check(self.lib.kt_topk_keys(p["keys"], n, self.k, p["ti"], p["ts"], p["ws"], self.ws_bytes, stream),
+                   "sweep topk")
 
     def run_device(self, idx: torch.Tensor | None = None, *, base: int = 0, count: int | None = None,
                    visited: torch.Tensor | None = None):
-        """Scores into self.z[:n]; returns (top_idx, top_score) device views."""
+        """Scores into self.z[:n]; returns (top_idx, top_score) device views.  `idx`:
+        int64 or int32 device indices, or None for base + arange(count)."""
         n = idx.numel() if idx is not None else int(count)
         if n > self.max_batch or n <= 0:
             raise DomainError("sweep batch size out of range")
+        if idx is not None and idx.dtype not in (torch.int64, torch.int32):
+            raise DomainError("sweep indices must be int64 or int32")
         st = torch.cuda.current_stream(self.dev).cuda_stream
-        ip = None if idx is None else idx.data_ptr()
-        self._score(ip, base, n, self.z.data_ptr(), st)
-        self._topk(ip, base, n, st, visited)
+        i64 = idx.data_ptr() if idx is not None and idx.dtype == torch.int64 else None
+        i32 = idx.data_ptr() if idx is not None and idx.dtype == torch.int32 else None
+        p = self._p
+        if visited is None:
+            self.score(i64, i32, base, n, st)
+            self.rank(n, st)
+        else:  # exclusion list: the top-k rebuilds keys from scores and tests membership
+            if i32 is not None:
+                raise DomainError("visited exclusion takes int64 indices")
+            _lib.check(self.lib.kt_score_indices(p["tab"], self.dims, p["flat"], i64, base, n, p["z"], None,
+                                                 p["err"], st), "sweep score")
+            _lib.check(self.lib.kt_topk(p["z"], i64, base, n, visited.data_ptr(), visited.numel(), self.k, p["ti"],
+                                        p["ts"], p["ws"], self.ws_bytes, st), "sweep topk")
         return self.top_idx, self.top_score
 
     def run_host(self, idx_host: torch.Tensor, check: bool = True):
-        """End to end: pinned host int64 indices -> (host scores, host top-k idx, scores)."""
+        """End to end: pinned host indices -> (host scores, host top-k idx, scores).
+
+        int64 or int32 indices (the spaces this path takes are below 2^32).  One native
+        call (kt_sweep_host): the scorer reads the pinned indices in place over PCIe
+        (int32 halves those bytes), the scores return D2H while the top-k runs."""
         n = idx_host.numel()
         if n > self.max_batch or n <= 0:
             raise DomainError("sweep batch size out of range")
+        if idx_host.dtype not in (torch.int64, torch.int32):
+            raise DomainError("sweep indices must be int64 or int32")
+        if not idx_host.is_pinned():
+            raise DomainError("run_host needs pinned host indices (torch pin_memory)")
         comp = torch.cuda.current_stream(self.dev)
-        step = -(-n // self.chunks)
-        bounds = [(a, min(a + step, n)) for a in range(0, n, step)]
-        with torch.cuda.stream(self.s_h2d):
-            self.s_h2d.wait_stream(comp)
-            for i, (a, b) in enumerate(bounds):
-                self.idx[a:b].copy_(idx_host[a:b], non_blocking=True)
-                self.ev_in[i].record(self.s_h2d)
-        for i, (a, b) in enumerate(bounds):
-            comp.wait_event(self.ev_in[i])
-            self._score(self.idx.data_ptr() + 8 * a, 0, b - a, self.z.data_ptr() + 4 * a, comp.cuda_stream)
-            self.ev_out[i].record(comp)
-            with torch.cuda.stream(self.s_d2h):
-                self.s_d2h.wait_event(self.ev_out[i])
-                self.h_z[a:b].copy_(self.z[a:b], non_blocking=True)
-        self._topk(self.idx.data_ptr(), 0, n, comp.cuda_stream)
-        self.h_top_idx.copy_(self.top_idx, non_blocking=True)
-        self.h_top_score.copy_(self.top_score, non_blocking=True)
-        comp.wait_stream(self.s_d2h)
+        p = self._p
+        _lib.check(self.lib.kt_sweep_host(p["tab"], self.dims, p["flat"], idx_host.data_ptr(),
+                                          idx_host.element_size(), n, p["keys"], p["z"], self.h_z.data_ptr(),
+                                          self.k, p["ti"], p["ts"], self.h_top_idx.data_ptr(),
+                                          self.h_top_score.data_ptr(), p["ws"], self.ws_bytes, p["err"],
+                                          comp.cuda_stream, self.s_d2h.cuda_stream), "sweep (host)")
         self.ev_done.record(comp)
         self.ev_done.synchronize()
         if check and int(self.err.item()):

@@ -269,3 +269,64 @@ def test_single_graph_api(cuda_device, g_model):
     z = ps.score_indices(m, spec, space, lay, np.array([31337])).item()
     assert math.isclose(pm.forward(g, m), z, rel_tol=1e-5, abs_tol=1e-6)
     assert math.isclose(pm.predict_gflops(g, m), pm.denormalize_label(m, pm.forward(g, m)))
+
+
+def test_sweeper_end_to_end_int64_and_int32_hosts(cuda_device, g_model):
+    """Sweeper.run_host (pinned host indices read in place by the scorer, scores + top-k
+    out) equals the device-resident sweep, for int64 and narrowed int32 indices."""
+    m = device_model(g_model)
+    spec = pk.KernelSpec("conv2d", 56, 64, 64, 3, 3, 1)
+    space = pk.build_knob_space(spec)
+    lay = _layout(spec, "super")
+    sw = ps.Sweeper(m, spec, space, lay, 100_000, k=64)
+    idx = torch.from_numpy(np.random.default_rng(11).integers(0, space.size, 99_999))
+    ti, ts = sw.run_device(idx.cuda())
+    z_dev, ti, ts = sw.z[:99_999].clone(), ti.clone(), ts.clone()
+    for host in (idx.pin_memory(), idx.to(torch.int32).pin_memory()):
+        z_h, ti_h, ts_h = sw.run_host(host)
+        assert torch.equal(z_h, z_dev.cpu())
+        assert torch.equal(ti_h, ti.cpu()) and torch.equal(ts_h, ts.cpu())
+
+
+def test_sweeper_fused_keys_match_score_topk(cuda_device, g_model):
+    """The scorer-built (score, index) keys rank exactly like kt_topk over the scores
+    (the exclusion-list path), for int64 / int32 / implicit indices, ties and padding."""
+    m = device_model(g_model)
+    spec = pk.KernelSpec("conv2d", 56, 64, 64, 3, 3, 1)
+    space = pk.build_knob_space(spec)
+    lay = _layout(spec, "super")
+    sw = ps.Sweeper(m, spec, space, lay, 70_000, k=300)
+    none = torch.empty(0, dtype=torch.int64, device="cuda")
+    rng = np.random.default_rng(5)
+    idx = rng.integers(0, space.size, 65_537)
+    idx[100:400] = idx[7]  # duplicates: equal scores, the index breaks the tie
+    d64 = torch.from_numpy(idx).cuda()
+    ref_i, ref_s = (t.clone() for t in sw.run_device(d64, visited=none))
+    z_ref = sw.z[:idx.size].clone()
+    for arg in (d64, d64.to(torch.int32)):
+        ti, ts = sw.run_device(arg)
+        assert torch.equal(sw.z[:idx.size], z_ref)
+        assert torch.equal(ti, ref_i) and torch.equal(ts, ref_s)
+    ti, ts = sw.run_device(base=1000, count=5000)
+    ri, rs = sw.run_device(torch.arange(1000, 6000, device="cuda"), visited=none)
+    assert torch.equal(ti, ri) and torch.equal(ts, rs)
+    z = ps.score_indices(m, spec, space, lay, idx)
+    z = z.cpu().numpy() if isinstance(z, torch.Tensor) else np.asarray(z)
+    order = np.lexsort((idx, -z.astype(np.float64)))[:300]
+    assert np.array_equal(ref_i.cpu().numpy(), idx[order])
+
+
+def test_sweeper_out_of_range_index_excluded(cuda_device, g_model):
+    m = device_model(g_model)
+    spec = pk.KernelSpec("conv2d", 56, 64, 64, 3, 3, 1)
+    space = pk.build_knob_space(spec)
+    sw = ps.Sweeper(m, spec, space, _layout(spec, "super"), 1000, k=8)
+    idx = torch.arange(0, 1000, dtype=torch.int64)
+    idx[3] = space.size + 5
+    ti, _ = sw.run_device(idx.cuda())
+    assert int(sw.err.item()) != 0 and torch.isnan(sw.z[3]) and space.size + 5 not in ti.tolist()
+    sw.err.zero_()
+    with pytest.raises(pg.DomainError):
+        sw.run_host(idx.pin_memory())
+    with pytest.raises(pg.DomainError):
+        sw.run_host(torch.arange(10))  # not pinned
