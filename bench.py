@@ -167,17 +167,15 @@ def load_traffic():
 # --- secondary configs (C2 pretrain step, C3 MAML, C4 fine-tune) ----------------------
 
 
-def synthetic_corpus(n_kernels=47, per_kernel=200, ops=None, seed="bench-corpus"):
-    """Conftest-shaped corpus (47 kernel classes x 200 configs, super-graph layout) with
-    synthetic labels: the oracle platform model is out of scope, throughput does not
-    depend on label values."""
-    from paper_2102_04199_b200 import graphs as pg
+def synthetic_entries(n_kernels=47, per_kernel=200, ops=None, seed="bench-corpus"):
+    """Conftest-shaped index-based corpus (47 kernel classes x 200 configs) as
+    KernelRecords (harness.py:97-102) with synthetic labels: the oracle platform model
+    is out of scope, throughput does not depend on label values."""
     from paper_2102_04199_b200 import kernels as pk
-    from paper_2102_04199_b200.meta import LabeledSample
+    from paper_2102_04199_b200.dataset import KernelRecords
     from paper_2102_04199_b200.util import rng_from
 
     rng = rng_from(seed)
-    tmpl = pg.build_super_template(pk.OP_TYPES)
     ops = ops or pk.OP_TYPES
     out, seen = [], set()
     while len(seen) < n_kernels:
@@ -191,10 +189,55 @@ def synthetic_corpus(n_kernels=47, per_kernel=200, ops=None, seed="bench-corpus"
             continue
         seen.add(spec.signature())
         space = pk.build_knob_space(spec)
-        for c in pk.sample_configs(space, per_kernel, rng):
-            g = pg.config_graph(spec, c, space, template=tmpl)
-            out.append(LabeledSample(g, spec.signature(), float(2.0 ** rng.uniform(-10.0, 12.0))))
+        idx = np.array([pk.config_index(space, c) for c in pk.sample_configs(space, per_kernel, rng)], dtype=np.int64)
+        gfl = 2.0 ** rng.uniform(-10.0, 12.0, size=idx.size)
+        out.append(KernelRecords(spec, idx, gfl, np.ones(idx.size, dtype=bool)))
     return out
+
+
+def synthetic_corpus(entries=None, ops=None):
+    """The corpus as a device IndexedDataset (super-graph layout), optionally restricted to `ops`."""
+    from paper_2102_04199_b200.dataset import IndexedDataset
+
+    entries = entries if entries is not None else synthetic_entries()
+    if ops:
+        entries = [e for e in entries if e.spec.op_type in ops]
+    return IndexedDataset(entries, augmented=True)
+
+
+def bench_dataset(entries, reps=5):
+    """8(f) rank 2: materialising the index-based corpus for training.  Device path
+    (IndexedDataset: one encode launch per kernel class + array-built CSR) against the
+    per-sample host path the reference takes (config_graph per sample, harness.py:179-192,
+    then packing), both ending in the same packed device batch."""
+    import torch
+
+    from paper_2102_04199_b200 import graphs as pg
+    from paper_2102_04199_b200 import kernels as pk
+    from paper_2102_04199_b200 import model as pm
+    from paper_2102_04199_b200.dataset import IndexedDataset
+
+    n = sum(e.indices.size for e in entries)
+    IndexedDataset(entries, True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        IndexedDataset(entries, True)
+    torch.cuda.synchronize()
+    dev_s = (time.perf_counter() - t0) / reps
+    t0 = time.perf_counter()
+    tmpl = pg.build_super_template(pk.OP_TYPES)
+    graphs = []
+    for e in entries:
+        space = pk.build_knob_space(e.spec)
+        graphs += [pg.config_graph(e.spec, pk.index_config(space, int(i)), space, tmpl) for i in e.indices]
+    pm.pack_graphs(graphs, torch.device("cuda", torch.cuda.current_device()))
+    torch.cuda.synchronize()
+    host_s = time.perf_counter() - t0
+    return {"metric": "training corpus materialisation", "value": n / dev_s, "unit": "samples/s",
+            "seconds": dev_s, "host_graph_path_seconds": host_s, "speedup_vs_host_graph_path": host_s / dev_s,
+            "config": f"{len(entries)} kernel classes, {n} samples, super layout; device IndexedDataset vs "
+                      "config_graph-per-sample + pack_graphs (same packed batch)"}
 
 
 def bench_maml(m, corpus, steps, warmup, first_order=True):
@@ -250,7 +293,9 @@ def bench_pretrain_step(m, corpus, steps, warmup):
     from paper_2102_04199_b200.util import rng_from
 
     dev = pm.flat_params(m).device
-    pk_ = pm.pack_graphs([s.graph for s in corpus], dev)
+    from paper_2102_04199_b200.dataset import packed_of
+
+    pk_ = packed_of(corpus, dev)
     y_all = np.array([pm.normalize_label(m, s.label_gflops) for s in corpus], dtype=np.float32)
     rng = rng_from("bench-pretrain")
     batches = [rng.choice(len(corpus), 512, replace=False) for _ in range(warmup + steps)]
@@ -614,17 +659,19 @@ def run_ours(args):
         from paper_2102_04199_b200 import meta as pmeta
         from paper_2102_04199_b200 import model as pm
 
-        corpus = synthetic_corpus()
+        entries = synthetic_entries()
+        corpus = synthetic_corpus(entries)
         fn, ln = pmeta.dataset_norms(corpus)  # meta.py:81-101 over the corpus, as pretrain does
         m = pm.model_from_flat(m._flat, m, feature_norm=fn, label_norm=ln)
         line["maml"] = bench_maml(m, corpus, args.meta_steps, 10)
         if ws == 1:
             line["maml_so"] = bench_maml(m, corpus, max(args.meta_steps // 2, 10), 5, first_order=False)
-            line["pretrain"] = bench_pretrain_step(m, [s for s in corpus if s.kernel_class.split("/")[0] in
-                                                       ("conv2d", "winograd", "depthwise")], 50, 5)
+            line["pretrain"] = bench_pretrain_step(m, synthetic_corpus(entries, ("conv2d", "winograd", "depthwise")),
+                                                   50, 5)
             line["fine_tune"] = bench_fine_tune(m, corpus)
             line["aggregation"] = bench_aggregate(m)
             line["sa_explore"] = bench_sa(m)
+            line["dataset"] = bench_dataset(entries)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -187,16 +187,14 @@ int kt_head_forward(const kt_dims* dims, const float* params, const float* u, in
 
 /* ---- end-to-end sweep step from host memory (the predictor seam, search.py:9-10) ---------- */
 /* Pinned host indices (int64 or uint32: idx_bytes 8 / 4) are read in place by the
- * scorer (zero-copy: the host-to-device transfer happens inside the kernel), which
- * writes the scores and the (score, index) keys; the scores return D2H on stream_d2h
- * while kt_topk_keys ranks the keys; the top-k returns on stream_compute.
- * Asynchronous: on return stream_compute orders the whole step (synchronise it before
- * reading z_host / top_*_host).  keys_dev, z_dev: B entries. */
+ * scorer and the scores written in place to pinned z_host (zero-copy both ways: the
+ * host<->device transfer happens inside the kernel); the scorer's (score, index) keys
+ * (keys_dev, B entries) are ranked by kt_topk_keys and the top-k copied to the host.
+ * Asynchronous on `stream` (synchronise it before reading z_host / top_*_host). */
 int kt_sweep_host(const kt_spec_table* tab, const kt_dims* dims, const float* params,
-                  const void* idx_host, int32_t idx_bytes, int64_t B, uint64_t* keys_dev, float* z_dev,
-                  float* z_host, int32_t k, int64_t* top_idx_dev, float* top_score_dev,
-                  int64_t* top_idx_host, float* top_score_host, void* topk_ws, int64_t topk_ws_bytes,
-                  int32_t* err_dev, void* stream_compute, void* stream_d2h);
+                  const void* idx_host, int32_t idx_bytes, int64_t B, uint64_t* keys_dev, float* z_host,
+                  int32_t k, int64_t* top_idx_dev, float* top_score_dev, int64_t* top_idx_host,
+                  float* top_score_host, void* topk_ws, int64_t topk_ws_bytes, int32_t* err_dev, void* stream);
 
 /* ---- simulated-annealing exploration (sa_explore, search.py:202-254) ----------------------- */
 /* One proposal step for n_chains chains from pre-drawn randoms (the host draws them

@@ -38,7 +38,7 @@ from .util import rng_from, stable_digest
 __version__ = "0.1.0"
 
 
-_LAZY = ("model", "meta", "search", "dist")
+_LAZY = ("model", "meta", "search", "dist", "dataset")
 
 
 def __getattr__(name):

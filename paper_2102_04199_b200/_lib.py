@@ -104,8 +104,8 @@ _SIGS = {
     "kt_maml_workspace_bytes": (i64, [ctypes.POINTER(Dims), i32, i32, i32]),
     "kt_maml_tasks": (ctypes.c_int, [ctypes.POINTER(Dims), vp, vp, vp, vp, vp, vp, vp, i32, f32, i32, i32, vp, vp,
                                      vp, i64, vp]),
-    "kt_sweep_host": (ctypes.c_int, [vp, ctypes.POINTER(Dims), vp, vp, i32, i64, vp, vp, vp, i32, vp, vp, vp, vp, vp,
-                                     i64, vp, vp, vp]),
+    "kt_sweep_host": (ctypes.c_int, [vp, ctypes.POINTER(Dims), vp, vp, i32, i64, vp, vp, i32, vp, vp, vp, vp, vp,
+                                     i64, vp, vp]),
     "kt_score_indices_ex": (ctypes.c_int, [vp, ctypes.POINTER(Dims), vp, vp, vp, i64, i64, vp, vp, vp, vp, vp]),
     "kt_topk_keys": (ctypes.c_int, [vp, i64, i32, vp, vp, vp, i64, vp]),
     "kt_sa_propose": (ctypes.c_int, [vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp]),

@@ -184,7 +184,6 @@ class Sweeper:
         self.h_z = torch.empty(max_batch, dtype=torch.float32, pin_memory=True)
         self.h_top_idx = torch.empty(k, dtype=torch.int64, pin_memory=True)
         self.h_top_score = torch.empty(k, dtype=torch.float32, pin_memory=True)
-        self.s_d2h = torch.cuda.Stream(dev)
         self.ev_done = torch.cuda.Event()
         self._p = dict(tab=self.tab.data_ptr(), flat=self.flat.data_ptr(), err=self.err.data_ptr(),
                        ws=self.ws.data_ptr(), ti=self.top_idx.data_ptr(), ts=self.top_score.data_ptr(),
@@ -231,8 +230,8 @@ class Sweeper:
         """End to end: pinned host indices -> (host scores, host top-k idx, scores).
 
         int64 or int32 indices (the spaces this path takes are below 2^32).  One native
-        call (kt_sweep_host): the scorer reads the pinned indices in place over PCIe
-        (int32 halves those bytes), the scores return D2H while the top-k runs."""
+        call (kt_sweep_host): the scorer reads the pinned indices and writes the pinned
+        scores in place over PCIe (int32 halves the index bytes), then the top-k."""
         n = idx_host.numel()
         if n > self.max_batch or n <= 0:
             raise DomainError("sweep batch size out of range")
@@ -243,10 +242,9 @@ class Sweeper:
         comp = torch.cuda.current_stream(self.dev)
         p = self._p
         _lib.check(self.lib.kt_sweep_host(p["tab"], self.dims, p["flat"], idx_host.data_ptr(),
-                                          idx_host.element_size(), n, p["keys"], p["z"], self.h_z.data_ptr(),
-                                          self.k, p["ti"], p["ts"], self.h_top_idx.data_ptr(),
-                                          self.h_top_score.data_ptr(), p["ws"], self.ws_bytes, p["err"],
-                                          comp.cuda_stream, self.s_d2h.cuda_stream), "sweep (host)")
+                                          idx_host.element_size(), n, p["keys"], self.h_z.data_ptr(), self.k,
+                                          p["ti"], p["ts"], self.h_top_idx.data_ptr(), self.h_top_score.data_ptr(),
+                                          p["ws"], self.ws_bytes, p["err"], comp.cuda_stream), "sweep (host)")
         self.ev_done.record(comp)
         self.ev_done.synchronize()
         if check and int(self.err.item()):

@@ -19,6 +19,13 @@ Everything is keyed by `rng_from` so reruns are byte-identical.  Outputs:
   rank.npz       rank_history orderings (search.py:257) on tie-heavy scores
   sa.npz         sa_explore histories (search.py:202-254) and sa_propose picks
                  (search.py:266-281) driven by a synthetic, index-keyed predictor
+  dataset/       a small reference gen_dataset (harness.py:164-176) written by the
+                 reference's save_dataset (harness.py:195-216): kernels.yaml,
+                 samples.csv, manifest.json
+  dataset.npz    on that dataset: dataset_norms (meta.py:81-101) of the raw and the
+                 augmented dataset_samples (harness.py:179-192), their labels and
+                 kernel classes, grad (model.py:218) of an index-picked raw batch,
+                 and pretrain (meta.py:104-123, one epoch) on the augmented samples
 """
 
 from __future__ import annotations
@@ -37,6 +44,7 @@ from kerntune import kernels as rk  # noqa: E402
 from kerntune import meta as rmeta  # noqa: E402
 from kerntune import model as rm  # noqa: E402
 from kerntune import search as rs  # noqa: E402
+from kerntune import harness as rh  # noqa: E402
 from kerntune.harness import DatasetParams, sample_kernel  # noqa: E402
 from kerntune.oracle import get_profile, measure  # noqa: E402
 from kerntune.util import rng_from  # noqa: E402
@@ -265,9 +273,48 @@ def sa_goldens():
     np.savez_compressed(os.path.join(OUT, "sa.npz"), **out)
 
 
+def flat_theta(m):
+    """Flat parameter vector in the device layout: gcn layers, agg, (w_i, b_i) pairs."""
+    parts = list(m.gcn.layers) + [m.agg.sum_weights]
+    parts += [t for w, b in zip(m.head.weights, m.head.biases) for t in (w, b)]
+    return np.concatenate([np.asarray(a).ravel() for a in parts])
+
+
+def dataset_goldens():
+    params = DatasetParams(n_kernels=7, configs_per_kernel=24)
+    ds = rh.gen_dataset(params, rng_from("golden-dataset"))
+    rh.save_dataset(ds, os.path.join(OUT, "dataset"))
+    out = {}
+    for tag, aug in (("raw", False), ("super", True)):
+        samples = rh.dataset_samples(ds, augmented=aug)
+        fn, ln = rmeta.dataset_norms(samples)
+        out[f"{tag}/fmean"], out[f"{tag}/fstd"] = fn.mean, fn.std
+        out[f"{tag}/lnorm"] = np.array([ln.mean, ln.std])
+        out[f"{tag}/labels"] = np.array([s.label_gflops for s in samples])
+        if aug:
+            cfg = rmeta.MetaConfig(pretrain_epochs=1, gamma=0.005)
+            mp = rmeta.pretrain(samples, cfg, rng_from("golden-dataset-pretrain"))
+            out["pretrain/theta"] = flat_theta(mp)
+        else:
+            out["classes"] = np.array([s.kernel_class for s in samples])
+            m = rm.init_model(rng_from("golden-dataset-model"))
+            m = replace(m, feature_norm=fn, label_norm=ln)
+            pick = rng_from("golden-dataset-pick").choice(len(samples), 48, replace=False)
+            loss, g = rm.grad(m, [(samples[int(i)].graph, samples[int(i)].label_gflops) for i in pick], "all")
+            out["grad/pick"] = pick.astype(np.int64)
+            out["grad/loss"] = np.array(loss)
+            out["grad/flat"] = np.concatenate([a.ravel() for a in list(g.gcn) + [g.agg] + [
+                t for w, b in zip(g.head_weights, g.head_biases) for t in (w, b)]])
+            out["grad/theta"] = flat_theta(m)
+    np.savez_compressed(os.path.join(OUT, "dataset.npz"), **out)
+
+
 def main():
     if sys.argv[1:] == ["sa"]:
         sa_goldens()
+        return
+    if sys.argv[1:] == ["dataset"]:
+        dataset_goldens()
         return
     golden_graph_text()
     encode_goldens()
@@ -278,6 +325,7 @@ def main():
     meta_goldens(items, m)
     rank_goldens()
     sa_goldens()
+    dataset_goldens()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))
 

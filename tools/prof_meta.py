@@ -11,7 +11,7 @@ from paper_2102_04199_b200 import model as pm
 
 dev = torch.device("cuda", 0)
 m = bench.bench_model(dev)
-corpus = bench.synthetic_corpus(n_kernels=8, per_kernel=64)
+corpus = bench.synthetic_corpus(bench.synthetic_entries(n_kernels=8, per_kernel=64))
 fn, ln = pmeta.dataset_norms(corpus)
 m = pm.model_from_flat(m._flat, m, feature_norm=fn, label_norm=ln)
 print(bench.bench_fine_tune(m, corpus, reps=3))
