@@ -611,6 +611,352 @@ __global__ void __launch_bounds__(TC_ROWS, 4) gcn_layer_tc_kernel(LayerArgs a) {
   }
 }
 
+
+// ---- pipelined tensor-core layer: TMA-staged tiles, aggregate-then-transform --------------------
+//
+// out = ReLU((A Xn) W) for tiles of whole graphs (<= 128 rows, contiguous in HBM):
+//   thread 0 (producer)  1-D bulk copies (cp.async.bulk, TMA engine) of the next S tiles'
+//                        input rows into an S-stage shared-memory ring, one copy per tile;
+//   row r (thread r)     sums a_rj * xn_j over its CSR row straight out of the staged tile
+//                        (layer 1 z-normalises and masks the fp64 rows on the fly), splits
+//                        the sum hi/lo and tcgen05.st's it into TMEM (the A operand);
+//   elected thread       3 x K/8 tcgen05.mma kind::tf32 (3xTF32), D in TMEM;
+//   row r                tcgen05.ld's D, applies ReLU, writes the row into an output
+//                        staging tile; thread 0 bulk-stores the tile (one copy).
+// Loads run S tiles ahead and stores drain asynchronously, so HBM traffic overlaps the
+// aggregation / MMA of the tile in flight; three CTAs per SM (128 TMEM columns each).
+// Aggregating first (A X) W is the order the reference's einsum takes for layer 1
+// (SURVEY.md 8(a)); for layer 2 it equals A (H W) up to fp32 rounding.
+template <int DIN, bool IN64, int S, int OB>
+__global__ void __launch_bounds__(TC_ROWS, 3) gcn_layer_pipe_kernel(LayerArgs a, int rp_cap, int nz_cap) {
+  constexpr int K = (DIN + 7) & ~7;
+  constexpr int DOUT = 32;
+  constexpr int ESZ = IN64 ? 8 : 4;
+  constexpr int ROWB = DIN * ESZ;             // input row bytes (16-byte multiple)
+  constexpr int STAGE = TC_ROWS * ROWB;       // input stage bytes
+  constexpr int OUTB = TC_ROWS * DOUT * 4;    // output staging bytes
+  static_assert(ROWB % 16 == 0, "bulk copies need 16-byte rows");
+  extern __shared__ __align__(1024) unsigned char smem[];
+  float* bh = reinterpret_cast<float*>(smem);
+  float* bl = bh + DOUT * K;
+  unsigned char* stage0 = reinterpret_cast<unsigned char*>(bl + DOUT * K);
+  float* outb0 = reinterpret_cast<float*>(stage0 + S * STAGE);
+  int* s_rp = reinterpret_cast<int*>(outb0 + OB * TC_ROWS * DOUT);
+  int* s_col = s_rp + ((rp_cap + 3) & ~3);
+  float* s_val = reinterpret_cast<float*>(s_col + ((nz_cap + 3) & ~3));
+  uint8_t* s_mask = reinterpret_cast<uint8_t*>(s_val + ((nz_cap + 3) & ~3));
+  __shared__ PatSmem P;
+  __shared__ float s_mean[KT_MAX_DIM], s_rstd[KT_MAX_DIM];
+  __shared__ double d_mean[KT_MAX_DIM], d_rstd[KT_MAX_DIM];
+  __shared__ __align__(8) uint64_t full[S];
+  __shared__ __align__(8) uint64_t mma_bar;
+  __shared__ uint32_t tmem_slot;
+  __shared__ int s_gptr[TC_ROWS + 1];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  (void)s_mean;
+  (void)s_rstd;
+
+  const int64_t n_tiles = (a.B + a.G - 1) / a.G;
+  auto tile_rows = [&](int64_t t, int64_t& r0) {
+    const int64_t g0 = t * a.G;
+    const int64_t g1 = g0 + a.G < a.B ? g0 + a.G : a.B;
+    r0 = tile_row0(a, g0);
+    return static_cast<int>(tile_row0(a, g1) - r0);
+  };
+  auto issue_load = [&](int64_t t, int st) {
+    int64_t r0;
+    const int rows = tile_rows(t, r0);
+    const uint32_t bytes = static_cast<uint32_t>(rows) * ROWB;
+    mbar_expect(&full[st], bytes);
+    bulk_load(stage0 + st * STAGE, static_cast<const unsigned char*>(a.in) + r0 * ROWB, bytes, &full[st]);
+  };
+
+  // ---- setup ---------------------------------------------------------------------------------
+  for (int e = tid; e < DOUT * K; e += TC_ROWS) {  // B = W^T: row n, column k
+    const int n = e / K, k = e - n * K;
+    const float v = k < DIN ? a.W[k * DOUT + n] : 0.0f;
+    const float h = tc::tf32_trunc(v);
+    const int off = tc::kmajor_offset(n, k, K) >> 2;
+    bh[off] = h;
+    bl[off] = v - h;
+  }
+  if (tid == 0) {
+    int rp = 0, nz = 0, mk = 0;
+    for (int p = 0; p < a.n_pat; ++p) {
+      P.n[p] = a.pat_n[p];
+      P.rp_off[p] = rp;
+      P.nz_off[p] = nz;
+      P.mask_off[p] = mk;
+      nz += a.pat_rp[rp + P.n[p]];
+      rp += P.n[p] + 1;
+      mk += P.n[p];
+    }
+    for (int st = 0; st < S; ++st) mbar_init1(&full[st]);
+    tc::mbar_init(&mma_bar, 1);
+    tc::fence_async_smem();
+    // the first S tiles start streaming while the rest of the setup runs
+    for (int st = 0; st < S; ++st)
+      if (blockIdx.x + static_cast<int64_t>(st) * gridDim.x < n_tiles)
+        issue_load(blockIdx.x + static_cast<int64_t>(st) * gridDim.x, st);
+  }
+  if (IN64)
+    for (int c = tid; c < DIN; c += TC_ROWS) {
+      d_mean[c] = a.fmean[c];
+      d_rstd[c] = 1.0 / a.fstd[c];
+    }
+  if (warp == 0) tc::tmem_alloc(&tmem_slot, 128);
+  __syncthreads();
+  {
+    int tot_rp = 0, tot_nz = 0, tot_mask = 0;
+    for (int p = 0; p < a.n_pat; ++p) {
+      tot_rp += P.n[p] + 1;
+      tot_mask += P.n[p];
+      tot_nz += a.pat_rp[P.rp_off[p] + P.n[p]];
+    }
+    for (int i = tid; i < tot_rp; i += TC_ROWS) s_rp[i] = a.pat_rp[i];
+    for (int i = tid; i < tot_nz; i += TC_ROWS) {
+      s_col[i] = a.pat_col[i];
+      s_val[i] = a.pat_val[i];
+    }
+    if (IN64)
+      for (int i = tid; i < tot_mask; i += TC_ROWS) s_mask[i] = a.pat_mask ? a.pat_mask[i] : 1;
+  }
+  if (IN64) {
+    // drop masked columns from the CSR once (their normalised rows are exactly 0), so the
+    // row loop never tests the mask
+    __syncthreads();
+    if (tid == 0) {
+      int w = 0;
+      for (int p = 0; p < a.n_pat; ++p) {
+        int* rp = s_rp + P.rp_off[p];
+        const int src0 = P.nz_off[p];
+        P.nz_off[p] = w;
+        int prev = rp[0];
+        rp[0] = 0;
+        for (int l = 0; l < P.n[p]; ++l) {
+          const int e_end = rp[l + 1];
+          for (int e = prev; e < e_end; ++e) {
+            const int j = s_col[src0 + e];
+            if (s_mask[P.mask_off[p] + j]) {
+              s_col[w] = j;
+              s_val[w] = s_val[src0 + e];
+              ++w;
+            }
+          }
+          prev = e_end;
+          rp[l + 1] = w - P.nz_off[p];
+        }
+      }
+    }
+  }
+  const int u_g = a.node_ptr ? 0 : tid / a.n_uniform;  // uniform graphs: fixed row -> graph map
+  tc::fence_async_smem();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const uint32_t lane_addr = static_cast<uint32_t>((32 * warp) << 16);
+  const uint32_t T_AH = 0, T_AL = 32, T_D = 64;
+  const uint32_t idesc = tc::idesc_tf32(128, DOUT);
+
+  int64_t it = 0;
+  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+    const int st = static_cast<int>(it % S);
+    const int64_t g0 = t * a.G;
+    const int ng = static_cast<int>((g0 + a.G < a.B ? g0 + a.G : a.B) - g0);
+    int64_t r0;
+    const int rows = tile_rows(t, r0);
+    if (tid <= ng) s_gptr[tid] = static_cast<int>(tile_row0(a, g0 + tid) - r0);
+    tc::mbar_wait(&full[st], static_cast<uint32_t>((it / S) & 1));
+    __syncthreads();  // (A) s_gptr ready
+    // ---- 1. y_r = sum_j a_rj xn_j out of the staged tile -> hi / lo -> TMEM -------------------------
+    float y[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) y[k] = 0.0f;
+    constexpr int NP = IN64 ? 1 : DIN / 4;
+    static_assert(IN64 || (NP & (NP - 1)) == 0, "rotation needs a power-of-two piece count");
+    const int rot = tid & (NP - 1);
+    const unsigned char* tile = stage0 + st * STAGE;
+    int p = 0, base = 0, e_lo = 0, e_hi = 0;
+    if (tid < rows) {
+      int my_g = u_g;
+      if (a.node_ptr)
+        while (my_g + 1 < ng && s_gptr[my_g + 1] <= tid) ++my_g;
+      base = a.node_ptr ? s_gptr[my_g] : my_g * a.n_uniform;
+      p = a.pat_id ? a.pat_id[g0 + my_g] : 0;
+      e_lo = P.nz_off[p] + s_rp[P.rp_off[p] + tid - base];
+      e_hi = P.nz_off[p] + s_rp[P.rp_off[p] + tid - base + 1];
+    }
+    // hub rows (star roots: 13 of a graph's 73 nonzeros) are summed by the whole warp
+    // below, so the per-row loop runs <= HUB iterations
+    // (layer 1: a root's neighbours are masked loop nodes, skipped cheaply in the row loop)
+    constexpr int HUB = IN64 ? (1 << 30) : 4;
+    const bool hub = e_hi - e_lo > HUB;
+    {
+      for (int e = hub ? e_hi : e_lo; e < e_hi; ++e) {
+        const int j = s_col[e];
+        const float w = s_val[e];
+        if constexpr (IN64) {
+          const double2* src = reinterpret_cast<const double2*>(tile + (base + j) * ROWB);
+#pragma unroll
+          for (int i = 0; i < DIN / 2; ++i) {
+            const double2 d = src[i];
+            const float x0 = static_cast<float>((d.x - d_mean[2 * i]) * d_rstd[2 * i]);
+            const float x1 = static_cast<float>((d.y - d_mean[2 * i + 1]) * d_rstd[2 * i + 1]);
+            y[2 * i] = fmaf(w, x0, y[2 * i]);
+            y[2 * i + 1] = fmaf(w, x1, y[2 * i + 1]);
+          }
+        } else {
+          // 16-byte pieces read in a per-row rotated order (piece (i + rot) % NP): eight
+          // consecutive rows then hit eight different bank groups of the 128-byte rows
+          const float4* src = reinterpret_cast<const float4*>(tile + (base + j) * ROWB);
+#pragma unroll
+          for (int i = 0; i < NP; ++i) {
+            const float4 v = src[(i + rot) & (NP - 1)];
+            y[4 * i] = fmaf(w, v.x, y[4 * i]);
+            y[4 * i + 1] = fmaf(w, v.y, y[4 * i + 1]);
+            y[4 * i + 2] = fmaf(w, v.z, y[4 * i + 2]);
+            y[4 * i + 3] = fmaf(w, v.w, y[4 * i + 3]);
+          }
+        }
+      }
+      if constexpr (!IN64) {  // undo the rotation: piece c <- accumulator (c - rot) % NP (barrel shift)
+#pragma unroll
+        for (int sh = 1; sh < NP; sh <<= 1) {
+          if (rot & sh) {
+            float r[K];
+#pragma unroll
+            for (int c = 0; c < NP; ++c)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) r[4 * c + q] = y[4 * ((c - sh) & (NP - 1)) + q];
+#pragma unroll
+            for (int k = 0; k < 4 * NP; ++k) y[k] = r[k];
+          }
+        }
+      }
+    }
+    {  // hub rows: lane c sums feature c over the hub's edges (same edge order), then the
+       // hub's lane collects the DIN sums by shuffles
+      const int lane = tid & 31;
+      unsigned hubs = __ballot_sync(0xffffffffu, hub);
+      while (hubs) {
+        const int src = __ffs(hubs) - 1;
+        hubs &= hubs - 1;
+        const int h_lo = __shfl_sync(0xffffffffu, e_lo, src), h_hi = __shfl_sync(0xffffffffu, e_hi, src);
+        const int h_base = __shfl_sync(0xffffffffu, base, src);
+        float yc = 0.0f;
+        if (lane < DIN)
+          for (int e = h_lo; e < h_hi; ++e) {
+            const int j = s_col[e];
+            const float w = s_val[e];
+            if constexpr (IN64) {
+              const double d = reinterpret_cast<const double*>(tile + (h_base + j) * ROWB)[lane];
+              yc = fmaf(w, static_cast<float>((d - d_mean[lane]) * d_rstd[lane]), yc);
+            } else {
+              yc = fmaf(w, reinterpret_cast<const float*>(tile + (h_base + j) * ROWB)[lane], yc);
+            }
+          }
+#pragma unroll
+        for (int k = 0; k < DIN; ++k) {
+          const float v = __shfl_sync(0xffffffffu, yc, k);
+          if (lane == src) y[k] = v;
+        }
+      }
+    }
+    {
+      float hi[K], lo[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        hi[k] = tc::tf32_trunc(y[k]);
+        lo[k] = y[k] - hi[k];
+      }
+#pragma unroll
+      for (int k0 = 0; k0 + 16 <= K; k0 += 16) {
+        tc::tmem_st16(tmem + lane_addr + T_AH + k0, hi + k0);
+        tc::tmem_st16(tmem + lane_addr + T_AL + k0, lo + k0);
+      }
+      if constexpr (K % 16 == 8) {
+        float h16[16], l16[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          h16[k] = k < 8 ? hi[K - 8 + k] : 0.f;
+          l16[k] = k < 8 ? lo[K - 8 + k] : 0.f;
+        }
+        tc::tmem_st16(tmem + lane_addr + T_AH + K - 8, h16);
+        tc::tmem_st16(tmem + lane_addr + T_AL + K - 8, l16);
+      }
+      tc::tmem_wait_st();
+    }
+    if (tid == 0) {
+      if (OB == 1) bulk_wait_read0(); else bulk_wait_read1();  // staging buffer it % OB is free again
+    }
+    tc::tc_fence_before();
+    __syncthreads();  // (B) stage consumed, A in TMEM
+    // ---- 2. refill the stage; D = A W on the tensor cores ------------------------------------------
+    if (warp == 0) {
+      tc::tc_fence_after();
+      if (tid == 0 && t + static_cast<int64_t>(S) * gridDim.x < n_tiles)
+        issue_load(t + static_cast<int64_t>(S) * gridDim.x, st);
+      __syncwarp();
+      if (tc::elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < K / 8; ++kk) {
+          tc::mma_tf32_ts(tmem + T_D, tmem + T_AH + 8 * kk, tc::kdesc(bh, K, kk), idesc, kk > 0);
+          tc::mma_tf32_ts(tmem + T_D, tmem + T_AH + 8 * kk, tc::kdesc(bl, K, kk), idesc, 1);
+          tc::mma_tf32_ts(tmem + T_D, tmem + T_AL + 8 * kk, tc::kdesc(bh, K, kk), idesc, 1);
+        }
+        tc::mma_commit(&mma_bar);
+      }
+      __syncwarp();
+    }
+    tc::mbar_wait(&mma_bar, static_cast<uint32_t>(it & 1));
+    __syncwarp();
+    tc::tc_fence_after();
+    // ---- 3. ReLU(D) -> output staging -> one bulk store -----------------------------------------
+    float* ob = outb0 + (it % OB) * (TC_ROWS * DOUT);
+    {
+      float v[32];
+      tc::tmem_ld32(tmem + lane_addr + T_D, v);
+      tc::tmem_wait_ld();
+      if (tid < rows) {
+        float4* dst = reinterpret_cast<float4*>(ob + tid * DOUT);
+        // rows are 128 B: store piece (q + r) % 8 at step q so that eight consecutive rows hit
+        // eight different bank groups; the registers are rotated to match (barrel shift)
+        const int orot = tid & 7;
+#pragma unroll
+        for (int sh = 1; sh < 8; sh <<= 1) {
+          if (orot & sh) {
+            float r[32];
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) r[4 * c + q] = v[4 * ((c + sh) & 7) + q];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) v[k] = r[k];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          if (a.relu) o = make_float4(fmaxf(o.x, 0.f), fmaxf(o.y, 0.f), fmaxf(o.z, 0.f), fmaxf(o.w, 0.f));
+          dst[(q + orot) & 7] = o;
+        }
+      }
+    }
+    fence_proxy_async();
+    tc::tc_fence_before();
+    __syncthreads();  // (C) staging tile complete; TMEM D reads done
+    if (tid == 0) bulk_store(a.out + r0 * DOUT, ob, static_cast<uint32_t>(rows) * DOUT * 4);
+  }
+  if (tid == 0) bulk_wait0();
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, 128);
+  }
+}
+
 }  // namespace agg
 }  // namespace kt
 
@@ -675,7 +1021,26 @@ extern "C" int kt_gcn_layer(const void* in, int32_t in_f64, const double* fmean,
                      max_nodes <= agg::TC_ROWS &&
                      (reinterpret_cast<uintptr_t>(in) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
                      !(getenv("KT_AGG_FFMA") && getenv("KT_AGG_FFMA")[0] == '1');
-  if (tc_ok) {
+  const bool pipe_ok = tc_ok && !(getenv("KT_AGG_TC1") && getenv("KT_AGG_TC1")[0] == '1');
+  if (pipe_ok) {
+    // TMA-staged tiles of whole graphs (<= 128 rows), three CTAs per SM
+    a.G = agg::TC_ROWS / max_nodes;
+    const int rp_cap = n_pat * (max_nodes + 1), nz_cap = pat_nnz;
+    const size_t csr = ((static_cast<size_t>(rp_cap) + 3) & ~3) * 4 + ((static_cast<size_t>(nz_cap) + 3) & ~3) * 8 +
+                       static_cast<size_t>(n_pat) * max_nodes + 16;
+    const int64_t tiles = (B + a.G - 1) / a.G;
+    const int tgrid = static_cast<int>(tiles < 3 * kNumSMs ? tiles : 3 * kNumSMs);
+    auto plaunch = [&](auto kern, int K, int stage_bytes, int S, int OB) {
+      const size_t psm = static_cast<size_t>(2 * 32 * K) * 4 + static_cast<size_t>(S) * stage_bytes +
+                         static_cast<size_t>(OB) * agg::TC_ROWS * 32 * 4 + csr;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(psm));
+      kern<<<tgrid, agg::TC_ROWS, psm, as_stream(stream)>>>(a, rp_cap, nz_cap);
+    };
+    if (d_in == 12)
+      plaunch(agg::gcn_layer_pipe_kernel<12, true, 3, 2>, 16, agg::TC_ROWS * 12 * 8, 3, 2);
+    else
+      plaunch(agg::gcn_layer_pipe_kernel<32, false, 3, 1>, 32, agg::TC_ROWS * 32 * 4, 3, 1);
+  } else if (tc_ok) {
     // tiles of whole graphs, <= 128 rows; 4 CTAs per SM (128 TMEM columns each)
     a.G = agg::TC_ROWS / max_nodes;
     const int K = (d_in + 7) & ~7;
