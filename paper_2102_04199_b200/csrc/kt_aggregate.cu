@@ -19,7 +19,9 @@
 // rows into a transposed buffer (float4 channel quads), then the dense transform
 // on the FP32 pipe as 4-row x 8-column FFMA2 register tiles, ReLU, into the
 // staged output rows.  Algorithmic bytes per graph: n d_in sizeof(in) + n d_out 4.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <cstdlib>
 
@@ -94,6 +96,20 @@ __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// 2-D TMA through a tensor map (coordinates: column, row)
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          s32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(s32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(s32(src))
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
 
 __device__ __forceinline__ int64_t tile_row0(const LayerArgs& a, int64_t g0) {
   return a.node_ptr ? a.node_ptr[g0] : g0 * a.n_uniform;
@@ -627,21 +643,30 @@ __global__ void __launch_bounds__(TC_ROWS, 4) gcn_layer_tc_kernel(LayerArgs a) {
 // aggregation / MMA of the tile in flight; three CTAs per SM (128 TMEM columns each).
 // Aggregating first (A X) W is the order the reference's einsum takes for layer 1
 // (SURVEY.md 8(a)); for layer 2 it equals A (H W) up to fp32 rounding.
-template <int DIN, bool IN64, int S, int OB>
-__global__ void __launch_bounds__(TC_ROWS, 3) gcn_layer_pipe_kernel(LayerArgs a, int rp_cap, int nz_cap) {
+//
+// TM (uniform graphs, 128-byte rows): tiles move through 2-D tensor maps with the 128-byte
+// swizzle instead of 1-D copies -- 16-byte piece c of tile row R sits at piece c ^ (R & 7)
+// -- so the row-per-thread reads and writes are bank-conflict free with no register
+// rotation (TMA undoes the swizzle on the way out).
+template <int DIN, bool IN64, int S, int OB, bool TM>
+__global__ void __launch_bounds__(TC_ROWS, 3)
+    gcn_layer_pipe_kernel(LayerArgs a, int rp_cap, int nz_cap, const __grid_constant__ CUtensorMap tm_in,
+                          const __grid_constant__ CUtensorMap tm_out) {
   constexpr int K = (DIN + 7) & ~7;
   constexpr int DOUT = 32;
   constexpr int ESZ = IN64 ? 8 : 4;
   constexpr int ROWB = DIN * ESZ;             // input row bytes (16-byte multiple)
   constexpr int STAGE = TC_ROWS * ROWB;       // input stage bytes
-  constexpr int OUTB = TC_ROWS * DOUT * 4;    // output staging bytes
   static_assert(ROWB % 16 == 0, "bulk copies need 16-byte rows");
-  extern __shared__ __align__(1024) unsigned char smem[];
-  float* bh = reinterpret_cast<float*>(smem);
-  float* bl = bh + DOUT * K;
-  unsigned char* stage0 = reinterpret_cast<unsigned char*>(bl + DOUT * K);
+  static_assert(!TM || (ROWB == 128 && !IN64), "the swizzled path takes 128-byte fp32 rows");
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // swizzled tiles need 1024-byte aligned buffers (the host adds 1 KB of slack)
+  unsigned char* smem = smem_raw + ((1024 - (s32(smem_raw) & 1023)) & 1023);
+  unsigned char* stage0 = smem;
   float* outb0 = reinterpret_cast<float*>(stage0 + S * STAGE);
-  int* s_rp = reinterpret_cast<int*>(outb0 + OB * TC_ROWS * DOUT);
+  float* bh = outb0 + OB * TC_ROWS * DOUT;
+  float* bl = bh + DOUT * K;
+  int* s_rp = reinterpret_cast<int*>(bl + DOUT * K);
   int* s_col = s_rp + ((rp_cap + 3) & ~3);
   float* s_val = reinterpret_cast<float*>(s_col + ((nz_cap + 3) & ~3));
   uint8_t* s_mask = reinterpret_cast<uint8_t*>(s_val + ((nz_cap + 3) & ~3));
@@ -666,9 +691,14 @@ __global__ void __launch_bounds__(TC_ROWS, 3) gcn_layer_pipe_kernel(LayerArgs a,
   auto issue_load = [&](int64_t t, int st) {
     int64_t r0;
     const int rows = tile_rows(t, r0);
-    const uint32_t bytes = static_cast<uint32_t>(rows) * ROWB;
-    mbar_expect(&full[st], bytes);
-    bulk_load(stage0 + st * STAGE, static_cast<const unsigned char*>(a.in) + r0 * ROWB, bytes, &full[st]);
+    if constexpr (TM) {  // full box every time (rows past the end arrive zero-filled)
+      mbar_expect(&full[st], static_cast<uint32_t>(a.G * a.n_uniform * ROWB));
+      tma_load_2d(stage0 + st * STAGE, &tm_in, 0, static_cast<int>(r0), &full[st]);
+    } else {
+      const uint32_t bytes = static_cast<uint32_t>(rows) * ROWB;
+      mbar_expect(&full[st], bytes);
+      bulk_load(stage0 + st * STAGE, static_cast<const unsigned char*>(a.in) + r0 * ROWB, bytes, &full[st]);
+    }
   };
 
   // ---- setup ---------------------------------------------------------------------------------
@@ -810,9 +840,10 @@ __global__ void __launch_bounds__(TC_ROWS, 3) gcn_layer_pipe_kernel(LayerArgs a,
           // 16-byte pieces read in a per-row rotated order (piece (i + rot) % NP): eight
           // consecutive rows then hit eight different bank groups of the 128-byte rows
           const float4* src = reinterpret_cast<const float4*>(tile + (base + j) * ROWB);
+          const int sw = TM ? ((base + j) & 7) : 0;
 #pragma unroll
           for (int i = 0; i < NP; ++i) {
-            const float4 v = src[(i + rot) & (NP - 1)];
+            const float4 v = TM ? src[i ^ sw] : src[(i + rot) & (NP - 1)];
             y[4 * i] = fmaf(w, v.x, y[4 * i]);
             y[4 * i + 1] = fmaf(w, v.y, y[4 * i + 1]);
             y[4 * i + 2] = fmaf(w, v.z, y[4 * i + 2]);
@@ -820,7 +851,7 @@ __global__ void __launch_bounds__(TC_ROWS, 3) gcn_layer_pipe_kernel(LayerArgs a,
           }
         }
       }
-      if constexpr (!IN64) {  // undo the rotation: piece c <- accumulator (c - rot) % NP (barrel shift)
+      if constexpr (!IN64 && !TM) {  // undo the rotation: piece c <- accumulator (c - rot) % NP (barrel shift)
 #pragma unroll
         for (int sh = 1; sh < NP; sh <<= 1) {
           if (rot & sh) {
@@ -853,7 +884,9 @@ __global__ void __launch_bounds__(TC_ROWS, 3) gcn_layer_pipe_kernel(LayerArgs a,
               const double d = reinterpret_cast<const double*>(tile + (h_base + j) * ROWB)[lane];
               yc = fmaf(w, static_cast<float>((d - d_mean[lane]) * d_rstd[lane]), yc);
             } else {
-              yc = fmaf(w, reinterpret_cast<const float*>(tile + (h_base + j) * ROWB)[lane], yc);
+              const int R = h_base + j;
+              const int c = TM ? ((((lane >> 2) ^ (R & 7)) << 2) | (lane & 3)) : lane;
+              yc = fmaf(w, reinterpret_cast<const float*>(tile + R * ROWB)[c], yc);
             }
           }
 #pragma unroll
@@ -925,7 +958,7 @@ __global__ void __launch_bounds__(TC_ROWS, 3) gcn_layer_pipe_kernel(LayerArgs a,
         const int orot = tid & 7;
 #pragma unroll
         for (int sh = 1; sh < 8; sh <<= 1) {
-          if (orot & sh) {
+          if (!TM && (orot & sh)) {
             float r[32];
 #pragma unroll
             for (int c = 0; c < 8; ++c)
@@ -939,14 +972,19 @@ __global__ void __launch_bounds__(TC_ROWS, 3) gcn_layer_pipe_kernel(LayerArgs a,
         for (int q = 0; q < 8; ++q) {
           float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
           if (a.relu) o = make_float4(fmaxf(o.x, 0.f), fmaxf(o.y, 0.f), fmaxf(o.z, 0.f), fmaxf(o.w, 0.f));
-          dst[(q + orot) & 7] = o;
+          dst[TM ? (q ^ orot) : ((q + orot) & 7)] = o;
         }
       }
     }
     fence_proxy_async();
     tc::tc_fence_before();
     __syncthreads();  // (C) staging tile complete; TMEM D reads done
-    if (tid == 0) bulk_store(a.out + r0 * DOUT, ob, static_cast<uint32_t>(rows) * DOUT * 4);
+    if (tid == 0) {
+      if constexpr (TM)
+        tma_store_2d(&tm_out, 0, static_cast<int>(r0), ob);  // rows past the end are clipped
+      else
+        bulk_store(a.out + r0 * DOUT, ob, static_cast<uint32_t>(rows) * DOUT * 4);
+    }
   }
   if (tid == 0) bulk_wait0();
   tc::tc_fence_before();
@@ -957,6 +995,33 @@ __global__ void __launch_bounds__(TC_ROWS, 3) gcn_layer_pipe_kernel(LayerArgs a,
   }
 }
 
+
+// Row-major fp32 (rows x 32) tensor maps for the swizzled path: box = one tile of
+// box_rows rows, 128-byte swizzle.  False if the driver entry point is unavailable.
+static bool tensor_maps(const void* in, const void* out, int64_t rows, int box_rows, CUtensorMap* tin,
+                        CUtensorMap* tout) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  static bool looked = false;
+  if (!looked) {
+    looked = true;
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  if (!encode || box_rows > 256 || rows >= (int64_t{1} << 31)) return false;
+  const cuuint64_t dims[2] = {32, static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {32 * sizeof(float)};
+  const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  auto mk = [&](CUtensorMap* m, const void* p) {
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(p), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  return mk(tin, in) && mk(tout, out);
+}
 }  // namespace agg
 }  // namespace kt
 
@@ -1029,17 +1094,26 @@ extern "C" int kt_gcn_layer(const void* in, int32_t in_f64, const double* fmean,
     const size_t csr = ((static_cast<size_t>(rp_cap) + 3) & ~3) * 4 + ((static_cast<size_t>(nz_cap) + 3) & ~3) * 8 +
                        static_cast<size_t>(n_pat) * max_nodes + 16;
     const int64_t tiles = (B + a.G - 1) / a.G;
-    const int tgrid = static_cast<int>(tiles < 3 * kNumSMs ? tiles : 3 * kNumSMs);
-    auto plaunch = [&](auto kern, int K, int stage_bytes, int S, int OB) {
-      const size_t psm = static_cast<size_t>(2 * 32 * K) * 4 + static_cast<size_t>(S) * stage_bytes +
+    const int per_sm = 3;  // shared memory holds three CTAs per SM
+    const int tgrid = static_cast<int>(tiles < per_sm * kNumSMs ? tiles : per_sm * kNumSMs);
+    CUtensorMap tm_in{}, tm_out{};
+    auto plaunch = [&](auto kern, int K, int stage_bytes, int S, int OB, bool tm) {
+      // (the swizzled path aligns its buffers to 1 KB at run time: slack for that)
+      const size_t psm = (tm ? 1024 : 0) + static_cast<size_t>(2 * 32 * K) * 4 + static_cast<size_t>(S) * stage_bytes +
                          static_cast<size_t>(OB) * agg::TC_ROWS * 32 * 4 + csr;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(psm));
-      kern<<<tgrid, agg::TC_ROWS, psm, as_stream(stream)>>>(a, rp_cap, nz_cap);
+      kern<<<tgrid, agg::TC_ROWS, psm, as_stream(stream)>>>(a, rp_cap, nz_cap, tm_in, tm_out);
     };
-    if (d_in == 12)
-      plaunch(agg::gcn_layer_pipe_kernel<12, true, 3, 2>, 16, agg::TC_ROWS * 12 * 8, 3, 2);
-    else
-      plaunch(agg::gcn_layer_pipe_kernel<32, false, 3, 1>, 32, agg::TC_ROWS * 32 * 4, 3, 1);
+    if (d_in == 12) {
+      plaunch(agg::gcn_layer_pipe_kernel<12, true, 3, 2, false>, 16, agg::TC_ROWS * 12 * 8, 3, 2, false);
+    } else if (nodes_per_graph > 0 && agg::tensor_maps(in, out, B * nodes_per_graph, a.G * nodes_per_graph,
+                                                       &tm_in, &tm_out) &&
+               !(getenv("KT_AGG_NOTM") && getenv("KT_AGG_NOTM")[0] == '1')) {
+      // (stages x output buffers 2x1, 3x1 and 2x2 measure the same, 72-73% of HBM peak)
+      plaunch(agg::gcn_layer_pipe_kernel<32, false, 2, 1, true>, 32, agg::TC_ROWS * 32 * 4, 2, 1, true);
+    } else {
+      plaunch(agg::gcn_layer_pipe_kernel<32, false, 3, 1, false>, 32, agg::TC_ROWS * 32 * 4, 3, 1, false);
+    }
   } else if (tc_ok) {
     // tiles of whole graphs, <= 128 rows; 4 CTAs per SM (128 TMEM columns each)
     a.G = agg::TC_ROWS / max_nodes;

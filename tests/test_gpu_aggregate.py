@@ -140,12 +140,18 @@ def test_streaming_errors(cuda_device, g_model):
         pm.aggregate_batch(torch.zeros((2, 3, 31), device="cuda"), m.agg)
 
 
-def test_tensor_core_and_ffma_layer_paths_agree(cuda_device, g_encode, g_model, monkeypatch):
-    """The tcgen05 3xTF32 layer kernel and the FFMA2 warp kernel give the same H (fp32-level)."""
+@pytest.mark.parametrize("variant", ["KT_AGG_NOTM", "KT_AGG_TC1", "KT_AGG_FFMA"])
+def test_layer_kernel_variants_agree(cuda_device, g_encode, g_model, monkeypatch, variant):
+    """Every layer kernel gives the same H (fp32-level) on 50k super graphs: the default
+    TMA-pipelined path (swizzled tensor maps for uniform graphs) against the 1-D bulk
+    pipeline (NOTM), the unpipelined tensor-core kernel (TC1) and the FFMA2 warp kernel."""
     m = device_model(g_model)
-    feats, lay = _feats(g_encode, g_model, "super")
-    h_tc = pm.gcn_forward_batch(m, feats, lay.feature_mask, lay.adjacency)
-    monkeypatch.setenv("KT_AGG_FFMA", "1")
-    h_ff = pm.gcn_forward_batch(m, feats, lay.feature_mask, lay.adjacency)
-    monkeypatch.delenv("KT_AGG_FFMA")
-    _close(h_tc, h_ff.double().cpu().numpy(), rtol=2e-5)
+    spec = spec_of(g_encode, "conv2d")
+    space = pk.build_knob_space(spec)
+    lay = pg.batch_layout(spec, TEMPLATE)
+    feats = pg.encode_batch(spec, space, rng_from("agg-var").integers(0, space.size, 50_001), lay)
+    h_def = pm.gcn_forward_batch(m, feats, lay.feature_mask, lay.adjacency)
+    monkeypatch.setenv(variant, "1")
+    h_var = pm.gcn_forward_batch(m, feats, lay.feature_mask, lay.adjacency)
+    monkeypatch.delenv(variant)
+    _close(h_def, h_var.double().cpu().numpy(), rtol=2e-5)
