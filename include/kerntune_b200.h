@@ -196,6 +196,31 @@ int kt_sweep_host(const kt_spec_table* tab, const kt_dims* dims, const float* pa
                   int32_t k, int64_t* top_idx_dev, float* top_score_dev, int64_t* top_idx_host,
                   float* top_score_host, void* topk_ws, int64_t topk_ws_bytes, int32_t* err_dev, void* stream);
 
+/* ---- GP surrogate + batch UCB of the meta-BO proposer (search.py:39-159, 284-340) ---------- */
+/* All fp64, device pointers.  Coordinates are (points x d) row-major, d <= 16.
+ * gp_kernel (search.py:72-76): out (n1 x n2) = exp(-0.5 max(|a|^2 + |b|^2 - 2 a.b, 0)), a = x/ls. */
+int kt_gp_gram(const double* x1, int32_t n1, const double* x2, int32_t n2, int32_t d, const double* ls, double* out,
+               void* stream);
+/* gp_fit's per-lengthscale work (search.py:79-121) for n_cand lengthscale vectors at once
+ * (ls: n_cand x d): L (n_cand x n x n, the lower Cholesky factor of K + nv I stored
+ * COLUMN-major) with nv escalated tenfold from `noise` until the factorisation succeeds
+ * or nv >= max_jitter; alpha (n_cand x n) = K^-1 y; info (n_cand x 3) = {fitted nv,
+ * marginal log likelihood, status (0 ok, 1 not positive definite at max_jitter)}. n <= 1024. */
+int kt_gp_factor(const double* x, int32_t n, int32_t d, const double* ls, int32_t n_cand, const double* y,
+                 double noise, double max_jitter, double* L, double* alpha, double* info, void* stream);
+/* gp_predict_many (search.py:129-139) at P points xp: mean, var = max(1 - |L^-1 k(x,xp)|^2, 0);
+ * if cov != NULL also _gp_posterior_cov (search.py:152-157): cov (P x P) = k(xp,xp) - v^T v
+ * (needs kt_gp_workspace_bytes(n, P, 0)).  L as written by kt_gp_factor. */
+int64_t kt_gp_workspace_bytes(int32_t n, int32_t P, int32_t take);
+int kt_gp_posterior(const double* x, int32_t n, int32_t d, const double* ls, const double* L, const double* alpha,
+                    const double* xp, int32_t P, double* mean, double* var, double* cov, void* workspace,
+                    int64_t workspace_bytes, void* stream);
+/* bo_propose_batch's sequential UCB with hallucinated downdates (search.py:324-340):
+ * picks (take) = positions into the pool, in pick order.  P <= 4096, take <= 64;
+ * workspace >= take * P * 8 bytes. */
+int kt_gp_ucb(const double* mean, const double* cov, int32_t P, double noise, double beta, int32_t take,
+              int32_t* picks, void* workspace, int64_t workspace_bytes, void* stream);
+
 /* ---- simulated-annealing exploration (sa_explore, search.py:202-254) ----------------------- */
 /* One proposal step for n_chains chains from pre-drawn randoms (the host draws them
  * from the caller's numpy Generator in the reference's order): the chosen knob of

@@ -538,3 +538,78 @@ def sa_propose(predict_idx, cards, size, sched, visited, rng, batch) -> list:
     if len(picks) < batch:
         picks += draw_unvisited(size, visited | set(picks), batch - len(picks), rng)
     return picks
+
+
+# --- GP surrogate + batch UCB (search.py:39-159, 284-340) ------------------------------------
+
+GP_LENGTHSCALES = (0.1, 0.3, 1.0, 3.0)  # search.py:37
+GP_MAX_JITTER = 1e-1                     # search.py:38
+
+
+def gp_kernel(x1, x2, ls) -> np.ndarray:
+    """RBF on lengthscale-scaled coordinates (search.py:72-76)."""
+    a = x1 / ls
+    b = x2 / ls
+    d2 = (a * a).sum(axis=1)[:, None] + (b * b).sum(axis=1)[None, :] - 2.0 * a @ b.T
+    return np.exp(-0.5 * np.maximum(d2, 0.0))
+
+
+def gp_chol(k, noise):
+    """Cholesky of k + nv I with tenfold jitter escalation (search.py:79-91); None when
+    even MAX_JITTER fails (the reference raises NumericError)."""
+    nv = noise
+    while True:
+        try:
+            return np.linalg.cholesky(k + nv * np.eye(k.shape[0])), nv
+        except np.linalg.LinAlgError:
+            pass
+        if nv >= GP_MAX_JITTER:
+            return None, nv
+        nv *= 10.0
+
+
+def gp_fit(x, y, noise, ls=None):
+    """(lengthscales, L, alpha, noise) maximising the marginal likelihood over the grid
+    (search.py:94-121); ls fixes the lengthscales instead."""
+    n, d = x.shape
+    cands = [np.full(d, v) for v in GP_LENGTHSCALES] if ls is None else [np.asarray(ls, dtype=np.float64)]
+    best = None
+    for c in cands:
+        l, nv = gp_chol(gp_kernel(x, x, c), noise)
+        z = np.linalg.solve(l, y)  # cho_solve: L z = y, L^T alpha = z
+        alpha = np.linalg.solve(l.T, z)
+        mll = -0.5 * float(y @ alpha) - float(np.log(np.diag(l)).sum()) - 0.5 * n * math.log(2.0 * math.pi)
+        if best is None or mll > best[0]:
+            best = (mll, c, l, alpha, nv)
+    return best[1], best[2], best[3], best[4]
+
+
+def gp_posterior(x, ls, l, alpha, xp):
+    """(mean, var, cov) of the latent function at xp (search.py:129-157)."""
+    kxn = gp_kernel(x, xp, ls)
+    v = np.linalg.solve(l, kxn)
+    mean = kxn.T @ alpha
+    var = np.maximum(1.0 - (v * v).sum(axis=0), 0.0)
+    cov = gp_kernel(xp, xp, ls) - v.T @ v
+    return mean, var, cov
+
+
+def ucb_batch(mean, cov, noise, beta, take) -> list:
+    """Sequential UCB with hallucinated downdates (search.py:324-340): positions into
+    the (sorted) pool, in pick order."""
+    var = np.maximum(np.diag(cov).copy(), 0.0)
+    cov = cov.copy()
+    active = np.ones(len(mean), dtype=bool)
+    out = []
+    for _ in range(take):
+        ucb = mean + math.sqrt(beta) * np.sqrt(np.maximum(var, 0.0))
+        ucb[~active] = -np.inf
+        z = int(np.argmax(ucb))
+        out.append(z)
+        active[z] = False
+        denom = var[z] + noise
+        if denom > 0.0:
+            c = cov[:, z].copy()
+            var = np.maximum(var - c * c / denom, 0.0)
+            cov = cov - np.outer(c, c) / denom
+    return out

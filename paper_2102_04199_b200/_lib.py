@@ -108,6 +108,11 @@ _SIGS = {
                                      i64, vp, vp]),
     "kt_score_indices_ex": (ctypes.c_int, [vp, ctypes.POINTER(Dims), vp, vp, vp, i64, i64, vp, vp, vp, vp, vp]),
     "kt_topk_keys": (ctypes.c_int, [vp, i64, i32, vp, vp, vp, i64, vp]),
+    "kt_gp_gram": (ctypes.c_int, [vp, i32, vp, i32, i32, vp, vp, vp]),
+    "kt_gp_factor": (ctypes.c_int, [vp, i32, i32, vp, i32, vp, ctypes.c_double, ctypes.c_double, vp, vp, vp, vp]),
+    "kt_gp_workspace_bytes": (i64, [i32, i32, i32]),
+    "kt_gp_posterior": (ctypes.c_int, [vp, i32, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp, i64, vp]),
+    "kt_gp_ucb": (ctypes.c_int, [vp, vp, i32, ctypes.c_double, ctypes.c_double, i32, vp, vp, i64, vp]),
     "kt_sa_propose": (ctypes.c_int, [vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "kt_sa_accept": (ctypes.c_int, [i32, i32, vp, vp, f64, vp, vp, vp, vp]),
     "kt_topk_workspace_bytes": (i64, [i64, i32]),

@@ -445,3 +445,182 @@ def sa_propose(predict, space: KnobSpace, sched: SaSchedule, visited: set, rng, 
     if len(picks) < batch:
         picks += draw_unvisited(space, visited | set(picks), batch - len(picks), rng)
     return [index_config(space, i) for i in picks]
+
+
+# --- GP surrogate + batch UCB (search.py:39-159, 284-340), the meta-BO proposer ---------------
+
+LENGTHSCALE_GRID = (0.1, 0.3, 1.0, 3.0)  # search.py:37
+MAX_JITTER_NOISE = 1e-1                  # search.py:38
+
+
+@dataclass
+class GpSurrogate:
+    """search.py:54-66, same fields (host numpy arrays).  The device copies of the
+    observations and the factor ride along in `_dev` so predictions do not re-upload."""
+    x: np.ndarray
+    y: np.ndarray
+    lengthscales: np.ndarray | None = None
+    noise_variance: float = 1e-4
+    chol: np.ndarray | None = None
+    alpha: np.ndarray | None = None
+    fitted_noise: float | None = None
+    _dev: dict | None = None
+
+    @property
+    def n_obs(self) -> int:
+        return int(self.x.shape[0]) if np.asarray(self.x).ndim == 2 else 0
+
+
+def knob_coordinates(space: KnobSpace, configs: list) -> np.ndarray:
+    """Each knob's value index mapped to [0, 1) by index / cardinality (search.py:65-69)."""
+    cards = np.array([len(k.values) for k in space.knobs], dtype=np.float64)
+    mat = np.array([c.choices for c in configs], dtype=np.float64).reshape(len(configs), -1)
+    return mat / cards
+
+
+def _d64(a, dev) -> torch.Tensor:
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+
+
+def _gp_device():
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def gp_kernel(x1, x2, lengthscales) -> np.ndarray:
+    """RBF Gram matrix (search.py:72-76), computed on the device."""
+    dev = _gp_device()
+    a, b, ls = _d64(x1, dev), _d64(x2, dev), _d64(lengthscales, dev)
+    out = torch.empty((a.shape[0], b.shape[0]), dtype=torch.float64, device=dev)
+    lib = _lib.load()
+    _lib.check(lib.kt_gp_gram(a.data_ptr(), a.shape[0], b.data_ptr(), b.shape[0], a.shape[1], ls.data_ptr(),
+                              out.data_ptr(), _lib.stream_handle()), "gp_kernel")
+    return out.cpu().numpy()
+
+
+def gp_fit(s: GpSurrogate, select_lengthscale: bool = True) -> GpSurrogate:
+    """Refresh the factorization; optionally pick the isotropic lengthscale by marginal
+    likelihood over the grid (search.py:94-121).  All candidates factor concurrently
+    (one CTA each, jitter escalation on the device); the first best likelihood wins, and
+    a candidate that is not positive definite even at MAX_JITTER_NOISE raises
+    NumericError, as the reference does."""
+    from dataclasses import replace
+
+    if s.n_obs == 0:
+        return s
+    x = np.asarray(s.x, dtype=np.float64)
+    n, d = x.shape
+    if select_lengthscale or s.lengthscales is None:
+        cands = np.stack([np.full(d, v) for v in LENGTHSCALE_GRID])
+    else:
+        cands = np.asarray(s.lengthscales, dtype=np.float64)[None, :]
+    dev = _gp_device()
+    xd, yd, lsd = _d64(x, dev), _d64(s.y, dev), _d64(cands, dev)
+    nc = cands.shape[0]
+    L = torch.empty((nc, n, n), dtype=torch.float64, device=dev)
+    alpha = torch.empty((nc, n), dtype=torch.float64, device=dev)
+    info = torch.empty((nc, 3), dtype=torch.float64, device=dev)
+    lib = _lib.load()
+    _lib.check(lib.kt_gp_factor(xd.data_ptr(), n, d, lsd.data_ptr(), nc, yd.data_ptr(), float(s.noise_variance),
+                                MAX_JITTER_NOISE, L.data_ptr(), alpha.data_ptr(), info.data_ptr(),
+                                _lib.stream_handle()), "gp_fit")
+    inf = info.cpu().numpy()
+    best = None
+    for c in range(nc):
+        if inf[c, 2] != 0.0:
+            raise NumericError(f"kernel matrix not positive definite even at noise {inf[c, 0]:g}")
+        if best is None or inf[c, 1] > inf[best, 1]:
+            best = c
+    Lb = L[best]
+    dev_state = {"x": xd, "ls": lsd[best].contiguous(), "L": Lb, "alpha": alpha[best]}
+    return replace(s, lengthscales=cands[best].copy(), chol=Lb.cpu().numpy().T.copy(),
+                   alpha=alpha[best].cpu().numpy(), fitted_noise=float(inf[best, 0]), _dev=dev_state)
+
+
+def _require_fitted(s: GpSurrogate) -> None:
+    if s.chol is None or s.alpha is None:
+        raise DomainError("surrogate not fitted; call gp_fit first")
+
+
+def _dev_state(s: GpSurrogate) -> dict:
+    if s._dev is not None:
+        return s._dev
+    dev = _gp_device()  # a surrogate fitted elsewhere (e.g. the reference): upload its factor
+    return {"x": _d64(s.x, dev), "ls": _d64(s.lengthscales, dev),
+            "L": _d64(np.asarray(s.chol).T, dev), "alpha": _d64(s.alpha, dev)}
+
+
+def _posterior(s: GpSurrogate, xp: np.ndarray, want_cov: bool):
+    st = _dev_state(s)
+    n, d = st["x"].shape
+    dev = st["x"].device
+    xpd = _d64(xp, dev)
+    P = xpd.shape[0]
+    mean = torch.empty(P, dtype=torch.float64, device=dev)
+    var = torch.empty(P, dtype=torch.float64, device=dev)
+    lib = _lib.load()
+    cov = ws = None
+    wsb = 0
+    if want_cov:
+        cov = torch.empty((P, P), dtype=torch.float64, device=dev)
+        wsb = int(lib.kt_gp_workspace_bytes(n, P, 0))
+        ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    _lib.check(lib.kt_gp_posterior(st["x"].data_ptr(), n, d, st["ls"].data_ptr(), st["L"].data_ptr(),
+                                   st["alpha"].data_ptr(), xpd.data_ptr(), P, mean.data_ptr(), var.data_ptr(),
+                                   _lib.ptr(cov), _lib.ptr(ws), wsb, _lib.stream_handle()), "gp posterior")
+    return mean, var, cov
+
+
+def gp_predict_many(s: GpSurrogate, x: np.ndarray) -> tuple:
+    """Exact posterior (means, variances) of the latent function (search.py:129-139)."""
+    x = np.asarray(x, dtype=np.float64)
+    if s.n_obs == 0:
+        return np.zeros(x.shape[0]), np.ones(x.shape[0])
+    _require_fitted(s)
+    mean, var, _ = _posterior(s, x, False)
+    return mean.cpu().numpy(), var.cpu().numpy()
+
+
+def gp_predict(s: GpSurrogate, x) -> tuple:
+    mean, var = gp_predict_many(s, np.asarray(x, dtype=np.float64)[None, :])
+    return float(mean[0]), float(var[0])
+
+
+def bo_propose_batch(s: GpSurrogate, space: KnobSpace, batch: int, beta_ucb: float, candidate_pool: int,
+                     visited: set, rng, pool: list | None = None) -> list:
+    """Sequential UCB over a candidate pool with hallucinated batch downdates
+    (search.py:284-340).  Pool construction and RNG draws are the reference's; the
+    posterior covariance and the UCB loop run on the device (kt_gp_posterior, kt_gp_ucb)."""
+    from .kernels import config_index, index_config
+
+    if batch < 1:
+        raise DomainError("batch must be >= 1")
+    if pool is None:
+        indices = draw_unvisited(space, visited, candidate_pool, rng)
+    else:
+        seen: set = set()
+        indices = []
+        for c in pool:
+            i = config_index(space, c)
+            if i in visited or i in seen:
+                continue
+            seen.add(i)
+            indices.append(i)
+    if not indices:
+        raise DomainError("empty candidate pool")
+    indices = sorted(indices)
+    take = min(batch, len(indices))
+    if s.n_obs == 0:
+        pick = rng.permutation(len(indices))[:take]
+        return [index_config(space, indices[int(i)]) for i in pick]
+    _require_fitted(s)
+    configs = [index_config(space, i) for i in indices]
+    mean, _, cov = _posterior(s, knob_coordinates(space, configs), True)
+    noise = s.fitted_noise if s.fitted_noise is not None else s.noise_variance
+    P = len(indices)
+    lib = _lib.load()
+    picks = torch.empty(take, dtype=torch.int32, device=mean.device)
+    wsb = int(lib.kt_gp_workspace_bytes(0, P, take))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=mean.device)
+    _lib.check(lib.kt_gp_ucb(mean.data_ptr(), cov.data_ptr(), P, float(noise), float(beta_ucb), take,
+                             picks.data_ptr(), ws.data_ptr(), wsb, _lib.stream_handle()), "bo_propose_batch")
+    return [configs[int(p)] for p in picks.cpu().numpy()]

@@ -80,3 +80,8 @@ def cuda_device():
 @pytest.fixture(scope="session")
 def g_dataset():
     return load_golden("dataset")
+
+
+@pytest.fixture(scope="session")
+def g_gp():
+    return load_golden("gp")

@@ -22,6 +22,9 @@ Everything is keyed by `rng_from` so reruns are byte-identical.  Outputs:
   dataset/       a small reference gen_dataset (harness.py:164-176) written by the
                  reference's save_dataset (harness.py:195-216): kernels.yaml,
                  samples.csv, manifest.json
+  gp.npz         GP surrogate (search.py:39-159): gp_fit with lengthscale selection and
+                 jitter escalation, gp_predict_many, _gp_posterior_cov and
+                 bo_propose_batch picks, on synthetic observations in knob coordinates
   dataset.npz    on that dataset: dataset_norms (meta.py:81-101) of the raw and the
                  augmented dataset_samples (harness.py:179-192), their labels and
                  kernel classes, grad (model.py:218) of an index-picked raw batch,
@@ -309,7 +312,57 @@ def dataset_goldens():
     np.savez_compressed(os.path.join(OUT, "dataset.npz"), **out)
 
 
+GP_CASES = ((40, 64, 4, 2.0), (200, 512, 16, 2.0), (7, 30, 5, 0.5), (512, 512, 8, 2.0))  # (n_obs, pool, batch, beta)
+
+
+def gp_goldens():
+    space = rk.build_knob_space(BENCH_SPEC)
+    out = {}
+    for case, (n, pool, batch, beta) in enumerate(GP_CASES):
+        rng = rng_from("golden-gp", case)
+        obs = rk.sample_configs(space, n, rng)
+        x = rs.knob_coordinates(space, obs)
+        raw = np.sin(3.0 * x).sum(axis=1) + 0.1 * rng.normal(size=n)
+        y = (raw - raw.mean()) / raw.std()
+        s = rs.gp_fit(rs.GpSurrogate(x=x, y=y, noise_variance=1e-4), select_lengthscale=True)
+        pool_cfgs = rk.sample_configs(space, pool, rng)
+        coords = rs.knob_coordinates(space, pool_cfgs)
+        mean, var = rs.gp_predict_many(s, coords)
+        cov = rs._gp_posterior_cov(s, coords)
+        visited = set(rk.config_index(space, c) for c in obs)
+        picks = rs.bo_propose_batch(s, space, batch, beta, pool, visited, rng_from("golden-gp-bo", case),
+                                    pool=pool_cfgs)
+        out[f"c{case}/x"], out[f"c{case}/y"] = x, y
+        out[f"c{case}/ls"], out[f"c{case}/alpha"] = s.lengthscales, s.alpha
+        out[f"c{case}/noise"] = np.array(s.fitted_noise)
+        out[f"c{case}/pool_idx"] = np.array([rk.config_index(space, c) for c in pool_cfgs], dtype=np.int64)
+        out[f"c{case}/mean"], out[f"c{case}/var"] = mean, var
+        # keep the fixture small: full factor / covariance for the small cases, sampled rows otherwise
+        rows = np.arange(n) if n <= 64 else np.linspace(0, n - 1, 12).astype(np.int64)
+        out[f"c{case}/chol_rows"], out[f"c{case}/chol"] = rows, s.chol[rows]
+        crow = np.arange(pool) if pool <= 64 else np.linspace(0, pool - 1, 12).astype(np.int64)
+        out[f"c{case}/cov_rows"], out[f"c{case}/cov"] = crow, cov[crow]
+        out[f"c{case}/picks"] = np.array([rk.config_index(space, c) for c in picks], dtype=np.int64)
+        out[f"c{case}/obs_idx"] = np.array([rk.config_index(space, c) for c in obs], dtype=np.int64)
+        # refit at fixed lengthscales (the tune loop between hyper refits)
+        s2 = rs.gp_fit(rs.GpSurrogate(x=x, y=y, lengthscales=np.full(x.shape[1], 0.3), noise_variance=1e-4),
+                       select_lengthscale=False)
+        out[f"c{case}/alpha_fixed"] = s2.alpha
+    # a kernel matrix that needs jitter escalation: duplicated observations
+    xd = np.repeat(rs.knob_coordinates(space, rk.sample_configs(space, 20, rng_from("golden-gp-dup"))), 3, axis=0)
+    yd = np.linspace(-1.0, 1.0, xd.shape[0])
+    sd = rs.gp_fit(rs.GpSurrogate(x=xd, y=yd, lengthscales=np.full(xd.shape[1], 1.0), noise_variance=1e-20),
+                   select_lengthscale=False)
+    out["dup/x"], out["dup/y"], out["dup/ls"] = xd, yd, sd.lengthscales
+    out["dup/noise"], out["dup/alpha"] = np.array(sd.fitted_noise), sd.alpha
+    out["cases"] = np.array(GP_CASES, dtype=np.float64)
+    np.savez_compressed(os.path.join(OUT, "gp.npz"), **out)
+
+
 def main():
+    if sys.argv[1:] == ["gp"]:
+        gp_goldens()
+        return
     if sys.argv[1:] == ["sa"]:
         sa_goldens()
         return
@@ -326,6 +379,7 @@ def main():
     rank_goldens()
     sa_goldens()
     dataset_goldens()
+    gp_goldens()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))
 
