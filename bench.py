@@ -445,6 +445,58 @@ def bench_sa(m, reps=20):
             "config": "SaSchedule defaults, conv2d bench spec, super layout; wall clock incl. host RNG draws"}
 
 
+def bench_gp(n=512, pool=512, batch=16, reps=10, cpu_reps=3):
+    """8(f) rank 3: the meta-BO proposer's GP work per tuning round at the TuneConfig sizes
+    (gp_obs_window 512 observations, candidate_pool 512): gp_fit over the 4-lengthscale
+    grid + bo_propose_batch (posterior covariance + sequential UCB), device against the
+    oracle restatement (numpy / LAPACK fp64, the reference's algorithm) on the host."""
+    import torch
+
+    from oracle import kt_oracle as ko
+    from paper_2102_04199_b200 import kernels as pk
+    from paper_2102_04199_b200 import search as ps
+    from paper_2102_04199_b200.util import rng_from
+
+    space = pk.build_knob_space(pk.KernelSpec(*SPEC_ARGS))
+    rng = rng_from("bench-gp")
+    obs = pk.sample_configs(space, n, rng)
+    x = ps.knob_coordinates(space, obs)
+    raw = np.sin(3.0 * x).sum(axis=1) + 0.1 * rng.normal(size=n)
+    y = (raw - raw.mean()) / raw.std()
+    pool_cfgs = pk.sample_configs(space, pool, rng)
+    visited = set(pk.config_index(space, c) for c in obs)
+
+    def dev_round():
+        s = ps.gp_fit(ps.GpSurrogate(x=x, y=y, noise_variance=1e-4), select_lengthscale=True)
+        return ps.bo_propose_batch(s, space, batch, 2.0, pool, visited, rng_from("bench-gp-bo"), pool=pool_cfgs)
+
+    for _ in range(2):
+        dev_round()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        dev_round()
+    torch.cuda.synchronize()
+    dev_ms = 1e3 * (time.perf_counter() - t0) / reps
+
+    def cpu_round():
+        ls, l, alpha, nv = ko.gp_fit(x, y, 1e-4)
+        idx = sorted(pk.config_index(space, c) for c in pool_cfgs)
+        xp = ps.knob_coordinates(space, [pk.index_config(space, i) for i in idx])
+        mean, _, cov = ko.gp_posterior(x, ls, l, alpha, xp)
+        return ko.ucb_batch(mean, cov, nv, 2.0, batch)
+
+    t0 = time.perf_counter()
+    for _ in range(cpu_reps):
+        cpu_round()
+    cpu_ms = 1e3 * (time.perf_counter() - t0) / cpu_reps
+    return {"metric": "GP round (gp_fit over the lengthscale grid + bo_propose_batch)", "value": dev_ms,
+            "unit": "ms/round", "higher_is_better": False, "cpu_oracle_ms": cpu_ms, "speedup": cpu_ms / dev_ms,
+            "config": f"{n} observations x 8 knob coordinates, pool {pool}, batch {batch}, fp64; wall clock incl. "
+                      "host pool construction and result copies; CPU: oracle restatement (numpy/LAPACK) on the "
+                      "host cores"}
+
+
 # --- CPU arms -------------------------------------------------------------------------# --- CPU arms -------------------------------------------------------------------------
 
 
@@ -672,6 +724,7 @@ def run_ours(args):
             line["aggregation"] = bench_aggregate(m)
             line["sa_explore"] = bench_sa(m)
             line["dataset"] = bench_dataset(entries)
+            line["gp"] = bench_gp()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:

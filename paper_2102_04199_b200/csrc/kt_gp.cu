@@ -6,13 +6,14 @@
 // by sequential UCB over a 512-candidate pool with hallucinated variance downdates
 // (bo_propose_batch).  Here:
 //   factor_kernel     one CTA per lengthscale candidate: Gram entries on the fly from
-//                     the scaled coordinates (smem), left-looking Cholesky into a
-//                     column-major factor (thread = row: coalesced column reads), jitter
+//                     the scaled coordinates (smem), blocked left-looking Cholesky into a
+//                     column-major factor (thread = row, 16-column panels in registers), jitter
 //                     escalation inside the kernel, forward / backward solves for alpha,
 //                     and the marginal likelihood -- no host round trips;
-//   posterior_kernel  32 pool points per CTA: k(x, xp) into shared memory, mean, the
-//                     triangular solve v = L^-1 k(x, xp) for 32 right-hand sides at once
-//                     (8 warps split the rows of each column update), var = 1 - |v|^2;
+//   posterior_kernel  16 pool points per CTA: k(x, xp) into shared memory, mean, the
+//                     blocked triangular solve v = L^-1 k(x, xp) for the 16 right-hand
+//                     sides (diagonal blocks by one warp, trailing rows by the CTA),
+//                     var = 1 - |v|^2;
 //   cov_kernel        k(xp, xp) - v^T v (64 x 64 output tiles, fp64 FMA);
 //   ucb_kernel        one CTA: the sequential UCB loop.  Only the picked columns of the
 //                     downdated covariance are ever needed, so column t is rebuilt from
@@ -28,11 +29,11 @@ namespace gp {
 
 constexpr int MAXD = 16;     // knob coordinates per point
 constexpr int MAXN = 1024;   // observations (gp_obs_window is 512)
-constexpr int FT = 1024;     // factor kernel threads
-constexpr int PC = 32;       // pool points per posterior CTA
+constexpr int PC = 16;       // pool points per posterior CTA
 constexpr int PT = 256;      // posterior kernel threads
 constexpr int UT = 1024;     // ucb kernel threads
 constexpr int MAXP = 4096;   // candidate pool
+constexpr int PW = 16;       // Cholesky / triangular-solve panel width
 
 __device__ __forceinline__ double gram(const double* a, double aa, const double* b, double bb, int d) {
   double ab = 0.0;
@@ -61,6 +62,7 @@ __device__ double block_sum(double v, double* red) {
 
 // grid = candidates; x (n x d), ls (cand x d), L (cand x n x n, column-major lower factor),
 // alpha (cand x n), info (cand x 3: fitted noise, mll, status 0 ok / 1 not PD at max jitter)
+template <int FT>
 __global__ void __launch_bounds__(FT) factor_kernel(const double* __restrict__ x, int n, int d,
                                                     const double* __restrict__ ls_all, const double* __restrict__ y,
                                                     double noise, double max_jitter, double* __restrict__ L_all,
@@ -81,31 +83,77 @@ __global__ void __launch_bounds__(FT) factor_kernel(const double* __restrict__ x
   for (int i = tid; i < n; i += FT) AA[i] = sq_norm(A + i * d, d);
   __syncthreads();
 
+  // Blocked left-looking Cholesky, thread = row, panels of PW columns held in registers:
+  //   1. acc[c] = K[i][j0 + c] - sum_{k < j0} L[i][k] L[j0 + c][k]: the earlier columns are
+  //      read once per panel (column-major L: coalesced in i), the panel rows' values are
+  //      staged through shared memory 16 columns at a time;
+  //   2. the panel is factored right-looking in registers, the pivot row's entries
+  //      broadcast through shared memory;
+  //   3. the panel's columns are written out.
+  __shared__ double S[PW][PW], pv[PW];
   double nv = noise;
   int status = 0;
+  const int i = tid;
   for (;;) {
     if (tid == 0) s_fail = 0;
     __syncthreads();
-    for (int j = 0; j < n; ++j) {
-      // rows i >= j: dot_i = sum_{k<j} L[i][k] L[j][k] (column-major: coalesced in i)
-      for (int i = j + tid; i < n; i += FT) {
-        double dot = 0.0;
-        for (int k = 0; k < j; ++k) dot = fma(L[static_cast<size_t>(k) * n + i], L[static_cast<size_t>(k) * n + j], dot);
-        double kij = gram(A + i * d, AA[i], A + j * d, AA[j], d);
-        if (i == j) {
-          const double s = (kij + nv) - dot;
-          if (!(s > 0.0)) s_fail = 1;
-          s_diag = sqrt(s);
-          L[static_cast<size_t>(j) * n + j] = s_diag;
+    for (int j0 = 0; j0 < n && !s_fail; j0 += PW) {
+      const int nb = n - j0 < PW ? n - j0 : PW;
+      const bool mine = i >= j0 && i < n;
+      double acc[PW];
+#pragma unroll
+      for (int c = 0; c < PW; ++c) {
+        acc[c] = 0.0;
+        if (mine && c < nb && i >= j0 + c) {
+          acc[c] = gram(A + i * d, AA[i], A + (j0 + c) * d, AA[j0 + c], d);
+          if (i == j0 + c) acc[c] += nv;
         }
-        R[i] = kij - dot;  // (stash; row j's own slot is unused)
       }
-      __syncthreads();
+      for (int k0 = 0; k0 < j0; k0 += PW) {
+        if (tid < PW * PW) {
+          const int kk = tid / PW, c = tid % PW;
+          S[kk][c] = c < nb ? L[static_cast<size_t>(k0 + kk) * n + j0 + c] : 0.0;
+        }
+        __syncthreads();
+        if (mine) {
+#pragma unroll 4
+          for (int kk = 0; kk < PW; ++kk) {
+            const double lik = L[static_cast<size_t>(k0 + kk) * n + i];
+#pragma unroll
+            for (int c = 0; c < PW; ++c) acc[c] = fma(-lik, S[kk][c], acc[c]);
+          }
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int c = 0; c < PW; ++c) {
+        if (c < nb) {
+          const int j = j0 + c;
+          if (i == j) {
+            const double sdiag = acc[c];
+            if (!(sdiag > 0.0)) s_fail = 1;
+            acc[c] = sqrt(sdiag);
+            s_diag = acc[c];
+          }
+          __syncthreads();
+          if (s_fail) break;
+          if (i > j && i < n) acc[c] = acc[c] / s_diag;
+          if (i > j && i < j0 + nb) pv[i - j0] = acc[c];  // L[t][j] of the panel rows t
+          __syncthreads();
+          if (i > j && i < n) {
+#pragma unroll
+            for (int c2 = c + 1; c2 < PW; ++c2)
+              if (c2 < nb) acc[c2] = fma(-acc[c], pv[c2], acc[c2]);
+          }
+        }
+      }
       if (s_fail) break;
-      const double dj = s_diag;
-      for (int i = j + 1 + tid; i < n; i += FT) L[static_cast<size_t>(j) * n + i] = R[i] / dj;
+#pragma unroll
+      for (int c = 0; c < PW; ++c)
+        if (c < nb && mine && i >= j0 + c) L[static_cast<size_t>(j0 + c) * n + i] = acc[c];
       __syncthreads();
     }
+    __syncthreads();
     if (!s_fail) break;
     if (nv >= max_jitter) {
       status = 1;
@@ -186,21 +234,52 @@ __global__ void __launch_bounds__(PT) posterior_kernel(const double* __restrict_
     Rv[e] = gram(A + i * d, AA[i], Bp[p], BB[p], d);
   }
   __syncthreads();
-  if (w == 0 && p0 + lane < P) {  // mean = k(x, xp)^T alpha (sequential in i)
+  if (w == 0 && lane < PC && p0 + lane < P) {  // mean = k(x, xp)^T alpha (sequential in i)
     double m = 0.0;
     for (int i = 0; i < n; ++i) m = fma(Rv[i * PC + lane], alpha[i], m);
     mean[p0 + lane] = m;
   }
-  // forward substitution for the 32 columns: after v_j, rows i > j lose L[i][j] v_j
-  for (int j = 0; j < n; ++j) {
-    const double vj = Rv[j * PC + lane] / L[static_cast<size_t>(j) * n + j];
+  // blocked forward substitution for the PC columns, panels of PW rows:
+  //   (a) the PW x PW diagonal block of L is staged in shared memory and warp 0
+  //       (lane = column) solves the panel rows;
+  //   (b) every later row loses sum_c L[i][j0 + c] v[j0 + c] (thread = row x 4 columns).
+  __shared__ double Ld[PW][PW];
+  constexpr int QPR = PC / 4;  // column quads per row
+  const int rq = tid / QPR, cq = (tid % QPR) * 4;
+  for (int j0 = 0; j0 < n; j0 += PW) {
+    const int nb = n - j0 < PW ? n - j0 : PW;
+    if (tid < PW * PW) {
+      const int r = tid / PW, c = tid % PW;
+      Ld[r][c] = r < nb && c <= r ? L[static_cast<size_t>(j0 + c) * n + j0 + r] : 0.0;
+    }
     __syncthreads();
-    for (int i = j + 1 + w; i < n; i += PT / 32)
-      Rv[i * PC + lane] = fma(-L[static_cast<size_t>(j) * n + i], vj, Rv[i * PC + lane]);
-    if (w == 0) Rv[j * PC + lane] = vj;
+    if (w == 0 && lane < PC) {
+      for (int c = 0; c < nb; ++c) {
+        const double vj = Rv[(j0 + c) * PC + lane] / Ld[c][c];
+        Rv[(j0 + c) * PC + lane] = vj;
+        for (int r = c + 1; r < nb; ++r) Rv[(j0 + r) * PC + lane] = fma(-Ld[r][c], vj, Rv[(j0 + r) * PC + lane]);
+      }
+    }
+    __syncthreads();
+    for (int i = j0 + nb + rq; i < n; i += PT / QPR) {
+      double r0 = Rv[i * PC + cq], r1 = Rv[i * PC + cq + 1], r2 = Rv[i * PC + cq + 2], r3 = Rv[i * PC + cq + 3];
+#pragma unroll 4
+      for (int c = 0; c < nb; ++c) {
+        const double l = L[static_cast<size_t>(j0 + c) * n + i];
+        const double* vr = Rv + (j0 + c) * PC + cq;
+        r0 = fma(-l, vr[0], r0);
+        r1 = fma(-l, vr[1], r1);
+        r2 = fma(-l, vr[2], r2);
+        r3 = fma(-l, vr[3], r3);
+      }
+      Rv[i * PC + cq] = r0;
+      Rv[i * PC + cq + 1] = r1;
+      Rv[i * PC + cq + 2] = r2;
+      Rv[i * PC + cq + 3] = r3;
+    }
     __syncthreads();
   }
-  if (w == 0 && p0 + lane < P) {
+  if (w == 0 && lane < PC && p0 + lane < P) {
     double s = 0.0;
     for (int i = 0; i < n; ++i) s += Rv[i * PC + lane] * Rv[i * PC + lane];  // (v * v).sum(axis=0)
     var[p0 + lane] = fmax(1.0 - s, 0.0);
@@ -390,8 +469,15 @@ int kt_gp_factor(const double* x, int32_t n, int32_t d, const double* ls, int32_
   KT_REQUIRE(noise > 0.0, KT_E_ARG, "kt_gp_factor: noise must be positive (jitter escalates tenfold)");
   const size_t smem = (static_cast<size_t>(n) * d + 2 * n) * 8;
   KT_REQUIRE(smem <= 200 * 1024, KT_E_UNSUPPORTED, "kt_gp_factor: coordinates do not fit shared memory");
-  cudaFuncSetAttribute(gp::factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  gp::factor_kernel<<<n_cand, gp::FT, smem, as_stream(stream)>>>(x, n, d, ls, y, noise, max_jitter, L, alpha, info);
+  // thread = row: 512 threads (128 registers each) up to the default observation window
+  if (n <= 512) {
+    cudaFuncSetAttribute(gp::factor_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    gp::factor_kernel<512><<<n_cand, 512, smem, as_stream(stream)>>>(x, n, d, ls, y, noise, max_jitter, L, alpha, info);
+  } else {
+    cudaFuncSetAttribute(gp::factor_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    gp::factor_kernel<1024><<<n_cand, 1024, smem, as_stream(stream)>>>(x, n, d, ls, y, noise, max_jitter, L, alpha,
+                                                                      info);
+  }
   note_launches(1);
   return check_launch("kt_gp_factor");
 }
