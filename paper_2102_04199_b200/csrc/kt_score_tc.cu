@@ -86,10 +86,6 @@ struct __align__(1024) Smem {
   float nconst[KT_MAX_LOOPS][8];
   int tab_off[KT_MAX_AXES];
   int64_t vtile[2][GT];           // per tile parity: the graphs' config indices (INT64_MIN: padding)
-  short sel[2][KT_MAX_AXES][GT];  // per tile buffer, graph: packed table entry of each axis' tile choice
-  unsigned char unr[2][GT];       // per graph: bit a = inner loop of axis a unrolled
-  unsigned char okf[2][GT];       // per graph: valid config index
-  uint64_t dec_full[2], dec_free[2];
   // digit extraction for slot d (axes 0..5, 6 = auto_unroll knob, 7 = explicit knob):
   // choice = (v / dmult[d]) % dcard[d], both divisions by magic multiply
   unsigned long long dm_magic[8], dc_magic[8];
@@ -206,10 +202,6 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       mbar_init(&S.d2_empty[b], 8);
     }
     mbar_init(&S.u_full, 8);
-    mbar_init(&S.dec_full[0], 1);
-    mbar_init(&S.dec_full[1], 1);
-    mbar_init(&S.dec_free[0], 4);
-    mbar_init(&S.dec_free[1], 4);
     mbar_init(&S.z_full, 8);
     mbar_init(&S.d3_full, 1);
     mbar_init(&S.d4_full, 1);

@@ -16,7 +16,6 @@ extern "C" int kt_score_indices_ex(const kt_spec_table* tab, const kt_dims* dims
 extern "C" int kt_topk_keys(const uint64_t* keys, int64_t B, int32_t k, int64_t* top_idx, float* top_score,
                             void* workspace, int64_t workspace_bytes, void* stream);
 
-
 extern "C" int kt_sweep_host(const kt_spec_table* tab, const kt_dims* dims, const float* params,
                              const void* idx_host, int32_t idx_bytes, int64_t B, uint64_t* keys_dev, float* z_host,
                              int32_t k, int64_t* top_idx_dev, float* top_score_dev, int64_t* top_idx_host,
