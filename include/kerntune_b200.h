@@ -128,16 +128,19 @@ int kt_encode_raw_choices(const kt_spec_table* tab, const int64_t* choices, int6
 int kt_score_indices(const kt_spec_table* tab, const kt_dims* dims, const float* params,
                      const int64_t* idx, int64_t idx_base, int64_t B,
                      float* z_out, float* u_out, int32_t* err_flag, void* stream);
-/* Same contract on the FP32 FMA pipe (FFMA2 register tiles) instead of tcgen05
- * 3xTF32 tensor cores; kept as the second, independent implementation the parity
- * tests hold the tensor-core kernel against. */
 /* kt_score_indices with more inputs / outputs: indices as int64 (idx), as uint32
  * (idx32, may point at pinned host memory: zero-copy) or idx_base + i; optional
  * keys_out (B x uint64) receives rank_history keys, (descending-order score code) << 32
- * | index, EMPTY (all ones) for invalid indices, for kt_topk_keys. */
+ * | index, EMPTY (all ones) for invalid indices, for kt_topk_keys; optional key_hist
+ * (2048 uint32 bins, e.g. kt_topk_key_hist(workspace)) accumulates the keys' first
+ * radix digit (key >> 53) so that kt_topk_keys(..., hist_ready = 1) can skip that pass. */
 int kt_score_indices_ex(const kt_spec_table* tab, const kt_dims* dims, const float* params,
                         const int64_t* idx, const uint32_t* idx32, int64_t idx_base, int64_t B,
-                        float* z_out, float* u_out, uint64_t* keys_out, int32_t* err_flag, void* stream);
+                        float* z_out, float* u_out, uint64_t* keys_out, uint32_t* key_hist,
+                        int32_t* err_flag, void* stream);
+/* Same contract as kt_score_indices on the FP32 FMA pipe (FFMA2 register tiles) instead
+ * of tcgen05 3xTF32 tensor cores; kept as the second, independent implementation the
+ * parity tests hold the tensor-core kernel against. */
 int kt_score_indices_fp32(const kt_spec_table* tab, const kt_dims* dims, const float* params,
                           const int64_t* idx, int64_t idx_base, int64_t B,
                           float* z_out, float* u_out, int32_t* err_flag, void* stream);
@@ -301,9 +304,14 @@ int kt_topk(const float* scores, const int64_t* idx, int64_t idx_base, int64_t B
             const int64_t* visited, int64_t n_visited, int32_t k,
             int64_t* top_idx, float* top_score, void* workspace, int64_t workspace_bytes,
             void* stream);
-/* Top-k of precomputed keys (kt_score_indices_ex keys_out): ascending key order. */
-int kt_topk_keys(const uint64_t* keys, int64_t B, int32_t k, int64_t* top_idx, float* top_score,
-                 void* workspace, int64_t workspace_bytes, void* stream);
+/* Top-k of precomputed keys (kt_score_indices_ex keys_out): ascending key order.
+ * hist_ready != 0: the workspace's first-digit histogram (kt_topk_key_hist) already
+ * holds these keys' counts (filled by the scorer).  Every kt_topk* call leaves that
+ * histogram zeroed; a fresh workspace must be zeroed once before a scorer fills it.
+ * One cooperative launch (radix select, gather, sort); k <= 1024. */
+int kt_topk_keys(const uint64_t* keys, int64_t B, int32_t k, int32_t hist_ready, int64_t* top_idx,
+                 float* top_score, void* workspace, int64_t workspace_bytes, void* stream);
+uint32_t* kt_topk_key_hist(void* workspace);
 /* Merge world x k (score, index) candidate lists (the all-gathered per-rank top-k). */
 int kt_topk_merge(const float* scores, const int64_t* idx, int64_t n, int32_t k,
                   int64_t* top_idx, float* top_score, void* workspace, int64_t workspace_bytes,

@@ -106,8 +106,9 @@ _SIGS = {
                                      vp, i64, vp]),
     "kt_sweep_host": (ctypes.c_int, [vp, ctypes.POINTER(Dims), vp, vp, i32, i64, vp, vp, i32, vp, vp, vp, vp, vp,
                                      i64, vp, vp]),
-    "kt_score_indices_ex": (ctypes.c_int, [vp, ctypes.POINTER(Dims), vp, vp, vp, i64, i64, vp, vp, vp, vp, vp]),
-    "kt_topk_keys": (ctypes.c_int, [vp, i64, i32, vp, vp, vp, i64, vp]),
+    "kt_score_indices_ex": (ctypes.c_int, [vp, ctypes.POINTER(Dims), vp, vp, vp, i64, i64, vp, vp, vp, vp, vp, vp]),
+    "kt_topk_keys": (ctypes.c_int, [vp, i64, i32, i32, vp, vp, vp, i64, vp]),
+    "kt_topk_key_hist": (vp, [vp]),
     "kt_gp_gram": (ctypes.c_int, [vp, i32, vp, i32, i32, vp, vp, vp]),
     "kt_gp_factor": (ctypes.c_int, [vp, i32, i32, vp, i32, vp, ctypes.c_double, ctypes.c_double, vp, vp, vp, vp]),
     "kt_gp_workspace_bytes": (i64, [i32, i32, i32]),

@@ -86,6 +86,7 @@ struct __align__(1024) Smem {
   float nconst[KT_MAX_LOOPS][8];
   int tab_off[KT_MAX_AXES];
   int64_t vtile[2][GT];           // per tile parity: the graphs' config indices (INT64_MIN: padding)
+  unsigned int khist[2048];       // first radix digit (key >> 53) of this CTA's top-k keys
   // digit extraction for slot d (axes 0..5, 6 = auto_unroll knob, 7 = explicit knob):
   // choice = (v / dmult[d]) % dcard[d], both divisions by magic multiply
   unsigned long long dm_magic[8], dc_magic[8];
@@ -139,7 +140,7 @@ __global__ void __launch_bounds__(NT, 1)
 score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float* __restrict__ params,
                 const int64_t* __restrict__ idx, const uint32_t* __restrict__ idx32, int64_t idx_base, int64_t B,
                 float* __restrict__ z_out, float* __restrict__ u_out, unsigned long long* __restrict__ keys_out,
-                int32_t* __restrict__ err) {
+                unsigned int* __restrict__ key_hist, int32_t* __restrict__ err) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const kt_spec_table& T = *tab;
@@ -218,6 +219,8 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     S.nconst[k][7] = 0.f;
   }
   if (warp == 8) tmem_alloc(&S.tmem_base, 512);
+  if (key_hist)
+    for (int i = tid; i < 2048; i += NT) S.khist[i] = 0;
   __syncthreads();
   for (int a = 0; a < na; ++a) {
     const int n = T.axis_knob[a] >= 0 ? static_cast<int>(T.card[T.axis_knob[a]]) : 1;
@@ -598,8 +601,10 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         if (keys_out) {  // rank_history key for kt_topk_keys: (descending score code, index)
           const uint32_t b = __float_as_uint(zv);
           const uint32_t asc = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-          keys_out[gi] = ok && zv == zv ? (static_cast<unsigned long long>(~asc) << 32) | static_cast<uint32_t>(v)
-                                        : ~0ull;
+          const unsigned long long key =
+              ok && zv == zv ? (static_cast<unsigned long long>(~asc) << 32) | static_cast<uint32_t>(v) : ~0ull;
+          keys_out[gi] = key;
+          if (key_hist) atomicAdd(&S.khist[static_cast<int>(key >> 53)], 1u);  // kt_topk_keys' first digit
         }
       }
       named_sync(1 + quad, 64);  // S.part consumed before the next tile overwrites it
@@ -613,6 +618,9 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+  if (key_hist)
+    for (int i = tid; i < 2048; i += NT)
+      if (S.khist[i]) atomicAdd(&key_hist[i], S.khist[i]);
 }
 
 }  // namespace tcs
@@ -626,7 +634,8 @@ static bool default_dims_tc(const kt_dims& d) {
 
 extern "C" int kt_score_indices_ex(const kt_spec_table* tab, const kt_dims* dims, const float* params,
                                    const int64_t* idx, const uint32_t* idx32, int64_t idx_base, int64_t B,
-                                   float* z_out, float* u_out, uint64_t* keys_out, int32_t* err_flag, void* stream) {
+                                   float* z_out, float* u_out, uint64_t* keys_out, uint32_t* key_hist,
+                                   int32_t* err_flag, void* stream) {
   using namespace kt;
   KT_REQUIRE(tab && dims && params && z_out && err_flag, KT_E_ARG, "kt_score_indices: null pointer");
   KT_REQUIRE(B > 0, KT_E_EMPTY, "kt_score_indices: empty batch");
@@ -642,7 +651,7 @@ extern "C" int kt_score_indices_ex(const kt_spec_table* tab, const kt_dims* dims
   const int grid = static_cast<int>(n_tiles < kNumSMs ? n_tiles : kNumSMs);
   tcs::score_tc_kernel<<<grid, tcs::NT, smem, as_stream(stream)>>>(
       tab, *dims, params, idx, idx32, idx_base, B, z_out, u_out, reinterpret_cast<unsigned long long*>(keys_out),
-      err_flag);
+      keys_out ? key_hist : nullptr, err_flag);
   note_launches(1);
   return check_launch("kt_score_indices");
 }
@@ -650,5 +659,6 @@ extern "C" int kt_score_indices_ex(const kt_spec_table* tab, const kt_dims* dims
 extern "C" int kt_score_indices(const kt_spec_table* tab, const kt_dims* dims, const float* params,
                                 const int64_t* idx, int64_t idx_base, int64_t B, float* z_out,
                                 float* u_out, int32_t* err_flag, void* stream) {
-  return kt_score_indices_ex(tab, dims, params, idx, nullptr, idx_base, B, z_out, u_out, nullptr, err_flag, stream);
+  return kt_score_indices_ex(tab, dims, params, idx, nullptr, idx_base, B, z_out, u_out, nullptr, nullptr, err_flag,
+                             stream);
 }

@@ -12,9 +12,11 @@
 
 extern "C" int kt_score_indices_ex(const kt_spec_table* tab, const kt_dims* dims, const float* params,
                                    const int64_t* idx, const uint32_t* idx32, int64_t idx_base, int64_t B,
-                                   float* z_out, float* u_out, uint64_t* keys_out, int32_t* err_flag, void* stream);
-extern "C" int kt_topk_keys(const uint64_t* keys, int64_t B, int32_t k, int64_t* top_idx, float* top_score,
-                            void* workspace, int64_t workspace_bytes, void* stream);
+                                   float* z_out, float* u_out, uint64_t* keys_out, uint32_t* key_hist,
+                                   int32_t* err_flag, void* stream);
+extern "C" int kt_topk_keys(const uint64_t* keys, int64_t B, int32_t k, int32_t hist_ready, int64_t* top_idx,
+                            float* top_score, void* workspace, int64_t workspace_bytes, void* stream);
+extern "C" uint32_t* kt_topk_key_hist(void* workspace);
 
 extern "C" int kt_sweep_host(const kt_spec_table* tab, const kt_dims* dims, const float* params,
                              const void* idx_host, int32_t idx_bytes, int64_t B, uint64_t* keys_dev, float* z_host,
@@ -33,9 +35,9 @@ extern "C" int kt_sweep_host(const kt_spec_table* tab, const kt_dims* dims, cons
   // plus the (score, index) keys in HBM; the radix top-k ranks the keys
   int rc = kt_score_indices_ex(tab, dims, params, idx_bytes == 8 ? static_cast<const int64_t*>(idx_host) : nullptr,
                                idx_bytes == 4 ? static_cast<const uint32_t*>(idx_host) : nullptr, 0, B, z_host,
-                               nullptr, keys_dev, err_dev, st);
+                               nullptr, keys_dev, kt_topk_key_hist(topk_ws), err_dev, st);
   if (rc) return rc;
-  rc = kt_topk_keys(keys_dev, B, k, top_idx_dev, top_score_dev, topk_ws, topk_ws_bytes, st);
+  rc = kt_topk_keys(keys_dev, B, k, 1, top_idx_dev, top_score_dev, topk_ws, topk_ws_bytes, st);
   if (rc) return rc;
   cudaMemcpyAsync(top_idx_host, top_idx_dev, static_cast<size_t>(k) * 8, cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(top_score_host, top_score_dev, static_cast<size_t>(k) * 4, cudaMemcpyDeviceToHost, st);

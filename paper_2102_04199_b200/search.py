@@ -178,7 +178,7 @@ class Sweeper:
         self.keys = torch.empty(max_batch, dtype=torch.int64, device=dev)
         self.err = torch.zeros(1, dtype=torch.int32, device=dev)
         self.ws_bytes = int(self.lib.kt_topk_workspace_bytes(max_batch, k))
-        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        self.ws = torch.zeros(self.ws_bytes, dtype=torch.uint8, device=dev)  # (its histogram starts at zero)
         self.top_idx = torch.empty(k, dtype=torch.int64, device=dev)
         self.top_score = torch.empty(k, dtype=torch.float32, device=dev)
         self.h_z = torch.empty(max_batch, dtype=torch.float32, pin_memory=True)
@@ -187,18 +187,19 @@ class Sweeper:
         self.ev_done = torch.cuda.Event()
         self._p = dict(tab=self.tab.data_ptr(), flat=self.flat.data_ptr(), err=self.err.data_ptr(),
                        ws=self.ws.data_ptr(), ti=self.top_idx.data_ptr(), ts=self.top_score.data_ptr(),
-                       z=self.z.data_ptr(), keys=self.keys.data_ptr())
+                       z=self.z.data_ptr(), keys=self.keys.data_ptr(),
+                       hist=self.lib.kt_topk_key_hist(self.ws.data_ptr()))
 
     def score(self, idx64_ptr, idx32_ptr, base: int, n: int, stream) -> None:
         """The scorer launch alone: z[:n] and keys[:n] (raw pointers; bench timing hook)."""
         p = self._p
         _lib.check(self.lib.kt_score_indices_ex(p["tab"], self.dims, p["flat"], idx64_ptr, idx32_ptr, base, n,
-                                                p["z"], None, p["keys"], p["err"], stream), "sweep score")
+                                                p["z"], None, p["keys"], p["hist"], p["err"], stream), "sweep score")
 
     def rank(self, n: int, stream) -> None:
-        """Top-k of keys[:n] into top_idx / top_score."""
+        """Top-k of keys[:n] into top_idx / top_score (the scorer filled the first digit's bins)."""
         p = self._p
-        _lib.check(self.lib.kt_topk_keys(p["keys"], n, self.k, p["ti"], p["ts"], p["ws"], self.ws_bytes, stream),
+        _lib.check(self.lib.kt_topk_keys(p["keys"], n, self.k, 1, p["ti"], p["ts"], p["ws"], self.ws_bytes, stream),
                    "sweep topk")
 
     def run_device(self, idx: torch.Tensor | None = None, *, base: int = 0, count: int | None = None,

@@ -330,3 +330,31 @@ def test_sweeper_out_of_range_index_excluded(cuda_device, g_model):
         sw.run_host(idx.pin_memory())
     with pytest.raises(pg.DomainError):
         sw.run_host(torch.arange(10))  # not pinned
+
+
+@pytest.mark.parametrize("dist", ["equal", "few", "nan", "normal"])
+@pytest.mark.parametrize("n,k", [(1_000_003, 1024), (70_000, 1), (300, 512), (513, 512)])
+def test_topk_adversarial_distributions(cuda_device, dist, n, k):
+    """The one-kernel radix select on score distributions that stress its digit passes:
+    all-equal scores (ties resolved on the index word), a handful of values, NaNs, and
+    B <= k / B = k + 1; the workspace is reused across calls."""
+    rng = np.random.default_rng(hash((dist, n, k)) % 2**32)
+    if dist == "equal":
+        z = np.full(n, 0.75, dtype=np.float32)
+    elif dist == "few":
+        z = rng.choice(np.array([-1.0, 0.0, 0.5, 3.0], dtype=np.float32), n)
+    elif dist == "nan":
+        z = rng.normal(size=n).astype(np.float32)
+        z[rng.integers(0, n, n // 10)] = np.nan
+    else:
+        z = rng.normal(size=n).astype(np.float32)
+    idx = rng.permutation(np.arange(10 * n, dtype=np.int64))[:n]
+    zt, it = torch.from_numpy(z).cuda(), torch.from_numpy(idx).cuda()
+    for _ in range(2):
+        ti, ts = ps.topk(zt, k, it)
+    key = np.where(np.isnan(z), np.inf, -z.astype(np.float64))  # NaN ranks last
+    order = np.lexsort((idx, key))[: min(k, n)]
+    got = ti.cpu().numpy()
+    assert got[: min(k, n)].tolist() == idx[order].tolist()
+    if k > n:
+        assert (got[n:] == -1).all()
