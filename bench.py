@@ -575,10 +575,14 @@ def run_ours(args):
     from paper_2102_04199_b200.util import rng_from
 
     rank, local, ws = dist_env()
+    # (debug hooks for exercising the N>1 path on a one-GPU box: every rank on cuda:0 over gloo)
+    if os.environ.get("KT_BENCH_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("KT_BENCH_BACKEND", "nccl")
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
     lib = _lib.load()
 
     m = bench_model(dev)
