@@ -8,8 +8,7 @@ ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 from paper_2102_04199_b200 import build as B  # noqa: E402
 
-VARIANTS = {"base": [], "no_xst": ["-DKT_DBG_NO_XST"], "no_epi": ["-DKT_DBG_NO_EPI"],
-            "no_both": ["-DKT_DBG_NO_XST", "-DKT_DBG_NO_EPI"]}
+VARIANTS = {"base": []}
 VARIANTS.update({k: v for k, v in (a.split("=", 1) for a in sys.argv[1:] if "=" in a) for v in [v.split(",")]})
 
 
@@ -58,4 +57,8 @@ for name in VARIANTS:
         ps.score_indices(m, spec, space, lay, idx)
     e1.record()
     torch.cuda.synchronize()
-    print(f"{name:12s} {e0.elapsed_time(e1) / 20:.4f} ms per 1M", flush=True)
+    z = ps.score_indices(m, spec, space, lay, idx)
+    if name == "base":
+        z_base = z.clone()
+    dz = (z - z_base).abs().max().item() * m.label_norm.std * 0.6931471805599453  # GFLOPS relative error
+    print(f"{name:12s} {e0.elapsed_time(e1) / 20:.4f} ms per 1M   max GFLOPS rel diff vs base {dz:.2e}", flush=True)
