@@ -8,6 +8,8 @@
 // sums the rows in a fixed order in fp64 (deterministic, no atomics), chunking
 // batches larger than the workspace.  kt_pretrain_sgd keeps the parameters in
 // shared memory and runs the whole sequential SGD loop in one CTA.
+#include <cstdlib>
+
 #include "kt_graph.cuh"
 
 namespace kt {
@@ -172,6 +174,33 @@ pergraph_kernel(kt_dims dims, const float* __restrict__ params, const double* __
   }
 }
 
+// Small batches: one CTA (CT threads) per graph.  The same per-graph arithmetic as the
+// warp form (each output element is still owned by one thread with a sequential inner
+// loop), spread over 8x the threads, so a 512-graph batch fills the GPU.
+constexpr int CT = 256;
+
+__global__ void __launch_bounds__(CT)
+pergraph_cta_kernel(kt_dims dims, const float* __restrict__ params, const double* __restrict__ fmean,
+                    const double* __restrict__ fstd, const double* __restrict__ feats,
+                    const uint8_t* __restrict__ mask, const int64_t* __restrict__ node_ptr, int npg, int nmax,
+                    const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                    const float* __restrict__ val, const int64_t* __restrict__ gidx, const float* __restrict__ y,
+                    int64_t b0, int64_t nb, float inv_b, int head_only, int D, float* __restrict__ pg_grad,
+                    float* __restrict__ pg_sq) {
+  extern __shared__ __align__(16) float sm[];
+  const Slab S = carve(sm, dims, nmax, D);
+  const CtaGroup G{static_cast<int>(threadIdx.x), CT};
+  for (int64_t i = blockIdx.x; i < nb; i += gridDim.x) {
+    const int64_t b = b0 + i;
+    const int64_t g = gidx ? gidx[b] : b;
+    const GraphView v = graph_view(g, node_ptr, npg, row_ptr, col, val, mask);
+    const float sq = graph_grad(G, dims, params, v, feats, fmean, fstd, y[b], inv_b, head_only != 0, S,
+                                pg_grad + i * dims.n_params, D);
+    if (threadIdx.x == 0) pg_sq[i] = sq;
+    __syncthreads();
+  }
+}
+
 // acc[p] (+)= sum_i pg[i][p] in fixed order, fp64
 __global__ void reduce_kernel(const float* __restrict__ pg, int64_t nb, int P, double* __restrict__ acc, int first,
                               const float* __restrict__ pg_sq, double* __restrict__ sq_acc) {
@@ -285,11 +314,24 @@ int kt_grad(const kt_dims* dims, const float* params, const double* fmean, const
   int launches = 0;
   for (int64_t b0 = 0; b0 < B; b0 += chunk) {
     const int64_t nb = B - b0 < chunk ? B - b0 : chunk;
-    int64_t blocks = (nb + train::WARPS - 1) / train::WARPS;
-    if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
-    train::pergraph_kernel<<<(int)blocks, train::WARPS * 32, smem, st>>>(
-        *dims, params, fmean, fstd, feats, mask, node_ptr, nodes_per_graph, max_nodes, row_ptr, col, val, graph_idx,
-        y, b0, nb, inv_b, head_only, D, pg, pg_sq);
+    if (nb <= kNumSMs * 8 && !(getenv("KT_GRAD_WARP") && getenv("KT_GRAD_WARP")[0] == '1')) {
+      // small batch: a CTA per graph (the warp form would leave most of the GPU idle)
+      const size_t csm = sizeof(float) * train::slab_floats(*dims, max_nodes, D);
+      static size_t csm_attr = 0;
+      if (csm > 48 * 1024 && csm > csm_attr) {
+        cudaFuncSetAttribute(train::pergraph_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+        csm_attr = csm;
+      }
+      train::pergraph_cta_kernel<<<(int)nb, train::CT, csm, st>>>(
+          *dims, params, fmean, fstd, feats, mask, node_ptr, nodes_per_graph, max_nodes, row_ptr, col, val,
+          graph_idx, y, b0, nb, inv_b, head_only, D, pg, pg_sq);
+    } else {
+      int64_t blocks = (nb + train::WARPS - 1) / train::WARPS;
+      if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
+      train::pergraph_kernel<<<(int)blocks, train::WARPS * 32, smem, st>>>(
+          *dims, params, fmean, fstd, feats, mask, node_ptr, nodes_per_graph, max_nodes, row_ptr, col, val,
+          graph_idx, y, b0, nb, inv_b, head_only, D, pg, pg_sq);
+    }
     train::reduce_kernel<<<(P + 255) / 256, 256, 0, st>>>(pg, nb, P, acc, b0 == 0, pg_sq, sq_acc);
     launches += 2;
   }
