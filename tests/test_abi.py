@@ -63,3 +63,12 @@ def test_error_codes_map_to_reference_taxonomy():
     for code in (_lib.KT_E_CUDA, _lib.KT_E_NUMERIC):
         with pytest.raises(NumericError):
             _lib.check(code, "x")
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: a missing extension raises instead of degrading."""
+    from paper_2102_04199_b200 import _lib
+    from paper_2102_04199_b200.errors import NumericError
+
+    with pytest.raises(NumericError):
+        _lib.load(tmp_path / "libkerntune_b200.so")
