@@ -71,16 +71,24 @@ __device__ float graph_grad(const Grp& G, const kt_dims& dims, const float* P, c
   }
   readout(G, S.H[L], n, dl, D, P + dims.off_agg, S.act[0], S.arg);
   G.sync();
+  // head layers: four threads per output (k split four ways, quad shuffles), so the
+  // 64-wide layers keep every thread of the group busy
+  const unsigned qm = 0xFu << (G.r & 28);
   for (int i = 0; i < nh; ++i) {
     const int din = dims.head[i], dout = dims.head[i + 1];
     const float* W = P + dims.off_hw[i];
     const float* b = P + dims.off_hb[i];
-    for (int c = G.r; c < dout; c += G.n) {
+    for (int e = G.r; e < 4 * dout; e += G.n) {
+      const int c = e >> 2;
       float acc = 0.0f;
-      for (int k = 0; k < din; ++k) acc = fmaf(S.act[i][k], W[k * dout + c], acc);
-      acc += b[c];
-      S.zh[i][c] = acc;
-      S.act[i + 1][c] = i == nh - 1 ? acc : fmaxf(acc, 0.0f);
+      for (int k = e & 3; k < din; k += 4) acc = fmaf(S.act[i][k], W[k * dout + c], acc);
+      acc += __shfl_xor_sync(qm, acc, 1);
+      acc += __shfl_xor_sync(qm, acc, 2);
+      if ((e & 3) == 0) {
+        acc += b[c];
+        S.zh[i][c] = acc;
+        S.act[i + 1][c] = i == nh - 1 ? acc : fmaxf(acc, 0.0f);
+      }
     }
     G.sync();
   }
@@ -101,10 +109,13 @@ __device__ float graph_grad(const Grp& G, const kt_dims& dims, const float* P, c
       gw[e] = S.act[i][k] * S.dz[c];
     }
     for (int c = G.r; c < dout; c += G.n) gout[dims.off_hb[i] + c] = S.dz[c];
-    for (int k = G.r; k < din; k += G.n) {
+    for (int e = G.r; e < 4 * din; e += G.n) {
+      const int k = e >> 2;
       float acc = 0.0f;
-      for (int c = 0; c < dout; ++c) acc = fmaf(S.dz[c], W[k * dout + c], acc);
-      S.da[k] = acc;
+      for (int c = e & 3; c < dout; c += 4) acc = fmaf(S.dz[c], W[k * dout + c], acc);
+      acc += __shfl_xor_sync(qm, acc, 1);
+      acc += __shfl_xor_sync(qm, acc, 2);
+      if ((e & 3) == 0) S.da[k] = acc;
     }
     G.sync();
   }
