@@ -20,7 +20,10 @@ int check_dims(const kt_dims& d);
 
 namespace meta {
 
-constexpr int NT = 256;
+#ifndef KT_META_NT
+#define KT_META_NT 256
+#endif
+constexpr int NT = KT_META_NT;  // threads per CTA (one head vector per CTA)
 constexpr int HMAX = 2 * KT_MAX_DIM;  // widest head vector (input 2 d_L)
 
 struct Head {
