@@ -899,9 +899,12 @@ __global__ void __launch_bounds__(TC_ROWS, 3)
     {
       float hi[K], lo[K];
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
+      for (int k = 0; k < K; k += 2) {  // remainders as packed fp32x2 subtractions
         hi[k] = tc::tf32_trunc(y[k]);
-        lo[k] = y[k] - hi[k];
+        hi[k + 1] = tc::tf32_trunc(y[k + 1]);
+        const float2 l = fsub2(make_float2(y[k], y[k + 1]), make_float2(hi[k], hi[k + 1]));
+        lo[k] = l.x;
+        lo[k + 1] = l.y;
       }
 #pragma unroll
       for (int k0 = 0; k0 + 16 <= K; k0 += 16) {

@@ -329,9 +329,12 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         lt += static_cast<dbl>(level ? l2.y : l2.x);
         float hl[32];
 #pragma unroll
-        for (int f = 0; f < 16; ++f) {
+        for (int f = 0; f < 16; f += 2) {
           hl[f] = tf32_trunc(x[f]);
-          hl[16 + f] = x[f] - hl[f];
+          hl[f + 1] = tf32_trunc(x[f + 1]);
+          const float2 l = fsub2(make_float2(x[f], x[f + 1]), make_float2(hl[f], hl[f + 1]));
+          hl[16 + f] = l.x;
+          hl[17 + f] = l.y;
         }
         const int s = static_cast<int>(q % XS);
         if (g == 0) TRACE(20, q);
@@ -468,10 +471,14 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       for (int h = 0; h < 2; ++h) {
         float hi[16], lo[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float r = relu(v[16 * h + j]);
-          hi[j] = tf32_trunc(r);
-          lo[j] = r - hi[j];
+        for (int j = 0; j < 16; j += 2) {  // remainders as packed fp32x2 subtractions
+          const float2 r = make_float2(relu(v[16 * h + j]), relu(v[16 * h + j + 1]));
+          const float2 t = make_float2(tf32_trunc(r.x), tf32_trunc(r.y));
+          const float2 l = fsub2(r, t);
+          hi[j] = t.x;
+          hi[j + 1] = t.y;
+          lo[j] = l.x;
+          lo[j + 1] = l.y;
         }
         tmem_st16(tmem + lane + T_R + 64 * b + 16 * h, hi);
         tmem_st16(tmem + lane + T_R + 64 * b + 32 + 16 * h, lo);
