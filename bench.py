@@ -663,9 +663,21 @@ def run_ours(args):
     h0 = torch.cuda.Event(enable_timing=True)
     h1 = torch.cuda.Event(enable_timing=True)
     h0.record()
-    for i in range(args.steps):
-        z_h, ti_h, ts_h = sw.run_host(host_slices[i % 4], check=False)
-        if ws > 1:
+    if ws == 1:
+        # one step in flight while the previous step's host results are consumed (submit / wait);
+        # every step still reads its indices from and writes its results to host memory
+        prev = None
+        best = 0
+        for i in range(args.steps):
+            t = sw.submit(host_slices[i % 4])
+            if prev is not None:
+                z_h, ti_h, ts_h = sw.wait(prev, check=False)
+                best += int(ti_h[0])
+            prev = t
+        z_h, ti_h, ts_h = sw.wait(prev, check=False)
+    else:
+        for i in range(args.steps):
+            z_h, ti_h, ts_h = sw.run_host(host_slices[i % 4], check=False)
             dist.all_gather_into_tensor(gather_s, sw.top_score)
             dist.all_gather_into_tensor(gather_i, sw.top_idx)
             mi, _ = ps.topk_merge(gather_s, gather_i, TOPK)

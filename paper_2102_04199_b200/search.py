@@ -181,10 +181,14 @@ class Sweeper:
         self.ws = torch.zeros(self.ws_bytes, dtype=torch.uint8, device=dev)  # (its histogram starts at zero)
         self.top_idx = torch.empty(k, dtype=torch.int64, device=dev)
         self.top_score = torch.empty(k, dtype=torch.float32, device=dev)
-        self.h_z = torch.empty(max_batch, dtype=torch.float32, pin_memory=True)
-        self.h_top_idx = torch.empty(k, dtype=torch.int64, pin_memory=True)
-        self.h_top_score = torch.empty(k, dtype=torch.float32, pin_memory=True)
-        self.ev_done = torch.cuda.Event()
+        # two host result slots, so one end-to-end step can be in flight while the caller
+        # consumes the previous one (submit / wait)
+        self.h_z = torch.empty((2, max_batch), dtype=torch.float32, pin_memory=True)
+        self.h_top_idx = torch.empty((2, k), dtype=torch.int64, pin_memory=True)
+        self.h_top_score = torch.empty((2, k), dtype=torch.float32, pin_memory=True)
+        self.ev_slot = [torch.cuda.Event(), torch.cuda.Event()]
+        self._next_slot = 0
+        self._pending = [None, None]
         self._p = dict(tab=self.tab.data_ptr(), flat=self.flat.data_ptr(), err=self.err.data_ptr(),
                        ws=self.ws.data_ptr(), ti=self.top_idx.data_ptr(), ts=self.top_score.data_ptr(),
                        z=self.z.data_ptr(), keys=self.keys.data_ptr(),
@@ -227,8 +231,10 @@ class Sweeper:
                                         p["ts"], p["ws"], self.ws_bytes, st), "sweep topk")
         return self.top_idx, self.top_score
 
-    def run_host(self, idx_host: torch.Tensor, check: bool = True):
-        """End to end: pinned host indices -> (host scores, host top-k idx, scores).
+    def submit(self, idx_host: torch.Tensor) -> int:
+        """Enqueue one end-to-end step (pinned host indices -> host scores + top-k) and
+        return at once with a ticket; `wait(ticket)` returns its results.  Two steps may
+        be in flight (the host result buffers alternate).
 
         int64 or int32 indices (the spaces this path takes are below 2^32).  One native
         call (kt_sweep_host): the scorer reads the pinned indices and writes the pinned
@@ -240,17 +246,35 @@ class Sweeper:
             raise DomainError("sweep indices must be int64 or int32")
         if not idx_host.is_pinned():
             raise DomainError("run_host needs pinned host indices (torch pin_memory)")
+        slot = self._next_slot
+        if self._pending[slot] is not None:  # that slot's previous step must be consumed first
+            self.wait(slot)
         comp = torch.cuda.current_stream(self.dev)
         p = self._p
         _lib.check(self.lib.kt_sweep_host(p["tab"], self.dims, p["flat"], idx_host.data_ptr(),
-                                          idx_host.element_size(), n, p["keys"], self.h_z.data_ptr(), self.k,
-                                          p["ti"], p["ts"], self.h_top_idx.data_ptr(), self.h_top_score.data_ptr(),
-                                          p["ws"], self.ws_bytes, p["err"], comp.cuda_stream), "sweep (host)")
-        self.ev_done.record(comp)
-        self.ev_done.synchronize()
+                                          idx_host.element_size(), n, p["keys"], self.h_z[slot].data_ptr(),
+                                          self.k, p["ti"], p["ts"], self.h_top_idx[slot].data_ptr(),
+                                          self.h_top_score[slot].data_ptr(), p["ws"], self.ws_bytes, p["err"],
+                                          comp.cuda_stream), "sweep (host)")
+        self.ev_slot[slot].record(comp)
+        self._pending[slot] = n
+        self._next_slot ^= 1
+        return slot
+
+    def wait(self, ticket: int, check: bool = True):
+        """Results of a submitted step: (host scores, host top-k idx, top-k scores)."""
+        n = self._pending[ticket]
+        if n is None:
+            raise DomainError("no step in flight for this ticket")
+        self.ev_slot[ticket].synchronize()
+        self._pending[ticket] = None
         if check and int(self.err.item()):
             raise DomainError("config index out of range for the knob space")
-        return self.h_z[:n], self.h_top_idx, self.h_top_score
+        return self.h_z[ticket, :n], self.h_top_idx[ticket], self.h_top_score[ticket]
+
+    def run_host(self, idx_host: torch.Tensor, check: bool = True):
+        """End to end, synchronously: submit + wait."""
+        return self.wait(self.submit(idx_host), check)
 
 
 # --- simulated-annealing exploration (search.py:177-281), the tuner's caller of the model ------

@@ -286,6 +286,15 @@ def test_sweeper_end_to_end_int64_and_int32_hosts(cuda_device, g_model):
         z_h, ti_h, ts_h = sw.run_host(host)
         assert torch.equal(z_h, z_dev.cpu())
         assert torch.equal(ti_h, ti.cpu()) and torch.equal(ts_h, ts.cpu())
+    # two steps in flight (alternating host result slots): each ticket keeps its own results
+    other = torch.from_numpy(np.random.default_rng(12).integers(0, space.size, 50_000))
+    t1 = sw.submit(idx.pin_memory())
+    t2 = sw.submit(other.to(torch.int32).pin_memory())
+    z2, ti2, _ = (x.clone() for x in sw.wait(t2))
+    z1, ti1, _ = sw.wait(t1)
+    assert torch.equal(z1, z_dev.cpu()) and torch.equal(ti1, ti.cpu())
+    ti_o, _ = sw.run_device(other.cuda())
+    assert torch.equal(z2, sw.z[:50_000].cpu()) and torch.equal(ti2, ti_o.cpu())
 
 
 def test_sweeper_fused_keys_match_score_topk(cuda_device, g_model):
