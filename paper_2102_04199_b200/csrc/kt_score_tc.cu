@@ -500,7 +500,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     const float c_r = static_cast<float>(1.0 / sqrt(18.0 * (T.n_pairs + 1)));
     const float b3 = params[dims.off_hb[2]];
     const bool tr = g == 0 && eh == 0;
-    float2 tot[8], rs[8];
+    float2 tot[8], rs[8];  // per channel: sum of s, sum of |s| (sum relu(s) = (sum s + sum |s|) / 2)
     float mx[16];
     int kc = 0;       // chunk index within the current tile (no 64-bit % / on this path)
     int64_t ti = 0;   // local tile index
@@ -526,7 +526,8 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         for (int i = 0; i < 8; ++i) {
           const float2 s2 = make_float2(v[2 * i], v[2 * i + 1]);
           tot[i] = fadd2(tot[i], s2);
-          rs[i] = fadd2(rs[i], make_float2(relu(s2.x), relu(s2.y)));
+          rs[i].x += fabsf(s2.x);  // sum |s| (FADD with the |.| operand modifier); sum relu = (sum s + sum |s|) / 2
+          rs[i].y += fabsf(s2.y);
           mx[2 * i] = fmaxf(mx[2 * i], s2.x);
           mx[2 * i + 1] = fmaxf(mx[2 * i + 1], s2.y);
         }
@@ -545,7 +546,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         for (int i = 0; i < 4; ++i) {
           const int jl = 4 * jq + i, j = 16 * eh + jl;
           const float tj = (jl & 1) ? tot[jl >> 1].y : tot[jl >> 1].x;
-          const float rj = (jl & 1) ? rs[jl >> 1].y : rs[jl >> 1].x;
+          const float rj = 0.5f * (((jl & 1) ? rs[jl >> 1].y : rs[jl >> 1].x) + tj);
           const float root = relu(c_r * tj);
           us[i] = S.agg[j] * (root + c_ft * rj);
           um[i] = fmaxf(root, c_t * mx[jl]);
