@@ -12,6 +12,9 @@
 // and writes g; kt_task_sum adds the per-task rows in a fixed order (fp64),
 // after which the outer update theta - beta * sum is one kt_sgd (on one GPU)
 // or an NCCL all-reduce of the sum followed by kt_sgd (data parallel).
+#include <cooperative_groups.h>
+#include <cstdlib>
+
 #include "kt_graph.cuh"
 
 namespace kt {
@@ -94,12 +97,13 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // constant).  Rows are u[ridx[r]] (or u[r]) and labels y[ridx[r]] (or y[r]).
 // out (h.P floats, smem) is overwritten.  Returns the mse.
 __device__ float head_pass_scalar(const Head& h, const float* th, const float* v, const float* u,
-                                  const int64_t* ridx, const float* y, int n, float* out, const Scratch& S) {
+                                  const int64_t* ridx, const float* y, int n, float* out, const Scratch& S,
+                                  int n_norm) {
   const int nh = h.nh, HS = h.HS, RC = h.RC;
   const bool hvp = v != nullptr;
   for (int e = threadIdx.x; e < h.P; e += NT) out[e] = 0.0f;
   float sq_local = 0.0f;
-  const float two_n = 2.0f / static_cast<float>(n);
+  const float two_n = 2.0f / static_cast<float>(n_norm);
   for (int r0 = 0; r0 < n; r0 += RC) {
     const int nr = n - r0 < RC ? n - r0 : RC;
     __syncthreads();
@@ -236,7 +240,7 @@ __device__ float head_pass_scalar(const Head& h, const float* th, const float* v
     }
   }
   const float sq = block_sum(sq_local, S.red());
-  return sq / static_cast<float>(n);
+  return sq / static_cast<float>(n_norm);
 }
 
 
@@ -249,13 +253,14 @@ __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<floa
 //   dW        4 x 4 (k, c) tile per thread, float4 row loads, summed over the chunk rows in order
 //   propagate 2 rows x 4 k per thread, float4 loads along c
 __device__ float head_pass_tiled(const Head& h, const float* th, const float* v, const float* u,
-                                 const int64_t* ridx, const float* y, int n, float* out, const Scratch& S) {
+                                 const int64_t* ridx, const float* y, int n, float* out, const Scratch& S,
+                                 int n_norm) {
   const int nh = h.nh, HS = h.HS, RC = h.RC;
   const bool hvp = v != nullptr;
   const int tid = threadIdx.x;
   for (int e = tid; e < h.P; e += NT) out[e] = 0.0f;
   float sq_local = 0.0f;
-  const float two_n = 2.0f / static_cast<float>(n);
+  const float two_n = 2.0f / static_cast<float>(n_norm);
   for (int r0 = 0; r0 < n; r0 += RC) {
     const int nr = n - r0 < RC ? n - r0 : RC;
     const int nr2 = (nr + 1) & ~1;  // rows padded to pairs (pad row is zero)
@@ -479,7 +484,7 @@ __device__ float head_pass_tiled(const Head& h, const float* th, const float* v,
     }
   }
   const float sq = block_sum(sq_local, S.red());
-  return sq / static_cast<float>(n);
+  return sq / static_cast<float>(n_norm);
 }
 
 __device__ __forceinline__ bool tiled_ok(const Head& h) {
@@ -489,10 +494,13 @@ __device__ __forceinline__ bool tiled_ok(const Head& h) {
   return true;
 }
 
+// n rows; the loss is the mean over n_norm rows (n_norm = n unless the rows are one
+// share of a larger batch split over a cluster)
 __device__ float head_pass(const Head& h, const float* th, const float* v, const float* u, const int64_t* ridx,
-                           const float* y, int n, float* out, const Scratch& S) {
-  return tiled_ok(h) ? head_pass_tiled(h, th, v, u, ridx, y, n, out, S)
-                     : head_pass_scalar(h, th, v, u, ridx, y, n, out, S);
+                           const float* y, int n, float* out, const Scratch& S, int n_norm = 0) {
+  if (n_norm <= 0) n_norm = n;
+  return tiled_ok(h) ? head_pass_tiled(h, th, v, u, ridx, y, n, out, S, n_norm)
+                     : head_pass_scalar(h, th, v, u, ridx, y, n, out, S, n_norm);
 }
 
 struct TaskSet {
@@ -607,6 +615,64 @@ head_kernel(kt_dims dims, int rc, const float* __restrict__ theta, const float* 
   for (int e = threadIdx.x; e < h.P; e += NT) out[e] = th[e];
 }
 
+// fine_tune_embedded over a thread-block cluster: CTA c of C owns rows [c n / C, (c+1) n / C)
+// and parameter slice [c P / C, (c+1) P / C).  Per step every CTA computes its rows'
+// gradient share (scaled by the full batch: the mean is over n), then reduces its
+// parameter slice over the C shares read from the peers' shared memory (distributed
+// shared memory, fixed CTA order), updates that slice, and finally gathers the other
+// slices from their owners -- two cluster barriers per step, no global traffic.
+__global__ void __launch_bounds__(NT)
+fine_tune_cluster_kernel(kt_dims dims, int rc, const float* __restrict__ theta, const float* __restrict__ u,
+                         const float* __restrict__ y, int n, int steps, float alpha, float* __restrict__ out,
+                         float* __restrict__ mse_out) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) float sm[];
+  __shared__ float s_mse;
+  const Head h = head_of(dims, rc);
+  const int P4 = (h.P + 3) & ~3;
+  float* th = sm;
+  float* gb = th + P4;
+  const Scratch S = carve(gb + 2 * P4, h, false);
+  const int C = static_cast<int>(cl.num_blocks()), c = static_cast<int>(cl.block_rank());
+  const int r0 = static_cast<int>(static_cast<int64_t>(n) * c / C), r1 = static_cast<int>(static_cast<int64_t>(n) * (c + 1) / C);
+  const int p0 = static_cast<int>(static_cast<int64_t>(h.P) * c / C), p1 = static_cast<int>(static_cast<int64_t>(h.P) * (c + 1) / C);
+  const int d0 = h.dim[0];
+  for (int e = threadIdx.x; e < h.P; e += NT) th[e] = theta[e];
+  __syncthreads();
+  for (int st = 0; st < steps; ++st) {
+    float part = 0.0f;
+    if (r1 > r0) {
+      part = head_pass(h, th, nullptr, u + static_cast<int64_t>(r0) * d0, nullptr, y + r0, r1 - r0, gb, S, n);
+    } else {
+      for (int e = threadIdx.x; e < h.P; e += NT) gb[e] = 0.0f;
+    }
+    if (threadIdx.x == 0) s_mse = part;
+    cl.sync();  // every CTA's gradient share is complete
+    for (int e = p0 + static_cast<int>(threadIdx.x); e < p1; e += NT) {
+      float g = 0.0f;
+      for (int q = 0; q < C; ++q) g += cl.map_shared_rank(gb, q)[e];
+      th[e] -= alpha * g;
+    }
+    if (c == 0 && threadIdx.x == 0 && mse_out) {
+      float m = 0.0f;
+      for (int q = 0; q < C; ++q) m += *cl.map_shared_rank(&s_mse, q);
+      mse_out[st] = m;
+    }
+    cl.sync();  // every slice updated
+    for (int q = 0; q < C; ++q) {
+      if (q == c) continue;
+      const int a0 = static_cast<int>(static_cast<int64_t>(h.P) * q / C);
+      const int a1 = static_cast<int>(static_cast<int64_t>(h.P) * (q + 1) / C);
+      const float* src = cl.map_shared_rank(th, q);
+      for (int e = a0 + static_cast<int>(threadIdx.x); e < a1; e += NT) th[e] = src[e];
+    }
+    __syncthreads();
+  }
+  cl.sync();  // peers may still read this CTA's slice of theta
+  for (int e = p0 + static_cast<int>(threadIdx.x); e < p1; e += NT) out[e] = th[e];
+}
+
 static size_t task_smem(const Head& h, bool so) { return sizeof(float) * (4 * ((h.P + 3) & ~3) + scratch_floats(h, so)); }
 static size_t head_smem(const Head& h, bool hvp) { return sizeof(float) * (3 * ((h.P + 3) & ~3) + scratch_floats(h, hvp)); }
 
@@ -686,12 +752,38 @@ int kt_fine_tune(const kt_dims* dims, const float* theta, const float* u, const 
   int rc = meta::check_head(*dims);
   if (rc) return rc;
   const meta::Head h = meta::fit_rows(*dims, 32, false, false);
-  static size_t cached = 0;
   const size_t smem = meta::head_smem(h, false);
-  rc = meta::set_smem(meta::head_kernel, smem, cached);
-  if (rc) return rc;
-  meta::head_kernel<<<1, meta::NT, smem, as_stream(stream)>>>(*dims, h.RC, theta, nullptr, u, y, (int)n, steps, alpha,
-                                                               theta_out, mse_out);
+  const char* one = getenv("KT_FT_ONE_CTA");
+  int C = n >= 16 && !(one && one[0] == '1') ? (n >= 64 ? 8 : 4) : 1;
+  const char* cs = getenv("KT_FT_CLUSTER");  // experiment hook: cluster size
+  if (cs && atoi(cs) >= 1 && atoi(cs) <= 16) C = atoi(cs);
+  if (C > 1) {  // rows and parameters split over a cluster (distributed shared memory)
+    static size_t ccached = 0;
+    rc = meta::set_smem(meta::fine_tune_cluster_kernel, smem, ccached);
+    if (rc) return rc;
+    if (C > 8) cudaFuncSetAttribute(meta::fine_tune_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(meta::NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = as_stream(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, meta::fine_tune_cluster_kernel, *dims, h.RC, theta, u, y, (int)n,
+                                             (int)steps, alpha, theta_out, mse_out);
+    KT_REQUIRE(e == cudaSuccess, KT_E_CUDA, "kt_fine_tune: cluster launch failed (%s)", cudaGetErrorString(e));
+  } else {
+    static size_t cached = 0;
+    rc = meta::set_smem(meta::head_kernel, smem, cached);
+    if (rc) return rc;
+    meta::head_kernel<<<1, meta::NT, smem, as_stream(stream)>>>(*dims, h.RC, theta, nullptr, u, y, (int)n, steps,
+                                                                 alpha, theta_out, mse_out);
+  }
   note_launches(1);
   return check_launch("kt_fine_tune");
 }
