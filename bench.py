@@ -445,6 +445,45 @@ def bench_sa(m, reps=20):
             "config": "SaSchedule defaults, conv2d bench spec, super layout; wall clock incl. host RNG draws"}
 
 
+def bench_predict(m, n=4096, reps=50):
+    """C1: predict on 4,096 conv2d candidates through the reference-facing predictor
+    (search.py:534-541 meta_energy: list[KnobConfig] in, float64 scores out), the super
+    layout; plus the device-resident form (indices already in HBM)."""
+    import torch
+
+    from paper_2102_04199_b200 import graphs as pg
+    from paper_2102_04199_b200 import kernels as pk
+    from paper_2102_04199_b200 import search as ps
+    from paper_2102_04199_b200.util import rng_from
+
+    spec = pk.KernelSpec(*SPEC_ARGS)
+    space = pk.build_knob_space(spec)
+    lay = pg.batch_layout(spec, pg.build_super_template(pk.OP_TYPES))
+    pred = ps.CostModelPredictor(m, spec, space, lay)
+    cfgs = pk.sample_configs(space, n, rng_from("bench-cfgs"))
+    for _ in range(3):
+        pred(cfgs)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        pred(cfgs)
+    api_ms = 1e3 * (time.perf_counter() - t0) / reps
+    idx = torch.from_numpy(np.array([pk.config_index(space, c) for c in cfgs], dtype=np.int64)).cuda()
+    for _ in range(3):
+        ps.score_indices(m, spec, space, lay, idx, check=False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        ps.score_indices(m, spec, space, lay, idx, check=False)
+    e1.record()
+    torch.cuda.synchronize()
+    dev_ms = e0.elapsed_time(e1) / reps
+    return {"metric": "C1 predict, 4,096 conv2d candidates", "value": api_ms, "unit": "ms/call",
+            "higher_is_better": False, "device_ms": dev_ms, "graphs_per_s_api": n / (api_ms / 1e3),
+            "config": "CostModelPredictor(configs) -> float64 host scores (incl. host config->index conversion); "
+                      "device_ms: score_indices on device-resident indices; reference CPU: 135-173 ms (SURVEY 8(a))"}
+
+
 def bench_gp(n=512, pool=512, batch=16, reps=10, cpu_reps=3):
     """8(f) rank 3: the meta-BO proposer's GP work per tuning round at the TuneConfig sizes
     (gp_obs_window 512 observations, candidate_pool 512): gp_fit over the 4-lengthscale
@@ -748,6 +787,7 @@ def run_ours(args):
             line["sa_explore"] = bench_sa(m)
             line["dataset"] = bench_dataset(entries)
             line["gp"] = bench_gp()
+            line["predict"] = bench_predict(m)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
