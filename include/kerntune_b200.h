@@ -80,6 +80,15 @@ typedef struct kt_spec_table {
   float nrm_unroll1[KT_MAX_LOOPS];               /* slot 4 when unrolled */
   double fmean[KT_F], fstd[KT_F];
   uint64_t card_magic[KT_MAX_KNOBS];    /* floor(2^64 / card) + 1 (card >= 2): exact u32 division */
+  /* knob digits the fused scorer extracts per row, d = 0..5 the axes' tile knobs, 6 the
+   * auto-unroll knob, 7 the explicit-unroll knob: digit = (v / mult) % card (exact u32
+   * magic-number divisions; mult / card 1 and magic 0 for an absent knob) */
+  uint32_t digit_mult[8];
+  uint32_t digit_card[8];
+  uint64_t digit_mult_magic[8];
+  uint64_t digit_card_magic[8];
+  int32_t choice_off[KT_MAX_AXES + 1];  /* axis a's first entry in the concatenated per-choice tables */
+  int32_t pad2;
 } kt_spec_table;
 
 /* Model dimensions and flat-vector offsets (in floats). */

@@ -57,6 +57,12 @@ class SpecTable(ctypes.Structure):
         ("fmean", f64 * KT_F),
         ("fstd", f64 * KT_F),
         ("card_magic", u64 * KT_MAX_KNOBS),
+        ("digit_mult", u32 * 8),
+        ("digit_card", u32 * 8),
+        ("digit_mult_magic", u64 * 8),
+        ("digit_card_magic", u64 * 8),
+        ("choice_off", i32 * (KT_MAX_AXES + 1)),
+        ("pad2", i32),
     ]
 
 

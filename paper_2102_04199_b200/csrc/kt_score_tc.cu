@@ -84,7 +84,7 @@ struct __align__(1024) Smem {
   float2 nrm_i[TAB];
   double2 l2[TAB];  // numpy log2 of (outer, inner) extent
   float nconst[KT_MAX_LOOPS][8];
-  int tab_off[KT_MAX_AXES];
+  int tab_off[KT_MAX_AXES + 1];  // start of each axis' choices in the per-choice tables; [n_axes] = total
   int64_t vtile[2][GT];           // per tile parity: the graphs' config indices (INT64_MIN: padding)
   unsigned int khist[2048];       // first radix digit (key >> 53) of this CTA's top-k keys
   // digit extraction for slot d (axes 0..5, 6 = auto_unroll knob, 7 = explicit knob):
@@ -108,15 +108,35 @@ __device__ __forceinline__ uint32_t udiv(uint32_t v, uint32_t d, uint64_t magic)
   return d == 1 ? v : static_cast<uint32_t>(__umul64hi(static_cast<uint64_t>(v), magic));
 }
 
-__device__ __forceinline__ void stage_operand(const float* W, int K_src, int N, int K, float* hi, float* lo, int tid) {
-  // B operand = W^T (rows n, K-major) from row-major W[k][n]; K beyond K_src zero
-  for (int e = tid; e < N * K; e += NT) {
-    const int n = e / K, k = e - n * K;
-    const float v = k < K_src ? W[k * N + n] : 0.0f;
-    const float h = tf32_hi(v);
-    const int off = kmajor_offset(n, k, K) >> 2;
-    hi[off] = h;
-    lo[off] = v - h;
+// B operand = W^T (rows n, K-major) from row-major W[k][n]; K beyond K_src zero.  Split
+// into a load half and a store half so that a thread's loads for all four operands are in
+// flight together (the staging is on the critical path of every launch).
+template <int N, int K>
+struct OperandRegs {
+  static constexpr int IT = (N * K + NT - 1) / NT;
+  float v[IT];
+};
+template <int N, int K>
+__device__ __forceinline__ void load_operand(OperandRegs<N, K>& r, const float* W, int K_src, int tid) {
+#pragma unroll
+  for (int i = 0; i < OperandRegs<N, K>::IT; ++i) {
+    const int e = tid + i * NT, n = e / K, k = e - n * K;
+    r.v[i] = e < N * K && k < K_src ? __ldg(W + k * N + n) : 0.0f;
+  }
+}
+template <int N, int K>
+__device__ __forceinline__ void store_operand(const OperandRegs<N, K>& r, float* hi, float* lo, int tid) {
+  constexpr int IT = OperandRegs<N, K>::IT;
+  const float* v = r.v;
+#pragma unroll
+  for (int i = 0; i < IT; ++i) {
+    const int e = tid + i * NT, n = e / K, k = e - n * K;
+    if (e < N * K) {
+      const float h = tf32_hi(v[i]);
+      const int off = kmajor_offset(n, k, K) >> 2;
+      hi[off] = h;
+      lo[off] = v[i] - h;
+    }
   }
 }
 
@@ -144,6 +164,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const kt_spec_table& T = *tab;
+  if (threadIdx.x == 0) TRACE(27, 0);  // kernel entry
   const int tid = threadIdx.x, warp = tid >> 5;
   if (T.space_size > 0xffffffffull) {  // 32-bit digit arithmetic below; larger spaces use kt_embed_csr
     if (blockIdx.x == 0 && tid == 0) atomicOr(err, 2);
@@ -151,10 +172,20 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
   }
 
   // ---- setup: operands, tables, barriers, TMEM ------------------------------------------
-  stage_operand(params + dims.off_gcn[0], KT_F, 32, 16, S.b1h, S.b1l, tid);
-  stage_operand(params + dims.off_gcn[1], 32, 32, 32, S.b2h, S.b2l, tid);
-  stage_operand(params + dims.off_hw[0], H, H, H, S.b3h, S.b3l, tid);
-  stage_operand(params + dims.off_hw[1], H, H, H, S.b4h, S.b4l, tid);
+  {
+    OperandRegs<32, 16> r1;
+    OperandRegs<32, 32> r2;
+    OperandRegs<H, H> r3, r4;
+    load_operand(r1, params + dims.off_gcn[0], KT_F, tid);
+    load_operand(r2, params + dims.off_gcn[1], 32, tid);
+    load_operand(r3, params + dims.off_hw[0], H, tid);
+    load_operand(r4, params + dims.off_hw[1], H, tid);
+    store_operand(r1, S.b1h, S.b1l, tid);
+    store_operand(r2, S.b2h, S.b2l, tid);
+    store_operand(r3, S.b3h, S.b3l, tid);
+    store_operand(r4, S.b4h, S.b4l, tid);
+  }
+  if (tid == 0) TRACE(30, 0);
   if (tid < H) {
     S.bias0[tid] = params[dims.off_hb[0] + tid];
     S.bias1[tid] = params[dims.off_hb[1] + tid];
@@ -169,27 +200,19 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
   if (tid < KT_MAX_AXES) S.axis_knob[tid] = T.axis_knob[tid];
   if (tid < 4) S.auto_vals[tid] = T.auto_vals[tid];
   if (tid < 2) S.expl_vals[tid] = T.expl_vals[tid];
+  if (tid < 8) {  // digit divisors, computed on the host (graphs.build_spec_table)
+    S.dmult[tid] = T.digit_mult[tid];
+    S.dcard[tid] = T.digit_card[tid];
+    S.dm_magic[tid] = T.digit_mult_magic[tid];
+    S.dc_magic[tid] = T.digit_card_magic[tid];
+    S.tab_off[tid < KT_MAX_AXES + 1 ? tid : KT_MAX_AXES] = T.choice_off[tid < KT_MAX_AXES + 1 ? tid : KT_MAX_AXES];
+    if (tid == 0) {
+      S.auto_knob = T.auto_knob;
+      S.expl_knob = T.expl_knob;
+      TRACE(30, 5);
+    }
+  }
   if (tid == 0) {
-    S.auto_knob = T.auto_knob;
-    S.expl_knob = T.expl_knob;
-    for (int d = 0; d < 8; ++d) {
-      const int kn = d < KT_MAX_AXES ? (d < T.n_axes ? T.axis_knob[d] : -1) : (d == 6 ? T.auto_knob : T.expl_knob);
-      uint64_t mult = 1;
-      uint32_t card = 1;
-      if (kn >= 0) {
-        for (int j = kn + 1; j < T.n_knobs; ++j) mult *= T.card[j];
-        card = T.card[kn];
-      }
-      S.dmult[d] = static_cast<uint32_t>(mult);
-      S.dcard[d] = card;
-      S.dm_magic[d] = mult > 1 ? ~0ull / mult + 1 : 0ull;
-      S.dc_magic[d] = card > 1 ? ~0ull / card + 1 : 0ull;
-    }
-    int off = 0;
-    for (int a = 0; a < na; ++a) {
-      S.tab_off[a] = off;
-      off += T.axis_knob[a] >= 0 ? static_cast<int>(T.card[T.axis_knob[a]]) : 1;
-    }
     for (int s = 0; s < XS; ++s) {
       mbar_init(&S.x_full[s], 4);
       mbar_init(&S.x_empty[s], 1);
@@ -206,6 +229,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     mbar_init(&S.z_full, 8);
     mbar_init(&S.d3_full, 1);
     mbar_init(&S.d4_full, 1);
+    TRACE(30, 1);
   }
   if (tid < KT_MAX_LOOPS) {
     const int k = tid;
@@ -219,23 +243,27 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     S.nconst[k][7] = 0.f;
   }
   if (warp == 8) tmem_alloc(&S.tmem_base, 512);
+  if (tid == 256) TRACE(30, 2);
   if (key_hist)
     for (int i = tid; i < 2048; i += NT) S.khist[i] = 0;
   __syncthreads();
-  for (int a = 0; a < na; ++a) {
-    const int n = T.axis_knob[a] >= 0 ? static_cast<int>(T.card[T.axis_knob[a]]) : 1;
-    for (int c = tid; c < n; c += NT) {
-      const int e = S.tab_off[a] + c;
-      S.oi[e] = make_int2(T.outer[a][c], T.inner[a][c]);
-      S.nrm_o[e] = make_float4(T.nrm_ext[a][c], T.nrm_log2ext[a][c], T.nrm_stride[a][c], 0.f);
-      S.nrm_i[e] = make_float2(T.nrm_ext[na + a][c], T.nrm_log2ext[na + a][c]);
-      S.l2[e] = make_double2(T.raw_log2[0][a][c], T.raw_log2[1][a][c]);
-    }
+  if (tid == 0) TRACE(30, 3);
+  // per-choice tables, one flat pass over every axis' entries (loads independent across threads)
+  for (int e = tid; e < S.tab_off[na]; e += NT) {
+    int a = 0;
+    while (a + 1 < na && S.tab_off[a + 1] <= e) ++a;
+    const int c = e - S.tab_off[a];
+    S.oi[e] = make_int2(T.outer[a][c], T.inner[a][c]);
+    S.nrm_o[e] = make_float4(T.nrm_ext[a][c], T.nrm_log2ext[a][c], T.nrm_stride[a][c], 0.f);
+    S.nrm_i[e] = make_float2(T.nrm_ext[na + a][c], T.nrm_log2ext[na + a][c]);
+    S.l2[e] = make_double2(T.raw_log2[0][a][c], T.raw_log2[1][a][c]);
   }
+  if (tid == 0) TRACE(30, 4);
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0) TRACE(28, 0);  // prologue done
   const uint32_t tmem = S.tmem_base;
   const int64_t n_tiles = (B + GT - 1) / GT;
   const int64_t my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -629,6 +657,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
   if (key_hist)
     for (int i = tid; i < 2048; i += NT)
       if (S.khist[i]) atomicAdd(&key_hist[i], S.khist[i]);
+  if (threadIdx.x == 0) TRACE(29, 0);  // kernel exit
 }
 
 }  // namespace tcs

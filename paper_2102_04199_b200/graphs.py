@@ -400,6 +400,24 @@ def build_spec_table(spec: KernelSpec, space: KnobSpace, layout: BatchLayout,
             for s, v in consts.items():
                 t.nrm_const[k][s] = _norm32(v, fmean, fstd, s)
             t.nrm_unroll1[k] = _norm32(1.0, fmean, fstd, 4)
+    # the scorer's per-row digit extraction (host-computed so the kernel prologue has no
+    # 64-bit divisions): digit d of index v is (v // mult) % card
+    cards = [len(k.values) for k in space.knobs]
+    magic = lambda x: (2**64 // x + 1) if x >= 2 else 0
+    for d in range(8):
+        kn = (t.axis_knob[d] if d < na else -1) if d < 6 else (t.auto_knob if d == 6 else t.expl_knob)
+        mult = int(np.prod(cards[kn + 1:], dtype=np.int64)) if kn >= 0 else 1
+        card = cards[kn] if kn >= 0 else 1
+        if mult >= 2**32:
+            mult = 2**32 - 1  # (spaces >= 2^32 never reach the u32 digit path)
+        t.digit_mult[d], t.digit_card[d] = mult, card
+        t.digit_mult_magic[d], t.digit_card_magic[d] = magic(mult), magic(card)
+    off = 0
+    for a in range(6):
+        t.choice_off[a] = off
+        if a < na:
+            off += cards[t.axis_knob[a]] if t.axis_knob[a] >= 0 else 1
+    t.choice_off[6] = off
     return t
 
 

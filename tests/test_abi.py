@@ -39,8 +39,9 @@ def test_library_exports_every_declared_symbol(lib):
 
 def test_struct_layouts_match_c(lib):
     # offsets of the last members pin the whole layout (checked against gcc's sizeof)
-    assert ctypes.sizeof(_lib.SpecTable) == 47160
+    assert ctypes.sizeof(_lib.SpecTable) == 47384
     assert _lib.SpecTable.fstd.offset == 47000
+    assert _lib.SpecTable.choice_off.offset == 47352
     assert ctypes.sizeof(_lib.Dims) == 128
 
 

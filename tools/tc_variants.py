@@ -1,5 +1,6 @@
 """Time debug variants of the tensor-core scorer (compile-time -D switches) on 1M candidates.
     python tools/tc_variants.py --build      (here)   /   python tools/tc_variants.py   (GPU box)"""
+import os
 import pathlib
 import subprocess
 import sys
@@ -47,7 +48,7 @@ for name in VARIANTS:
         spec = pk.KernelSpec(*bench.SPEC_ARGS)
         space = pk.build_knob_space(spec)
         lay = pg.batch_layout(spec, pg.build_super_template(pk.OP_TYPES))
-        idx = torch.randint(0, space.size, (1 << 20,), device=dev)
+        idx = torch.randint(0, space.size, (int(os.environ.get("TCV_B", 1 << 20)),), device=dev)
     for _ in range(3):
         ps.score_indices(m, spec, space, lay, idx)
     torch.cuda.synchronize()
@@ -61,4 +62,4 @@ for name in VARIANTS:
     if name == "base":
         z_base = z.clone()
     dz = (z - z_base).abs().max().item() * m.label_norm.std * 0.6931471805599453  # GFLOPS relative error
-    print(f"{name:12s} {e0.elapsed_time(e1) / 20:.4f} ms per 1M   max GFLOPS rel diff vs base {dz:.2e}", flush=True)
+    print(f"{name:12s} {e0.elapsed_time(e1) / 20:.4f} ms per call (B={idx.numel()})   max GFLOPS rel diff vs base {dz:.2e}", flush=True)
