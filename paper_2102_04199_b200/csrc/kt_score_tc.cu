@@ -60,16 +60,32 @@ using namespace kt::tc;
 constexpr int NT = 608;  // 19 warps
 constexpr int GT = 128;   // graphs per tile (one TMEM lane each)
 constexpr int H = 64;
-constexpr int XS = 4;     // X ring slots
+#ifndef KT_XS
+#define KT_XS 4
+#endif
+#ifndef KT_N1
+#define KT_N1 2
+#endif
+#ifndef KT_NR
+#define KT_NR 2
+#endif
+#ifndef KT_N2
+#define KT_N2 2
+#endif
+constexpr int XS = KT_XS;  // X ring slots
+constexpr int N1 = KT_N1;  // D1 buffers
+constexpr int NR = KT_NR;  // R buffers
+constexpr int N2 = KT_N2;  // D2 buffers
 constexpr int TAB = 448;
 
 // TMEM column map (512 allocated)
-constexpr uint32_t T_X = 0;     // X[s]: hi at 32 s, lo at 32 s + 16       [0, 128)
-constexpr uint32_t T_D1 = 128;  // D1[b] at 128 + 32 b                    [128, 192)
-constexpr uint32_t T_R = 192;   // R[b]: hi at 192 + 64 b, lo at +32        [192, 320)
-constexpr uint32_t T_D2 = 320;  // D2[b] at 320 + 32 b                    [320, 384)
-constexpr uint32_t T_D3 = 384;  //                                         [384, 448)
-constexpr uint32_t T_D4 = 448;  //                                         [448, 512)
+constexpr uint32_t T_X = 0;                  // X[s]: hi at 32 s, lo at 32 s + 16
+constexpr uint32_t T_D1 = T_X + 32 * XS;     // D1[b] at T_D1 + 32 b
+constexpr uint32_t T_R = T_D1 + 32 * N1;     // R[b]: hi at T_R + 64 b, lo at +32
+constexpr uint32_t T_D2 = T_R + 64 * NR;     // D2[b] at T_D2 + 32 b
+constexpr uint32_t T_D3 = T_D2 + 32 * N2;    // head layer 1 accumulator (64 columns)
+constexpr uint32_t T_D4 = T_D3 + 64;         // head layer 2 accumulator (64 columns)
+static_assert(T_D4 + 64 <= 512, "TMEM budget: 512 columns");
 
 struct __align__(1024) Smem {
   float b1h[32 * 16], b1l[32 * 16];  // W1^T (N=32, K=16; K 12..15 zero), K-major core matrices
@@ -97,7 +113,7 @@ struct __align__(1024) Smem {
   int auto_vals[4], expl_vals[2];
   int auto_knob, expl_knob;
   uint64_t x_full[XS], x_empty[XS];
-  uint64_t d1_full[2], d1_empty[2], r_full[2], r_empty[2], d2_full[2], d2_empty[2];
+  uint64_t d1_full[N1], d1_empty[N1], r_full[NR], r_empty[NR], d2_full[N2], d2_empty[N2];
   uint64_t u_full, z_full, d3_full, d4_full;
   uint32_t tmem_base;
 };
@@ -217,11 +233,15 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       mbar_init(&S.x_full[s], 4);
       mbar_init(&S.x_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < N1; ++b) {
       mbar_init(&S.d1_full[b], 1);
       mbar_init(&S.d1_empty[b], 4);
+    }
+    for (int b = 0; b < NR; ++b) {
       mbar_init(&S.r_full[b], 4);
       mbar_init(&S.r_empty[b], 1);
+    }
+    for (int b = 0; b < N2; ++b) {
       mbar_init(&S.d2_full[b], 1);
       mbar_init(&S.d2_empty[b], 8);
     }
@@ -392,10 +412,10 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       tc_fence_after();
     };
     auto g1 = [&](int64_t q) {
-      const int s = static_cast<int>(q % XS), b = static_cast<int>(q & 1);
+      const int s = static_cast<int>(q % XS), b = static_cast<int>(q % N1);
       if ((tid & 31) == 0) TRACE(22, q);
       wait_bar(&S.x_full[s], static_cast<uint32_t>((q / XS) & 1));
-      wait_bar(&S.d1_empty[b], static_cast<uint32_t>(((q >> 1) & 1) ^ 1));
+      wait_bar(&S.d1_empty[b], static_cast<uint32_t>(((q / N1) & 1) ^ 1));
       if ((tid & 31) == 0) TRACE(23, q);
       const uint32_t xh = tmem + T_X + 32 * s, xl = xh + 16, d = tmem + T_D1 + 32 * b;
       if (elect_one()) {
@@ -412,13 +432,12 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       __syncwarp();
     };
     auto g2 = [&](int64_t q) {
-      const int b = static_cast<int>(q & 1);
-      const uint32_t ph = static_cast<uint32_t>((q >> 1) & 1);
+      const int b = static_cast<int>(q % NR), b2 = static_cast<int>(q % N2);
       if ((tid & 31) == 0) TRACE(17, q);
-      wait_bar(&S.r_full[b], ph);
-      wait_bar(&S.d2_empty[b], ph ^ 1);
+      wait_bar(&S.r_full[b], static_cast<uint32_t>((q / NR) & 1));
+      wait_bar(&S.d2_empty[b2], static_cast<uint32_t>(((q / N2) & 1) ^ 1));
       if ((tid & 31) == 0) TRACE(18, q);
-      const uint32_t rh = tmem + T_R + 64 * b, rl = rh + 32, d = tmem + T_D2 + 32 * b;
+      const uint32_t rh = tmem + T_R + 64 * b, rl = rh + 32, d = tmem + T_D2 + 32 * b2;
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
@@ -427,7 +446,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
           mma_tf32_ts(d, rl + 8 * kk, kdesc(S.b2h, 32, kk), id32, 1);
         }
         mma_commit(&S.r_empty[b]);
-        mma_commit(&S.d2_full[b]);
+        mma_commit(&S.d2_full[b2]);
         TRACE(2, q);
       }
       __syncwarp();
@@ -478,20 +497,19 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     const int g = tid;
     const uint32_t lane = static_cast<uint32_t>((32 * warp) << 16);
     for (int64_t q = 0; q < n_chunks; ++q) {
-      const int b = static_cast<int>(q & 1);
-      const uint32_t ph = static_cast<uint32_t>((q >> 1) & 1);
-      mbar_wait(&S.d1_full[b], ph);
+      const int b1 = static_cast<int>(q % N1), b = static_cast<int>(q % NR);
+      mbar_wait(&S.d1_full[b1], static_cast<uint32_t>((q / N1) & 1));
       __syncwarp();
       if (g == 0) TRACE(5, q);
       tc_fence_after();
       float v[32];
-      tmem_ld16(tmem + lane + T_D1 + 32 * b, v);
-      tmem_ld16(tmem + lane + T_D1 + 32 * b + 16, v + 16);
+      tmem_ld16(tmem + lane + T_D1 + 32 * b1, v);
+      tmem_ld16(tmem + lane + T_D1 + 32 * b1 + 16, v + 16);
       tmem_wait_ld();
       if (g == 0) TRACE(13, q);
       tc_fence_before();
-      warp_arrive(&S.d1_empty[b]);
-      mbar_wait(&S.r_empty[b], ph ^ 1);  // GEMM2 of chunk q-2 has finished reading R[b]
+      warp_arrive(&S.d1_empty[b1]);
+      mbar_wait(&S.r_empty[b], static_cast<uint32_t>(((q / NR) & 1) ^ 1));  // GEMM2 of chunk q-NR read R[b]
       __syncwarp();
       if (g == 0) TRACE(14, q);
       tc_fence_after();
@@ -533,14 +551,14 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     int kc = 0;       // chunk index within the current tile (no 64-bit % / on this path)
     int64_t ti = 0;   // local tile index
     for (int64_t q = 0; q < n_chunks; ++q) {
-      const int b = static_cast<int>(q & 1);
+      const int b = static_cast<int>(q % N2);
       if (kc == 0) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) tot[j] = rs[j] = make_float2(0.0f, 0.0f);
 #pragma unroll
         for (int j = 0; j < 16; ++j) mx[j] = 0.0f;  // max_k ReLU(s_k) = max(0, max_k s_k)
       }
-      mbar_wait(&S.d2_full[b], static_cast<uint32_t>((q >> 1) & 1));
+      mbar_wait(&S.d2_full[b], static_cast<uint32_t>((q / N2) & 1));
       __syncwarp();
       if (tr) TRACE(7, q);
       tc_fence_after();
