@@ -240,14 +240,14 @@ def bench_dataset(entries, reps=5):
                       "config_graph-per-sample + pack_graphs (same packed batch)"}
 
 
-def bench_maml(m, corpus, steps, warmup, first_order=True):
+def bench_maml(m, corpus, steps, warmup, first_order=True, tasks_per_step=32):
     import torch
     import torch.distributed as dist
 
     from paper_2102_04199_b200 import meta as pmeta
     from paper_2102_04199_b200.util import rng_from
 
-    cfg = pmeta.MetaConfig(n_way=3, k_shot=2, meta_batch=32, inner_steps=1, first_order=first_order)
+    cfg = pmeta.MetaConfig(n_way=3, k_shot=2, meta_batch=tasks_per_step, inner_steps=1, first_order=first_order)
     tr = pmeta.MetaTrainer(m, corpus, cfg)
     rank, _, ws = dist_env()
     plan = tr.plan(rng_from("metatrain", "super", 0), warmup + steps, shard=(rank, ws))
@@ -271,9 +271,10 @@ def bench_maml(m, corpus, steps, warmup, first_order=True):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     st = tr.stats(plan, bufs)
-    return {"metric": "MAML meta-train tasks/sec", "value": 32 / (ms / 1e3), "unit": "tasks/s",
+    return {"metric": "MAML meta-train tasks/sec", "value": tasks_per_step / (ms / 1e3), "unit": "tasks/s",
             "ms_per_step": ms, "steps": steps,
-            "config": f"C3: 3-way 2-shot, 32 tasks/outer step, 1 inner step, {'FO' if first_order else 'SO'}, "
+            "config": f"C3: 3-way 2-shot, {tasks_per_step} tasks/outer step, 1 inner step, "
+                      f"{'FO' if first_order else 'SO'}, "
                       "frozen GCN (corpus embedded once; exact, the GCN does not move in meta_step), super N=25, "
                       f"47x200 synthetic corpus; 2 launches/step, {'one CUDA graph replay' if ws == 1 else 'eager'}; "
                       f"tasks sharded over {ws} GPU(s) with an NCCL all-reduce of sum_i g_i per step",
@@ -778,6 +779,8 @@ def run_ours(args):
         fn, ln = pmeta.dataset_norms(corpus)  # meta.py:81-101 over the corpus, as pretrain does
         m = pm.model_from_flat(m._flat, m, feature_norm=fn, label_norm=ln)
         line["maml"] = bench_maml(m, corpus, args.meta_steps, 10)
+        if ws > 1:  # weak form: 32 tasks per GPU per outer step (one all-reduce per step either way)
+            line["maml_weak"] = bench_maml(m, corpus, args.meta_steps, 10, tasks_per_step=32 * ws)
         if ws == 1:
             line["maml_so"] = bench_maml(m, corpus, max(args.meta_steps // 2, 10), 5, first_order=False)
             line["pretrain"] = bench_pretrain_step(m, synthetic_corpus(entries, ("conv2d", "winograd", "depthwise")),
