@@ -22,6 +22,7 @@ Everything is keyed by `rng_from` so reruns are byte-identical.  Outputs:
   dataset/       a small reference gen_dataset (harness.py:164-176) written by the
                  reference's save_dataset (harness.py:195-216): kernels.yaml,
                  samples.csv, manifest.json
+  ckpt_v1.npz    the golden model written by the reference's save_model (model.py:441-455)
   gp.npz         GP surrogate (search.py:39-159): gp_fit with lengthscale selection and
                  jitter escalation, gp_predict_many, _gp_posterior_cov and
                  bo_propose_batch picks, on synthetic observations in knob coordinates
@@ -359,7 +360,19 @@ def gp_goldens():
     np.savez_compressed(os.path.join(OUT, "gp.npz"), **out)
 
 
+def ckpt_golden():
+    from kerntune.util import rng_from as rf
+
+    m = rm.init_model(rf("golden-ckpt"))
+    m = replace(m, feature_norm=rm.FeatureNorm(np.linspace(-1.0, 1.0, 12), np.linspace(0.5, 2.0, 12)),
+                label_norm=rm.LabelNorm(-5.62, 7.08))
+    rm.save_model(m, os.path.join(OUT, "ckpt_v1.npz"))
+
+
 def main():
+    if sys.argv[1:] == ["ckpt"]:
+        ckpt_golden()
+        return
     if sys.argv[1:] == ["gp"]:
         gp_goldens()
         return
@@ -380,6 +393,7 @@ def main():
     sa_goldens()
     dataset_goldens()
     gp_goldens()
+    ckpt_golden()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))
 

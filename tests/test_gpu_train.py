@@ -253,3 +253,37 @@ def test_meta_trainer_graph_replay_equals_eager(cuda_device, g_model, super_samp
     assert torch.equal(pm.flat_params(rep.model()), pm.flat_params(eager.model()))
     assert torch.equal(bufs2["stats"], bufs["stats"])
 
+
+
+def test_checkpoint_interchange_with_reference(cuda_device, tmp_path):
+    """load_model reads the reference's own npz v1 file (tests/golden/ckpt_v1.npz, written by
+    kerntune.model.save_model); save_model writes the same keys, shapes and (fp32-exact) values."""
+    import os
+
+    ref_path = os.path.join(os.path.dirname(__file__), "golden", "ckpt_v1.npz")
+    m = pm.load_model(ref_path)
+    with np.load(ref_path) as z:
+        ref = {k: z[k] for k in z.files}
+    for i, w in enumerate(m.gcn.layers):
+        assert np.array_equal(w.cpu().numpy(), ref[f"gcn_{i}"].astype(np.float32))
+    for i, (w, b) in enumerate(zip(m.head.weights, m.head.biases)):
+        assert np.array_equal(w.cpu().numpy(), ref[f"head_w{i}"].astype(np.float32))
+        assert np.array_equal(b.cpu().numpy(), ref[f"head_b{i}"].astype(np.float32))
+    assert np.array_equal(m.feature_norm.mean, ref["feat_mean"]) and np.array_equal(m.feature_norm.std, ref["feat_std"])
+    assert (m.label_norm.mean, m.label_norm.std) == tuple(ref["label_norm"])
+    out = tmp_path / "ours.npz"
+    pm.save_model(m, out)
+    with np.load(out) as z:
+        ours = {k: z[k] for k in z.files}
+    assert sorted(ours) == sorted(ref)
+    for k in ref:
+        assert ours[k].shape == ref[k].shape and ours[k].dtype == ref[k].dtype, k
+        if k.startswith(("gcn_", "head_", "agg_")):
+            assert np.array_equal(ours[k], ref[k].astype(np.float32).astype(np.float64)), k
+        else:
+            assert np.array_equal(ours[k], ref[k]), k
+    m2 = pm.load_model(out)
+    assert torch.equal(pm.flat_params(m2), pm.flat_params(m))
+    np.savez(tmp_path / "bad.npz", version=np.array(2))
+    with pytest.raises(pg.DomainError):
+        pm.load_model(tmp_path / "bad.npz")
