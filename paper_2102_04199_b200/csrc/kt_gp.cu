@@ -72,7 +72,6 @@ __global__ void __launch_bounds__(FT) factor_kernel(const double* __restrict__ x
   double* AA = A + n * d;      // n squared norms
   double* R = AA + n;          // n: solve right-hand side
   __shared__ double red[FT / 32];
-  __shared__ double s_diag;
   __shared__ int s_fail;
   const int c = blockIdx.x, tid = threadIdx.x;
   const double* ls = ls_all + c * d;
@@ -90,7 +89,8 @@ __global__ void __launch_bounds__(FT) factor_kernel(const double* __restrict__ x
   //   2. the panel is factored right-looking in registers, the pivot row's entries
   //      broadcast through shared memory;
   //   3. the panel's columns are written out.
-  __shared__ double S[PW][PW], pv[PW];
+  constexpr int KC = 4 * PW;
+  __shared__ double S[KC][PW], Pd[PW][PW + 1];
   double nv = noise;
   int status = 0;
   const int i = tid;
@@ -109,43 +109,66 @@ __global__ void __launch_bounds__(FT) factor_kernel(const double* __restrict__ x
           if (i == j0 + c) acc[c] += nv;
         }
       }
-      for (int k0 = 0; k0 < j0; k0 += PW) {
-        if (tid < PW * PW) {
-          const int kk = tid / PW, c = tid % PW;
-          S[kk][c] = c < nb ? L[static_cast<size_t>(k0 + kk) * n + j0 + c] : 0.0;
+      for (int k0 = 0; k0 < j0; k0 += KC) {  // KC earlier columns staged per barrier pair
+        const int kc = j0 - k0 < KC ? j0 - k0 : KC;  // (a multiple of PW)
+        for (int e = tid; e < KC * PW; e += FT) {
+          const int kk = e / PW, c = e % PW;
+          S[kk][c] = kk < kc && c < nb ? L[static_cast<size_t>(k0 + kk) * n + j0 + c] : 0.0;
         }
         __syncthreads();
         if (mine) {
-#pragma unroll 4
-          for (int kk = 0; kk < PW; ++kk) {
-            const double lik = L[static_cast<size_t>(k0 + kk) * n + i];
+          for (int kb = 0; kb < kc; kb += PW) {
+            double li[PW];  // the row's factor entries: all loads in flight before the FMAs
 #pragma unroll
-            for (int c = 0; c < PW; ++c) acc[c] = fma(-lik, S[kk][c], acc[c]);
+            for (int kk = 0; kk < PW; ++kk) li[kk] = L[static_cast<size_t>(k0 + kb + kk) * n + i];
+#pragma unroll
+            for (int kk = 0; kk < PW; ++kk) {
+#pragma unroll
+              for (int c = 0; c < PW; ++c) acc[c] = fma(-li[kk], S[kb + kk][c], acc[c]);
+            }
           }
         }
         __syncthreads();
       }
+      // diagonal block: the panel rows hand their sums to warp 0, which factors the
+      // nb x nb block alone (lane = row, warp barriers only); every row below then solves
+      // its nb panel entries against it -- one CTA barrier per panel instead of two per column
+      if (i >= j0 && i < j0 + nb) {
 #pragma unroll
-      for (int c = 0; c < PW; ++c) {
-        if (c < nb) {
-          const int j = j0 + c;
-          if (i == j) {
-            const double sdiag = acc[c];
+        for (int c = 0; c < PW; ++c) Pd[i - j0][c] = acc[c];
+      }
+      __syncthreads();
+      if (tid < 32) {
+        const int r = tid;
+        for (int c = 0; c < nb; ++c) {
+          if (r == c) {
+            const double sdiag = Pd[c][c];
             if (!(sdiag > 0.0)) s_fail = 1;
-            acc[c] = sqrt(sdiag);
-            s_diag = acc[c];
+            Pd[c][c] = sqrt(sdiag);
           }
-          __syncthreads();
-          if (s_fail) break;
-          if (i > j && i < n) acc[c] = acc[c] / s_diag;
-          if (i > j && i < j0 + nb) pv[i - j0] = acc[c];  // L[t][j] of the panel rows t
-          __syncthreads();
-          if (i > j && i < n) {
+          __syncwarp();
+          if (r > c && r < nb) Pd[r][c] /= Pd[c][c];
+          __syncwarp();
+          if (r > c && r < nb)
+            for (int c2 = c + 1; c2 <= r; ++c2) Pd[r][c2] = fma(-Pd[r][c], Pd[c2][c], Pd[r][c2]);
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      if (s_fail) break;
+      if (i >= j0 + nb && i < n) {  // rows below: acc <- acc L_d^-T (forward substitution over the panel)
 #pragma unroll
-            for (int c2 = c + 1; c2 < PW; ++c2)
-              if (c2 < nb) acc[c2] = fma(-acc[c], pv[c2], acc[c2]);
+        for (int c = 0; c < PW; ++c) {
+          if (c < nb) {
+            double v = acc[c];
+#pragma unroll
+            for (int c2 = 0; c2 < c; ++c2) v = fma(-acc[c2], Pd[c][c2], v);
+            acc[c] = v / Pd[c][c];
           }
         }
+      } else if (mine) {
+#pragma unroll
+        for (int c = 0; c < PW; ++c) acc[c] = Pd[i - j0][c];
       }
       if (s_fail) break;
 #pragma unroll
@@ -175,21 +198,55 @@ __global__ void __launch_bounds__(FT) factor_kernel(const double* __restrict__ x
     const int col = static_cast<int>(e / n), row = static_cast<int>(e % n);
     if (row < col) L[e] = 0.0;
   }
-  // cho_solve: L z = y (column sweep), then L^T alpha = z (column sweep backwards)
+  // cho_solve, blocked by panels of PW rows: L z = y forward, then L^T alpha = z backward.
+  // Warp 0 solves each PW x PW diagonal block (warp barriers only); the CTA then updates
+  // every remaining row with the panel's solved values (two CTA barriers per panel).
   for (int i = tid; i < n; i += FT) R[i] = y[i];
   __syncthreads();
-  for (int j = 0; j < n; ++j) {
-    const double zj = R[j] / L[static_cast<size_t>(j) * n + j];
+  for (int j0 = 0; j0 < n; j0 += PW) {
+    const int nb = n - j0 < PW ? n - j0 : PW;
+    if (tid < 32) {
+      for (int c = 0; c < nb; ++c) {
+        const int j = j0 + c;
+        const double zj = R[j] / L[static_cast<size_t>(j) * n + j];
+        __syncwarp();
+        if (tid == 0) R[j] = zj;
+        if (tid > c && tid < nb) R[j0 + tid] = fma(-L[static_cast<size_t>(j) * n + j0 + tid], zj, R[j0 + tid]);
+        __syncwarp();
+      }
+    }
     __syncthreads();
-    for (int i = j + 1 + tid; i < n; i += FT) R[i] = fma(-L[static_cast<size_t>(j) * n + i], zj, R[i]);
-    if (tid == 0) R[j] = zj;
+    for (int i = j0 + nb + tid; i < n; i += FT) {
+      double v = R[i];
+#pragma unroll
+      for (int c = 0; c < PW; ++c)
+        if (c < nb) v = fma(-L[static_cast<size_t>(j0 + c) * n + i], R[j0 + c], v);
+      R[i] = v;
+    }
     __syncthreads();
   }
-  for (int j = n - 1; j >= 0; --j) {
-    const double aj = R[j] / L[static_cast<size_t>(j) * n + j];
+  for (int j1 = n; j1 > 0; j1 -= PW) {  // panel [j0, j1), last panel first
+    const int j0 = j1 - PW > 0 ? j1 - PW : 0;
+    const int nb = j1 - j0;
+    if (tid < 32) {
+      for (int c = nb - 1; c >= 0; --c) {
+        const int j = j0 + c;
+        const double aj = R[j] / L[static_cast<size_t>(j) * n + j];
+        __syncwarp();
+        if (tid == 0) R[j] = aj;
+        if (tid < c) R[j0 + tid] = fma(-L[static_cast<size_t>(j0 + tid) * n + j], aj, R[j0 + tid]);
+        __syncwarp();
+      }
+    }
     __syncthreads();
-    for (int i = tid; i < j; i += FT) R[i] = fma(-L[static_cast<size_t>(i) * n + j], aj, R[i]);
-    if (tid == 0) R[j] = aj;
+    for (int i = tid; i < j0; i += FT) {  // R[i] -= sum_c L[j0 + c][i] alpha[j0 + c]
+      const double* row = L + static_cast<size_t>(i) * n + j0;  // column i of L, rows j0..: contiguous
+      double v = R[i];
+#pragma unroll
+      for (int c = 0; c < PW; ++c)
+        if (c < nb) v = fma(-row[c], R[j0 + c], v);
+      R[i] = v;
+    }
     __syncthreads();
   }
   double ya = 0.0, ld = 0.0;
@@ -262,10 +319,14 @@ __global__ void __launch_bounds__(PT) posterior_kernel(const double* __restrict_
     }
     __syncthreads();
     for (int i = j0 + nb + rq; i < n; i += PT / QPR) {
+      double li[PW];  // the row's panel entries of L: all loads in flight before the FMAs
+#pragma unroll
+      for (int c = 0; c < PW; ++c) li[c] = c < nb ? L[static_cast<size_t>(j0 + c) * n + i] : 0.0;
       double r0 = Rv[i * PC + cq], r1 = Rv[i * PC + cq + 1], r2 = Rv[i * PC + cq + 2], r3 = Rv[i * PC + cq + 3];
-#pragma unroll 4
-      for (int c = 0; c < nb; ++c) {
-        const double l = L[static_cast<size_t>(j0 + c) * n + i];
+#pragma unroll
+      for (int c = 0; c < PW; ++c) {
+        if (c >= nb) break;
+        const double l = li[c];
         const double* vr = Rv + (j0 + c) * PC + cq;
         r0 = fma(-l, vr[0], r0);
         r1 = fma(-l, vr[1], r1);

@@ -557,7 +557,8 @@ def gp_fit(s: GpSurrogate, select_lengthscale: bool = True) -> GpSurrogate:
             best = c
     Lb = L[best]
     dev_state = {"x": xd, "ls": lsd[best].contiguous(), "L": Lb, "alpha": alpha[best]}
-    return replace(s, lengthscales=cands[best].copy(), chol=Lb.cpu().numpy().T.copy(),
+    # the factor is column-major on the device: its transpose is the row-major lower L
+    return replace(s, lengthscales=cands[best].copy(), chol=Lb.t().contiguous().cpu().numpy(),
                    alpha=alpha[best].cpu().numpy(), fitted_noise=float(inf[best, 0]), _dev=dev_state)
 
 
@@ -624,8 +625,7 @@ def bo_propose_batch(s: GpSurrogate, space: KnobSpace, batch: int, beta_ucb: flo
     else:
         seen: set = set()
         indices = []
-        for c in pool:
-            i = config_index(space, c)
+        for i in configs_to_indices(space, pool).tolist():  # (vectorised config_index)
             if i in visited or i in seen:
                 continue
             seen.add(i)
@@ -638,8 +638,14 @@ def bo_propose_batch(s: GpSurrogate, space: KnobSpace, batch: int, beta_ucb: flo
         pick = rng.permutation(len(indices))[:take]
         return [index_config(space, indices[int(i)]) for i in pick]
     _require_fitted(s)
-    configs = [index_config(space, i) for i in indices]
-    mean, _, cov = _posterior(s, knob_coordinates(space, configs), True)
+    # knob coordinates straight from the indices (mixed-radix decode, knob 0 most significant)
+    cards = np.array([len(k.values) for k in space.knobs], dtype=np.int64)
+    rest = np.array(indices, dtype=np.int64)
+    ch = np.empty((rest.size, cards.size), dtype=np.float64)
+    for j in range(cards.size - 1, -1, -1):
+        ch[:, j] = rest % cards[j]
+        rest //= cards[j]
+    mean, _, cov = _posterior(s, ch / cards, True)
     noise = s.fitted_noise if s.fitted_noise is not None else s.noise_variance
     P = len(indices)
     lib = _lib.load()
@@ -648,4 +654,4 @@ def bo_propose_batch(s: GpSurrogate, space: KnobSpace, batch: int, beta_ucb: flo
     ws = torch.empty(wsb, dtype=torch.uint8, device=mean.device)
     _lib.check(lib.kt_gp_ucb(mean.data_ptr(), cov.data_ptr(), P, float(noise), float(beta_ucb), take,
                              picks.data_ptr(), ws.data_ptr(), wsb, _lib.stream_handle()), "bo_propose_batch")
-    return [configs[int(p)] for p in picks.cpu().numpy()]
+    return [index_config(space, indices[int(p)]) for p in picks.cpu().numpy()]
