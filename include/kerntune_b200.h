@@ -303,6 +303,13 @@ int kt_maml_tasks(const kt_dims* dims, const float* theta, const float* u, const
                   const int64_t* s_off, const int64_t* s_idx, const int64_t* q_off, const int64_t* q_idx,
                   int32_t T, float alpha, int32_t inner_steps, int32_t first_order, float* g_sum,
                   double* stats, void* workspace, int64_t workspace_bytes, void* stream);
+/* meta_step on one GPU (meta.py:223-257): kt_maml_tasks with the outer update
+ * theta <- theta - beta * g_sum (in place) folded into the task-sum pass (two launches
+ * instead of three). */
+int kt_maml_step(const kt_dims* dims, float* theta, const float* u, const float* y, const int64_t* s_off,
+                 const int64_t* s_idx, const int64_t* q_off, const int64_t* q_idx, int32_t T, float alpha,
+                 int32_t inner_steps, int32_t first_order, float beta, float* g_sum, double* stats,
+                 void* workspace, int64_t workspace_bytes, void* stream);
 
 /* ---- ranking (search.py:257-264) ------------------------------------------------------ */
 /* Top-k of (score desc, index asc) over B candidates; `visited` (sorted int64,

@@ -566,12 +566,14 @@ maml_task_kernel(kt_dims dims, int rc, const float* __restrict__ theta, TaskSet 
 
 // sum_out[p] = sum_t g[t][p] (fixed order, fp64 accumulate); stats = (sum ls, sum lq)
 __global__ void task_sum_kernel(const float* __restrict__ g, int T, int P, float* __restrict__ sum_out,
-                                const float* __restrict__ losses, double* __restrict__ stats) {
+                                const float* __restrict__ losses, double* __restrict__ stats, float beta = 0.0f,
+                                float* __restrict__ theta = nullptr) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p < P) {
     double s = 0.0;
     for (int t = 0; t < T; ++t) s += static_cast<double>(g[static_cast<int64_t>(t) * P + p]);
     sum_out[p] = static_cast<float>(s);
+    if (theta) theta[p] = theta[p] - beta * static_cast<float>(s);  // kt_sgd's arithmetic (kt_maml_step)
   }
   if (stats && blockIdx.x == 0 && threadIdx.x < 2) {
     double s = 0.0;
@@ -824,6 +826,38 @@ int kt_maml_tasks(const kt_dims* dims, const float* theta, const float* u, const
   meta::task_sum_kernel<<<(h.P + 255) / 256, 256, 0, st>>>(g, T, h.P, g_sum, losses, stats);
   note_launches(2);
   return check_launch("kt_maml_tasks");
+}
+
+int kt_maml_step(const kt_dims* dims, float* theta, const float* u, const float* y, const int64_t* s_off,
+                 const int64_t* s_idx, const int64_t* q_off, const int64_t* q_idx, int32_t T, float alpha,
+                 int32_t inner_steps, int32_t first_order, float beta, float* g_sum, double* stats, void* workspace,
+                 int64_t workspace_bytes, void* stream) {
+  using namespace kt;
+  KT_REQUIRE(dims && theta && u && y && s_off && s_idx && q_off && q_idx && g_sum && workspace, KT_E_ARG,
+             "kt_maml_step: null pointer");
+  KT_REQUIRE(T > 0, KT_E_EMPTY, "kt_maml_step: empty task batch");
+  KT_REQUIRE(inner_steps >= 1, KT_E_ARG, "kt_maml_step: inner_steps must be >= 1");
+  KT_REQUIRE(workspace_bytes >= kt_maml_workspace_bytes(dims, T, inner_steps, first_order), KT_E_ARG,
+             "kt_maml_step: workspace too small");
+  int rc = meta::check_head(*dims);
+  if (rc) return rc;
+  const bool so = !first_order;
+  const meta::Head h = meta::fit_rows(*dims, 8, true, so);
+  static size_t cached = 0;
+  const size_t smem = meta::task_smem(h, so);
+  rc = meta::set_smem(meta::maml_task_kernel, smem, cached);
+  if (rc) return rc;
+  float* g = static_cast<float*>(workspace);
+  float* losses = g + (int64_t)T * h.P;
+  float* thws = losses + 2 * T;
+  meta::TaskSet ts{u, y, s_off, s_idx, q_off, q_idx};
+  cudaStream_t st = as_stream(stream);
+  meta::maml_task_kernel<<<T, meta::NT, smem, st>>>(*dims, h.RC, theta, ts, T, alpha, inner_steps, first_order,
+                                                    thws, g, losses);
+  // task sum (fixed order, fp64) and the outer update in one pass over the parameters
+  meta::task_sum_kernel<<<(h.P + 255) / 256, 256, 0, st>>>(g, T, h.P, g_sum, losses, stats, beta, theta);
+  note_launches(2);
+  return check_launch("kt_maml_step");
 }
 
 }  // extern "C"
