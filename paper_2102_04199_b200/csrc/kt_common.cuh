@@ -26,6 +26,31 @@ void note_launches(int n);  // kernel launches issued (kt_launch_count)
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Kernel attributes are per-device state: launch sites cache "already set" per device,
+// so a process that drives several GPUs (or switches devices) sets them on each.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev >= 0 && dev < kMaxDevices ? dev : 0;
+}
+struct SmemAttr {
+  size_t done[kMaxDevices] = {};
+  // raise the kernel's dynamic shared memory limit to `bytes` (once per device and size)
+  template <class K>
+  void ensure(K kernel, size_t bytes) {
+    const int dev = current_device();
+    if (bytes > 48 * 1024 && bytes > done[dev]) {
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+      done[dev] = bytes;
+    }
+  }
+};
+struct PerDeviceInt {
+  int v[kMaxDevices] = {};
+  int& get() { return v[current_device()]; }
+};
+
 // ---- packed fp32x2 FMA (FFMA2).  ptxas folds a scalar broadcast into the
 // `Rn.F32` operand form, so `ffma2(s, pair, acc)` costs one issue slot for two FMAs.
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {

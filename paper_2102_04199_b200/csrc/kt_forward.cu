@@ -97,11 +97,8 @@ int kt_embed_csr(const kt_dims* dims, const float* params, const double* fmean, 
   for (int i = 1; i <= dims->n_gcn; ++i) D = D > dims->gcn[i] ? D : dims->gcn[i];
   D = (D + 3) & ~3;
   const size_t smem = sizeof(float) * fwd::WARPS * (2 * max_nodes * D + 4 * KT_MAX_DIM);
-  static size_t smem_attr = 0;
-  if (smem > 48 * 1024 && smem > smem_attr) {
-    cudaFuncSetAttribute(fwd::embed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    smem_attr = smem;
-  }
+  static SmemAttr attr;
+  attr.ensure(fwd::embed_kernel, smem);
   int64_t blocks = (B + fwd::WARPS - 1) / fwd::WARPS;
   if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
   fwd::embed_kernel<<<(int)blocks, fwd::WARPS * 32, smem, as_stream(stream)>>>(

@@ -696,12 +696,9 @@ static int check_head(const kt_dims& d) {
 }
 
 template <class K>
-static int set_smem(K kernel, size_t smem, size_t& cached) {
+static int set_smem(K kernel, size_t smem, SmemAttr& cached) {
   KT_REQUIRE(smem <= 227 * 1024, KT_E_UNSUPPORTED, "head too large for shared memory (%zu bytes)", smem);
-  if (smem > 48 * 1024 && smem > cached) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cached = smem;
-  }
+  cached.ensure(kernel, smem);
   return KT_OK;
 }
 
@@ -718,7 +715,7 @@ int kt_head_loss_grad(const kt_dims* dims, const float* theta, const float* u, c
   int rc = meta::check_head(*dims);
   if (rc) return rc;
   const meta::Head h = meta::fit_rows(*dims, 32, false, false);
-  static size_t cached = 0;
+  static SmemAttr cached;
   const size_t smem = meta::head_smem(h, false);
   rc = meta::set_smem(meta::head_kernel, smem, cached);
   if (rc) return rc;
@@ -736,7 +733,7 @@ int kt_head_hvp(const kt_dims* dims, const float* theta, const float* u, const f
   int rc = meta::check_head(*dims);
   if (rc) return rc;
   const meta::Head h = meta::fit_rows(*dims, 32, false, true);
-  static size_t cached = 0;
+  static SmemAttr cached;
   const size_t smem = meta::head_smem(h, true);
   rc = meta::set_smem(meta::head_kernel, smem, cached);
   if (rc) return rc;
@@ -760,7 +757,7 @@ int kt_fine_tune(const kt_dims* dims, const float* theta, const float* u, const 
   const char* cs = getenv("KT_FT_CLUSTER");  // experiment hook: cluster size
   if (cs && atoi(cs) >= 1 && atoi(cs) <= 16) C = atoi(cs);
   if (C > 1) {  // rows and parameters split over a cluster (distributed shared memory)
-    static size_t ccached = 0;
+    static SmemAttr ccached;
     rc = meta::set_smem(meta::fine_tune_cluster_kernel, smem, ccached);
     if (rc) return rc;
     if (C > 8) cudaFuncSetAttribute(meta::fine_tune_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -780,7 +777,7 @@ int kt_fine_tune(const kt_dims* dims, const float* theta, const float* u, const 
                                              (int)steps, alpha, theta_out, mse_out);
     KT_REQUIRE(e == cudaSuccess, KT_E_CUDA, "kt_fine_tune: cluster launch failed (%s)", cudaGetErrorString(e));
   } else {
-    static size_t cached = 0;
+    static SmemAttr cached;
     rc = meta::set_smem(meta::head_kernel, smem, cached);
     if (rc) return rc;
     meta::head_kernel<<<1, meta::NT, smem, as_stream(stream)>>>(*dims, h.RC, theta, nullptr, u, y, (int)n, steps,
@@ -812,7 +809,7 @@ int kt_maml_tasks(const kt_dims* dims, const float* theta, const float* u, const
   if (rc) return rc;
   const bool so = !first_order;
   const meta::Head h = meta::fit_rows(*dims, 8, true, so);
-  static size_t cached = 0;
+  static SmemAttr cached;
   const size_t smem = meta::task_smem(h, so);
   rc = meta::set_smem(meta::maml_task_kernel, smem, cached);
   if (rc) return rc;
@@ -843,7 +840,7 @@ int kt_maml_step(const kt_dims* dims, float* theta, const float* u, const float*
   if (rc) return rc;
   const bool so = !first_order;
   const meta::Head h = meta::fit_rows(*dims, 8, true, so);
-  static size_t cached = 0;
+  static SmemAttr cached;
   const size_t smem = meta::task_smem(h, so);
   rc = meta::set_smem(meta::maml_task_kernel, smem, cached);
   if (rc) return rc;

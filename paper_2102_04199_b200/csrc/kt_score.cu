@@ -430,7 +430,8 @@ extern "C" int kt_score_indices_fp32(const kt_spec_table* tab, const kt_dims* di
   KT_REQUIRE(B > 0, KT_E_EMPTY, "kt_score_indices: empty batch");
   KT_REQUIRE(default_dims(*dims), KT_E_UNSUPPORTED,
              "kt_score_indices: fused scorer needs F=12, gcn (32,32), head (64,64)");
-  static int grid_cap = 0;
+  static PerDeviceInt grid_caps;
+  int& grid_cap = grid_caps.get();
   const int smem = static_cast<int>(sizeof(score::Smem));
   if (!grid_cap) {
     cudaFuncSetAttribute(score::score_star_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -696,12 +696,9 @@ extern "C" int kt_score_indices_ex(const kt_spec_table* tab, const kt_dims* dims
   KT_REQUIRE(B > 0, KT_E_EMPTY, "kt_score_indices: empty batch");
   KT_REQUIRE(default_dims_tc(*dims), KT_E_UNSUPPORTED,
              "kt_score_indices: fused scorer needs F=12, gcn (32,32), head (64,64)");
-  static bool attr = false;
+  static SmemAttr attr;
   const int smem = static_cast<int>(sizeof(tcs::Smem));
-  if (!attr) {
-    cudaFuncSetAttribute(tcs::score_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  attr.ensure(tcs::score_tc_kernel, static_cast<size_t>(smem));
   const int64_t n_tiles = (B + tcs::GT - 1) / tcs::GT;
   const int grid = static_cast<int>(n_tiles < kNumSMs ? n_tiles : kNumSMs);
   tcs::score_tc_kernel<<<grid, tcs::NT, smem, as_stream(stream)>>>(

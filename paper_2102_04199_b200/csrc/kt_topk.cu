@@ -266,7 +266,8 @@ static int run(const Src& src_in, int k, int hist_ready, int64_t* top_idx, float
   unsigned int* hist3 = reinterpret_cast<unsigned int*>(static_cast<char*>(ws) + 64);
   unsigned long long* buf = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 64 + 3 * NB * 4);
   const size_t smem = static_cast<size_t>(CAP) * 8;
-  static int per_sm = 0;
+  static PerDeviceInt per_sms;
+  int& per_sm = per_sms.get();
   if (!per_sm) {
     cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel, NT, smem);

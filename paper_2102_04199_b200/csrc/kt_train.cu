@@ -309,11 +309,8 @@ int kt_grad(const kt_dims* dims, const float* params, const double* fmean, const
   const int D = train::row_stride(*dims);
   const size_t smem = sizeof(float) * train::WARPS * train::slab_floats(*dims, max_nodes, D);
   KT_REQUIRE(smem <= 220 * 1024, KT_E_UNSUPPORTED, "kt_grad: model/graph too large for shared memory");
-  static size_t smem_attr = 0;
-  if (smem > 48 * 1024 && smem > smem_attr) {
-    cudaFuncSetAttribute(train::pergraph_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    smem_attr = smem;
-  }
+  static SmemAttr smem_attr;
+  smem_attr.ensure(train::pergraph_kernel, smem);
   cudaStream_t st = as_stream(stream);
   const int P = dims->n_params;
   const int64_t chunk = train::chunk_of(B);
@@ -328,11 +325,8 @@ int kt_grad(const kt_dims* dims, const float* params, const double* fmean, const
     if (nb <= kNumSMs * 8 && !(getenv("KT_GRAD_WARP") && getenv("KT_GRAD_WARP")[0] == '1')) {
       // small batch: a CTA per graph (the warp form would leave most of the GPU idle)
       const size_t csm = sizeof(float) * train::slab_floats(*dims, max_nodes, D);
-      static size_t csm_attr = 0;
-      if (csm > 48 * 1024 && csm > csm_attr) {
-        cudaFuncSetAttribute(train::pergraph_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
-        csm_attr = csm;
-      }
+      static SmemAttr csm_attr;
+      csm_attr.ensure(train::pergraph_cta_kernel, csm);
       train::pergraph_cta_kernel<<<(int)nb, train::CT, csm, st>>>(
           *dims, params, fmean, fstd, feats, mask, node_ptr, nodes_per_graph, max_nodes, row_ptr, col, val,
           graph_idx, y, b0, nb, inv_b, head_only, D, pg, pg_sq);
@@ -379,11 +373,8 @@ int kt_pretrain_sgd(const kt_dims* dims, float* params, const double* fmean, con
   const int P4 = (dims->n_params + 3) & ~3;
   const size_t smem = sizeof(float) * (2 * P4 + train::slab_floats(*dims, max_nodes, D));
   KT_REQUIRE(smem <= 220 * 1024, KT_E_UNSUPPORTED, "kt_pretrain_sgd: model too large for shared memory");
-  static size_t smem_attr = 0;
-  if (smem > 48 * 1024 && smem > smem_attr) {
-    cudaFuncSetAttribute(train::pretrain_sgd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    smem_attr = smem;
-  }
+  static SmemAttr smem_attr;
+  smem_attr.ensure(train::pretrain_sgd_kernel, smem);
   train::pretrain_sgd_kernel<<<1, 256, smem, as_stream(stream)>>>(*dims, params, fmean, fstd, feats, mask, node_ptr,
                                                                    nodes_per_graph, max_nodes, row_ptr, col, val,
                                                                    order, y, n_steps, gamma, D);
