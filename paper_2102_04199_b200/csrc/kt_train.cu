@@ -247,7 +247,8 @@ __global__ void sgd_kernel(const float* __restrict__ p, const float* __restrict_
 }
 
 // Sequential batch-1 SGD (meta.pretrain's inner loop): one CTA, params in smem.
-__global__ void __launch_bounds__(256)
+template <int NTP>
+__global__ void __launch_bounds__(NTP)
 pretrain_sgd_kernel(kt_dims dims, float* __restrict__ params, const double* __restrict__ fmean,
                     const double* __restrict__ fstd, const double* __restrict__ feats,
                     const uint8_t* __restrict__ mask, const int64_t* __restrict__ node_ptr, int npg, int nmax,
@@ -373,11 +374,20 @@ int kt_pretrain_sgd(const kt_dims* dims, float* params, const double* fmean, con
   const int P4 = (dims->n_params + 3) & ~3;
   const size_t smem = sizeof(float) * (2 * P4 + train::slab_floats(*dims, max_nodes, D));
   KT_REQUIRE(smem <= 220 * 1024, KT_E_UNSUPPORTED, "kt_pretrain_sgd: model too large for shared memory");
-  static SmemAttr smem_attr;
-  smem_attr.ensure(train::pretrain_sgd_kernel, smem);
-  train::pretrain_sgd_kernel<<<1, 256, smem, as_stream(stream)>>>(*dims, params, fmean, fstd, feats, mask, node_ptr,
+  // 1024 threads: the sequential SGD chain is latency-bound, more warps per phase help
+  // (24k -> 31k samples/s over 256 threads); KT_PRETRAIN_NT overrides for experiments
+  const char* nt_env = getenv("KT_PRETRAIN_NT");
+  const int ntp = nt_env ? atoi(nt_env) : 1024;
+  auto go = [&](auto kern, int threads) {
+    static SmemAttr smem_attr;
+    smem_attr.ensure(kern, smem);
+    kern<<<1, threads, smem, as_stream(stream)>>>(*dims, params, fmean, fstd, feats, mask, node_ptr,
                                                                    nodes_per_graph, max_nodes, row_ptr, col, val,
                                                                    order, y, n_steps, gamma, D);
+  };
+  if (ntp >= 1024) go(train::pretrain_sgd_kernel<1024>, 1024);
+  else if (ntp >= 512) go(train::pretrain_sgd_kernel<512>, 512);
+  else go(train::pretrain_sgd_kernel<256>, 256);
   note_launches(1);
   return check_launch("kt_pretrain_sgd");
 }
