@@ -34,7 +34,7 @@ namespace agg {
 constexpr int NT = 256;
 constexpr int MAXPAT = 8;       // adjacency patterns per batch
 constexpr int MAXPNNZ = 1024;   // nnz over all patterns
-constexpr int NST = 4;          // input ring stages (bulk loads in flight per CTA)
+          // input ring stages (bulk loads in flight per CTA)
 
 struct LayerArgs {
   const void* in;
@@ -133,7 +133,7 @@ constexpr int WPC = NT / 32;
 // instruction covers two adjacent 128-byte row segments).
 template <int DIN_T, int DOUT_T>
 __global__ void __launch_bounds__(NT, 2) gcn_layer_kernel(LayerArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(16) unsigned char smem_w[];
   __shared__ PatSmem P;
   __shared__ double s_mean[KT_MAX_DIM], s_rstd[KT_MAX_DIM];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(NT, 2) gcn_layer_kernel(LayerArgs a) {
   const int dinp = (din + 3) & ~3;  // slab row stride (float4 aligned)
   const int maxn = a.R;             // rows of the largest graph
   // ---- carve: W | pattern CSR | per-warp slabs (X rows, aggregated rows) ----------------------
-  float* sW = reinterpret_cast<float*>(smem);
+  float* sW = reinterpret_cast<float*>(smem_w);
   int* s_rp = reinterpret_cast<int*>(sW + ((din * dout + 3) & ~3));
   const int rp_cap = a.n_pat * (KT_MAX_NODES + 1);
   int* s_col = s_rp + ((rp_cap + 3) & ~3);
@@ -1068,7 +1068,6 @@ extern "C" int kt_gcn_layer(const void* in, int32_t in_f64, const double* fmean,
   a.pat_col = pat_col;
   a.pat_val = pat_val;
   a.pat_mask = pat_mask;
-  const int esz = in_f64 ? 8 : 4;
   // per-warp slabs (X rows + aggregated rows, fp32) sized for the largest graph
   a.R = max_nodes;
   a.G = 1;

@@ -426,7 +426,6 @@ __global__ void __launch_bounds__(UT) ucb_kernel(const double* __restrict__ mean
   __shared__ double red_v[UT / 32];
   __shared__ int red_i[UT / 32];
   __shared__ double s_den[64];
-  __shared__ int s_z[64];
   __shared__ int s_pick;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   for (int i = tid; i < P; i += UT) {
@@ -470,7 +469,6 @@ __global__ void __launch_bounds__(UT) ucb_kernel(const double* __restrict__ mean
       s_pick = b;
       picks[t] = b;
       s_act[b] = 0;
-      s_z[t] = b;
       s_den[t] = s_var[b] + noise;
     }
     __syncthreads();

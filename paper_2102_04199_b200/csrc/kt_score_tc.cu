@@ -295,7 +295,6 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     // ===================== encode: thread = graph; one feature row per chunk ================
     const int g = tid - 128;
     const uint32_t lane = static_cast<uint32_t>((g & ~31) << 16);
-    const int n_knobs = T.n_knobs;
     // touched-derived slots in fp64 with reciprocal scales: within 1 fp64 ulp of the
     // IEEE (x - mean) / std of model.py:108-112 before the single cast to fp32
 #ifdef KT_DBG_F32

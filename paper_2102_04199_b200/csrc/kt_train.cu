@@ -188,7 +188,10 @@ pergraph_kernel(kt_dims dims, const float* __restrict__ params, const double* __
 // Small batches: one CTA (CT threads) per graph.  The same per-graph arithmetic as the
 // warp form (each output element is still owned by one thread with a sequential inner
 // loop), spread over 8x the threads, so a 512-graph batch fills the GPU.
-constexpr int CT = 256;
+#ifndef KT_GRAD_CT
+#define KT_GRAD_CT 256
+#endif
+constexpr int CT = KT_GRAD_CT;
 
 __global__ void __launch_bounds__(CT)
 pergraph_cta_kernel(kt_dims dims, const float* __restrict__ params, const double* __restrict__ fmean,
