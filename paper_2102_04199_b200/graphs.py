@@ -16,7 +16,6 @@ context slots, scatter into iterval rows -- and returns a device tensor.
 from __future__ import annotations
 
 import ctypes
-import math
 from dataclasses import dataclass
 
 import numpy as np
@@ -25,9 +24,7 @@ from .errors import DomainError
 from .kernels import (
     AXES_BY_OP,
     AXIS_ORDER,
-    MAX_AXES,
     MAX_KNOBS,
-    MAX_LOOPS,
     REDUCTION_AXES,
     KernelSpec,
     KnobConfig,

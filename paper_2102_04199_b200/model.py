@@ -20,7 +20,7 @@ All compute goes through libkerntune_b200.so; nothing here falls back to CPU.
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, field, replace
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
