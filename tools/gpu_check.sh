@@ -12,6 +12,12 @@ timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 echo "bench rc=$?" >> gpurun_out/bench.err
 timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 echo "ref rc=$?" >> gpurun_out/bench_ref.err
+# N>1 code path on a one-GPU box: two ranks sharing cuda:0 over gloo (correctness of the sharded
+# sweep / e2e / MAML paths, not a scaling number)
+KT_BENCH_SAME_DEVICE=1 KT_BENCH_BACKEND=gloo timeout 600 python -m torch.distributed.run --standalone \
+  --nproc-per-node 2 bench.py --gpus 2 --steps 20 --warmup 3 --no-cpu-baseline --meta-steps 20 \
+  > gpurun_out/bench_n2_gloo.json 2> gpurun_out/bench_n2_gloo.err
+echo "n2 rc=$?" >> gpurun_out/bench_n2_gloo.err
 if [ "${SKIP_NCU:-0}" != "1" ]; then
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-extras > gpurun_out/ncu_launches.log 2>&1
