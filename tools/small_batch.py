@@ -22,7 +22,8 @@ st = _lib.stream_handle()
 for B in (16, 128, 1024, 18944, 1 << 20):
     idx = torch.randint(0, space.size, (B,), device=dev)
     z = torch.empty(B, device=dev)
-    f = lambda: lib.kt_score_indices(tab.data_ptr(), d, flat.data_ptr(), idx.data_ptr(), 0, B, z.data_ptr(), None,
+    fn = lib.kt_score_indices_fp32 if os.environ.get("ENGINE") == "fp32" else lib.kt_score_indices
+    f = lambda: fn(tab.data_ptr(), d, flat.data_ptr(), idx.data_ptr(), 0, B, z.data_ptr(), None,
                                      err.data_ptr(), st)
     for _ in range(5):
         f()
