@@ -664,6 +664,12 @@ def run_ours(args):
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
+    # N > 1: step i's top-k exchange (all-gather of k x 12 B per rank) and merge overlap step
+    # i+1's scoring -- the gathers run asynchronously from a per-step copy of the rank's top-k,
+    # and step i's merge is enqueued after step i+1's kernels
+    pend = None
+    slots = [(torch.empty_like(sw.top_score), torch.empty_like(sw.top_idx),
+              torch.empty_like(gather_s), torch.empty_like(gather_i)) for _ in range(2)] if ws > 1 else None
     for i in range(args.steps):
         sl = pool[((i + args.warmup) % POOL_SLICES) * BATCH : ((i + args.warmup) % POOL_SLICES + 1) * BATCH]
         k0s[i].record()
@@ -671,9 +677,20 @@ def run_ours(args):
         k1s[i].record()
         sw.rank(BATCH, cur.cuda_stream)
         if ws > 1:
-            dist.all_gather_into_tensor(gather_s, sw.top_score)
-            dist.all_gather_into_tensor(gather_i, sw.top_idx)
-            ps.topk_merge(gather_s, gather_i, TOPK)
+            ts_i, ti_i, gs_i, gi_i = slots[i % 2]
+            ts_i.copy_(sw.top_score)
+            ti_i.copy_(sw.top_idx)
+            w = (dist.all_gather_into_tensor(gs_i, ts_i, async_op=True),
+                 dist.all_gather_into_tensor(gi_i, ti_i, async_op=True))
+            if pend is not None:
+                for wk in pend[0]:
+                    wk.wait()
+                ps.topk_merge(pend[1], pend[2], TOPK)
+            pend = (w, gs_i, gi_i)
+    if pend is not None:
+        for wk in pend[0]:
+            wk.wait()
+        ps.topk_merge(pend[1], pend[2], TOPK)
     t1.record()
     torch.cuda.synchronize()
     if ws > 1:
