@@ -167,8 +167,10 @@ def check(rc: int, what: str) -> None:
 
 
 def ptr(t) -> int | None:
-    """Device pointer of a torch tensor (None -> NULL)."""
-    return None if t is None else t.data_ptr()
+    """Device pointer of a torch tensor (None -> NULL; an int is already an address)."""
+    if t is None or isinstance(t, int):
+        return t
+    return t.data_ptr()
 
 
 def stream_handle(device=None) -> int:

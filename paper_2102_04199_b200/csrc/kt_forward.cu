@@ -45,6 +45,45 @@ embed_kernel(kt_dims dims, const float* __restrict__ params, const double* __res
   }
 }
 
+// Small batches (the single-graph API path, model.py:153-169): one CTA per graph so
+// each output element of a layer gets its own thread.  Same per-element operation
+// order as embed_kernel, so the two agree bit for bit.
+constexpr int CTA_THREADS = 256;
+
+__global__ void __launch_bounds__(CTA_THREADS)
+embed_cta_kernel(kt_dims dims, const float* __restrict__ params, const double* __restrict__ fmean,
+                 const double* __restrict__ fstd, const double* __restrict__ feats, const uint8_t* __restrict__ mask,
+                 const int64_t* __restrict__ node_ptr, int npg, int max_nodes, const int32_t* __restrict__ row_ptr,
+                 const int32_t* __restrict__ col, const float* __restrict__ val, const int64_t* __restrict__ gidx,
+                 int64_t B, int D, float* __restrict__ u_out, float* __restrict__ z_out) {
+  extern __shared__ __align__(16) float sm[];
+  float* A = sm;
+  float* Bf = A + max_nodes * D;
+  float* h0 = Bf + max_nodes * D;
+  float* h1 = h0 + 2 * KT_MAX_DIM;
+  const int dl = dims.gcn[dims.n_gcn];
+  const CtaGroup G{static_cast<int>(threadIdx.x), CTA_THREADS};
+  for (int64_t g = blockIdx.x; g < B; g += gridDim.x) {
+    const GraphView v = graph_view(gidx ? gidx[g] : g, node_ptr, npg, row_ptr, col, val, mask);
+    load_features(G, v, feats, dims.F, fmean, fstd, A, D);
+    G.sync();
+    for (int l = 0; l < dims.n_gcn; ++l) {
+      csr_aggregate(G, v, A, Bf, dims.gcn[l], D);
+      G.sync();
+      dense(G, Bf, params + dims.off_gcn[l], A, v.n, dims.gcn[l], dims.gcn[l + 1], D, true);
+      G.sync();
+    }
+    readout(G, A, v.n, dl, D, params + dims.off_agg, h0, static_cast<int*>(nullptr));
+    G.sync();
+    for (int c = G.r; c < 2 * dl; c += G.n) u_out[g * 2 * dl + c] = h0[c];
+    if (z_out) {
+      const float z = head_row(G, dims, params, h0, h1);
+      if (G.r == 0) z_out[g] = z;
+    }
+    G.sync();
+  }
+}
+
 __global__ void __launch_bounds__(WARPS * 32)
 head_kernel(kt_dims dims, const float* __restrict__ params, const float* __restrict__ u, int64_t B,
             float* __restrict__ z_out) {
@@ -96,6 +135,16 @@ int kt_embed_csr(const kt_dims* dims, const float* params, const double* fmean, 
   int D = dims->F;
   for (int i = 1; i <= dims->n_gcn; ++i) D = D > dims->gcn[i] ? D : dims->gcn[i];
   D = (D + 3) & ~3;
+  if (B <= kNumSMs) {
+    const size_t smem1 = sizeof(float) * (2 * max_nodes * D + 4 * KT_MAX_DIM);
+    static SmemAttr attr1;
+    attr1.ensure(fwd::embed_cta_kernel, smem1);
+    fwd::embed_cta_kernel<<<(int)B, fwd::CTA_THREADS, smem1, as_stream(stream)>>>(
+        *dims, params, fmean, fstd, feats, mask, node_ptr, nodes_per_graph, max_nodes, row_ptr, col, val, graph_idx,
+        B, D, u_out, z_out);
+    note_launches(1);
+    return check_launch("kt_embed_csr");
+  }
   const size_t smem = sizeof(float) * fwd::WARPS * (2 * max_nodes * D + 4 * KT_MAX_DIM);
   static SmemAttr attr;
   attr.ensure(fwd::embed_kernel, smem);

@@ -212,9 +212,10 @@ def feature_multiset(graph: CodeGraph) -> list:
 def normalized_adjacency(num_nodes: int, edges) -> np.ndarray:
     """D^-1/2 (A + I) D^-1/2 in fp64, same operation order as graphs.py:234-241."""
     a = np.zeros((num_nodes, num_nodes))
-    for s, d in edges:
-        a[s, d] = 1.0
-        a[d, s] = 1.0
+    if len(edges):
+        e = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
+        a[e[:, 0], e[:, 1]] = 1.0
+        a[e[:, 1], e[:, 0]] = 1.0
     a[np.diag_indices(num_nodes)] += 1.0
     dinv = 1.0 / np.sqrt(a.sum(axis=1))
     return a * dinv[:, None] * dinv[None, :]

@@ -19,6 +19,8 @@ All compute goes through libkerntune_b200.so; nothing here falls back to CPU.
 
 from __future__ import annotations
 
+import contextlib
+import functools
 import math
 from dataclasses import dataclass, field
 
@@ -82,8 +84,22 @@ class Gradients:
 # --- layout of the flat parameter vector ---------------------------------------------
 
 
+_NULL_CTX = contextlib.nullcontext()
+
+
+def _on(dev):
+    """torch.cuda.device(dev), skipped when dev already is the current device."""
+    if dev.index is None or dev.index == torch.cuda.current_device():
+        return _NULL_CTX
+    return torch.cuda.device(dev)
+
+
 def make_dims(feature_dim: int, gcn_dims, head_hidden) -> _lib.Dims:
-    gcn_dims, head_hidden = tuple(gcn_dims), tuple(head_hidden)
+    return _make_dims(int(feature_dim), tuple(int(v) for v in gcn_dims), tuple(int(v) for v in head_hidden))
+
+
+@functools.lru_cache(maxsize=64)
+def _make_dims(feature_dim: int, gcn_dims: tuple, head_hidden: tuple) -> _lib.Dims:
     if not gcn_dims or len(gcn_dims) > _lib.KT_MAX_LAYERS or len(head_hidden) + 1 > _lib.KT_MAX_LAYERS + 1:
         raise DomainError("model depth beyond the compiled limits")
     d = _lib.Dims()
@@ -362,10 +378,81 @@ def pack_graphs(graphs, dev) -> PackedGraphs:
     row_ptr = np.zeros(node_ptr[-1] + 1, dtype=np.int64)
     np.add.at(row_ptr, rows + 1, 1)
     row_ptr = np.cumsum(row_ptr)
-    up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)
-    return PackedGraphs(up(feats, np.float64), up(mask, np.uint8), up(node_ptr, np.int64),
-                        up(row_ptr, np.int32), up(cols, np.int32), up(vals, np.float32),
-                        int(sizes.max()), len(graphs))
+    # one staging buffer, one H2D copy, typed device views carved at 16-byte offsets
+    parts = [(feats, np.float64), (mask, np.uint8), (node_ptr, np.int64),
+             (row_ptr, np.int32), (cols, np.int32), (vals, np.float32)]
+    offs, off = [], 0
+    for a, dt in parts:
+        offs.append(off)
+        off += (a.size * np.dtype(dt).itemsize + 15) // 16 * 16
+    host = np.empty(max(off, 16), dtype=np.uint8)
+    for (a, dt), o in zip(parts, offs):
+        n = a.size * np.dtype(dt).itemsize
+        host[o:o + n] = np.ascontiguousarray(a, dtype=dt).reshape(-1).view(np.uint8)
+    buf = torch.from_numpy(host).to(dev)
+    views = []
+    for (a, dt), o in zip(parts, offs):
+        n = a.size * np.dtype(dt).itemsize
+        views.append(buf[o:o + n].view(_TORCH_DT[np.dtype(dt)]).view(a.shape))
+    return PackedGraphs(*views, int(sizes.max()), len(graphs))
+
+
+_TORCH_DT = {np.dtype(np.float64): torch.float64, np.dtype(np.uint8): torch.uint8,
+             np.dtype(np.int64): torch.int64, np.dtype(np.int32): torch.int32,
+             np.dtype(np.float32): torch.float32}
+
+
+class _PackedOne:
+    """One graph packed in a single device buffer; fields are device addresses
+    (embed_graphs only passes pointers), `buf` keeps the allocation alive."""
+    __slots__ = ("buf", "feats", "mask", "node_ptr", "row_ptr", "col", "val", "max_nodes", "n_graphs")
+
+
+def _packed_one(graph, dev):
+    """Device pack of one graph, memoised on the graph object per device (the
+    single-graph API path: embed / forward / predict_gflops).  Same arrays as
+    pack_graphs([graph]), built without the batch concatenations and uploaded
+    with one copy."""
+    key = str(dev)
+    memo = getattr(graph, "_kt_packed", None)
+    if memo is not None and memo[0] == key:
+        return memo[1]
+    t = tensors_for(graph)
+    x, adj = t.feature_matrix, t.normalized_adjacency
+    n = x.shape[0]
+    if n > _lib.KT_MAX_NODES:
+        raise DomainError(f"graph with {n} nodes exceeds the device limit {_lib.KT_MAX_NODES}")
+    if x.shape[1] != FEATURE_DIM:
+        raise DomainError("feature width mismatch")
+    nzm = adj != 0
+    _, c = np.nonzero(nzm)
+    nnz = c.size
+    a16 = lambda b: (b + 15) // 16 * 16
+    o_mask = a16(x.size * 8)
+    o_np = o_mask + a16(n)
+    o_rp = o_np + 16
+    o_col = o_rp + a16((n + 1) * 4)
+    o_val = o_col + a16(nnz * 4)
+    host = np.empty(o_val + a16(nnz * 4), dtype=np.uint8)
+    host[:x.size * 8].view(np.float64)[:] = x.reshape(-1)
+    host[o_mask:o_mask + n] = t.feature_mask
+    host[o_np:o_np + 16].view(np.int64)[:] = (0, n)
+    rp = host[o_rp:o_rp + (n + 1) * 4].view(np.int32)
+    rp[0] = 0
+    np.cumsum(np.count_nonzero(nzm, axis=1), out=rp[1:])
+    host[o_col:o_col + nnz * 4].view(np.int32)[:] = c
+    host[o_val:o_val + nnz * 4].view(np.float32)[:] = adj[nzm]
+    pk = _PackedOne()
+    pk.buf = torch.from_numpy(host).to(dev)
+    base = pk.buf.data_ptr()
+    pk.feats, pk.mask, pk.node_ptr = base, base + o_mask, base + o_np
+    pk.row_ptr, pk.col, pk.val = base + o_rp, base + o_col, base + o_val
+    pk.max_nodes, pk.n_graphs = n, 1
+    try:
+        graph._kt_packed = (key, pk)
+    except AttributeError:
+        pass
+    return pk
 
 
 # --- batched forward ----------------------------------------------------------------------
@@ -394,7 +481,7 @@ def embed_batch(m: ModelState, feats, mask, adj) -> torch.Tensor:
     d = dims_of(m)
     u = torch.empty((b, 2 * d.gcn[d.n_gcn]), dtype=torch.float32, device=dev)
     lib = _lib.load()
-    with torch.cuda.device(dev):
+    with _on(dev):
         _lib.check(lib.kt_embed_csr(d, _lib.ptr(flat), _lib.ptr(mean), _lib.ptr(std), _lib.ptr(x),
                                     _lib.ptr(mk), None, n, n, _lib.ptr(rp), _lib.ptr(col), _lib.ptr(val), None, b,
                                     _lib.ptr(u), None, _lib.stream_handle()), "embed_batch")
@@ -413,7 +500,7 @@ def head_forward_batch(u, head: HeadParams) -> torch.Tensor:
         raise DomainError("empty batch")
     z = torch.empty(uu.shape[0], dtype=torch.float32, device=dev)
     lib = _lib.load()
-    with torch.cuda.device(dev):
+    with _on(dev):
         _lib.check(lib.kt_head_forward(head_only_dims(shapes), _lib.ptr(vec), _lib.ptr(uu), uu.shape[0],
                                        _lib.ptr(z), _lib.stream_handle()), "head_forward_batch")
     return z
@@ -423,13 +510,13 @@ def embed_graphs(m: ModelState, graphs, with_scores: bool = False):
     """Embeddings (and optionally scores) of a list of CodeGraphs of any sizes."""
     flat = flat_params(m)
     dev = flat.device
-    pk = pack_graphs(graphs, dev)
+    pk = _packed_one(graphs[0], dev) if len(graphs) == 1 else pack_graphs(graphs, dev)
     mean, std = _norm_tensors(m, dev)
     d = dims_of(m)
     u = torch.empty((pk.n_graphs, 2 * d.gcn[d.n_gcn]), dtype=torch.float32, device=dev)
     z = torch.empty(pk.n_graphs, dtype=torch.float32, device=dev) if with_scores else None
     lib = _lib.load()
-    with torch.cuda.device(dev):
+    with _on(dev):
         _lib.check(lib.kt_embed_csr(d, _lib.ptr(flat), _lib.ptr(mean), _lib.ptr(std), _lib.ptr(pk.feats),
                                     _lib.ptr(pk.mask), _lib.ptr(pk.node_ptr), 0, pk.max_nodes,
                                     _lib.ptr(pk.row_ptr), _lib.ptr(pk.col), _lib.ptr(pk.val), None, pk.n_graphs,
@@ -506,7 +593,7 @@ def _gcn_layers(m: ModelState, x64: torch.Tensor, n_graphs: int, n_uniform: int,
             raise DomainError(f"GCN input width {h.shape[1]} != weight rows {d_in}")
         out = torch.empty((rows, d_out), dtype=torch.float32, device=dev)
         wc = w.contiguous()
-        with torch.cuda.device(dev):
+        with _on(dev):
             _lib.check(lib.kt_gcn_layer(_lib.ptr(h), int(i == 0), _lib.ptr(mean), _lib.ptr(std), _lib.ptr(wc),
                                         d_in, d_out, 1, n_graphs, n_uniform, _lib.ptr(node_ptr), _lib.ptr(pat_id),
                                         pats.n_pat, _lib.ptr(pats.pat_n), _lib.ptr(pats.rp), _lib.ptr(pats.col),
@@ -580,7 +667,7 @@ def aggregate_batch(h, agg: AggParams, node_ptr=None) -> torch.Tensor:
             raise DomainError("empty batch")
     u = torch.empty((b, 2 * d), dtype=torch.float32, device=dev)
     lib = _lib.load()
-    with torch.cuda.device(dev):
+    with _on(dev):
         _lib.check(lib.kt_readout(_lib.ptr(hh), d, b, n, _lib.ptr(np_t), _lib.ptr(w.contiguous()), _lib.ptr(u),
                                   _lib.stream_handle()), "aggregate_batch")
     return u
@@ -669,7 +756,7 @@ def _grad_packed(m: ModelState, pk: PackedGraphs, y: torch.Tensor, scope: str, g
     g = torch.empty_like(flat)
     loss = torch.empty(1, dtype=torch.float64, device=dev)
     new = torch.empty_like(flat) if lr is not None else None
-    with torch.cuda.device(dev):
+    with _on(dev):
         _lib.check(lib.kt_grad(d, _lib.ptr(flat), _lib.ptr(mean), _lib.ptr(std), _lib.ptr(pk.feats),
                                _lib.ptr(pk.mask), None if npg else _lib.ptr(pk.node_ptr), npg, pk.max_nodes,
                                _lib.ptr(pk.row_ptr), _lib.ptr(pk.col), _lib.ptr(pk.val), _lib.ptr(graph_idx),
@@ -758,7 +845,7 @@ def head_loss_grad(vec, like: HeadParams, u, y):
     g = torch.empty_like(v)
     mse = torch.empty(1, dtype=torch.float32, device=dev)
     lib = _lib.load()
-    with torch.cuda.device(dev):
+    with _on(dev):
         _lib.check(lib.kt_head_loss_grad(d, _lib.ptr(v), _lib.ptr(uu), _lib.ptr(yy), uu.shape[0], _lib.ptr(g),
                                          _lib.ptr(mse), _lib.stream_handle()), "head_loss_grad")
     return float(mse.item()), g
@@ -776,7 +863,7 @@ def head_hvp(vec, like: HeadParams, u, y, v) -> torch.Tensor:
     yy = _dev_vec(y, dev)
     out = torch.empty_like(th)
     lib = _lib.load()
-    with torch.cuda.device(dev):
+    with _on(dev):
         _lib.check(lib.kt_head_hvp(d, _lib.ptr(th), _lib.ptr(uu), _lib.ptr(yy), _lib.ptr(vv), uu.shape[0],
                                    _lib.ptr(out), _lib.stream_handle()), "head_hvp")
     return out

@@ -197,6 +197,23 @@ def test_embed_graphs_mixed_sizes_matches_reference(cuda_device, g_encode, g_mod
     assert math.isclose(pm.forward(graphs[3], m), float(g_model["mixed/z"][3]), rel_tol=1e-4, abs_tol=1e-5)
 
 
+def test_embed_graphs_small_and_large_batch_paths_agree(cuda_device, g_encode, g_model):
+    """kt_embed_csr runs one CTA per graph for B <= 148 (single-graph API) and one warp
+    per graph above; both keep the per-element operation order, so bit-identical."""
+    m = device_model(g_model)
+    spec = spec_of(g_encode, OPS[0])
+    space = pk.build_knob_space(spec)
+    graphs = [pg.config_graph(spec, pk.index_config(space, int(i)), space, template=TEMPLATE)
+              for i in range(0, 300 * 7, 7)]
+    u_big, z_big = pm.embed_graphs(m, graphs, with_scores=True)
+    u_small, z_small = pm.embed_graphs(m, graphs[:100], with_scores=True)
+    assert torch.equal(u_big[:100], u_small) and torch.equal(z_big[:100], z_small)
+    for i in (0, 57, 299):
+        u1, z1 = pm.embed_graphs(m, [graphs[i]], with_scores=True)
+        assert torch.equal(u1[0], u_big[i]) and torch.equal(z1[0], z_big[i])
+        assert pm.forward(graphs[i], m) == float(z_big[i])
+
+
 def test_raw_segmented_batch_vs_oracle(cuda_device, g_model, g_meta):
     """Raw graphs of 17/21/25 nodes in one segmented CSR batch."""
     m = device_model(g_model)
