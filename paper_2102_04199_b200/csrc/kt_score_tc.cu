@@ -136,7 +136,7 @@ template <int N, int K>
 __device__ __forceinline__ void load_operand(OperandRegs<N, K>& r, const float* W, int K_src, int tid) {
 #pragma unroll
   for (int i = 0; i < OperandRegs<N, K>::IT; ++i) {
-    const int e = tid + i * NT, n = e / K, k = e - n * K;
+    const int e = tid + i * NT, k = e / N, n = e - k * N;  // n fastest: coalesced rows of W
     r.v[i] = e < N * K && k < K_src ? __ldg(W + k * N + n) : 0.0f;
   }
 }
@@ -146,7 +146,7 @@ __device__ __forceinline__ void store_operand(const OperandRegs<N, K>& r, float*
   const float* v = r.v;
 #pragma unroll
   for (int i = 0; i < IT; ++i) {
-    const int e = tid + i * NT, n = e / K, k = e - n * K;
+    const int e = tid + i * NT, k = e / N, n = e - k * N;
     if (e < N * K) {
       const float h = tf32_hi(v[i]);
       const int off = kmajor_offset(n, k, K) >> 2;

@@ -34,4 +34,10 @@ for B in (16, 128, 1024, 18944, 1 << 20):
         f()
     e1.record()
     torch.cuda.synchronize()
-    print(f"B={B:8d}  {1e3 * e0.elapsed_time(e1) / 50:9.1f} us per launch")
+    import time
+    t0 = time.perf_counter()
+    for _ in range(50):
+        f()
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    print(f"B={B:8d}  {1e3 * e0.elapsed_time(e1) / 50:9.1f} us per launch  host us {(t1 - t0) / 50 * 1e6:.1f}")
