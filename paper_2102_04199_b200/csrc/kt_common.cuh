@@ -46,6 +46,31 @@ struct SmemAttr {
     }
   }
 };
+// ---- programmatic dependent launch (PDL).  A kernel launched with launch_pdl may start
+// while the previous kernel in the stream is still running (once every CTA of that one
+// has called pdl_launch_dependents or exited); it must call pdl_wait() before touching
+// any memory an earlier kernel writes or reads.  Outside PDL both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+bool pdl_enabled();  // false when KT_NO_PDL is set (A/B switch)
+
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 struct PerDeviceInt {
   int v[kMaxDevices] = {};
   int& get() { return v[current_device()]; }

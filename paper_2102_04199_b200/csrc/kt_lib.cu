@@ -3,6 +3,8 @@
 #include <cstdarg>
 #include <cstdio>
 
+#include <cstdlib>
+
 #include "kt_common.cuh"
 
 namespace kt {
@@ -25,6 +27,11 @@ int fail(int code, const char* fmt, ...) {
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
   return code;
+}
+
+bool pdl_enabled() {
+  static const bool on = std::getenv("KT_NO_PDL") == nullptr;
+  return on;
 }
 
 int check_launch(const char* what) {

@@ -12,12 +12,17 @@
 
 namespace kt {
 namespace sa {
+// Each step is propose -> scorer -> accept, all three launched as programmatic
+// dependents: a kernel's launch (and the scorer's table prologue) overlaps the
+// previous kernel, and pdl_wait() orders every global access after it.
 
 __global__ void propose_kernel(const int32_t* __restrict__ cur, int n_chains, int n_knobs,
                                const int32_t* __restrict__ cards, const int64_t* __restrict__ mult,
                                const int32_t* __restrict__ knob, const uint8_t* __restrict__ nudge,
                                const int32_t* __restrict__ delta, const int32_t* __restrict__ resample,
                                int32_t* __restrict__ nxt, int64_t* __restrict__ nxt_idx) {
+  pdl_launch_dependents();  // the scorer may start its prologue now
+  pdl_wait();               // cur / nxt: the previous accept
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n_chains) return;
   const int kn = knob[c];
@@ -38,6 +43,8 @@ __global__ void propose_kernel(const int32_t* __restrict__ cur, int n_chains, in
 __global__ void accept_kernel(int n_chains, int n_knobs, const float* __restrict__ e_new,
                               const double* __restrict__ u, double temp, const int32_t* __restrict__ nxt,
                               int32_t* __restrict__ cur, double* __restrict__ energy) {
+  pdl_launch_dependents();
+  pdl_wait();  // e_new: the scorer
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n_chains) return;
   const double en = static_cast<double>(e_new[c]);
@@ -61,8 +68,10 @@ extern "C" int kt_sa_propose(const int32_t* cur, int32_t n_chains, int32_t n_kno
              "kt_sa_propose: null pointer");
   KT_REQUIRE(n_chains > 0, KT_E_EMPTY, "kt_sa_propose: no chains");
   KT_REQUIRE(n_knobs > 0 && n_knobs <= KT_MAX_KNOBS, KT_E_SHAPE, "kt_sa_propose: 1..%d knobs", KT_MAX_KNOBS);
-  kt::sa::propose_kernel<<<(n_chains + 127) / 128, 128, 0, kt::as_stream(stream)>>>(
-      cur, n_chains, n_knobs, cards, mult, knob, nudge, delta, resample, nxt, nxt_idx);
+  const cudaError_t e = kt::launch_pdl(kt::sa::propose_kernel, dim3((n_chains + 127) / 128), dim3(128), 0,
+                                       kt::as_stream(stream), cur, n_chains, n_knobs, cards, mult, knob, nudge,
+                                       delta, resample, nxt, nxt_idx);
+  KT_REQUIRE(e == cudaSuccess, KT_E_CUDA, "kt_sa_propose: %s", cudaGetErrorString(e));
   kt::note_launches(1);
   return kt::check_launch("kt_sa_propose");
 }
@@ -72,8 +81,9 @@ extern "C" int kt_sa_accept(int32_t n_chains, int32_t n_knobs, const float* e_ne
   KT_REQUIRE(e_new && u && nxt && cur && energy, KT_E_ARG, "kt_sa_accept: null pointer");
   KT_REQUIRE(n_chains > 0, KT_E_EMPTY, "kt_sa_accept: no chains");
   KT_REQUIRE(temp > 0.0, KT_E_RANGE, "kt_sa_accept: temperature must be positive");
-  kt::sa::accept_kernel<<<(n_chains + 127) / 128, 128, 0, kt::as_stream(stream)>>>(n_chains, n_knobs, e_new, u,
-                                                                                   temp, nxt, cur, energy);
+  const cudaError_t e = kt::launch_pdl(kt::sa::accept_kernel, dim3((n_chains + 127) / 128), dim3(128), 0,
+                                       kt::as_stream(stream), n_chains, n_knobs, e_new, u, temp, nxt, cur, energy);
+  KT_REQUIRE(e == cudaSuccess, KT_E_CUDA, "kt_sa_accept: %s", cudaGetErrorString(e));
   kt::note_launches(1);
   return kt::check_launch("kt_sa_accept");
 }

@@ -284,6 +284,10 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
   __syncthreads();
   tc_fence_after();
   if (threadIdx.x == 0) TRACE(28, 0);  // prologue done
+  // PDL: the prologue above reads only the constant tables and parameters; indices,
+  // outputs and key_hist belong to the stream order from here on.
+  pdl_wait();
+  pdl_launch_dependents();
   const uint32_t tmem = S.tmem_base;
   const int64_t n_tiles = (B + GT - 1) / GT;
   const int64_t my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -700,9 +704,11 @@ extern "C" int kt_score_indices_ex(const kt_spec_table* tab, const kt_dims* dims
   attr.ensure(tcs::score_tc_kernel, static_cast<size_t>(smem));
   const int64_t n_tiles = (B + tcs::GT - 1) / tcs::GT;
   const int grid = static_cast<int>(n_tiles < kNumSMs ? n_tiles : kNumSMs);
-  tcs::score_tc_kernel<<<grid, tcs::NT, smem, as_stream(stream)>>>(
-      tab, *dims, params, idx, idx32, idx_base, B, z_out, u_out, reinterpret_cast<unsigned long long*>(keys_out),
-      keys_out ? key_hist : nullptr, err_flag);
+  const cudaError_t e =
+      launch_pdl(tcs::score_tc_kernel, dim3(grid), dim3(tcs::NT), static_cast<size_t>(smem), as_stream(stream), tab,
+                 *dims, params, idx, idx32, idx_base, B, z_out, u_out,
+                 reinterpret_cast<unsigned long long*>(keys_out), keys_out ? key_hist : nullptr, err_flag);
+  KT_REQUIRE(e == cudaSuccess, KT_E_CUDA, "kt_score_indices: %s", cudaGetErrorString(e));
   note_launches(1);
   return check_launch("kt_score_indices");
 }
