@@ -517,6 +517,8 @@ maml_task_kernel(kt_dims dims, int rc, const float* __restrict__ theta, TaskSet 
                  int inner_steps, int first_order, float* __restrict__ theta_ws, float* __restrict__ g_out,
                  float* __restrict__ loss_out) {
   extern __shared__ __align__(16) float sm[];
+  pdl_launch_dependents();  // task_sum may launch now and wait for this grid
+  pdl_wait();               // theta: the previous step's update
   const Head h = head_of(dims, rc);
   const int P4 = (h.P + 3) & ~3;
   float* th = sm;             // current theta_k
@@ -568,6 +570,8 @@ maml_task_kernel(kt_dims dims, int rc, const float* __restrict__ theta, TaskSet 
 __global__ void task_sum_kernel(const float* __restrict__ g, int T, int P, float* __restrict__ sum_out,
                                 const float* __restrict__ losses, double* __restrict__ stats, float beta = 0.0f,
                                 float* __restrict__ theta = nullptr) {
+  pdl_launch_dependents();
+  pdl_wait();  // g / losses: the task kernel (PDL launch in kt_maml_step)
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p < P) {
     double s = 0.0;
@@ -849,10 +853,14 @@ int kt_maml_step(const kt_dims* dims, float* theta, const float* u, const float*
   float* thws = losses + 2 * T;
   meta::TaskSet ts{u, y, s_off, s_idx, q_off, q_idx};
   cudaStream_t st = as_stream(stream);
-  meta::maml_task_kernel<<<T, meta::NT, smem, st>>>(*dims, h.RC, theta, ts, T, alpha, inner_steps, first_order,
-                                                    thws, g, losses);
+  // both launched as programmatic dependents (PDL): each kernel's launch overlaps its predecessor
+  cudaError_t e = launch_pdl(meta::maml_task_kernel, dim3(T), dim3(meta::NT), smem, st, *dims, h.RC, theta, ts, T,
+                             alpha, inner_steps, first_order, thws, g, losses);
+  KT_REQUIRE(e == cudaSuccess, KT_E_CUDA, "kt_maml_step: %s", cudaGetErrorString(e));
   // task sum (fixed order, fp64) and the outer update in one pass over the parameters
-  meta::task_sum_kernel<<<(h.P + 255) / 256, 256, 0, st>>>(g, T, h.P, g_sum, losses, stats, beta, theta);
+  e = launch_pdl(meta::task_sum_kernel, dim3((h.P + 255) / 256), dim3(256), 0, st, g, T, h.P, g_sum, losses, stats,
+                 beta, theta);
+  KT_REQUIRE(e == cudaSuccess, KT_E_CUDA, "kt_maml_step: %s", cudaGetErrorString(e));
   note_launches(2);
   return check_launch("kt_maml_step");
 }
