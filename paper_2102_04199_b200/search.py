@@ -593,8 +593,8 @@ def gp_fit(s: GpSurrogate, select_lengthscale: bool = True) -> GpSurrogate:
             best = c
     Lb = L[best]
     dev_state = {"x": xd, "ls": lsd[best].contiguous(), "L": Lb, "alpha": alpha[best]}
-    # the factor is column-major on the device: its transpose is the row-major lower L
-    return replace(s, lengthscales=cands[best].copy(), chol=Lb.t().contiguous().cpu().numpy(),
+    # the factor is column-major on the device: its host copy's transpose view is the lower L
+    return replace(s, lengthscales=cands[best].copy(), chol=Lb.cpu().numpy().T,
                    alpha=alpha[best].cpu().numpy(), fitted_noise=float(inf[best, 0]), _dev=dev_state)
 
 
