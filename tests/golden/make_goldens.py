@@ -26,6 +26,11 @@ Everything is keyed by `rng_from` so reruns are byte-identical.  Outputs:
   gp.npz         GP surrogate (search.py:39-159): gp_fit with lengthscale selection and
                  jitter escalation, gp_predict_many, _gp_posterior_cov and
                  bo_propose_batch picks, on synthetic observations in knob coordinates
+  baseline.npz   the BASELINE.json configs through the reference: C1 predict 4,096 (raw,
+                 super: z, u, top-512), C5 262,144-candidate sweep (z, top-512), C2 grad +
+                 sgd_step at batch 512 mixed ops, raw and super, kink-free and unfiltered
+  metatrain.npz  meta_train (meta.py:260-268): theta and CSV log, FO 6 steps / SO 3 steps
+  rng.npz        raw rng_from streams for a set of keys (util.py:51-55)
   dataset.npz    on that dataset: dataset_norms (meta.py:81-101) of the raw and the
                  augmented dataset_samples (harness.py:179-192), their labels and
                  kernel classes, grad (model.py:218) of an index-picked raw batch,
@@ -369,6 +374,200 @@ def ckpt_golden():
     rm.save_model(m, os.path.join(OUT, "ckpt_v1.npz"))
 
 
+# --- BASELINE.json configs (C1 / C2 / C5) and meta_train ------------------------------
+
+BENCH_OPS = ("conv2d", "winograd", "depthwise")
+C5_N = 262_144
+KINK_MARGIN_FP32 = 1e-5  # fp32-safe margin for the acceptance-01 kink filter (see baseline_goldens)
+
+
+def fp32_exact(a):
+    """Round to fp32 and back: the device model holds fp32 weights, so the reference is run
+    on the same (fp32-representable) parameters and only the arithmetic differs."""
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+def bench_model_ref():
+    """bench.py bench_model(), in the reference: init_model(rng_from("bench-model")) with
+    feature norms of 3 x 4,096 encoded rows from rng_from("bench-norms", op) and the
+    conftest-corpus label norm; weights rounded to fp32."""
+    m = rm.init_model(rng_from("bench-model"))
+    tmpl = rg.build_super_template(rk.OP_TYPES)
+    rows = []
+    for op in BENCH_OPS:
+        spec = rk.KernelSpec(op, 56, 64, 64, 3, 3, 1)
+        space = rk.build_knob_space(spec)
+        lay = rg.batch_layout(spec, tmpl)
+        idx = rng_from("bench-norms", op).integers(0, space.size, 4096)
+        x = rg.encode_batch(spec, space, [rk.index_config(space, int(i)) for i in idx], lay)
+        rows.append(x[:, lay.iterval_rows, :].reshape(-1, 12))
+    st = np.concatenate(rows)
+    sd = st.std(axis=0)
+    m = replace(m, feature_norm=rm.FeatureNorm(st.mean(axis=0), np.where(sd < 1e-12, 1.0, sd)),
+                label_norm=rm.LabelNorm(-5.62, 7.08))
+    return replace(
+        m,
+        gcn=rm.GcnParams(layers=[fp32_exact(w) for w in m.gcn.layers]),
+        agg=rm.AggParams(sum_weights=fp32_exact(m.agg.sum_weights)),
+        head=rm.HeadParams(weights=[fp32_exact(w) for w in m.head.weights],
+                           biases=[fp32_exact(b) for b in m.head.biases]))
+
+
+def unique_rows(a):
+    """Compress tie-heavy arrays: unique rows + inverse (random conv2d configs collapse to a
+    few hundred distinct encoded graphs)."""
+    a = np.ascontiguousarray(a)
+    flat = a.reshape(a.shape[0], -1)
+    uniq, inv = np.unique(flat, axis=0, return_inverse=True)
+    return uniq.reshape((-1,) + a.shape[1:]), inv.astype(np.int32).ravel()
+
+
+def score_ref(m, spec, space, idx, tmpl, chunk=4096):
+    lay = rg.batch_layout(spec, tmpl)
+    us, zs = [], []
+    for s in range(0, len(idx), chunk):
+        cfgs = [rk.index_config(space, int(i)) for i in idx[s:s + chunk]]
+        x = rg.encode_batch(spec, space, cfgs, lay)
+        u = rm.embed_batch(m, x, lay.feature_mask, lay.adjacency)
+        us.append(u)
+        zs.append(rm.head_forward_batch(u, m.head))
+    return np.concatenate(us), np.concatenate(zs)
+
+
+def sweep_indices(n, size):
+    """n distinct indices from rng_from("sweep", 0) (the bench's rank-0 pool), first
+    occurrences kept: rank_history takes a dict, so a candidate appears once."""
+    rng = rng_from("sweep", 0)
+    out, seen = [], set()
+    while len(out) < n:
+        for v in rng.integers(0, size, n - len(out)):
+            if int(v) not in seen:
+                seen.add(int(v))
+                out.append(int(v))
+    return np.array(out, dtype=np.int64)
+
+
+def grad_flat(g):
+    return np.concatenate([a.ravel() for a in list(g.gcn) + [g.agg] + [
+        t for w, b in zip(g.head_weights, g.head_biases) for t in (w, b)]])
+
+
+def baseline_goldens():
+    """baseline.npz: the BASELINE.json configs run through the reference itself.
+
+    C1  predict 4,096 conv2d (sample_configs(space, 4096, rng_from("bench-cfgs"))), raw and
+        super: z, u (unique rows + inverse) and rank_history top-512 (search.py:257-264).
+    C5  262,144 distinct sweep indices from rng_from("sweep", 0), super: z (unique values +
+        inverse) and the top-512; the test regenerates the indices (checksum stored).
+    C2  grad (model.py:218) + sgd_step (model.py:288, gamma 0.005) on 512 mixed
+        conv2d/winograd/depthwise graphs (171 sampled configs per op, truncated to 512),
+        super and raw (N = 25/25/21, segmented), labels measure(platform-A) floored at 1e-3
+        (meta.py:81 convention), restricted to kink-free graphs: acceptance test 01's
+        _kink_free (pkg/tests/test_acceptance.py:84-122) with its margin lowered from the
+        finite-difference 5e-4 to 1e-5 -- far above fp32 rounding of O(1) pre-activations, so
+        no ReLU/max-routing decision can differ between fp32 and fp64; plus the same batch
+        without the filter (norm-wise bar only).
+    The model is bench.py's bench_model() with weights rounded to fp32."""
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    import test_acceptance as ta
+
+    ta._KINK_MARGIN = KINK_MARGIN_FP32
+    m = bench_model_ref()
+    tmpl = rg.build_super_template(rk.OP_TYPES)
+    out = {f"p/{k}": v for k, v in model_params(m).items()}
+    spec = BENCH_SPEC
+    space = rk.build_knob_space(spec)
+    # C1
+    cfgs = rk.sample_configs(space, 4096, rng_from("bench-cfgs"))
+    idx = np.array([rk.config_index(space, c) for c in cfgs], dtype=np.int64)
+    out["c1/idx"] = idx
+    for rep, t in (("raw", None), ("super", tmpl)):
+        u, z = score_ref(m, spec, space, idx, t)
+        out[f"c1/{rep}/z"] = z
+        out[f"c1/{rep}/u_uniq"], out[f"c1/{rep}/u_inv"] = unique_rows(u)
+        out[f"c1/{rep}/top"] = np.array(rs.rank_history(dict(zip(idx.tolist(), z.tolist())), set(), 512))
+    # C5
+    idx5 = sweep_indices(C5_N, space.size)
+    _, z5 = score_ref(m, spec, space, idx5, tmpl)
+    out["c5/idx_sum"] = np.array([idx5.sum(), (idx5 * np.arange(C5_N)).sum() % (1 << 61)], dtype=np.int64)
+    out["c5/n"] = np.array(C5_N)
+    out["c5/z_uniq"], out["c5/z_inv"] = unique_rows(z5[:, None])
+    out["c5/top"] = np.array(rs.rank_history(dict(zip(idx5.tolist(), z5.tolist())), set(), 512))
+    # C2
+    prof = get_profile("platform-A")
+    pool = []
+    for op in BENCH_OPS:
+        s = rk.KernelSpec(op, 56, 64, 64, 3, 3, 1)
+        sp = rk.build_knob_space(s)
+        for c in rk.sample_configs(sp, 4 * 171, rng_from("bench-c2", op)):
+            pool.append((op, s, sp, c))
+    for rep, t in (("raw", None), ("super", tmpl)):
+        plain, kf = [], []
+        for j, (op, s, sp, c) in enumerate(pool):
+            y = max(measure(s, c, prof, sp).gflops, 1e-3)
+            g = rg.config_graph(s, c, sp, template=t)
+            per_op_plain = sum(1 for q in plain if q[0] == op)
+            if per_op_plain < 171:
+                plain.append((op, rk.config_index(sp, c), y, g))
+            if sum(1 for q in kf if q[0] == op) < 171 and ta._kink_free(m, [(g, y)]):
+                kf.append((op, rk.config_index(sp, c), y, g))
+        for tag, items in (("plain", plain[:512]), ("kf", kf[:512])):
+            assert len(items) == 512, (rep, tag, len(items))
+            batch = [(g, y) for _, _, y, g in items]
+            loss, g = rm.grad(m, batch, "all")
+            key = f"c2/{rep}/{tag}"
+            out[f"{key}/op"] = np.array([BENCH_OPS.index(o) for o, _, _, _ in items], dtype=np.int64)
+            out[f"{key}/idx"] = np.array([i for _, i, _, _ in items], dtype=np.int64)
+            out[f"{key}/label"] = np.array([y for _, _, y, _ in items])
+            out[f"{key}/loss"] = np.array(loss)
+            out[f"{key}/grad"] = grad_flat(g)
+            m2 = rm.sgd_step(m, g, 0.005)
+            out[f"{key}/sgd"] = flat_theta(m2)
+    np.savez_compressed(os.path.join(OUT, "baseline.npz"), **out)
+
+
+def metatrain_goldens(items, m):
+    """meta_train (meta.py:260-268): sampling + meta_step + the CSV log, FO 6 steps and SO 3
+    steps, 3-way 2-shot, 32 tasks, on the golden corpus (super graphs)."""
+    import tempfile
+
+    template = rg.build_super_template(rk.OP_TYPES)
+    samples = [rmeta.LabeledSample(rg.config_graph(s, c, sp, template=template), s.signature(), y)
+               for s, sp, c, y in items]
+    out = {}
+    for order, fo, steps in (("fo", True, 6), ("so", False, 3)):
+        cfg = rmeta.MetaConfig(n_way=3, k_shot=2, meta_batch=32, inner_steps=1, outer_steps=steps,
+                               first_order=fo)
+        with tempfile.TemporaryDirectory() as d:
+            path = os.path.join(d, "log.csv")
+            m2 = rmeta.meta_train(m, samples, cfg, rng_from("golden-metatrain", order), path)
+            with open(path, encoding="utf-8") as f:
+                out[f"{order}/csv"] = np.frombuffer(f.read().encode(), dtype=np.uint8)
+        out[f"{order}/theta"] = rm.head_to_vec(m2.head)
+        out[f"{order}/steps"] = np.array(steps)
+    np.savez_compressed(os.path.join(OUT, "metatrain.npz"), **out)
+
+
+RNG_KEYS = (("golden-model",), ("sweep", 0), ("sweep", 7), ("metatrain", "super", 0), ("x", 1, 2.5, (1, "a"), True),
+            ("bench-cfgs",), ("", -3, 1e-300))
+
+
+def rng_goldens():
+    """rng.npz: raw stream bytes of the reference's rng_from (util.py:51-55) for a set of
+    keys (str / int / float / tuple / bool parts): the product's rng_from must reproduce
+    them byte for byte, since every seeded input (configs, tasks, init) flows from it."""
+    from kerntune.util import stable_digest
+
+    out = {}
+    for j, key in enumerate(RNG_KEYS):
+        g = rng_from(*key)
+        out[f"k{j}/digest"] = np.frombuffer(stable_digest(*key).encode(), dtype=np.uint8)
+        out[f"k{j}/raw"] = g.bit_generator.random_raw(16)
+        out[f"k{j}/ints"] = g.integers(0, 451_584_000, 8)
+        out[f"k{j}/normal"] = g.normal(size=4)
+    np.savez_compressed(os.path.join(OUT, "rng.npz"), **out)
+
+
 def main():
     if sys.argv[1:] == ["ckpt"]:
         ckpt_golden()
@@ -382,6 +581,21 @@ def main():
     if sys.argv[1:] == ["dataset"]:
         dataset_goldens()
         return
+    if sys.argv[1:] == ["rng"]:
+        rng_goldens()
+        return
+    if sys.argv[1:] == ["baseline"]:
+        baseline_goldens()
+        return
+    if sys.argv[1:] == ["metatrain"]:
+        items = corpus()
+        template = rg.build_super_template(rk.OP_TYPES)
+        samples = [rmeta.LabeledSample(rg.config_graph(s, c, sp, template=template), s.signature(), y)
+                   for s, sp, c, y in items]
+        fn, ln = rmeta.dataset_norms(samples)
+        m = replace(rm.init_model(rng_from("golden-model")), feature_norm=fn, label_norm=ln)
+        metatrain_goldens(items, m)
+        return
     golden_graph_text()
     encode_goldens()
     items = corpus()
@@ -394,6 +608,9 @@ def main():
     dataset_goldens()
     gp_goldens()
     ckpt_golden()
+    baseline_goldens()
+    metatrain_goldens(items, m)
+    rng_goldens()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))
 

@@ -2,8 +2,8 @@
 
 Tolerances (fp32 device vs fp64 reference; SURVEY.md 7 hard part 1):
   * gradients: per-tensor norm-wise rel <= 1e-4, and element-wise rel <= 1e-4
-    above an absolute floor of 1e-4 * max|g| (batch-sum cancellation leaves a few
-    tiny entries with larger relative error);
+    for every entry above an absolute floor of 1e-3 * max|g| of its tensor (fp32
+    batch-sum cancellation bounds the relative error of the smaller entries);
   * parameters after updates: element-wise rel <= 1e-5 (floor 1e-7);
   * losses: rel <= 1e-5.
 """
@@ -32,10 +32,10 @@ def assert_grad_close(got, want, rtol=1e-4):
         assert np.abs(got).max() == 0
         return
     assert np.linalg.norm(got - want) <= rtol * scale, f"norm-wise rel {np.linalg.norm(got - want) / scale:.2e}"
-    floor = 1e-4 * np.abs(want).max()
+    floor = 1e-3 * np.abs(want).max()
     big = np.abs(want) > floor
     rel = np.abs(got[big] - want[big]) / np.abs(want[big])
-    assert rel.max() <= rtol * 10, f"element-wise rel {rel.max():.2e}"
+    assert rel.max() <= rtol, f"element-wise rel {rel.max():.2e}"
 
 
 def assert_params_close(got, want, rtol=1e-5):
@@ -253,6 +253,40 @@ def test_meta_trainer_graph_replay_equals_eager(cuda_device, g_model, super_samp
     assert torch.equal(pm.flat_params(rep.model()), pm.flat_params(eager.model()))
     assert torch.equal(bufs2["stats"], bufs["stats"])
 
+
+
+def _parse_log(text):
+    lines = text.strip().split("\n")
+    rows = [ln.split(",") for ln in lines[1:]]
+    return lines[0], np.array([int(r[0]) for r in rows]), np.array([[float(r[1]), float(r[2])] for r in rows])
+
+
+@pytest.mark.parametrize("order", ["fo", "so"])
+def test_meta_train_matches_reference_run(cuda_device, g_model, super_samples, tmp_path, order):
+    """meta_train (meta.py:260-268) pinned to a reference run: sample_meta_tasks draws from
+    rng_from("golden-metatrain", order), meta_step per outer step, the CSV log
+    (tests/golden/metatrain.npz).  Both meta_train and the device-resident MetaTrainer."""
+    from paper_2102_04199_b200.util import rng_from
+    from tests.conftest import load_golden
+
+    g = load_golden("metatrain")
+    steps = int(g[f"{order}/steps"])
+    head, ref_steps, ref_losses = _parse_log(g[f"{order}/csv"].tobytes().decode())
+    m = device_model(g_model)
+    cfg = pmeta.MetaConfig(n_way=3, k_shot=2, meta_batch=32, inner_steps=1, outer_steps=steps,
+                           first_order=order == "fo")
+    log = tmp_path / "log.csv"
+    m2 = pmeta.meta_train(m, super_samples, cfg, rng_from("golden-metatrain", order), log)
+    h2, st2, l2 = _parse_log(log.read_text())
+    assert h2 == head == "step,support_loss,query_loss"
+    assert np.array_equal(st2, ref_steps)
+    np.testing.assert_allclose(l2, ref_losses, rtol=1e-5)
+    assert_params_close(pm.head_to_vec(m2.head).cpu().numpy(), g[f"{order}/theta"])
+    tr = pmeta.MetaTrainer(m, super_samples, cfg)
+    plan = tr.plan(rng_from("golden-metatrain", order), steps)
+    bufs = tr.run(plan)
+    np.testing.assert_allclose(tr.stats(plan, bufs), ref_losses, rtol=1e-5)
+    assert_params_close(pm.head_to_vec(tr.model().head).cpu().numpy(), g[f"{order}/theta"])
 
 
 def test_checkpoint_interchange_with_reference(cuda_device, tmp_path):

@@ -192,11 +192,105 @@ def test_oracle_rank_history(g_rank):
     assert top == [int(v) for v in g_rank["top"]]
 
 
-def test_rng_from_matches_reference_stream(g_model):
-    # init_model draws through rng_from("golden-model"); equal draws => equal stream
-    from paper_2102_04199_b200.util import rng_from, stable_digest
+RNG_KEYS = (("golden-model",), ("sweep", 0), ("sweep", 7), ("metatrain", "super", 0), ("x", 1, 2.5, (1, "a"), True),
+            ("bench-cfgs",), ("", -3, 1e-300))
 
-    assert stable_digest("x", 1, 2.5, (1, "a"), True) == stable_digest("x", 1, 2.5, (1, "a"), True)
-    a = rng_from("golden-model").uniform(size=4)
-    b = rng_from("golden-model").uniform(size=4)
-    assert a.tobytes() == b.tobytes()
+
+@pytest.mark.parametrize("j", range(len(RNG_KEYS)))
+def test_rng_from_matches_reference_stream(j):
+    """Byte golden of the reference's rng_from streams (util.py:17-55; tests/golden/rng.npz)."""
+    from paper_2102_04199_b200.util import rng_from, stable_digest
+    from tests.conftest import load_golden
+
+    g = load_golden("rng")
+    key = RNG_KEYS[j]
+    assert stable_digest(*key).encode() == g[f"k{j}/digest"].tobytes()
+    r = rng_from(*key)
+    assert r.bit_generator.random_raw(16).tobytes() == g[f"k{j}/raw"].tobytes()
+    assert r.integers(0, 451_584_000, 8).tobytes() == g[f"k{j}/ints"].tobytes()
+    assert r.normal(size=4).tobytes() == g[f"k{j}/normal"].tobytes()
+
+
+# --- BASELINE.json configs (tests/golden/baseline.npz) ----------------------------------
+
+
+@pytest.fixture(scope="module")
+def g_base():
+    from tests.conftest import load_golden
+
+    return load_golden("baseline")
+
+
+def _bench_conv2d(idx, rep):
+    ext = ko.extents("conv2d", 56, 64, 64, 3, 3, 1)
+    knobs = ko.knob_lists("conv2d", ext)
+    adj, rows, mask = ko.layout("conv2d", rep == "super")
+    ch = ko.decode([len(v) for _, v in knobs], idx)
+    return ko.encode("conv2d", ext, knobs, ch, adj.shape[0], rows), adj, mask
+
+
+@pytest.mark.parametrize("rep", ["raw", "super"])
+def test_oracle_c1_scores_and_ranking_match_reference(g_base, rep):
+    from tests._shared import expand_unique, rank_parity
+
+    p = oracle_params(g_base)
+    idx = g_base["c1/idx"]
+    x, adj, mask = _bench_conv2d(idx, rep)
+    u = ko.embed_batch(p, x, mask, adj)
+    np.testing.assert_allclose(u, expand_unique(g_base, f"c1/{rep}/u"), rtol=1e-12, atol=1e-12)
+    z = ko.head_forward_batch(u, p["head_w"], p["head_b"])
+    np.testing.assert_allclose(z, g_base[f"c1/{rep}/z"], rtol=1e-12, atol=1e-12)
+    top = ko.rank_history(idx, z, set(), 512)
+    assert top == g_base[f"c1/{rep}/top"].tolist()
+    assert rank_parity(top, g_base[f"c1/{rep}/top"], idx, g_base[f"c1/{rep}/z"])["exact"]
+
+
+def test_c5_indices_regenerate_from_rng(g_base):
+    from paper_2102_04199_b200.kernels import KernelSpec, build_knob_space
+    from tests._shared import sweep_indices
+
+    n = int(g_base["c5/n"])
+    idx = sweep_indices(n, build_knob_space(KernelSpec("conv2d", 56, 64, 64, 3, 3, 1)).size)
+    assert len(np.unique(idx)) == n
+    assert idx.sum() == g_base["c5/idx_sum"][0]
+    assert (idx * np.arange(n)).sum() % (1 << 61) == g_base["c5/idx_sum"][1]
+    assert set(g_base["c5/top"].tolist()) <= set(idx.tolist())
+
+
+def test_oracle_c2_grad_matches_reference(g_base):
+    """Batch-512 mixed-op super gradient (kink-free set) through the oracle."""
+    from paper_2102_04199_b200.kernels import OP_TYPES
+
+    p = oracle_params(g_base)
+    key = "c2/super/kf"
+    trip = []
+    for op_i, i in zip(g_base[f"{key}/op"], g_base[f"{key}/idx"]):
+        op = ("conv2d", "winograd", "depthwise")[int(op_i)]
+        assert op in OP_TYPES
+        ext = ko.extents(op, 56, 64, 64, 3, 3, 1)
+        knobs = ko.knob_lists(op, ext)
+        adj, rows, mask = ko.layout(op, True)
+        ch = ko.decode([len(v) for _, v in knobs], np.array([i]))
+        trip.append((ko.encode(op, ext, knobs, ch, adj.shape[0], rows)[0], adj, mask))
+    loss, g = ko.grad(p, trip, g_base[f"{key}/label"].tolist())
+    assert abs(loss - float(g_base[f"{key}/loss"])) <= 1e-12 * loss
+    flat = np.concatenate([a.ravel() for a in g["gcn"] + [g["agg"]] + [
+        t for w, b in zip(g["head_w"], g["head_b"]) for t in (w, b)]])
+    np.testing.assert_allclose(flat, g_base[f"{key}/grad"], rtol=1e-9, atol=1e-13)
+
+
+def test_rank_parity_helper():
+    from tests._shared import rank_parity
+
+    idx = np.arange(10)
+    z = np.array([5.0, 5.0, 4.0, 3.0, 3.0 + 1e-7, 2.0, 1.0, 1.0, 0.5, 0.0])
+    ref = ko.rank_history(idx, z, set(), 5)
+    assert ref == [0, 1, 2, 4, 3]
+    assert rank_parity(ref, ref, idx, z) == {"exact": True, "hard_flips": 0, "tie_flips": 0, "near_flips": 0,
+                                            "max_flip_gap": 0.0}
+    r = rank_parity([0, 1, 2, 3, 4], ref, idx, z)  # near tie (gap 1e-7 < 1e-5 * 3)
+    assert not r["exact"] and r["hard_flips"] == 0 and r["near_flips"] == 1
+    r = rank_parity([1, 0, 2, 4, 3], ref, idx, z)  # exact-tie class out of index order
+    assert r["hard_flips"] == 0 and r["tie_flips"] == 1 and r["near_flips"] == 0
+    r = rank_parity([0, 1, 4, 3, 5], ref, idx, z)  # dropped 2 (score 4) for 5 (score 2)
+    assert r["hard_flips"] >= 3
