@@ -537,7 +537,98 @@ def bench_gp(n=512, pool=512, batch=16, reps=10, cpu_reps=3):
                       "host cores"}
 
 
-# --- CPU arms -------------------------------------------------------------------------# --- CPU arms -------------------------------------------------------------------------
+def cpu_secondary(m, corpus_c2, corpus, reps=9):
+    """the reference path of C2 / C3 / C4 timed on this box's host cores
+    (oracle port, fp64 numpy, single-threaded BLAS per process), 1 process and P processes,
+    min / median over `reps` repetitions -- on the same batch / tasks / rows as the GPU
+    numbers (C2: the first 512-graph batch of rng_from("bench-pretrain"); C3: the first
+    32-task batch of rng_from("metatrain", "super", 0); C4: the 64 corpus rows)."""
+    from oracle import cpu_baseline as cb
+    from oracle import kt_oracle as ko
+    from paper_2102_04199_b200 import meta as pmeta
+    from paper_2102_04199_b200 import model as pm
+    from paper_2102_04199_b200.util import rng_from
+
+    p = oracle_params(m)
+
+    def trip(s):
+        sp = s.spec
+        return cb.graph_triple(sp.op_type, (sp.input_size, sp.in_channels, sp.out_channels, sp.kernel_size,
+                                            sp.stride, sp.padding), int(s.index), True)
+
+    out = {"host": cb.host_info()}
+    pick = rng_from("bench-pretrain").choice(len(corpus_c2), 512, replace=False)
+    graphs = [trip(corpus_c2[int(i)]) for i in pick]
+    labels = [corpus_c2[int(i)].label_gflops for i in pick]
+    out["c2"] = cb.time_secondary("c2", p, (graphs, labels), reps=reps)
+    shapes = [w.shape for w in p["head_w"]]
+    theta = ko.head_to_vec(p["head_w"], p["head_b"])
+    for order, fo in (("c3_fo", True), ("c3_so", False)):
+        cfg = pmeta.MetaConfig(n_way=3, k_shot=2, meta_batch=32, inner_steps=1, first_order=fo)
+        tasks = []
+        for t in pmeta.sample_meta_tasks(corpus, cfg, rng_from("metatrain", "super", 0)):
+            tasks.append(([trip(s) for s in t.support], np.array([ko.normalize_label(p, s.label_gflops)
+                                                                  for s in t.support]),
+                          [trip(s) for s in t.query], np.array([ko.normalize_label(p, s.label_gflops)
+                                                                for s in t.query])))
+        out[order] = cb.time_secondary("c3", p, (tasks, shapes, 0.01, fo, theta), reps=reps)
+    u, y = pmeta._embedded(m, corpus[:64])
+    out["c4"] = cb.time_fine_tune(theta, shapes, u.double().cpu().numpy(), y.double().cpu().numpy(), reps=reps)
+    return out
+
+
+def _beside(gpu_ms, cpu):
+    """GPU step time beside the 1-process / P-process CPU medians."""
+    r = {k: v for k, v in cpu.items()}
+    for k, v in cpu.items():
+        r[f"speedup_vs_{k}_median"] = v["median_ms"] / gpu_ms
+    return r
+
+
+def bench_parity(dev):
+    """Parity of the measured path against the reference, on the box: the C5 fixture
+    (tests/golden/baseline.npz, made by running the reference: 262,144 distinct sweep
+    candidates, fp64 scores and rank_history top-512) scored through the same Sweeper
+    the timed loop uses.  max_rel_gflops = max |2^((z - z_ref) sigma_y) - 1|;
+    rank_flips = candidate pairs the device top-512 orders differently from the
+    reference after tie-class canonicalisation (tests/parity_tools.rank_parity)."""
+    import torch
+
+    from paper_2102_04199_b200 import graphs as pg
+    from paper_2102_04199_b200 import kernels as pk
+    from paper_2102_04199_b200 import model as pm
+    from paper_2102_04199_b200 import search as ps
+    from tests.parity_tools import expand_unique, rank_parity, sweep_indices
+
+    with np.load(os.path.join(ROOT, "tests", "golden", "baseline.npz")) as z:
+        g = {k: z[k] for k in z.files}
+
+    class NS:
+        def __init__(self, **kw):
+            self.__dict__.update(kw)
+
+    ref = NS(gcn=NS(layers=[g["p/gcn0"], g["p/gcn1"]]), agg=NS(sum_weights=g["p/agg"]),
+             head=NS(weights=[g[f"p/hw{i}"] for i in range(3)], biases=[g[f"p/hb{i}"] for i in range(3)]),
+             feature_norm=NS(mean=g["p/fmean"], std=g["p/fstd"]),
+             label_norm=NS(mean=float(g["p/lnorm"][0]), std=float(g["p/lnorm"][1])))
+    m = pm.from_reference(ref, device=dev)
+    spec = pk.KernelSpec(*SPEC_ARGS)
+    space = pk.build_knob_space(spec)
+    n = int(g["c5/n"])
+    idx = sweep_indices(n, space.size)
+    sw = ps.Sweeper(m, spec, space, pg.batch_layout(spec, pg.build_super_template(pk.OP_TYPES)), n, k=TOPK)
+    ti, _ = sw.run_device(torch.from_numpy(idx).to(dev))
+    zz = sw.z[:n].double().cpu().numpy()
+    z_ref = expand_unique(g, "c5/z")[:, 0]
+    rel = float(np.abs(np.exp2((zz - z_ref) * m.label_norm.std) - 1.0).max())
+    r = rank_parity(ti.cpu().tolist(), g["c5/top"], idx, z_ref)
+    return {"max_rel_gflops": rel, "rank_flips": r["hard_flips"] + r["tie_flips"],
+            "near_tie_flips": r["near_flips"], "top512_equal": r["exact"],
+            "sample": f"C5 fixture: {n} distinct rng_from('sweep', 0) candidates, reference fp64 scores and "
+                      "rank_history top-512 (tests/golden/baseline.npz, generated by running the reference)"}
+
+
+# --- CPU arms -------------------------------------------------------------------------
 
 
 def cpu_sweep(m_params, n, seed_rank=0):
@@ -787,6 +878,8 @@ def run_ours(args):
     }
     if cpu:
         line["cpu_baseline"] = cpu
+    if rank == 0:
+        line["parity"] = bench_parity(dev)
     if not args.no_extras:
         from paper_2102_04199_b200 import meta as pmeta
         from paper_2102_04199_b200 import model as pm
@@ -796,6 +889,7 @@ def run_ours(args):
         fn, ln = pmeta.dataset_norms(corpus)  # meta.py:81-101 over the corpus, as pretrain does
         m = pm.model_from_flat(m._flat, m, feature_norm=fn, label_norm=ln)
         line["maml"] = bench_maml(m, corpus, args.meta_steps, 10)
+        line["maml_tasks_per_s"] = line["maml"]["value"]  # the metric's second half, compact
         if ws > 1:  # weak form: 32 tasks per GPU per outer step (one all-reduce per step either way)
             line["maml_weak"] = bench_maml(m, corpus, args.meta_steps, 10, tasks_per_step=32 * ws)
         if ws == 1:
@@ -803,12 +897,36 @@ def run_ours(args):
             line["pretrain"] = bench_pretrain_step(m, synthetic_corpus(entries, ("conv2d", "winograd", "depthwise")),
                                                    50, 5)
             line["fine_tune"] = bench_fine_tune(m, corpus)
+            if not args.no_cpu_baseline:
+                cs = cpu_secondary(m, synthetic_corpus(entries, ("conv2d", "winograd", "depthwise")), corpus)
+                line["cpu_host"] = cs["host"]
+                line["pretrain"]["cpu"] = _beside(line["pretrain"]["ms_per_step"], cs["c2"])
+                line["maml"]["cpu"] = _beside(line["maml"]["ms_per_step"], cs["c3_fo"])
+                line["maml_so"]["cpu"] = _beside(line["maml_so"]["ms_per_step"], cs["c3_so"])
+                line["fine_tune"]["cpu"] = _beside(line["fine_tune"]["value"], cs["c4"])
             line["aggregation"] = bench_aggregate(m)
             line["sa_explore"] = bench_sa(m)
             line["dataset"] = bench_dataset(entries)
             line["gp"] = bench_gp()
             line["predict"] = bench_predict(m)
     if rank == 0:
+        # compact summary last (the end of the line is what a truncated log keeps)
+        summ = {"graphs_per_s": value, "e2e_graphs_per_s": e2e["value"], "score_kernel_ms": kern_ms,
+                "roofline_frac": achieved / peak}
+        if "maml" in line:
+            summ["maml_fo_tasks_per_s"] = line["maml"]["value"]
+        if "maml_so" in line:
+            summ["maml_so_tasks_per_s"] = line["maml_so"]["value"]
+        if "pretrain" in line:
+            summ["pretrain_ms"] = line["pretrain"]["ms_per_step"]
+        if "fine_tune" in line:
+            summ["fine_tune_ms"] = line["fine_tune"]["value"]
+        if "aggregation" in line:
+            summ["aggregation_hbm_frac"] = [round(v["frac"], 3) for v in line["aggregation"]["kernels"].values()]
+        for k in ("maml_tasks_per_s", "parity"):
+            if k in line:
+                line[k] = line.pop(k)
+        line["summary"] = summ
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
