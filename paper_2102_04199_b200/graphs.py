@@ -16,6 +16,7 @@ context slots, scatter into iterval rows -- and returns a device tensor.
 from __future__ import annotations
 
 import ctypes
+import operator
 from dataclasses import dataclass
 
 import numpy as np
@@ -24,6 +25,7 @@ from .errors import DomainError
 from .kernels import (
     AXES_BY_OP,
     AXIS_ORDER,
+    KEY_SHIFT,
     MAX_KNOBS,
     REDUCTION_AXES,
     KernelSpec,
@@ -31,6 +33,7 @@ from .kernels import (
     KnobSpace,
     axis_extents,
     build_knob_space,
+    card_code,
     knob_value_map,
     resolved_tiles,
 )
@@ -445,9 +448,25 @@ def device_spec_table(spec, space, layout, fmean=None, fstd=None, device=None):
     return buf
 
 
+_KEY_OF = operator.attrgetter("_kt_key")
+
+
 def configs_to_indices(space: KnobSpace, configs) -> np.ndarray:
-    """Vectorised config_index over list[KnobConfig] (validated on the host)."""
-    cards = np.array(space.cardinalities, dtype=np.int64)
+    """Vectorised config_index over list[KnobConfig] (validated on the host).
+
+    Fast path: configs made by index_config (sample_configs, draw_unvisited picks, the SA /
+    BO proposers) carry their index keyed to the cardinalities (kernels.KnobConfig), so a
+    list converts with one pass over int attributes; anything else is re-encoded."""
+    n = len(configs)
+    cards_t = space.cardinalities
+    if n and space.size < (1 << KEY_SHIFT):
+        try:
+            keys = np.fromiter(map(_KEY_OF, configs), dtype=np.int64, count=n)
+        except AttributeError:
+            keys = None
+        if keys is not None and ((keys >> KEY_SHIFT) == card_code(cards_t)).all():
+            return keys & ((1 << KEY_SHIFT) - 1)
+    cards = np.array(cards_t, dtype=np.int64)
     ch = np.array([c.choices for c in configs], dtype=np.int64).reshape(len(configs), -1)
     if ch.shape[1] != len(cards):
         raise DomainError(f"config has {ch.shape[1]} choices, space has {len(cards)} knobs")

@@ -106,6 +106,26 @@ class KnobConfig:
         if any(c < 0 for c in self.choices):
             raise DomainError("negative choice index")
 
+    def __getstate__(self):
+        # the cached index key (see index_config) is process-local: never pickled or copied
+        return {"choices": self.choices}
+
+
+# Configs made by index_config carry their index, keyed to the knob cardinalities it was
+# decoded with: `_kt_key = index | code << KEY_SHIFT`, code a process-local number per
+# cardinality tuple (the mixed-radix index depends on nothing else).  The predictor seam
+# (graphs.configs_to_indices) then turns a list of 4,096 configs into indices with one
+# pass over int attributes instead of re-encoding 8 choices per config.
+KEY_SHIFT = 40
+_CARD_CODES: dict = {}
+
+
+def card_code(cards: tuple) -> int:
+    code = _CARD_CODES.get(cards)
+    if code is None:
+        code = _CARD_CODES[cards] = len(_CARD_CODES) + 1
+    return code
+
 
 def _conv_out(s: KernelSpec) -> int:
     return max((s.input_size + 2 * s.padding - s.kernel_size) // s.stride + 1, 1)
@@ -201,11 +221,15 @@ def index_config(space: KnobSpace, i: int) -> KnobConfig:
     """Inverse of config_index (kernels.py:278-286)."""
     if not 0 <= i < space.size:
         raise DomainError(f"index {i} out of range for space of size {space.size}")
-    digits = []
-    for card in reversed(space.cardinalities):
+    cards = space.cardinalities
+    key, digits = i, []
+    for card in reversed(cards):
         i, r = divmod(i, card)
         digits.append(r)
-    return KnobConfig(tuple(reversed(digits)))
+    cfg = KnobConfig(tuple(reversed(digits)))
+    if key < (1 << KEY_SHIFT):
+        object.__setattr__(cfg, "_kt_key", key | card_code(cards) << KEY_SHIFT)
+    return cfg
 
 
 def sample_configs(space: KnobSpace, n: int, rng) -> list:

@@ -155,6 +155,12 @@ def topk(scores: torch.Tensor, k: int, idx: torch.Tensor | None = None, *, base:
     b = scores.numel()
     if b == 0:
         raise DomainError("empty candidate set")
+    # the device keys pack the candidate index into 32 bits (score desc, index asc)
+    if idx is None:
+        if base < 0 or base + b > 2**32:
+            raise DomainError("topk ranks candidate indices below 2^32")
+    elif idx.dtype == torch.int64 and b and (int(idx.max()) >= 2**32 or int(idx.min()) < 0):
+        raise DomainError("topk ranks candidate indices below 2^32")
     vis = None
     if visited:
         vis = torch.from_numpy(np.array(sorted(int(v) for v in visited), dtype=np.int64)).to(dev)
@@ -224,7 +230,8 @@ class Sweeper:
         self.h_top_score = torch.empty((2, k), dtype=torch.float32, pin_memory=True)
         self.ev_slot = [torch.cuda.Event(), torch.cuda.Event()]
         self._next_slot = 0
-        self._pending = [None, None]
+        self._pending = [None, None]  # per slot: (ticket, n) of the step in flight
+        self._tickets = 0
         self._p = dict(tab=self.tab.data_ptr(), flat=self.flat.data_ptr(), err=self.err.data_ptr(),
                        ws=self.ws.data_ptr(), ti=self.top_idx.data_ptr(), ts=self.top_score.data_ptr(),
                        z=self.z.data_ptr(), keys=self.keys.data_ptr(),
@@ -283,8 +290,8 @@ class Sweeper:
         if not idx_host.is_pinned():
             raise DomainError("run_host needs pinned host indices (torch pin_memory)")
         slot = self._next_slot
-        if self._pending[slot] is not None:  # that slot's previous step must be consumed first
-            self.wait(slot)
+        if self._pending[slot] is not None:
+            raise DomainError("two sweep steps already in flight: wait() for the older one first")
         comp = torch.cuda.current_stream(self.dev)
         p = self._p
         _lib.check(self.lib.kt_sweep_host(p["tab"], self.dims, p["flat"], idx_host.data_ptr(),
@@ -293,20 +300,23 @@ class Sweeper:
                                           self.h_top_score[slot].data_ptr(), p["ws"], self.ws_bytes, p["err"],
                                           comp.cuda_stream), "sweep (host)")
         self.ev_slot[slot].record(comp)
-        self._pending[slot] = n
+        self._tickets += 1
+        self._pending[slot] = (self._tickets, n)
         self._next_slot ^= 1
-        return slot
+        return self._tickets
 
     def wait(self, ticket: int, check: bool = True):
-        """Results of a submitted step: (host scores, host top-k idx, top-k scores)."""
-        n = self._pending[ticket]
-        if n is None:
-            raise DomainError("no step in flight for this ticket")
-        self.ev_slot[ticket].synchronize()
-        self._pending[ticket] = None
+        """Results of a submitted step: (host scores, host top-k idx, top-k scores).  The
+        views stay valid until the step submitted after the next one reuses the slot."""
+        slot = next((i for i, p in enumerate(self._pending) if p is not None and p[0] == ticket), None)
+        if slot is None:
+            raise DomainError(f"no step in flight for ticket {ticket} (already consumed or never submitted)")
+        n = self._pending[slot][1]
+        self.ev_slot[slot].synchronize()
+        self._pending[slot] = None
         if check and int(self.err.item()):
             raise DomainError("config index out of range for the knob space")
-        return self.h_z[ticket, :n], self.h_top_idx[ticket], self.h_top_score[ticket]
+        return self.h_z[slot, :n], self.h_top_idx[slot], self.h_top_score[slot]
 
     def run_host(self, idx_host: torch.Tensor, check: bool = True):
         """End to end, synchronously: submit + wait."""
@@ -382,6 +392,7 @@ class DeviceAnnealer:
         if not _default_model(m) or space.size >= 2**32:
             raise DomainError("device annealing needs the default model dims and a space < 2^32")
         self.pred, self.sched, self.n = predictor, sched, n_chains
+        self.m = m
         self.lib = _lib.load()
         self.flat = flat_params(m)
         dev = self.dev = self.flat.device
@@ -477,19 +488,61 @@ class DeviceAnnealer:
 _ANNEALERS: dict = {}
 
 
+def _sa_explore_host(predict, space: KnobSpace, sched: SaSchedule, starts: list, rng) -> dict:
+    """The annealing loop on the host for an arbitrary `predict(list[KnobConfig])` callable
+    (search.py:202-254; e.g. the reference tune's xgb_energy, search.py:560): the same
+    Generator calls in the same order and the same acceptance rule as the device
+    annealer, so a shared seed and predictor give the same history."""
+    from .kernels import index_config
+
+    cards = np.array(space.cardinalities, dtype=np.int64)
+    mult = _space_multipliers(space)
+    n = len(starts)
+    rows = np.arange(n)
+    cur = np.array([index_config(space, i).choices for i in starts], dtype=np.int64).reshape(n, -1)
+
+    def score(mat):
+        idx = mat @ mult
+        e = np.asarray(predict([index_config(space, int(i)) for i in idx]), dtype=np.float64)
+        for i, v in zip(idx.tolist(), e.tolist()):
+            history[i] = v
+        return e
+
+    history: dict = {}
+    energy = score(cur)
+    temp = sched.initial_temp
+    for _ in range(sched.steps_per_round):
+        knob = rng.integers(0, len(cards), size=n)
+        nudge = rng.random(n) < 0.5
+        delta = rng.integers(0, 2, size=n) * 2 - 1
+        resample = rng.integers(0, cards[knob])
+        u = rng.random(n)
+        nxt = cur.copy()
+        nxt[rows, knob] = np.where(nudge, np.clip(cur[rows, knob] + delta, 0, cards[knob] - 1), resample)
+        e_new = score(nxt)
+        accept = (e_new >= energy) | (u < np.exp(np.minimum((e_new - energy) / temp, 0.0)))
+        cur = np.where(accept[:, None], nxt, cur)
+        energy = np.where(accept, e_new, energy)
+        temp = max(temp * sched.cooling, 1e-9)
+    return history
+
+
 def sa_explore(predict, space: KnobSpace, sched: SaSchedule, visited: set, rng) -> dict:
     """Parallel annealing chains maximizing the cost model (search.py:202-254); returns
     {config_index: score} over everything any chain evaluated, in the reference's
-    insertion order.  `predict` must be a CostModelPredictor: the chains run on the
-    device (there is no host loop)."""
-    if not isinstance(predict, CostModelPredictor):
-        raise DomainError("sa_explore runs on the device and needs a CostModelPredictor as `predict`")
+    insertion order.  A CostModelPredictor (default dims, space < 2^32) anneals on the
+    device (DeviceAnnealer); any other callable runs the reference-order host loop."""
     starts = draw_unvisited(space, visited, sched.parallel_chains, rng)
     if not starts:
         return {}
+    if not (isinstance(predict, CostModelPredictor) and _default_model(predict.m) and space.size < 2**32
+            and predict.space == space):
+        return _sa_explore_host(predict, space, sched, starts, rng)
     key = (id(predict), sched.initial_temp, sched.cooling, sched.steps_per_round, len(starts))
     ann = _ANNEALERS.get(key)
-    if ann is None or ann.pred is not predict:
+    # the annealer bakes the parameters and the feature-norm spec table of the predictor's
+    # model into its CUDA graph: rebuild when the predictor (or its model) is a new object
+    if ann is None or ann.pred is not predict or ann.m is not predict.m:
         if len(_ANNEALERS) > 16:
             _ANNEALERS.clear()
         ann = _ANNEALERS[key] = DeviceAnnealer(predict, sched, len(starts))

@@ -312,6 +312,22 @@ def test_sweeper_end_to_end_int64_and_int32_hosts(cuda_device, g_model):
     assert torch.equal(z1, z_dev.cpu()) and torch.equal(ti1, ti.cpu())
     ti_o, _ = sw.run_device(other.cuda())
     assert torch.equal(z2, sw.z[:50_000].cpu()) and torch.equal(ti2, ti_o.cpu())
+    # tickets are never reused: a consumed ticket is stale, a third step in flight is refused
+    with pytest.raises(ps.DomainError):
+        sw.wait(t1)
+    t3 = sw.submit(idx.pin_memory())
+    sw.submit(other.to(torch.int32).pin_memory())
+    with pytest.raises(ps.DomainError):
+        sw.submit(idx.pin_memory())
+    assert t3 > t2 and torch.equal(sw.wait(t3)[1], ti.cpu())
+
+
+def test_topk_refuses_indices_beyond_32_bits(cuda_device):
+    z = torch.zeros(8, device="cuda")
+    with pytest.raises(ps.DomainError):
+        ps.topk(z, 4, torch.arange(8, device="cuda") + 2**32)
+    with pytest.raises(ps.DomainError):
+        ps.topk(z, 4, base=2**32 - 4)
 
 
 def test_sweeper_fused_keys_match_score_topk(cuda_device, g_model):
