@@ -8,29 +8,42 @@
 // Loop-major tiling.  A tile is 128 graphs and TMEM lane g is graph g of the
 // tile for every accumulator.  The tile is processed as n_loops chunks; chunk k
 // holds loop row k of all 128 graphs:
-//   GEMM1  D1[128x32] = X_k[128x16] * W1            (A = X_k in TMEM, 2 K-steps x 3)
+//   GEMM1  D1[128x32] = X'_k[128x8] * B_k            (A = X'_k in TMEM, 1 K-step x 3)
 //   GEMM2  D2[128x32] = ReLU(D1) * W2 = s_k          (A = R_k in TMEM, 4 K-steps x 3)
 // so the star readout (sum_k s_k, sum_k ReLU(s_k), max_k s_k per channel) is a
 // per-thread running reduction over chunks -- no cross-lane traffic at all.
-// After the last chunk each epilogue thread owns its graph's readout row u:
-//   GEMM3  D3[128x64] = U * H0 (+b0, ReLU)          (A = U in smem, 8 K-steps x 3)
-//   GEMM4  D4[128x64] = Z1 * H1 (+b1, ReLU) . w3 + b3 (A = Z1 in smem)
+// After the last chunk each readout thread owns its graph's readout row u:
+//   GEMM3  D3[128x64] = U * H0                        (A = U in smem, 8 K-steps x 3)
+//   GEMM4  D4[128x64] = ReLU(D3 + b0) * H1            (A = Z1 in TMEM, 8 K-steps x 3)
+//   z = ReLU(D4 + b1) . w3 + b3
 //
-// Warp roles (608 threads = 19 warps, 1 CTA / SM, 512 TMEM columns):
-//   warps 0-3    R: thread = TMEM lane = graph; ReLU(D1) split hi/lo into R (TMEM)
-//   warps 4-7    encode: thread = graph; per row the axis' knob digit straight from
-//                the index (two magic-number divisions), then one
-//                normalised feature row per chunk (fp64 touched / log2 / z-norm,
-//                host tables for the rest), hi/lo split, tcgen05.st into an X slot
-//   warps 8, 17, 18  MMA issue, one stream each: GEMM1s, GEMM2s, head GEMMs (one
-//                elected lane issues; each waits only on its own operand barrier)
-//   warps 9-16   readout + head: two warps per lane quadrant, 16 channels each;
-//                running sum / ReLU-sum / max over the chunks, then the head
-//                epilogues (U -> smem, ReLU(D3 + b0) -> smem, (D4 + b1) . w3)
-// Rings: X 4 slots, D1 / R / D2 double-buffered; the R warps and the readout
-// warps never wait on each other, and the head of tile t overlaps the GCN
-// chunks of tile t+1 on the tensor pipe.  The issue warps carry the waits
-// (operand full + accumulator drained), keeping them off the CUDA-core stages.
+// Folded layer-1 operand.  Of the 12 feature slots of a loop row (model.py:108-112 on
+// graphs.py:89-126) six are constants of the loop position k (slots 2, 3, 10, 11, the
+// unroll slot 4 up to a 0/1 flag, slot 5 on inner loops), and the touched-derived pairs
+// are affine in one another: x8 = a8 x6 + b8 (arith = 2 touched) and x9 = a9 x7 + b9
+// (log2 arith = log2 touched + 1), a/b from the feature norm.  So
+//   x_k W1 = X'_k B_k,  X' = [x0, x1, x5 (outer rows), x6, x7, unroll flag, 1, 0]
+// with B_k (8 x 32) folded per loop row in the prologue (fp64 sums, one rounding):
+// rows W1[0], W1[1], W1[5], W1[6] + a8 W1[8], W1[7] + a9 W1[9], the unroll step, and
+// the loop row's constant bias.  Exact in real arithmetic; fp32-level in floating point;
+// a deterministic function of the features, so equal features still score equal.  GEMM1
+// is one K-step instead of two and an X slot is 16 TMEM columns instead of 32.
+//
+// Warp roles (768 threads = 6 warpgroups, 1 CTA / SM, 512 TMEM columns; registers
+// rebalanced per warpgroup with setmaxnreg):
+//   WG 0 (warps 0-3)    head: thread = TMEM lane = graph; per tile ReLU(D3 + b0) -> Z1
+//                       (TMEM, hi / lo), then ReLU(D4 + b1) . w3 + b3 -> score, top-k key
+//   WG 1 (warps 4-7)    encode: thread = graph; per row the axis' knob digit straight from
+//                       the index (two magic-number divisions), then the folded operand
+//                       row (fp64 touched / log2 / z-norm, host tables for the rest),
+//                       hi/lo split, tcgen05.st into an X slot
+//   WG 2 (warps 8-11)   R: thread = TMEM lane = graph; ReLU(D1) split hi/lo into R (TMEM)
+//   WG 3-4 (12-19)      readout, two warps per lane quadrant, 16 channels each: running
+//                       sum / ReLU-sum / max over the chunks; at a tile's end U -> TMEM
+//   WG 5 (warps 20-22)  MMA issue, one stream each: GEMM1s, GEMM2s, head GEMMs (one
+//                       elected lane issues; each waits only on its own operand barriers)
+// The head warps run a tile's head while the readout warps stream the next tile, so no
+// stage of the chunk pipeline ever waits for the head epilogue.
 #include "kt_encode.cuh"
 #include "kt_tc.cuh"
 
@@ -57,75 +70,75 @@ namespace tcs {
 
 using namespace kt::tc;
 
-constexpr int NT = 608;  // 19 warps
+constexpr int NT = 768;  // 24 warps = 6 warpgroups (roles by warpgroup, see the header)
+// per-warpgroup register budgets (setmaxnreg): 6 warps share an SMSP's 512 registers per
+// lane; the launch gives each 80, the roles rebalance them (sum <= 6 x 80)
+constexpr int REG_HEAD = 80, REG_ENC = 80, REG_R = 80, REG_RO = 96, REG_MMA = 40;
+static_assert(REG_HEAD + REG_ENC + REG_R + 2 * REG_RO + REG_MMA <= 6 * 80, "register budget");
 constexpr int GT = 128;   // graphs per tile (one TMEM lane each)
 constexpr int H = 64;
-#ifndef KT_XS
-#define KT_XS 4
-#endif
-#ifndef KT_N1
-#define KT_N1 2
-#endif
-#ifndef KT_NR
-#define KT_NR 2
-#endif
-#ifndef KT_N2
-#define KT_N2 2
-#endif
-constexpr int XS = KT_XS;  // X ring slots
-constexpr int N1 = KT_N1;  // D1 buffers
-constexpr int NR = KT_NR;  // R buffers
-constexpr int N2 = KT_N2;  // D2 buffers
+constexpr int XK = 8;     // folded layer-1 operand width (one tf32 K-step)
+constexpr int XS = 4;     // X ring slots
+constexpr int N1 = 2;     // D1 buffers
+constexpr int NR = 2;     // R buffers
+constexpr int N2 = 2;     // D2 buffers
 constexpr int TAB = 448;
 
 // TMEM column map (512 allocated)
-constexpr uint32_t T_X = 0;                  // X[s]: hi at 32 s, lo at 32 s + 16
-constexpr uint32_t T_D1 = T_X + 32 * XS;     // D1[b] at T_D1 + 32 b
+constexpr uint32_t T_X = 0;                  // X[s]: hi at 16 s, lo at 16 s + 8
+constexpr uint32_t T_D1 = T_X + 16 * XS;     // D1[b] at T_D1 + 32 b
 constexpr uint32_t T_R = T_D1 + 32 * N1;     // R[b]: hi at T_R + 64 b, lo at +32
 constexpr uint32_t T_D2 = T_R + 64 * NR;     // D2[b] at T_D2 + 32 b
-constexpr uint32_t T_D3 = T_D2 + 32 * N2;    // head layer 1 accumulator (64 columns)
-constexpr uint32_t T_D4 = T_D3 + 64;         // head layer 2 accumulator (64 columns)
-static_assert(T_D4 + 64 <= 512, "TMEM budget: 512 columns");
+constexpr uint32_t T_D34 = T_D2 + 32 * N2;   // head accumulator: D3, then D4 (64 columns)
+constexpr uint32_t T_Z = T_D34 + 64;         // head A operand, U then Z1 = ReLU(D3 + b0): hi at T_Z, lo at +64
+static_assert(T_Z + 128 <= 512, "TMEM budget: 512 columns");
 
 struct __align__(1024) Smem {
-  float b1h[32 * 16], b1l[32 * 16];  // W1^T (N=32, K=16; K 12..15 zero), K-major core matrices
+  float b1h[KT_MAX_LOOPS][32 * XK], b1l[KT_MAX_LOOPS][32 * XK];  // B_k^T (N=32, K=8) per loop row
   float b2h[32 * 32], b2l[32 * 32];  // W2^T
   float b3h[H * H], b3l[H * H];      // H0^T
   float b4h[H * H], b4l[H * H];      // H1^T
-  float ah[GT * H], al[GT * H];      // head A operand: U, then Z1 (K-major)
   float bias0[H], bias1[H], w3[H], agg[32];
-  float part[GT];  // head: half-1 partial dot per graph
   int2 oi[TAB];
   float4 nrm_o[TAB];
   float2 nrm_i[TAB];
   double2 l2[TAB];  // numpy log2 of (outer, inner) extent
-  float nconst[KT_MAX_LOOPS][8];
   int tab_off[KT_MAX_AXES + 1];  // start of each axis' choices in the per-choice tables; [n_axes] = total
-  int64_t vtile[2][GT];           // per tile parity: the graphs' config indices (INT64_MIN: padding)
+  // the graphs' config indices per tile (INT64_MIN: padding), tile ti in slot ti % 3, for
+  // the head warps (score validity, top-k key); v_free[slot] hands a slot back to the encode
+  int64_t vtile[3][GT];
   unsigned int khist[2048];       // first radix digit (key >> 53) of this CTA's top-k keys
   // digit extraction for slot d (axes 0..5, 6 = auto_unroll knob, 7 = explicit knob):
   // choice = (v / dmult[d]) % dcard[d], both divisions by magic multiply
   unsigned long long dm_magic[8], dc_magic[8];
   uint32_t dmult[8], dcard[8];
-  unsigned long long magic[KT_MAX_KNOBS];
-  uint32_t card[KT_MAX_KNOBS];
   int axis_knob[KT_MAX_AXES];
   int auto_vals[4], expl_vals[2];
   int auto_knob, expl_knob;
   uint64_t x_full[XS], x_empty[XS];
   uint64_t d1_full[N1], d1_empty[N1], r_full[NR], r_empty[NR], d2_full[N2], d2_empty[N2];
-  uint64_t u_full, z_full, d3_full, d4_full;
+  uint64_t u_full, uz_empty, z_full, d3_full, d4_full, d4_empty, v_free[3];
   uint32_t tmem_base;
 };
 
 __device__ __forceinline__ float relu(float v) { return fmaxf(v, 0.0f); }
+
+// Warpgroup register reallocation (all four warps of a warpgroup execute it).
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" : : "n"(N));
+}
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" : : "n"(N));
+}
 
 __device__ __forceinline__ uint32_t udiv(uint32_t v, uint32_t d, uint64_t magic) {
   return d == 1 ? v : static_cast<uint32_t>(__umul64hi(static_cast<uint64_t>(v), magic));
 }
 
 // B operand = W^T (rows n, K-major) from row-major W[k][n]; K beyond K_src zero.  Split
-// into a load half and a store half so that a thread's loads for all four operands are in
+// into a load half and a store half so that a thread's loads for all operands are in
 // flight together (the staging is on the critical path of every launch).
 template <int N, int K>
 struct OperandRegs {
@@ -140,36 +153,32 @@ __device__ __forceinline__ void load_operand(OperandRegs<N, K>& r, const float* 
     r.v[i] = e < N * K && k < K_src ? __ldg(W + k * N + n) : 0.0f;
   }
 }
+__device__ __forceinline__ void store_split(float* hi, float* lo, int off, float v) {
+  const float h = tf32_hi(v);
+  hi[off] = h;
+  lo[off] = v - h;
+}
 template <int N, int K>
 __device__ __forceinline__ void store_operand(const OperandRegs<N, K>& r, float* hi, float* lo, int tid) {
   constexpr int IT = OperandRegs<N, K>::IT;
-  const float* v = r.v;
 #pragma unroll
   for (int i = 0; i < IT; ++i) {
     const int e = tid + i * NT, k = e / N, n = e - k * N;
-    if (e < N * K) {
-      const float h = tf32_hi(v[i]);
-      const int off = kmajor_offset(n, k, K) >> 2;
-      hi[off] = h;
-      lo[off] = v[i] - h;
-    }
+    if (e < N * K) store_split(hi, lo, kmajor_offset(n, k, K) >> 2, r.v[i]);
   }
 }
 
-// thread-owned row `row` of a 128 x 64 K-major A operand: columns 4kq..4kq+3 as hi / lo
-__device__ __forceinline__ void store_head_quad(float* ah, float* al, int row, int kq, float4 v) {
-  float4 h, l;
-  h.x = tf32_trunc(v.x);
-  h.y = tf32_trunc(v.y);
-  h.z = tf32_trunc(v.z);
-  h.w = tf32_trunc(v.w);
-  l.x = v.x - h.x;
-  l.y = v.y - h.y;
-  l.z = v.z - h.z;
-  l.w = v.w - h.w;
-  const int off = kmajor_offset(row, 4 * kq, H) >> 2;
-  *reinterpret_cast<float4*>(ah + off) = h;
-  *reinterpret_cast<float4*>(al + off) = l;
+// 16 values -> hi (truncated tf32) / lo (exact remainder) halves, packed fp32x2 subtractions
+__device__ __forceinline__ void split16(const float* v, float* hi, float* lo) {
+#pragma unroll
+  for (int j = 0; j < 16; j += 2) {
+    const float2 t = make_float2(tf32_trunc(v[j]), tf32_trunc(v[j + 1]));
+    const float2 l = fsub2(make_float2(v[j], v[j + 1]), t);
+    hi[j] = t.x;
+    hi[j + 1] = t.y;
+    lo[j] = l.x;
+    lo[j + 1] = l.y;
+  }
 }
 
 __global__ void __launch_bounds__(NT, 1)
@@ -187,32 +196,8 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     return;
   }
 
-  // ---- setup: operands, tables, barriers, TMEM ------------------------------------------
-  {
-    OperandRegs<32, 16> r1;
-    OperandRegs<32, 32> r2;
-    OperandRegs<H, H> r3, r4;
-    load_operand(r1, params + dims.off_gcn[0], KT_F, tid);
-    load_operand(r2, params + dims.off_gcn[1], 32, tid);
-    load_operand(r3, params + dims.off_hw[0], H, tid);
-    load_operand(r4, params + dims.off_hw[1], H, tid);
-    store_operand(r1, S.b1h, S.b1l, tid);
-    store_operand(r2, S.b2h, S.b2l, tid);
-    store_operand(r3, S.b3h, S.b3l, tid);
-    store_operand(r4, S.b4h, S.b4l, tid);
-  }
-  if (tid == 0) TRACE(30, 0);
-  if (tid < H) {
-    S.bias0[tid] = params[dims.off_hb[0] + tid];
-    S.bias1[tid] = params[dims.off_hb[1] + tid];
-    S.w3[tid] = params[dims.off_hw[2] + tid];
-  }
-  if (tid < 32) S.agg[tid] = params[dims.off_agg + tid];
+  // ---- setup, part 1: constant tables, barriers, TMEM (overlaps the previous kernel) --
   const int na = T.n_axes, n_loops = T.n_loops;
-  if (tid < KT_MAX_KNOBS) {
-    S.card[tid] = T.card[tid];
-    S.magic[tid] = T.card_magic[tid];
-  }
   if (tid < KT_MAX_AXES) S.axis_knob[tid] = T.axis_knob[tid];
   if (tid < 4) S.auto_vals[tid] = T.auto_vals[tid];
   if (tid < 2) S.expl_vals[tid] = T.expl_vals[tid];
@@ -225,7 +210,6 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     if (tid == 0) {
       S.auto_knob = T.auto_knob;
       S.expl_knob = T.expl_knob;
-      TRACE(30, 5);
     }
   }
   if (tid == 0) {
@@ -246,28 +230,17 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       mbar_init(&S.d2_empty[b], 8);
     }
     mbar_init(&S.u_full, 8);
-    mbar_init(&S.z_full, 8);
+    mbar_init(&S.uz_empty, 1);
+    mbar_init(&S.z_full, 4);
     mbar_init(&S.d3_full, 1);
     mbar_init(&S.d4_full, 1);
-    TRACE(30, 1);
+    mbar_init(&S.d4_empty, 4);
+    for (int i = 0; i < 3; ++i) mbar_init(&S.v_free[i], 4);
   }
-  if (tid < KT_MAX_LOOPS) {
-    const int k = tid;
-    S.nconst[k][0] = T.nrm_const[k][2];
-    S.nconst[k][1] = T.nrm_const[k][3];
-    S.nconst[k][2] = T.nrm_const[k][4];
-    S.nconst[k][3] = T.nrm_unroll1[k];
-    S.nconst[k][4] = T.nrm_const[k][5];
-    S.nconst[k][5] = T.nrm_const[k][10];
-    S.nconst[k][6] = T.nrm_const[k][11];
-    S.nconst[k][7] = 0.f;
-  }
-  if (warp == 8) tmem_alloc(&S.tmem_base, 512);
-  if (tid == 256) TRACE(30, 2);
+  if (warp == 20) tmem_alloc(&S.tmem_base, 512);
   if (key_hist)
     for (int i = tid; i < 2048; i += NT) S.khist[i] = 0;
   __syncthreads();
-  if (tid == 0) TRACE(30, 3);
   // per-choice tables, one flat pass over every axis' entries (loads independent across threads)
   for (int e = tid; e < S.tab_off[na]; e += NT) {
     int a = 0;
@@ -278,16 +251,55 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     S.nrm_i[e] = make_float2(T.nrm_ext[na + a][c], T.nrm_log2ext[na + a][c]);
     S.l2[e] = make_double2(T.raw_log2[0][a][c], T.raw_log2[1][a][c]);
   }
-  if (tid == 0) TRACE(30, 4);
+  if (threadIdx.x == 0) TRACE(28, 0);  // table prologue done
+  // PDL: everything above reads only the constant spec table.  The parameters, indices,
+  // outputs and key_hist belong to the stream order from here on (a predecessor may write
+  // the parameters, e.g. kt_maml_step / kt_sgd in place).
+  pdl_wait();
+  pdl_launch_dependents();
+
+  // ---- setup, part 2: operands from the parameters --------------------------------
+  {
+    OperandRegs<32, 32> r2;
+    OperandRegs<H, H> r3, r4;
+    load_operand(r2, params + dims.off_gcn[1], 32, tid);
+    load_operand(r3, params + dims.off_hw[0], H, tid);
+    load_operand(r4, params + dims.off_hw[1], H, tid);
+    // folded layer-1 operand B_k (see the header), thread = (loop row k, channel n)
+    if (tid < n_loops * 32) {
+      const int k = tid >> 5, n = tid & 31;
+      const float* W1 = params + dims.off_gcn[0];
+      double w[KT_F];
+#pragma unroll
+      for (int f = 0; f < KT_F; ++f) w[f] = static_cast<double>(__ldg(W1 + f * 32 + n));
+      const bool inner = k >= na;
+      const double a8 = 2.0 * T.fstd[6] / T.fstd[8], b8 = (2.0 * T.fmean[6] - T.fmean[8]) / T.fstd[8];
+      const double a9 = T.fstd[7] / T.fstd[9], b9 = (T.fmean[7] + 1.0 - T.fmean[9]) / T.fstd[9];
+      const double c4 = T.nrm_const[k][4];
+      double bias = T.nrm_const[k][2] * w[2] + T.nrm_const[k][3] * w[3] + c4 * w[4] + T.nrm_const[k][10] * w[10] +
+                    T.nrm_const[k][11] * w[11] + b8 * w[8] + b9 * w[9];
+      if (inner) bias += T.nrm_const[k][5] * w[5];
+      const double rows[XK] = {w[0], w[1], inner ? 0.0 : w[5], w[6] + a8 * w[8], w[7] + a9 * w[9],
+                               inner ? (static_cast<double>(T.nrm_unroll1[k]) - c4) * w[4] : 0.0, bias, 0.0};
+#pragma unroll
+      for (int f = 0; f < XK; ++f)
+        store_split(S.b1h[k], S.b1l[k], kmajor_offset(n, f, XK) >> 2, static_cast<float>(rows[f]));
+    }
+    store_operand(r2, S.b2h, S.b2l, tid);
+    store_operand(r3, S.b3h, S.b3l, tid);
+    store_operand(r4, S.b4h, S.b4l, tid);
+  }
+  if (tid < H) {
+    S.bias0[tid] = params[dims.off_hb[0] + tid];
+    S.bias1[tid] = params[dims.off_hb[1] + tid];
+    S.w3[tid] = params[dims.off_hw[2] + tid];
+  }
+  if (tid < 32) S.agg[tid] = params[dims.off_agg + tid];
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (threadIdx.x == 0) TRACE(28, 0);  // prologue done
-  // PDL: the prologue above reads only the constant tables and parameters; indices,
-  // outputs and key_hist belong to the stream order from here on.
-  pdl_wait();
-  pdl_launch_dependents();
+  if (threadIdx.x == 0) TRACE(30, 0);  // operand prologue done
   const uint32_t tmem = S.tmem_base;
   const int64_t n_tiles = (B + GT - 1) / GT;
   const int64_t my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -295,19 +307,15 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
   const int64_t n_chunks = my_tiles * C;
   const uint64_t size = T.space_size;
 
-  if (warp >= 4 && warp < 8) {
-    // ===================== encode: thread = graph; one feature row per chunk ================
+  const int wg = warp >> 2;  // 0 head, 1 encode, 2 R, 3-4 readout, 5 MMA issue
+  if (wg == 1) {
+    setmaxnreg_inc<REG_ENC>();
+    // ===================== encode: thread = graph; one folded operand row per chunk =========
     const int g = tid - 128;
     const uint32_t lane = static_cast<uint32_t>((g & ~31) << 16);
     // touched-derived slots in fp64 with reciprocal scales: within 1 fp64 ulp of the
     // IEEE (x - mean) / std of model.py:108-112 before the single cast to fp32
-#ifdef KT_DBG_F32
-    using dbl = float;
-#else
-    using dbl = double;
-#endif
     const double m6 = T.fmean[6], r6 = 1.0 / T.fstd[6], m7 = T.fmean[7], r7 = 1.0 / T.fstd[7];
-    const double m8 = T.fmean[8], r8 = 1.0 / T.fstd[8], m9 = T.fmean[9] - 1.0, r9 = 1.0 / T.fstd[9];
     int64_t q = 0;
     auto index_of = [&](int64_t ti) -> int64_t {  // this thread's config index in tile ti
       const int64_t gi = (blockIdx.x + ti * gridDim.x) * GT + g;
@@ -325,20 +333,25 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     for (int64_t ti = 0; ti < my_tiles; ++ti) {
       const int64_t v64 = v_next;
       v_next = index_of(ti + 1);  // next tile's index load in flight during this tile
-      S.vtile[ti & 1][g] = v64;   // for the head epilogue (score validity, top-k key)
       const bool ok = v64 >= 0 && static_cast<uint64_t>(v64) < size;
+      {
+        const int vs = static_cast<int>(ti % 3);
+        mbar_wait(&S.v_free[vs], static_cast<uint32_t>(((ti / 3) & 1) ^ 1));  // head of tile ti-3 read it
+        S.vtile[vs][g] = v64;
+      }
       if (v64 != INT64_MIN && !ok) atomicOr(err, 1);
       const uint32_t v = ok ? static_cast<uint32_t>(v64) : 0u;
       const int autov = S.auto_knob >= 0 ? S.auto_vals[digit(v, 6)] : 0;
       const int expl = S.expl_knob >= 0 ? S.expl_vals[digit(v, 7)] : 0;
       const bool unr_on = expl != 0 && autov > 0;
+      const float one = ok ? 1.0f : 0.0f;
       // loops are emitted innermost first (k = n_loops-1 .. 0), so touched -- the
       // product of the extents of the loops inside loop k, multiplied innermost
       // outward as np.cumprod(e[::-1]) does -- accumulates exactly in fp64, and
       // log2(touched) accumulates as the sum of the numpy log2 of those extents
       // (log2(arith) = log2(2 touched) = that + 1).  Both are functions of the
       // extent vector only, so configs with equal features score identically.
-      dbl t = 1.0, lt = 0.0;
+      double t = 1.0, lt = 0.0;
       for (int c = 0; c < C; ++c, ++q) {
         const int k = C - 1 - c;
         const int level = k >= na;
@@ -346,46 +359,37 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         const int e = S.tab_off[a] + (S.axis_knob[a] >= 0 ? digit(v, a) : 0);
         const int2 oi = S.oi[e];
         if (g == 0) TRACE(19, q);
-        float x[16];
-#pragma unroll
-        for (int f = 12; f < 16; ++f) x[f] = 0.0f;
-        if (ok) {
-          if (level) {
-            const float2 ni = S.nrm_i[e];
-            x[0] = ni.x;
-            x[1] = ni.y;
-            x[5] = S.nconst[k][4];
-          } else {
-            const float4 no = S.nrm_o[e];
-            x[0] = no.x;
-            x[1] = no.y;
-            x[5] = no.z;
-          }
-          x[2] = S.nconst[k][0];
-          x[3] = S.nconst[k][1];
-          const bool unr = level && unr_on && oi.y <= autov;
-          x[4] = unr ? S.nconst[k][3] : S.nconst[k][2];
-          x[6] = static_cast<float>((t - static_cast<dbl>(m6)) * static_cast<dbl>(r6));
-          x[7] = static_cast<float>((lt - static_cast<dbl>(m7)) * static_cast<dbl>(r7));
-          x[8] = static_cast<float>((static_cast<dbl>(2.0) * t - static_cast<dbl>(m8)) * static_cast<dbl>(r8));
-          x[9] = static_cast<float>((lt - static_cast<dbl>(m9)) * static_cast<dbl>(r9));
-          x[10] = S.nconst[k][5];
-          x[11] = S.nconst[k][6];
+        float x[XK];
+        if (level) {
+          const float2 ni = S.nrm_i[e];
+          x[0] = ni.x;
+          x[1] = ni.y;
+          x[2] = 0.0f;
+          x[5] = unr_on && oi.y <= autov ? 1.0f : 0.0f;
         } else {
-#pragma unroll
-          for (int f = 0; f < 12; ++f) x[f] = 0.0f;
+          const float4 no = S.nrm_o[e];
+          x[0] = no.x;
+          x[1] = no.y;
+          x[2] = no.z;
+          x[5] = 0.0f;
         }
-        t *= static_cast<dbl>(level ? oi.y : oi.x);
-        const double2 l2 = S.l2[e];
-        lt += static_cast<dbl>(level ? l2.y : l2.x);
-        float hl[32];
+        x[3] = static_cast<float>((t - m6) * r6);
+        x[4] = static_cast<float>((lt - m7) * r7);
+        x[6] = 1.0f;
+        x[7] = 0.0f;
 #pragma unroll
-        for (int f = 0; f < 16; f += 2) {
+        for (int f = 0; f < XK; ++f) x[f] *= one;  // padding / invalid rows: all zero
+        t *= static_cast<double>(level ? oi.y : oi.x);
+        const double2 l2 = S.l2[e];
+        lt += level ? l2.y : l2.x;
+        float hl[16];
+#pragma unroll
+        for (int f = 0; f < XK; f += 2) {
           hl[f] = tf32_trunc(x[f]);
           hl[f + 1] = tf32_trunc(x[f + 1]);
           const float2 l = fsub2(make_float2(x[f], x[f + 1]), make_float2(hl[f], hl[f + 1]));
-          hl[16 + f] = l.x;
-          hl[17 + f] = l.y;
+          hl[XK + f] = l.x;
+          hl[XK + f + 1] = l.y;
         }
         const int s = static_cast<int>(q % XS);
         if (g == 0) TRACE(20, q);
@@ -393,112 +397,111 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         __syncwarp();
         if (g == 0) TRACE(21, q);
         tc_fence_after();
-#ifndef KT_DBG_NO_XST
-        tmem_st32(tmem + lane + T_X + 32 * s, hl);
-#endif
+        tmem_st16(tmem + lane + T_X + 16 * s, hl);
         tmem_wait_st();
         tc_fence_before();
         warp_arrive(&S.x_full[s]);
         if (g == 0) TRACE(0, q);
       }
     }
-  } else if (warp == 8 || warp == 17 || warp == 18) {
+  } else if (wg == 5) {
+    setmaxnreg_dec<REG_MMA>();
     // ===================== MMA: fixed issue order, blocking waits, one elected lane issues =====
-    // Order per chunk q: GEMM1(q + 2), GEMM2(q); the head of tile t is issued two
-    // (GEMM3) and three (GEMM4) chunks into tile t + 1, so its epilogue overlaps the
-    // next tile's GCN chunks.  Each wait parks the warp in hardware until the phase
-    // completes (no polling: a polling warp costs its SMSP neighbours issue slots).
+    // Each wait parks the warp in hardware until the phase completes (no polling: a
+    // polling warp costs its SMSP neighbours issue slots).
     const uint32_t id32 = idesc_tf32(128, 32), id64 = idesc_tf32(128, 64);
     auto wait_bar = [&](uint64_t* bar, uint32_t parity) {
       mbar_wait(bar, parity);
       __syncwarp();
       tc_fence_after();
     };
-    auto g1 = [&](int64_t q) {
-      const int s = static_cast<int>(q % XS), b = static_cast<int>(q % N1);
-      if ((tid & 31) == 0) TRACE(22, q);
-      wait_bar(&S.x_full[s], static_cast<uint32_t>((q / XS) & 1));
-      wait_bar(&S.d1_empty[b], static_cast<uint32_t>(((q / N1) & 1) ^ 1));
-      if ((tid & 31) == 0) TRACE(23, q);
-      const uint32_t xh = tmem + T_X + 32 * s, xl = xh + 16, d = tmem + T_D1 + 32 * b;
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < 2; ++kk) {
-          mma_tf32_ts(d, xh + 8 * kk, kdesc(S.b1h, 16, kk), id32, kk > 0);
-          mma_tf32_ts(d, xh + 8 * kk, kdesc(S.b1l, 16, kk), id32, 1);
-          mma_tf32_ts(d, xl + 8 * kk, kdesc(S.b1h, 16, kk), id32, 1);
-        }
-        mma_commit(&S.x_empty[s]);
-        mma_commit(&S.d1_full[b]);
-        TRACE(1, q);
-      }
-      __syncwarp();
-    };
-    auto g2 = [&](int64_t q) {
-      const int b = static_cast<int>(q % NR), b2 = static_cast<int>(q % N2);
-      if ((tid & 31) == 0) TRACE(17, q);
-      wait_bar(&S.r_full[b], static_cast<uint32_t>((q / NR) & 1));
-      wait_bar(&S.d2_empty[b2], static_cast<uint32_t>(((q / N2) & 1) ^ 1));
-      if ((tid & 31) == 0) TRACE(18, q);
-      const uint32_t rh = tmem + T_R + 64 * b, rl = rh + 32, d = tmem + T_D2 + 32 * b2;
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          mma_tf32_ts(d, rh + 8 * kk, kdesc(S.b2h, 32, kk), id32, kk > 0);
-          mma_tf32_ts(d, rh + 8 * kk, kdesc(S.b2l, 32, kk), id32, 1);
-          mma_tf32_ts(d, rl + 8 * kk, kdesc(S.b2h, 32, kk), id32, 1);
-        }
-        mma_commit(&S.r_empty[b]);
-        mma_commit(&S.d2_full[b2]);
-        TRACE(2, q);
-      }
-      __syncwarp();
-    };
-    auto g3 = [&](int64_t t) {
-      wait_bar(&S.u_full, static_cast<uint32_t>(t & 1));
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          mma_tf32(tmem + T_D3, kdesc(S.ah, H, kk), kdesc(S.b3h, H, kk), id64, kk > 0);
-          mma_tf32(tmem + T_D3, kdesc(S.ah, H, kk), kdesc(S.b3l, H, kk), id64, 1);
-          mma_tf32(tmem + T_D3, kdesc(S.al, H, kk), kdesc(S.b3h, H, kk), id64, 1);
-        }
-        mma_commit(&S.d3_full);
-        TRACE(3, t);
-      }
-      __syncwarp();
-    };
-    auto g4 = [&](int64_t t) {
-      wait_bar(&S.z_full, static_cast<uint32_t>(t & 1));
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          mma_tf32(tmem + T_D4, kdesc(S.ah, H, kk), kdesc(S.b4h, H, kk), id64, kk > 0);
-          mma_tf32(tmem + T_D4, kdesc(S.ah, H, kk), kdesc(S.b4l, H, kk), id64, 1);
-          mma_tf32(tmem + T_D4, kdesc(S.al, H, kk), kdesc(S.b4h, H, kk), id64, 1);
-        }
-        mma_commit(&S.d4_full);
-        TRACE(4, t);
-      }
-      __syncwarp();
-    };
     // Three independent issue streams, one warp each: tcgen05.commit tracks the MMAs of
     // the issuing thread only, so GEMM1s, GEMM2s and the head GEMMs need no common
     // program order -- their data dependencies all go through the ring barriers.
-    if (warp == 8) {
-      for (int64_t q = 0; q < n_chunks; ++q) g1(q);
-    } else if (warp == 17) {
-      for (int64_t q = 0; q < n_chunks; ++q) g2(q);
-    } else {
+    if (warp == 20) {
+      int c = 0;  // chunk within the tile -> loop row k = C - 1 - c (the encode order)
+      for (int64_t q = 0; q < n_chunks; ++q) {
+        const int s = static_cast<int>(q % XS), b = static_cast<int>(q % N1);
+        if ((tid & 31) == 0) TRACE(22, q);
+        wait_bar(&S.x_full[s], static_cast<uint32_t>((q / XS) & 1));
+        wait_bar(&S.d1_empty[b], static_cast<uint32_t>(((q / N1) & 1) ^ 1));
+        if ((tid & 31) == 0) TRACE(23, q);
+        const uint32_t xh = tmem + T_X + 16 * s, xl = xh + XK, d = tmem + T_D1 + 32 * b;
+        const int k = C - 1 - c;
+        if (elect_one()) {
+          mma_tf32_ts(d, xh, kdesc(S.b1h[k], XK, 0), id32, 0);
+          mma_tf32_ts(d, xh, kdesc(S.b1l[k], XK, 0), id32, 1);
+          mma_tf32_ts(d, xl, kdesc(S.b1h[k], XK, 0), id32, 1);
+          mma_commit(&S.x_empty[s]);
+          mma_commit(&S.d1_full[b]);
+          TRACE(1, q);
+        }
+        __syncwarp();
+        if (++c == C) c = 0;
+      }
+    } else if (warp == 21) {
+      for (int64_t q = 0; q < n_chunks; ++q) {
+
+        const int b = static_cast<int>(q % NR), b2 = static_cast<int>(q % N2);
+        if ((tid & 31) == 0) TRACE(17, q);
+        wait_bar(&S.r_full[b], static_cast<uint32_t>((q / NR) & 1));
+        wait_bar(&S.d2_empty[b2], static_cast<uint32_t>(((q / N2) & 1) ^ 1));
+        if ((tid & 31) == 0) TRACE(18, q);
+        const uint32_t rh = tmem + T_R + 64 * b, rl = rh + 32, d = tmem + T_D2 + 32 * b2;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            mma_tf32_ts(d, rh + 8 * kk, kdesc(S.b2h, 32, kk), id32, kk > 0);
+            mma_tf32_ts(d, rh + 8 * kk, kdesc(S.b2l, 32, kk), id32, 1);
+            mma_tf32_ts(d, rl + 8 * kk, kdesc(S.b2h, 32, kk), id32, 1);
+          }
+          mma_commit(&S.r_empty[b]);
+          mma_commit(&S.d2_full[b2]);
+          TRACE(2, q);
+        }
+        __syncwarp();
+      }
+    } else if (warp == 22) {
       for (int64_t t = 0; t < my_tiles; ++t) {
-        g3(t);
-        g4(t);
+        const uint32_t ph = static_cast<uint32_t>(t & 1);
+        // GEMM3: U (TMEM) x H0 into the head accumulator, once the head warps have read
+        // D4 of the previous tile out of it
+        wait_bar(&S.u_full, ph);
+        wait_bar(&S.d4_empty, ph ^ 1);
+        const uint32_t ah = tmem + T_Z, al = ah + 64;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            mma_tf32_ts(tmem + T_D34, ah + 8 * kk, kdesc(S.b3h, H, kk), id64, kk > 0);
+            mma_tf32_ts(tmem + T_D34, ah + 8 * kk, kdesc(S.b3l, H, kk), id64, 1);
+            mma_tf32_ts(tmem + T_D34, al + 8 * kk, kdesc(S.b3h, H, kk), id64, 1);
+          }
+          mma_commit(&S.d3_full);
+          TRACE(3, t);
+        }
+        __syncwarp();
+        // GEMM4: Z1 (TMEM, written over U) x H1, same accumulator (the head warps have read D3)
+        wait_bar(&S.z_full, ph);
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            mma_tf32_ts(tmem + T_D34, ah + 8 * kk, kdesc(S.b4h, H, kk), id64, kk > 0);
+            mma_tf32_ts(tmem + T_D34, ah + 8 * kk, kdesc(S.b4l, H, kk), id64, 1);
+            mma_tf32_ts(tmem + T_D34, al + 8 * kk, kdesc(S.b4h, H, kk), id64, 1);
+          }
+          mma_commit(&S.d4_full);
+          mma_commit(&S.uz_empty);  // the readout may write the next tile's U
+          TRACE(4, t);
+        }
+        __syncwarp();
       }
     }
-  } else if (warp < 4) {
+  } else if (wg == 2) {
+    setmaxnreg_inc<REG_R>();
     // ===================== R: ReLU(D1) -> R (hi, lo) in TMEM; thread = lane = graph ===============
-    const int g = tid;
-    const uint32_t lane = static_cast<uint32_t>((32 * warp) << 16);
+    const int quad = warp & 3;
+    const int g = 32 * quad + (tid & 31);
+    const uint32_t lane = static_cast<uint32_t>((32 * quad) << 16);
     for (int64_t q = 0; q < n_chunks; ++q) {
       const int b1 = static_cast<int>(q % N1), b = static_cast<int>(q % NR);
       mbar_wait(&S.d1_full[b1], static_cast<uint32_t>((q / N1) & 1));
@@ -512,6 +515,8 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       if (g == 0) TRACE(13, q);
       tc_fence_before();
       warp_arrive(&S.d1_empty[b1]);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = relu(v[j]);
       mbar_wait(&S.r_empty[b], static_cast<uint32_t>(((q / NR) & 1) ^ 1));  // GEMM2 of chunk q-NR read R[b]
       __syncwarp();
       if (g == 0) TRACE(14, q);
@@ -519,16 +524,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         float hi[16], lo[16];
-#pragma unroll
-        for (int j = 0; j < 16; j += 2) {  // remainders as packed fp32x2 subtractions
-          const float2 r = make_float2(relu(v[16 * h + j]), relu(v[16 * h + j + 1]));
-          const float2 t = make_float2(tf32_trunc(r.x), tf32_trunc(r.y));
-          const float2 l = fsub2(r, t);
-          hi[j] = t.x;
-          hi[j + 1] = t.y;
-          lo[j] = l.x;
-          lo[j + 1] = l.y;
-        }
+        split16(v + 16 * h, hi, lo);
         tmem_st16(tmem + lane + T_R + 64 * b + 16 * h, hi);
         tmem_st16(tmem + lane + T_R + 64 * b + 32 + 16 * h, lo);
       }
@@ -539,31 +535,32 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       warp_arrive(&S.r_full[b]);
       if (g == 0) TRACE(6, q);
     }
-  } else {
-    // ===================== readout + head: thread = lane = graph, 16 channels ====================
-    const int quad = warp & 3, eh = (warp - 9) >> 2;
+  } else if (wg >= 3) {
+    setmaxnreg_inc<REG_RO>();
+    // ===================== readout: thread = lane = graph, 16 channels =========================
+    const int quad = warp & 3, eh = wg - 3;
+
     const int g = 32 * quad + (tid & 31);
     const uint32_t lane = static_cast<uint32_t>((32 * quad) << 16);
     const float c_t = static_cast<float>(5.0 / 12.0);
     const float c_ft = static_cast<float>(5.0 / (6.0 * sqrt(6.0)) + 5.0 / 12.0);
     const float c_r = static_cast<float>(1.0 / sqrt(18.0 * (T.n_pairs + 1)));
-    const float b3 = params[dims.off_hb[2]];
     const bool tr = g == 0 && eh == 0;
     float2 tot[8], rs[8];  // per channel: sum of s, sum of |s| (sum relu(s) = (sum s + sum |s|) / 2)
     float mx[16];
     int kc = 0;       // chunk index within the current tile (no 64-bit % / on this path)
     int64_t ti = 0;   // local tile index
-    for (int64_t q = 0; q < n_chunks; ++q) {
-      const int b = static_cast<int>(q % N2);
+    for (int64_t p = 0; p < n_chunks; ++p) {
+      const int b = static_cast<int>(p % N2);
       if (kc == 0) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) tot[j] = rs[j] = make_float2(0.0f, 0.0f);
 #pragma unroll
         for (int j = 0; j < 16; ++j) mx[j] = 0.0f;  // max_k ReLU(s_k) = max(0, max_k s_k)
       }
-      mbar_wait(&S.d2_full[b], static_cast<uint32_t>((q / N2) & 1));
+      mbar_wait(&S.d2_full[b], static_cast<uint32_t>((p / N2) & 1));
       __syncwarp();
-      if (tr) TRACE(7, q);
+      if (tr) TRACE(7, p);
       tc_fence_after();
       {
         float v[16];
@@ -581,97 +578,128 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
           mx[2 * i + 1] = fmaxf(mx[2 * i + 1], s2.y);
         }
       }
-      if (tr) TRACE(8, q);
+      if (tr) TRACE(8, p);
       if (++kc < C) continue;
       kc = 0;
-      // ---- head of tile ti ------------------------------------------------------------
-      const uint32_t ph = static_cast<uint32_t>(ti & 1);
+      // ---- tile ti done: readout row U -> TMEM (the head GEMM's A operand), this warp's
+      // 16 sum and 16 max channels ----
       const int64_t gi = (blockIdx.x + ti * gridDim.x) * GT + g;
+      // (ordered so that the accumulators die early: sum part first, then max part)
       float4* urow = u_out && gi < B ? reinterpret_cast<float4*>(u_out + gi * H) : nullptr;
+      mbar_wait(&S.uz_empty, static_cast<uint32_t>((ti & 1) ^ 1));  // GEMM4 of tile ti-1 read Z1
+      __syncwarp();
+      tc_fence_after();
+      {
+        float u[16], lo[16];
 #pragma unroll
-      for (int jq = 0; jq < 4; ++jq) {  // channels 16 eh + 4 jq .. +3
-        float us[4], um[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int jl = 4 * jq + i, j = 16 * eh + jl;
+        for (int jl = 0; jl < 16; ++jl) {
           const float tj = (jl & 1) ? tot[jl >> 1].y : tot[jl >> 1].x;
           const float rj = 0.5f * (((jl & 1) ? rs[jl >> 1].y : rs[jl >> 1].x) + tj);
-          const float root = relu(c_r * tj);
-          us[i] = S.agg[j] * (root + c_ft * rj);
-          um[i] = fmaxf(root, c_t * mx[jl]);
+          u[jl] = S.agg[16 * eh + jl] * (relu(c_r * tj) + c_ft * rj);
         }
-        const float4 s4 = make_float4(us[0], us[1], us[2], us[3]);
-        const float4 m4 = make_float4(um[0], um[1], um[2], um[3]);
-        store_head_quad(S.ah, S.al, g, 4 * eh + jq, s4);
-        store_head_quad(S.ah, S.al, g, 8 + 4 * eh + jq, m4);
-        if (urow) {
-          urow[4 * eh + jq] = s4;
-          urow[8 + 4 * eh + jq] = m4;
+        if (urow)
+#pragma unroll
+          for (int jq = 0; jq < 4; ++jq) urow[4 * eh + jq] = make_float4(u[4 * jq], u[4 * jq + 1], u[4 * jq + 2], u[4 * jq + 3]);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {  // in-place split: u -> hi, lo
+          const float h = tf32_trunc(u[j]);
+          lo[j] = u[j] - h;
+          u[j] = h;
         }
+        tmem_st16(tmem + lane + T_Z + 16 * eh, u);
+        tmem_st16(tmem + lane + T_Z + 64 + 16 * eh, lo);
       }
-      fence_async_smem();
+      {
+        float u[16], lo[16];
+#pragma unroll
+        for (int jl = 0; jl < 16; ++jl)
+          u[jl] = fmaxf(relu(c_r * ((jl & 1) ? tot[jl >> 1].y : tot[jl >> 1].x)), c_t * mx[jl]);
+        if (urow)
+#pragma unroll
+          for (int jq = 0; jq < 4; ++jq)
+            urow[8 + 4 * eh + jq] = make_float4(u[4 * jq], u[4 * jq + 1], u[4 * jq + 2], u[4 * jq + 3]);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float h = tf32_trunc(u[j]);
+          lo[j] = u[j] - h;
+          u[j] = h;
+        }
+        tmem_st16(tmem + lane + T_Z + 32 + 16 * eh, u);
+        tmem_st16(tmem + lane + T_Z + 96 + 16 * eh, lo);
+      }
+      tmem_wait_st();
+      tc_fence_before();
       warp_arrive(&S.u_full);
       if (tr) TRACE(9, ti);
+      ++ti;
+    }
+  } else {  // (the head keeps the launch's 80 registers: REG_HEAD)
+    // ===================== head: thread = lane = graph, all 64 channels ===========================
+    const int quad = warp;
+    const int g = 32 * quad + (tid & 31);
+    const uint32_t lane = static_cast<uint32_t>((32 * quad) << 16);
+    const float b3 = params[dims.off_hb[2]];
+    const bool tr = g == 0;
+    for (int64_t ti = 0; ti < my_tiles; ++ti) {
+      const uint32_t ph = static_cast<uint32_t>(ti & 1);
       mbar_wait(&S.d3_full, ph);
       __syncwarp();
       if (tr) TRACE(10, ti);
       tc_fence_after();
+      const int64_t v = S.vtile[ti % 3][g];  // this tile's indices; the slot goes back to the encode
+      warp_arrive(&S.v_free[ti % 3]);
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {  // D3 columns 32 eh + 16 h ..
-        float z[16];
-        tmem_ld16(tmem + lane + T_D3 + 32 * eh + 16 * h, z);
+      for (int h = 0; h < 4; ++h) {  // D3 columns 16 h .. 16 h + 15 -> Z1 = ReLU(D3 + b0), hi / lo
+        float z[16], hi[16], lo[16];
+        tmem_ld16(tmem + lane + T_D34 + 16 * h, z);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int c0 = 32 * eh + 16 * h + 4 * i;
-          const float4 bb = *reinterpret_cast<const float4*>(S.bias0 + c0);
-          store_head_quad(S.ah, S.al, g, c0 >> 2,
-                          make_float4(relu(z[4 * i] + bb.x), relu(z[4 * i + 1] + bb.y), relu(z[4 * i + 2] + bb.z),
-                                      relu(z[4 * i + 3] + bb.w)));
-        }
+        for (int i = 0; i < 16; ++i) z[i] = relu(z[i] + S.bias0[16 * h + i]);
+        split16(z, hi, lo);
+        tmem_st16(tmem + lane + T_Z + 16 * h, hi);
+        tmem_st16(tmem + lane + T_Z + 64 + 16 * h, lo);
       }
-      fence_async_smem();
+      tmem_wait_st();
       tc_fence_before();
       warp_arrive(&S.z_full);
       mbar_wait(&S.d4_full, ph);
       __syncwarp();
       if (tr) TRACE(11, ti);
       tc_fence_after();
-      float acc = 0.0f;
-      {
-        float v[32];
-        tmem_ld16(tmem + lane + T_D4 + 32 * eh, v);
-        tmem_ld16(tmem + lane + T_D4 + 32 * eh + 16, v + 16);
-        tmem_wait_ld();
+      float acc0 = 0.0f, acc1 = 0.0f;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc = fmaf(relu(v[j] + S.bias1[32 * eh + j]), S.w3[32 * eh + j], acc);
+      for (int h = 0; h < 2; ++h) {
+        float v[32];
+        tmem_ld16(tmem + lane + T_D34 + 32 * h, v);
+        tmem_ld16(tmem + lane + T_D34 + 32 * h + 16, v + 16);
+        tmem_wait_ld();
+        float acc = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc = fmaf(relu(v[j] + S.bias1[32 * h + j]), S.w3[32 * h + j], acc);
+        if (h == 0) acc0 = acc; else acc1 = acc;
       }
       tc_fence_before();
-      // combine the two halves' partial dots: half 1 hands its value over through smem
-      if (eh == 1) S.part[g] = acc;
-      named_sync(1 + quad, 64);
-      if (eh == 0 && gi < B) {
-        const int64_t v = S.vtile[ti & 1][g];
+      warp_arrive(&S.d4_empty);
+      const int64_t gi = (blockIdx.x + ti * gridDim.x) * GT + g;
+      if (gi < B) {
         const bool ok = v >= 0 && static_cast<uint64_t>(v) < size;
-        const float zv = (b3 + acc) + S.part[g];
+        const float zv = (b3 + acc0) + acc1;
         z_out[gi] = ok ? zv : __int_as_float(0x7fc00000);
         if (keys_out) {  // rank_history key for kt_topk_keys: (descending score code, index)
-          const uint32_t b = __float_as_uint(zv);
-          const uint32_t asc = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+          const uint32_t bb = __float_as_uint(zv);
+          const uint32_t asc = (bb & 0x80000000u) ? ~bb : (bb | 0x80000000u);
           const unsigned long long key =
               ok && zv == zv ? (static_cast<unsigned long long>(~asc) << 32) | static_cast<uint32_t>(v) : ~0ull;
           keys_out[gi] = key;
           if (key_hist) atomicAdd(&S.khist[static_cast<int>(key >> 53)], 1u);  // kt_topk_keys' first digit
         }
       }
-      named_sync(1 + quad, 64);  // S.part consumed before the next tile overwrites it
       if (tr) TRACE(12, ti);
-      ++ti;
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == 20) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
