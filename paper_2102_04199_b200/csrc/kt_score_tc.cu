@@ -73,7 +73,7 @@ using namespace kt::tc;
 constexpr int NT = 768;  // 24 warps = 6 warpgroups (roles by warpgroup, see the header)
 // per-warpgroup register budgets (setmaxnreg): 6 warps share an SMSP's 512 registers per
 // lane; the launch gives each 80, the roles rebalance them (sum <= 6 x 80)
-constexpr int REG_HEAD = 80, REG_ENC = 80, REG_R = 80, REG_RO = 96, REG_MMA = 40;
+constexpr int REG_HEAD = 72, REG_ENC = 80, REG_R = 56, REG_RO = 104, REG_MMA = 64;
 static_assert(REG_HEAD + REG_ENC + REG_R + 2 * REG_RO + REG_MMA <= 6 * 80, "register budget");
 constexpr int GT = 128;   // graphs per tile (one TMEM lane each)
 constexpr int H = 64;
@@ -83,6 +83,12 @@ constexpr int N1 = 2;     // D1 buffers
 constexpr int NR = 2;     // R buffers
 constexpr int N2 = 2;     // D2 buffers
 constexpr int TAB = 448;
+#ifndef KT_ENC_PIPE
+#define KT_ENC_PIPE 0
+#endif
+#ifndef KT_HEAD_SLEEP
+#define KT_HEAD_SLEEP 256  // ns between probes of the head warpgroup's (long) waits
+#endif
 
 // TMEM column map (512 allocated)
 constexpr uint32_t T_X = 0;                  // X[s]: hi at 16 s, lo at 16 s + 8
@@ -106,8 +112,13 @@ struct __align__(1024) Smem {
   int tab_off[KT_MAX_AXES + 1];  // start of each axis' choices in the per-choice tables; [n_axes] = total
   // the graphs' config indices per tile (INT64_MIN: padding), tile ti in slot ti % 3, for
   // the head warps (score validity, top-k key); v_free[slot] hands a slot back to the encode
-  int64_t vtile[3][GT];
+  int64_t vtile[4][GT];
   unsigned int khist[2048];       // first radix digit (key >> 53) of this CTA's top-k keys
+#if KT_ENC_PIPE
+  float xstage[2][KT_MAX_LOOPS][6][GT];  // encode: feature rows of two tiles (thread-private)
+#else
+  float xstage[1][KT_MAX_LOOPS][6][GT];  // encode: a tile's feature rows (thread-private)
+#endif
   // digit extraction for slot d (axes 0..5, 6 = auto_unroll knob, 7 = explicit knob):
   // choice = (v / dmult[d]) % dcard[d], both divisions by magic multiply
   unsigned long long dm_magic[8], dc_magic[8];
@@ -117,7 +128,7 @@ struct __align__(1024) Smem {
   int auto_knob, expl_knob;
   uint64_t x_full[XS], x_empty[XS];
   uint64_t d1_full[N1], d1_empty[N1], r_full[NR], r_empty[NR], d2_full[N2], d2_empty[N2];
-  uint64_t u_full, uz_empty, z_full, d3_full, d4_full, d4_empty, v_free[3];
+  uint64_t u_full, uz_empty, z_full, d3_full, d4_full, d4_empty, v_free[4];
   uint32_t tmem_base;
 };
 
@@ -127,6 +138,14 @@ __device__ __forceinline__ float relu(float v) { return fmaxf(v, 0.0f); }
 template <int N>
 __device__ __forceinline__ void setmaxnreg_inc() {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" : : "n"(N));
+}
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec();
+// to N registers from the launch's 80, in whichever direction
+template <int N>
+__device__ __forceinline__ void setmaxnreg() {
+  if constexpr (N > 80) setmaxnreg_inc<N>();
+  if constexpr (N < 80) setmaxnreg_dec<N>();
 }
 template <int N>
 __device__ __forceinline__ void setmaxnreg_dec() {
@@ -179,6 +198,179 @@ __device__ __forceinline__ void split16(const float* v, float* hi, float* lo) {
     lo[j] = l.x;
     lo[j + 1] = l.y;
   }
+}
+
+// knob digit d of a (32-bit) config index: (v / dmult[d]) % dcard[d] (kernels.py:278-286)
+__device__ __forceinline__ int knob_digit(const Smem& S, uint32_t v, int d) {
+  const uint32_t qd = udiv(v, S.dmult[d], S.dm_magic[d]);
+  const uint32_t c = S.dcard[d];
+  return static_cast<int>(qd - udiv(qd, c, S.dc_magic[d]) * c);
+}
+
+struct EncodeCtx {
+  const int64_t* idx;
+  const uint32_t* idx32;
+  int64_t idx_base, B, my_tiles;
+  uint64_t size;
+  int32_t* err;
+  uint32_t tmem, lane;
+  int g;
+  double m6, r6, m7, r7;  // touched-derived slots: fp64 (x - mean) * (1 / std)
+};
+
+// A tile's per-graph encode state: the config index, the unroll knobs, the axes' table
+// entries and extents, and the running touched / log2 touched.
+template <int NA>
+struct EncodeTile {
+  float one;  // 1 for a valid config, 0 for padding / an invalid index (all-zero rows)
+  bool unr_on;
+  int autov;
+  int e[NA];
+  int2 oi[NA];
+  double t, lt;
+};
+
+template <int NA>
+__device__ __forceinline__ void encode_prepare(Smem& S, const EncodeCtx& X, int64_t ti, int64_t v64,
+                                               EncodeTile<NA>& st) {
+  const bool ok = v64 >= 0 && static_cast<uint64_t>(v64) < X.size;
+  mbar_wait(&S.v_free[ti & 3], static_cast<uint32_t>(((ti >> 2) & 1) ^ 1));  // head of tile ti-4 read it
+  S.vtile[ti & 3][X.g] = v64;
+  if (v64 != INT64_MIN && !ok) atomicOr(X.err, 1);
+  const uint32_t v = ok ? static_cast<uint32_t>(v64) : 0u;
+  st.autov = S.auto_knob >= 0 ? S.auto_vals[knob_digit(S, v, 6)] : 0;
+  const int expl = S.expl_knob >= 0 ? S.expl_vals[knob_digit(S, v, 7)] : 0;
+  st.unr_on = expl != 0 && st.autov > 0;
+  st.one = ok ? 1.0f : 0.0f;
+#pragma unroll
+  for (int a = 0; a < NA; ++a) st.e[a] = S.tab_off[a] + (S.axis_knob[a] >= 0 ? knob_digit(S, v, a) : 0);
+#pragma unroll
+  for (int a = 0; a < NA; ++a) st.oi[a] = S.oi[st.e[a]];
+  st.t = 1.0;
+  st.lt = 0.0;
+}
+
+// Feature row c (loop k = 2 NA - 1 - c, innermost first) of a tile into S.xstage[buf][c].
+// touched -- the product of the extents of the loops inside loop k, multiplied innermost
+// outward as np.cumprod(e[::-1]) does -- accumulates exactly in fp64, and log2(touched)
+// as the sum of the numpy log2 of those extents (log2(arith) = log2(2 touched) = that
+// + 1).  Both are functions of the extent vector only, so configs with equal features
+// score identically.
+template <int NA>
+__device__ __forceinline__ void encode_row(Smem& S, const EncodeCtx& X, EncodeTile<NA>& st, int c, int buf) {
+  const int k = 2 * NA - 1 - c;
+  const bool level = k >= NA;  // inner loop
+  const int a = level ? k - NA : k;
+  float x0, x1, x2, x5;
+  if (level) {
+    const float2 ni = S.nrm_i[st.e[a]];
+    x0 = ni.x;
+    x1 = ni.y;
+    x2 = 0.0f;
+    x5 = st.unr_on && st.oi[a].y <= st.autov ? 1.0f : 0.0f;  // unroll flag
+  } else {
+    const float4 no = S.nrm_o[st.e[a]];
+    x0 = no.x;
+    x1 = no.y;
+    x2 = no.z;  // stride slot
+    x5 = 0.0f;
+  }
+  float* r = &S.xstage[buf][c][0][X.g];
+  r[0 * GT] = x0;
+  r[1 * GT] = x1;
+  r[2 * GT] = x2;
+  r[3 * GT] = static_cast<float>((st.t - X.m6) * X.r6);
+  r[4 * GT] = static_cast<float>((st.lt - X.m7) * X.r7);
+  r[5 * GT] = x5;
+  st.t *= static_cast<double>(level ? st.oi[a].y : st.oi[a].x);
+  const double2 l2 = S.l2[st.e[a]];
+  st.lt += level ? l2.y : l2.x;
+}
+
+// Row c of a staged tile -> hi / lo split -> X slot of chunk q (tcgen05.st) -> GEMM1.
+__device__ __forceinline__ void encode_hand_over(Smem& S, const EncodeCtx& X, int c, int buf, float one, int64_t q) {
+  float x[XK];
+  const float* r = &S.xstage[buf][c][0][X.g];
+#pragma unroll
+  for (int f = 0; f < 6; ++f) x[f] = r[f * GT] * one;  // padding / invalid rows: all zero
+  x[6] = one;
+  x[7] = 0.0f;
+  float hl[16];
+#pragma unroll
+  for (int f = 0; f < XK; f += 2) {
+    hl[f] = tf32_trunc(x[f]);
+    hl[f + 1] = tf32_trunc(x[f + 1]);
+    const float2 l = fsub2(make_float2(x[f], x[f + 1]), make_float2(hl[f], hl[f + 1]));
+    hl[XK + f] = l.x;
+    hl[XK + f + 1] = l.y;
+  }
+  const int s = static_cast<int>(q % XS);
+  if (X.g == 0) TRACE(20, q);
+  mbar_wait(&S.x_empty[s], static_cast<uint32_t>(((q / XS) & 1) ^ 1));
+  __syncwarp();
+  if (X.g == 0) TRACE(21, q);
+  tc_fence_after();
+  tmem_st16(X.tmem + X.lane + T_X + 16 * s, hl);
+  tmem_wait_st();
+  tc_fence_before();
+  warp_arrive(&S.x_full[s]);
+  if (X.g == 0) TRACE(0, q);
+}
+
+// The encode warps' loop, specialised on the axis count so every per-axis / per-row
+// quantity lives in registers.  Per tile, phase 1 computes all feature rows (no waits:
+// the rows' digit extraction and table lookups are independent, only touched / log2
+// touched chain across rows), then phase 2 hands them to GEMM1 one X slot at a time.
+// KT_ENC_PIPE=1 interleaves the next tile's phase 1 with this tile's phase 2 instead.
+template <int NA>
+__device__ __forceinline__ void encode_loop(Smem& S, const EncodeCtx& X) {
+  constexpr int C = 2 * NA;
+  auto index_of = [&](int64_t ti) -> int64_t {  // this thread's config index in tile ti
+    const int64_t gi = (blockIdx.x + ti * gridDim.x) * GT + X.g;
+    if (ti >= X.my_tiles || gi >= X.B) return INT64_MIN;  // padding row
+    // idx32 may point at pinned host memory (zero-copy: the kernel's reads are the H2D transfer)
+    return X.idx32 ? static_cast<int64_t>(X.idx32[gi]) : X.idx ? __ldcs(X.idx + gi) : X.idx_base + gi;
+  };
+  if (X.my_tiles <= 0) return;
+  int64_t q = 0;
+#if KT_ENC_PIPE
+  EncodeTile<NA> cur, nxt;
+  encode_prepare<NA>(S, X, 0, index_of(0), cur);
+  int64_t v_next = index_of(1);  // loaded a tile ahead of use
+#pragma unroll
+  for (int c = 0; c < C; ++c) encode_row<NA>(S, X, cur, c, 0);
+  for (int64_t ti = 0; ti < X.my_tiles; ++ti) {
+    const bool more = ti + 1 < X.my_tiles;
+    if (more) {
+      encode_prepare<NA>(S, X, ti + 1, v_next, nxt);
+      v_next = index_of(ti + 2);
+    }
+    const int buf = static_cast<int>(ti & 1);
+#pragma unroll
+    for (int c = 0; c < C; ++c, ++q) {
+      if (X.g == 0) TRACE(19, q);
+      if (more) encode_row<NA>(S, X, nxt, c, buf ^ 1);
+      encode_hand_over(S, X, c, buf, cur.one, q);
+    }
+    cur.one = nxt.one;
+  }
+#else
+  int64_t v_next = index_of(0);
+  for (int64_t ti = 0; ti < X.my_tiles; ++ti) {
+    EncodeTile<NA> st;
+    if (X.g == 0) TRACE(24, ti);
+    encode_prepare<NA>(S, X, ti, v_next, st);
+    v_next = index_of(ti + 1);  // next tile's index load in flight during this tile
+    if (X.g == 0) TRACE(26, ti);
+#pragma unroll
+    for (int c = 0; c < C; ++c) encode_row<NA>(S, X, st, c, 0);
+#pragma unroll 1
+    for (int c = 0; c < C; ++c, ++q) {
+      if (X.g == 0) TRACE(19, q);
+      encode_hand_over(S, X, c, 0, st.one, q);
+    }
+  }
+#endif
 }
 
 __global__ void __launch_bounds__(NT, 1)
@@ -235,7 +427,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     mbar_init(&S.d3_full, 1);
     mbar_init(&S.d4_full, 1);
     mbar_init(&S.d4_empty, 4);
-    for (int i = 0; i < 3; ++i) mbar_init(&S.v_free[i], 4);
+    for (int i = 0; i < 4; ++i) mbar_init(&S.v_free[i], 4);
   }
   if (warp == 20) tmem_alloc(&S.tmem_base, 512);
   if (key_hist)
@@ -309,103 +501,24 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
 
   const int wg = warp >> 2;  // 0 head, 1 encode, 2 R, 3-4 readout, 5 MMA issue
   if (wg == 1) {
-    setmaxnreg_inc<REG_ENC>();
+    setmaxnreg<REG_ENC>();
     // ===================== encode: thread = graph; one folded operand row per chunk =========
     const int g = tid - 128;
-    const uint32_t lane = static_cast<uint32_t>((g & ~31) << 16);
     // touched-derived slots in fp64 with reciprocal scales: within 1 fp64 ulp of the
     // IEEE (x - mean) / std of model.py:108-112 before the single cast to fp32
     const double m6 = T.fmean[6], r6 = 1.0 / T.fstd[6], m7 = T.fmean[7], r7 = 1.0 / T.fstd[7];
-    int64_t q = 0;
-    auto index_of = [&](int64_t ti) -> int64_t {  // this thread's config index in tile ti
-      const int64_t gi = (blockIdx.x + ti * gridDim.x) * GT + g;
-      if (ti >= my_tiles || gi >= B) return INT64_MIN;  // padding row
-      // idx32 may point at pinned host memory (zero-copy: the kernel's reads are the H2D transfer)
-      return idx32 ? static_cast<int64_t>(idx32[gi]) : idx ? __ldcs(idx + gi) : idx_base + gi;
-    };
-    // knob digit d of the (32-bit) index: (v / dmult[d]) % dcard[d] (kernels.py:278-286)
-    auto digit = [&](uint32_t v, int d) -> int {
-      const uint32_t qd = udiv(v, S.dmult[d], S.dm_magic[d]);
-      const uint32_t c = S.dcard[d];
-      return static_cast<int>(qd - udiv(qd, c, S.dc_magic[d]) * c);
-    };
-    int64_t v_next = index_of(0);
-    for (int64_t ti = 0; ti < my_tiles; ++ti) {
-      const int64_t v64 = v_next;
-      v_next = index_of(ti + 1);  // next tile's index load in flight during this tile
-      const bool ok = v64 >= 0 && static_cast<uint64_t>(v64) < size;
-      {
-        const int vs = static_cast<int>(ti % 3);
-        mbar_wait(&S.v_free[vs], static_cast<uint32_t>(((ti / 3) & 1) ^ 1));  // head of tile ti-3 read it
-        S.vtile[vs][g] = v64;
-      }
-      if (v64 != INT64_MIN && !ok) atomicOr(err, 1);
-      const uint32_t v = ok ? static_cast<uint32_t>(v64) : 0u;
-      const int autov = S.auto_knob >= 0 ? S.auto_vals[digit(v, 6)] : 0;
-      const int expl = S.expl_knob >= 0 ? S.expl_vals[digit(v, 7)] : 0;
-      const bool unr_on = expl != 0 && autov > 0;
-      const float one = ok ? 1.0f : 0.0f;
-      // loops are emitted innermost first (k = n_loops-1 .. 0), so touched -- the
-      // product of the extents of the loops inside loop k, multiplied innermost
-      // outward as np.cumprod(e[::-1]) does -- accumulates exactly in fp64, and
-      // log2(touched) accumulates as the sum of the numpy log2 of those extents
-      // (log2(arith) = log2(2 touched) = that + 1).  Both are functions of the
-      // extent vector only, so configs with equal features score identically.
-      double t = 1.0, lt = 0.0;
-      for (int c = 0; c < C; ++c, ++q) {
-        const int k = C - 1 - c;
-        const int level = k >= na;
-        const int a = level ? k - na : k;
-        const int e = S.tab_off[a] + (S.axis_knob[a] >= 0 ? digit(v, a) : 0);
-        const int2 oi = S.oi[e];
-        if (g == 0) TRACE(19, q);
-        float x[XK];
-        if (level) {
-          const float2 ni = S.nrm_i[e];
-          x[0] = ni.x;
-          x[1] = ni.y;
-          x[2] = 0.0f;
-          x[5] = unr_on && oi.y <= autov ? 1.0f : 0.0f;
-        } else {
-          const float4 no = S.nrm_o[e];
-          x[0] = no.x;
-          x[1] = no.y;
-          x[2] = no.z;
-          x[5] = 0.0f;
-        }
-        x[3] = static_cast<float>((t - m6) * r6);
-        x[4] = static_cast<float>((lt - m7) * r7);
-        x[6] = 1.0f;
-        x[7] = 0.0f;
-#pragma unroll
-        for (int f = 0; f < XK; ++f) x[f] *= one;  // padding / invalid rows: all zero
-        t *= static_cast<double>(level ? oi.y : oi.x);
-        const double2 l2 = S.l2[e];
-        lt += level ? l2.y : l2.x;
-        float hl[16];
-#pragma unroll
-        for (int f = 0; f < XK; f += 2) {
-          hl[f] = tf32_trunc(x[f]);
-          hl[f + 1] = tf32_trunc(x[f + 1]);
-          const float2 l = fsub2(make_float2(x[f], x[f + 1]), make_float2(hl[f], hl[f + 1]));
-          hl[XK + f] = l.x;
-          hl[XK + f + 1] = l.y;
-        }
-        const int s = static_cast<int>(q % XS);
-        if (g == 0) TRACE(20, q);
-        mbar_wait(&S.x_empty[s], static_cast<uint32_t>(((q / XS) & 1) ^ 1));
-        __syncwarp();
-        if (g == 0) TRACE(21, q);
-        tc_fence_after();
-        tmem_st16(tmem + lane + T_X + 16 * s, hl);
-        tmem_wait_st();
-        tc_fence_before();
-        warp_arrive(&S.x_full[s]);
-        if (g == 0) TRACE(0, q);
-      }
+    const EncodeCtx X{idx, idx32, idx_base, B, my_tiles, size, err, tmem,
+                      static_cast<uint32_t>((g & ~31) << 16), g, m6, r6, m7, r7};
+    switch (na) {  // (kernels.py: 4 axes for 1-D ops, 5 depthwise, 6 the 2-D ops)
+      case 6: encode_loop<6>(S, X); break;
+      case 5: encode_loop<5>(S, X); break;
+      case 4: encode_loop<4>(S, X); break;
+      case 3: encode_loop<3>(S, X); break;
+      case 2: encode_loop<2>(S, X); break;
+      default: encode_loop<1>(S, X); break;
     }
   } else if (wg == 5) {
-    setmaxnreg_dec<REG_MMA>();
+    setmaxnreg<REG_MMA>();
     // ===================== MMA: fixed issue order, blocking waits, one elected lane issues =====
     // Each wait parks the warp in hardware until the phase completes (no polling: a
     // polling warp costs its SMSP neighbours issue slots).
@@ -466,7 +579,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         const uint32_t ph = static_cast<uint32_t>(t & 1);
         // GEMM3: U (TMEM) x H0 into the head accumulator, once the head warps have read
         // D4 of the previous tile out of it
-        wait_bar(&S.u_full, ph);
+        mbar_wait_sleep<KT_HEAD_SLEEP>(&S.u_full, ph);
         wait_bar(&S.d4_empty, ph ^ 1);
         const uint32_t ah = tmem + T_Z, al = ah + 64;
         if (elect_one()) {
@@ -481,7 +594,9 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         }
         __syncwarp();
         // GEMM4: Z1 (TMEM, written over U) x H1, same accumulator (the head warps have read D3)
-        wait_bar(&S.z_full, ph);
+        mbar_wait_sleep<64>(&S.z_full, ph);
+        __syncwarp();
+        tc_fence_after();
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
@@ -497,7 +612,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       }
     }
   } else if (wg == 2) {
-    setmaxnreg_inc<REG_R>();
+    setmaxnreg<REG_R>();
     // ===================== R: ReLU(D1) -> R (hi, lo) in TMEM; thread = lane = graph ===============
     const int quad = warp & 3;
     const int g = 32 * quad + (tid & 31);
@@ -536,7 +651,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       if (g == 0) TRACE(6, q);
     }
   } else if (wg >= 3) {
-    setmaxnreg_inc<REG_RO>();
+    setmaxnreg<REG_RO>();
     // ===================== readout: thread = lane = graph, 16 channels =========================
     const int quad = warp & 3, eh = wg - 3;
 
@@ -633,7 +748,8 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       if (tr) TRACE(9, ti);
       ++ti;
     }
-  } else {  // (the head keeps the launch's 80 registers: REG_HEAD)
+  } else {
+    setmaxnreg<REG_HEAD>();
     // ===================== head: thread = lane = graph, all 64 channels ===========================
     const int quad = warp;
     const int g = 32 * quad + (tid & 31);
@@ -642,12 +758,12 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     const bool tr = g == 0;
     for (int64_t ti = 0; ti < my_tiles; ++ti) {
       const uint32_t ph = static_cast<uint32_t>(ti & 1);
-      mbar_wait(&S.d3_full, ph);
+      mbar_wait_sleep<KT_HEAD_SLEEP>(&S.d3_full, ph);
       __syncwarp();
       if (tr) TRACE(10, ti);
       tc_fence_after();
-      const int64_t v = S.vtile[ti % 3][g];  // this tile's indices; the slot goes back to the encode
-      warp_arrive(&S.v_free[ti % 3]);
+      const int64_t v = S.vtile[ti & 3][g];  // this tile's indices; the slot goes back to the encode
+      warp_arrive(&S.v_free[ti & 3]);
 #pragma unroll
       for (int h = 0; h < 4; ++h) {  // D3 columns 16 h .. 16 h + 15 -> Z1 = ReLU(D3 + b0), hi / lo
         float z[16], hi[16], lo[16];
@@ -662,7 +778,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       tmem_wait_st();
       tc_fence_before();
       warp_arrive(&S.z_full);
-      mbar_wait(&S.d4_full, ph);
+      mbar_wait_sleep<KT_HEAD_SLEEP>(&S.d4_full, ph);
       __syncwarp();
       if (tr) TRACE(11, ti);
       tc_fence_after();

@@ -128,6 +128,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 #endif
 }
 
+// Wait for a phase that is typically far off (a warp idle for most of a tile): probe, then
+// sleep between probes, so the waiting warp issues a handful of instructions instead of
+// spinning through try_wait retries in its SMSP neighbours' issue slots.
+template <int SLEEP_NS>
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase);
+
 // Non-blocking probe: true once the phase with parity `phase` has completed.
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
   uint32_t ok;
@@ -139,6 +145,11 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
       : "r"(smem_u32(bar)), "r"(phase)
       : "memory");
   return ok != 0;
+}
+
+template <int SLEEP_NS>
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+  while (!mbar_test(bar, phase)) __nanosleep(SLEEP_NS);
 }
 
 // generic-proxy smem writes -> visible to the tensor core (async proxy)

@@ -41,4 +41,7 @@ for q in range(0, 64):
 print("tile    G3_iss   G4_iss   H_u_arr  H_d3    H_d4    H_done")
 for ti in range(6):
     print(f"{ti:4d} " + " ".join(f"{buf[e, ti] - t0:8d}" for e in (3, 4, 9, 10, 11, 12)))
+print("encode tile: top  ok  phase1_start  first_row")
+for ti in range(6):
+    print(ti, buf[24, ti] - t0, buf[25, ti] - t0, buf[26, ti] - t0, buf[19, ti * 12] - t0)
 print("kernel entry / prologue / exit:", buf[27, 0] - t0, buf[28, 0] - t0, buf[29, 0] - t0)
