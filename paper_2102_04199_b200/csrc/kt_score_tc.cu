@@ -70,21 +70,56 @@ namespace tcs {
 
 using namespace kt::tc;
 
-constexpr int NT = 768;  // 24 warps = 6 warpgroups (roles by warpgroup, see the header)
-// per-warpgroup register budgets (setmaxnreg): 6 warps share an SMSP's 512 registers per
-// lane; the launch gives each 80, the roles rebalance them (sum <= 6 x 80)
+#ifndef KT_R2
+#define KT_R2 1  // two R warpgroups, one per chunk parity
+#endif
+constexpr int WG_R = 2, WG_RO = WG_R + 1 + KT_R2, WG_MMA = WG_RO + 2;  // warpgroup of each role
+constexpr int NWG = WG_MMA + 1;
+constexpr int NT = 128 * NWG;  // (roles by warpgroup, see the header)
+// per-warpgroup register budgets (setmaxnreg): the NWG warps of an SMSP share its 512
+// registers per lane; the launch gives each REG_BASE, the roles rebalance them
+constexpr int REG_BASE = (512 / NWG) & ~7;
+#if KT_R2
+constexpr int REG_HEAD = 64, REG_ENC = 80, REG_R = 56, REG_RO = 96, REG_MMA = 56;
+#else
 constexpr int REG_HEAD = 72, REG_ENC = 80, REG_R = 56, REG_RO = 104, REG_MMA = 64;
-static_assert(REG_HEAD + REG_ENC + REG_R + 2 * REG_RO + REG_MMA <= 6 * 80, "register budget");
+#endif
+static_assert(REG_HEAD + REG_ENC + (1 + KT_R2) * REG_R + 2 * REG_RO + REG_MMA <= NWG * REG_BASE, "register budget");
 constexpr int GT = 128;   // graphs per tile (one TMEM lane each)
 constexpr int H = 64;
 constexpr int XK = 8;     // folded layer-1 operand width (one tf32 K-step)
 constexpr int XS = 4;     // X ring slots
+#ifndef KT_DR
+#define KT_DR 0
+#endif
+#if KT_DR
+// D1 and R share buffers: GEMM1 writes D1 into columns 0-31 of DR[b], the R warps
+// overwrite them with R hi and put R lo in columns 32-63, GEMM2 reads both; a buffer
+// returns to GEMM1 when GEMM2 is done with it.  Three buffers in the TMEM two D1 + two R
+// buffers took, so GEMM1, R and GEMM2 each run up to three chunks apart.
+constexpr int NB = 3;     // DR buffers
+constexpr int N1 = NB, NR = NB;
+#else
 constexpr int N1 = 2;     // D1 buffers
 constexpr int NR = 2;     // R buffers
+#endif
 constexpr int N2 = 2;     // D2 buffers
 constexpr int TAB = 448;
 #ifndef KT_ENC_PIPE
 #define KT_ENC_PIPE 0
+#endif
+// per-role wait flavour: 0 = try_wait (hardware-suspended), N = probe + N ns sleeps
+#ifndef KT_SLEEP_MMA
+#define KT_SLEEP_MMA 0
+#endif
+#ifndef KT_SLEEP_R
+#define KT_SLEEP_R 0
+#endif
+#ifndef KT_SLEEP_RO
+#define KT_SLEEP_RO 0
+#endif
+#ifndef KT_SLEEP_ENC
+#define KT_SLEEP_ENC 0
 #endif
 #ifndef KT_HEAD_SLEEP
 #define KT_HEAD_SLEEP 256  // ns between probes of the head warpgroup's (long) waits
@@ -92,9 +127,17 @@ constexpr int TAB = 448;
 
 // TMEM column map (512 allocated)
 constexpr uint32_t T_X = 0;                  // X[s]: hi at 16 s, lo at 16 s + 8
+#if KT_DR
+constexpr uint32_t T_D1 = T_X + 16 * XS;     // DR[b] at T_D1 + 64 b: D1, then R hi (cols 0-31) / lo (32-63)
+constexpr uint32_t T_R = T_D1;
+constexpr int D1_STRIDE = 64;
+constexpr uint32_t T_D2 = T_R + 64 * NR;     // D2[b] at T_D2 + 32 b
+#else
 constexpr uint32_t T_D1 = T_X + 16 * XS;     // D1[b] at T_D1 + 32 b
 constexpr uint32_t T_R = T_D1 + 32 * N1;     // R[b]: hi at T_R + 64 b, lo at +32
+constexpr int D1_STRIDE = 32;
 constexpr uint32_t T_D2 = T_R + 64 * NR;     // D2[b] at T_D2 + 32 b
+#endif
 constexpr uint32_t T_D34 = T_D2 + 32 * N2;   // head accumulator: D3, then D4 (64 columns)
 constexpr uint32_t T_Z = T_D34 + 64;         // head A operand, U then Z1 = ReLU(D3 + b0): hi at T_Z, lo at +64
 static_assert(T_Z + 128 <= 512, "TMEM budget: 512 columns");
@@ -134,6 +177,28 @@ struct __align__(1024) Smem {
 
 __device__ __forceinline__ float relu(float v) { return fmaxf(v, 0.0f); }
 
+// Position in an N-deep ring of buffers: slot i and the parity of its current phase
+// (no 64-bit % or / per chunk: N = 3 rings would pay a 64-bit division each time).
+template <int N>
+struct Ring {
+  int i = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ void next() {
+    if (++i == N) {
+      i = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
+template <int NS>
+__device__ __forceinline__ void role_wait(uint64_t* bar, uint32_t parity) {
+  if constexpr (NS == 0)
+    mbar_wait(bar, parity);
+  else
+    mbar_wait_sleep<NS>(bar, parity);
+}
+
 // Warpgroup register reallocation (all four warps of a warpgroup execute it).
 template <int N>
 __device__ __forceinline__ void setmaxnreg_inc() {
@@ -141,11 +206,11 @@ __device__ __forceinline__ void setmaxnreg_inc() {
 }
 template <int N>
 __device__ __forceinline__ void setmaxnreg_dec();
-// to N registers from the launch's 80, in whichever direction
+// to N registers from the launch's REG_BASE, in whichever direction
 template <int N>
 __device__ __forceinline__ void setmaxnreg() {
-  if constexpr (N > 80) setmaxnreg_inc<N>();
-  if constexpr (N < 80) setmaxnreg_dec<N>();
+  if constexpr (N > REG_BASE) setmaxnreg_inc<N>();
+  if constexpr (N < REG_BASE) setmaxnreg_dec<N>();
 }
 template <int N>
 __device__ __forceinline__ void setmaxnreg_dec() {
@@ -306,7 +371,7 @@ __device__ __forceinline__ void encode_hand_over(Smem& S, const EncodeCtx& X, in
   }
   const int s = static_cast<int>(q % XS);
   if (X.g == 0) TRACE(20, q);
-  mbar_wait(&S.x_empty[s], static_cast<uint32_t>(((q / XS) & 1) ^ 1));
+  role_wait<KT_SLEEP_ENC>(&S.x_empty[s], static_cast<uint32_t>(((q / XS) & 1) ^ 1));
   __syncwarp();
   if (X.g == 0) TRACE(21, q);
   tc_fence_after();
@@ -429,7 +494,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     mbar_init(&S.d4_empty, 4);
     for (int i = 0; i < 4; ++i) mbar_init(&S.v_free[i], 4);
   }
-  if (warp == 20) tmem_alloc(&S.tmem_base, 512);
+  if (warp == 4 * WG_MMA) tmem_alloc(&S.tmem_base, 512);
   if (key_hist)
     for (int i = tid; i < 2048; i += NT) S.khist[i] = 0;
   __syncthreads();
@@ -499,7 +564,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
   const int64_t n_chunks = my_tiles * C;
   const uint64_t size = T.space_size;
 
-  const int wg = warp >> 2;  // 0 head, 1 encode, 2 R, 3-4 readout, 5 MMA issue
+  const int wg = warp >> 2;  // 0 head, 1 encode, WG_R.. R, WG_RO.. readout, WG_MMA MMA issue
   if (wg == 1) {
     setmaxnreg<REG_ENC>();
     // ===================== encode: thread = graph; one folded operand row per chunk =========
@@ -517,29 +582,35 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       case 2: encode_loop<2>(S, X); break;
       default: encode_loop<1>(S, X); break;
     }
-  } else if (wg == 5) {
+  } else if (wg == WG_MMA) {
     setmaxnreg<REG_MMA>();
     // ===================== MMA: fixed issue order, blocking waits, one elected lane issues =====
     // Each wait parks the warp in hardware until the phase completes (no polling: a
     // polling warp costs its SMSP neighbours issue slots).
     const uint32_t id32 = idesc_tf32(128, 32), id64 = idesc_tf32(128, 64);
     auto wait_bar = [&](uint64_t* bar, uint32_t parity) {
-      mbar_wait(bar, parity);
+      role_wait<KT_SLEEP_MMA>(bar, parity);
       __syncwarp();
       tc_fence_after();
     };
     // Three independent issue streams, one warp each: tcgen05.commit tracks the MMAs of
     // the issuing thread only, so GEMM1s, GEMM2s and the head GEMMs need no common
     // program order -- their data dependencies all go through the ring barriers.
-    if (warp == 20) {
+    if (warp == 4 * WG_MMA) {
       int c = 0;  // chunk within the tile -> loop row k = C - 1 - c (the encode order)
-      for (int64_t q = 0; q < n_chunks; ++q) {
-        const int s = static_cast<int>(q % XS), b = static_cast<int>(q % N1);
+      Ring<XS> rx;
+      Ring<N1> r1;
+      for (int64_t q = 0; q < n_chunks; ++q, rx.next(), r1.next()) {
+        const int s = rx.i, b = r1.i;
         if ((tid & 31) == 0) TRACE(22, q);
-        wait_bar(&S.x_full[s], static_cast<uint32_t>((q / XS) & 1));
-        wait_bar(&S.d1_empty[b], static_cast<uint32_t>(((q / N1) & 1) ^ 1));
+        wait_bar(&S.x_full[s], rx.ph);
+#if KT_DR
+        wait_bar(&S.r_empty[b], r1.ph ^ 1);  // GEMM2 of chunk q - NB is done
+#else
+        wait_bar(&S.d1_empty[b], r1.ph ^ 1);
+#endif
         if ((tid & 31) == 0) TRACE(23, q);
-        const uint32_t xh = tmem + T_X + 16 * s, xl = xh + XK, d = tmem + T_D1 + 32 * b;
+        const uint32_t xh = tmem + T_X + 16 * s, xl = xh + XK, d = tmem + T_D1 + D1_STRIDE * b;
         const int k = C - 1 - c;
         if (elect_one()) {
           mma_tf32_ts(d, xh, kdesc(S.b1h[k], XK, 0), id32, 0);
@@ -552,13 +623,14 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         __syncwarp();
         if (++c == C) c = 0;
       }
-    } else if (warp == 21) {
-      for (int64_t q = 0; q < n_chunks; ++q) {
-
-        const int b = static_cast<int>(q % NR), b2 = static_cast<int>(q % N2);
+    } else if (warp == 4 * WG_MMA + 1) {
+      Ring<NR> rr;
+      Ring<N2> r2;
+      for (int64_t q = 0; q < n_chunks; ++q, rr.next(), r2.next()) {
+        const int b = rr.i, b2 = r2.i;
         if ((tid & 31) == 0) TRACE(17, q);
-        wait_bar(&S.r_full[b], static_cast<uint32_t>((q / NR) & 1));
-        wait_bar(&S.d2_empty[b2], static_cast<uint32_t>(((q / N2) & 1) ^ 1));
+        wait_bar(&S.r_full[b], rr.ph);
+        wait_bar(&S.d2_empty[b2], r2.ph ^ 1);
         if ((tid & 31) == 0) TRACE(18, q);
         const uint32_t rh = tmem + T_R + 64 * b, rl = rh + 32, d = tmem + T_D2 + 32 * b2;
         if (elect_one()) {
@@ -574,7 +646,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         }
         __syncwarp();
       }
-    } else if (warp == 22) {
+    } else if (warp == 4 * WG_MMA + 2) {
       for (int64_t t = 0; t < my_tiles; ++t) {
         const uint32_t ph = static_cast<uint32_t>(t & 1);
         // GEMM3: U (TMEM) x H0 into the head accumulator, once the head warps have read
@@ -611,28 +683,42 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         __syncwarp();
       }
     }
-  } else if (wg == 2) {
+  } else if (wg >= WG_R && wg < WG_RO) {
     setmaxnreg<REG_R>();
     // ===================== R: ReLU(D1) -> R (hi, lo) in TMEM; thread = lane = graph ===============
     const int quad = warp & 3;
     const int g = 32 * quad + (tid & 31);
     const uint32_t lane = static_cast<uint32_t>((32 * quad) << 16);
-    for (int64_t q = 0; q < n_chunks; ++q) {
-      const int b1 = static_cast<int>(q % N1), b = static_cast<int>(q % NR);
-      mbar_wait(&S.d1_full[b1], static_cast<uint32_t>((q / N1) & 1));
+#if KT_R2
+    // two R warpgroups, chunks of parity wg - WG_R each: buffer (q % 2) is theirs alone
+    static_assert(N1 == 2 && NR == 2, "R parity split needs 2-deep D1 / R rings");
+    Ring<1> r1, rr;
+    r1.i = rr.i = wg - WG_R;
+    for (int64_t q = wg - WG_R; q < n_chunks; q += 2, r1.ph ^= 1u, rr.ph ^= 1u) {
+#else
+    Ring<N1> r1;
+    Ring<NR> rr;
+    for (int64_t q = 0; q < n_chunks; ++q, r1.next(), rr.next()) {
+#endif
+      const int b1 = r1.i, b = rr.i;
+      role_wait<KT_SLEEP_R>(&S.d1_full[b1], r1.ph);
       __syncwarp();
       if (g == 0) TRACE(5, q);
       tc_fence_after();
       float v[32];
-      tmem_ld16(tmem + lane + T_D1 + 32 * b1, v);
-      tmem_ld16(tmem + lane + T_D1 + 32 * b1 + 16, v + 16);
+      tmem_ld16(tmem + lane + T_D1 + D1_STRIDE * b1, v);
+      tmem_ld16(tmem + lane + T_D1 + D1_STRIDE * b1 + 16, v + 16);
       tmem_wait_ld();
       if (g == 0) TRACE(13, q);
+#if !KT_DR
       tc_fence_before();
       warp_arrive(&S.d1_empty[b1]);
+#endif
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = relu(v[j]);
-      mbar_wait(&S.r_empty[b], static_cast<uint32_t>(((q / NR) & 1) ^ 1));  // GEMM2 of chunk q-NR read R[b]
+#if !KT_DR  // (with shared DR buffers the buffer is this stage's until it arrives r_full)
+      role_wait<KT_SLEEP_R>(&S.r_empty[b], rr.ph ^ 1);  // GEMM2 of q-NR read R[b]
+#endif
       __syncwarp();
       if (g == 0) TRACE(14, q);
       tc_fence_after();
@@ -650,10 +736,10 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       warp_arrive(&S.r_full[b]);
       if (g == 0) TRACE(6, q);
     }
-  } else if (wg >= 3) {
+  } else if (wg >= WG_RO && wg < WG_MMA) {
     setmaxnreg<REG_RO>();
     // ===================== readout: thread = lane = graph, 16 channels =========================
-    const int quad = warp & 3, eh = wg - 3;
+    const int quad = warp & 3, eh = wg - WG_RO;
 
     const int g = 32 * quad + (tid & 31);
     const uint32_t lane = static_cast<uint32_t>((32 * quad) << 16);
@@ -673,7 +759,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
 #pragma unroll
         for (int j = 0; j < 16; ++j) mx[j] = 0.0f;  // max_k ReLU(s_k) = max(0, max_k s_k)
       }
-      mbar_wait(&S.d2_full[b], static_cast<uint32_t>((p / N2) & 1));
+      role_wait<KT_SLEEP_RO>(&S.d2_full[b], static_cast<uint32_t>((p / N2) & 1));
       __syncwarp();
       if (tr) TRACE(7, p);
       tc_fence_after();
@@ -815,7 +901,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 20) {
+  if (warp == 4 * WG_MMA) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
