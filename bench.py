@@ -254,7 +254,9 @@ def bench_maml(m, corpus, steps, warmup, first_order=True, tasks_per_step=32):
     bufs = tr._buffers(plan)
     for s in range(warmup):
         tr.step(plan, bufs, s)
-    graph = tr.capture(plan, bufs, warmup, warmup + steps) if ws == 1 else None  # NCCL calls stay eager
+    # one CUDA graph for the timed steps; data parallel: the NCCL all-gathers are captured too
+    # (the gloo debug backend stages through the host and stays eager)
+    graph = tr.capture(plan, bufs, warmup, warmup + steps) if ws == 1 or dist.get_backend() == "nccl" else None
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -276,8 +278,9 @@ def bench_maml(m, corpus, steps, warmup, first_order=True, tasks_per_step=32):
             "config": f"C3: 3-way 2-shot, {tasks_per_step} tasks/outer step, 1 inner step, "
                       f"{'FO' if first_order else 'SO'}, "
                       "frozen GCN (corpus embedded once; exact, the GCN does not move in meta_step), super N=25, "
-                      f"47x200 synthetic corpus; 2 launches/step, {'one CUDA graph replay' if ws == 1 else 'eager'}; "
-                      f"tasks sharded over {ws} GPU(s) with an NCCL all-reduce of sum_i g_i per step",
+                      f"47x200 synthetic corpus; 2 launches/step, {'one CUDA graph replay' if graph is not None else 'eager'}; "
+                      f"tasks sharded over {ws} GPU(s): per-task gradient rows all-gathered (NCCL) and summed "
+                      "in task order on every rank (bit-identical to one GPU)",
             "final_query_loss": float(st[-1, 1])}
 
 

@@ -310,6 +310,19 @@ int kt_maml_step(const kt_dims* dims, float* theta, const float* u, const float*
                  const int64_t* s_idx, const int64_t* q_off, const int64_t* q_idx, int32_t T, float alpha,
                  int32_t inner_steps, int32_t first_order, float beta, float* g_sum, double* stats,
                  void* workspace, int64_t workspace_bytes, void* stream);
+/* Data-parallel meta_step, bit-identical to kt_maml_step: kt_maml_task_grads
+ * writes the per-task outer gradients g_i (maml_outer_grad, meta.py:167-196) of this rank's
+ * contiguous task share as rows g_rows (T x n_head_params) and per-task (support, query)
+ * losses (T x 2), no reduction; after an all-gather of the rows in task order,
+ * kt_task_sum_update sums all T rows in task order in fp64 into g_sum (and the losses into
+ * stats) and, if theta != NULL, applies theta -= beta * g_sum with kt_maml_step's
+ * arithmetic (meta.py:249-252: sum, not mean). */
+int kt_maml_task_grads(const kt_dims* dims, const float* theta, const float* u, const float* y,
+                       const int64_t* s_off, const int64_t* s_idx, const int64_t* q_off, const int64_t* q_idx,
+                       int32_t T, float alpha, int32_t inner_steps, int32_t first_order, float* g_rows,
+                       float* losses, void* workspace, int64_t workspace_bytes, void* stream);
+int kt_task_sum_update(const kt_dims* dims, const float* g_rows, const float* losses, int32_t T, float beta,
+                       float* theta, float* g_sum, double* stats, void* stream);
 
 /* ---- ranking (search.py:257-264) ------------------------------------------------------ */
 /* Top-k of (score desc, index asc) over B candidates; `visited` (sorted int64,

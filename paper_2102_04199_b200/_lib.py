@@ -110,6 +110,9 @@ _SIGS = {
     "kt_maml_workspace_bytes": (i64, [ctypes.POINTER(Dims), i32, i32, i32]),
     "kt_maml_tasks": (ctypes.c_int, [ctypes.POINTER(Dims), vp, vp, vp, vp, vp, vp, vp, i32, f32, i32, i32, vp, vp,
                                      vp, i64, vp]),
+    "kt_maml_task_grads": (ctypes.c_int, [ctypes.POINTER(Dims), vp, vp, vp, vp, vp, vp, vp, i32, f32, i32, i32, vp,
+                                          vp, vp, i64, vp]),
+    "kt_task_sum_update": (ctypes.c_int, [ctypes.POINTER(Dims), vp, vp, i32, f32, vp, vp, vp, vp]),
     "kt_maml_step": (ctypes.c_int, [ctypes.POINTER(Dims), vp, vp, vp, vp, vp, vp, vp, i32, f32, i32, i32, f32, vp,
                                     vp, vp, i64, vp]),
     "kt_sweep_host": (ctypes.c_int, [vp, ctypes.POINTER(Dims), vp, vp, i32, i64, vp, vp, i32, vp, vp, vp, vp, vp,

@@ -829,6 +829,48 @@ int kt_maml_tasks(const kt_dims* dims, const float* theta, const float* u, const
   return check_launch("kt_maml_tasks");
 }
 
+// Data-parallel meta_step in two halves whose composition is bit-identical to kt_maml_step
+// on one GPU: every rank writes the per-task gradient rows of its contiguous task share,
+// the rows are all-gathered in task order, and every rank sums all of them in task order.
+int kt_maml_task_grads(const kt_dims* dims, const float* theta, const float* u, const float* y,
+                       const int64_t* s_off, const int64_t* s_idx, const int64_t* q_off, const int64_t* q_idx,
+                       int32_t T, float alpha, int32_t inner_steps, int32_t first_order, float* g_rows,
+                       float* losses, void* workspace, int64_t workspace_bytes, void* stream) {
+  using namespace kt;
+  KT_REQUIRE(dims && theta && u && y && s_off && s_idx && q_off && q_idx && g_rows && losses && workspace, KT_E_ARG,
+             "kt_maml_task_grads: null pointer");
+  KT_REQUIRE(T > 0, KT_E_EMPTY, "kt_maml_task_grads: empty task batch");
+  KT_REQUIRE(inner_steps >= 1, KT_E_ARG, "kt_maml_task_grads: inner_steps must be >= 1");
+  KT_REQUIRE(workspace_bytes >= kt_maml_workspace_bytes(dims, T, inner_steps, first_order), KT_E_ARG,
+             "kt_maml_task_grads: workspace too small");
+  int rc = meta::check_head(*dims);
+  if (rc) return rc;
+  const bool so = !first_order;
+  const meta::Head h = meta::fit_rows(*dims, 8, true, so);
+  static SmemAttr cached;
+  const size_t smem = meta::task_smem(h, so);
+  rc = meta::set_smem(meta::maml_task_kernel, smem, cached);
+  if (rc) return rc;
+  meta::TaskSet ts{u, y, s_off, s_idx, q_off, q_idx};
+  meta::maml_task_kernel<<<T, meta::NT, smem, as_stream(stream)>>>(*dims, h.RC, theta, ts, T, alpha, inner_steps,
+                                                                   first_order, static_cast<float*>(workspace),
+                                                                   g_rows, losses);
+  note_launches(1);
+  return check_launch("kt_maml_task_grads");
+}
+
+int kt_task_sum_update(const kt_dims* dims, const float* g_rows, const float* losses, int32_t T, float beta,
+                       float* theta, float* g_sum, double* stats, void* stream) {
+  using namespace kt;
+  KT_REQUIRE(dims && g_rows && losses && g_sum, KT_E_ARG, "kt_task_sum_update: null pointer");
+  KT_REQUIRE(T > 0, KT_E_EMPTY, "kt_task_sum_update: empty task batch");
+  const int P = dims->n_head_params;
+  meta::task_sum_kernel<<<(P + 255) / 256, 256, 0, as_stream(stream)>>>(g_rows, T, P, g_sum, losses, stats, beta,
+                                                                       theta);
+  note_launches(1);
+  return check_launch("kt_task_sum_update");
+}
+
 int kt_maml_step(const kt_dims* dims, float* theta, const float* u, const float* y, const int64_t* s_off,
                  const int64_t* s_idx, const int64_t* q_off, const int64_t* q_idx, int32_t T, float alpha,
                  int32_t inner_steps, int32_t first_order, float beta, float* g_sum, double* stats, void* workspace,

@@ -666,9 +666,10 @@ def aggregate_batch(h, agg: AggParams, node_ptr=None) -> torch.Tensor:
         if b <= 0:
             raise DomainError("empty batch")
     u = torch.empty((b, 2 * d), dtype=torch.float32, device=dev)
+    wc = w.contiguous()  # (held: a bare pointer to a temporary could be reallocated before the launch)
     lib = _lib.load()
     with _on(dev):
-        _lib.check(lib.kt_readout(_lib.ptr(hh), d, b, n, _lib.ptr(np_t), _lib.ptr(w.contiguous()), _lib.ptr(u),
+        _lib.check(lib.kt_readout(_lib.ptr(hh), d, b, n, _lib.ptr(np_t), _lib.ptr(wc), _lib.ptr(u),
                                   _lib.stream_handle()), "aggregate_batch")
     return u
 
