@@ -95,14 +95,21 @@ __device__ __forceinline__ void dense(const Grp& G, const float* Ts, const float
   }
 }
 
-// Out (n x din) <- dZ W^T   (W is din x dout)
+// Out (n x din) <- dZ W^T   (W is din x dout).  Lanes of a warp own consecutive k, so a
+// plain c loop would read W[k dout + c] with a stride of dout words -- one shared-memory
+// bank for the whole warp when W sits in shared memory; each output instead starts its
+// (fixed-order) sum at c = k mod dout, which spreads the lanes over the banks.
 template <class Grp>
 __device__ __forceinline__ void dense_t(const Grp& G, const float* dZ, const float* __restrict__ W, float* Out,
                                         int n, int din, int dout, int D) {
   for (int e = G.r; e < n * din; e += G.n) {
     const int r = e / din, k = e - (e / din) * din;
     float acc = 0.0f;
-    for (int c = 0; c < dout; ++c) acc = fmaf(dZ[r * D + c], W[k * dout + c], acc);
+    int c = k % dout;
+    for (int j = 0; j < dout; ++j) {
+      acc = fmaf(dZ[r * D + c], W[k * dout + c], acc);
+      if (++c == dout) c = 0;
+    }
     Out[r * D + k] = acc;
   }
 }
