@@ -388,245 +388,7 @@ __global__ void __launch_bounds__(256) readout_kernel(const float* __restrict__ 
 }
 
 
-// ---- tensor-core layer: transform on tcgen05 (3xTF32), aggregation on the CUDA cores -------
-//
-// CTA = 4 warps = one tile of up to 128 rows (whole graphs); thread r owns row r,
-// which is also TMEM lane r.  Per tile:
-//   1. thread r holds its input row in registers (loaded one tile ahead), z-normalises
-//      fp64 rows, splits it hi/lo and tcgen05.st's both into TMEM (the A operand);
-//   2. one elected thread issues P = X W as 3 x (DIN/8) tcgen05.mma kind::tf32
-//      (A from TMEM, W^T hi/lo from smem, D in TMEM);
-//   3. thread r tcgen05.ld's P row r into a padded smem tile; after a CTA barrier it
-//      forms out_r = ReLU(sum_j a_rj P_j) over its CSR row and stores it to HBM.
-// Four CTAs per SM (128 TMEM columns each) overlap one another's load, MMA and
-// aggregation phases.  Per graph the CUDA cores issue ~10x fewer instructions than
-// the FFMA transform, so the kernel stays on the HBM roofline.
 constexpr int TC_ROWS = 128;
-constexpr int TC_PS = 36;  // P tile row stride (floats): float4 rows, spread banks
-
-template <int DIN, bool IN64>
-__global__ void __launch_bounds__(TC_ROWS, 4) gcn_layer_tc_kernel(LayerArgs a) {
-  constexpr int K = (DIN + 7) & ~7;   // MMA K (tf32: 8 per instruction)
-  constexpr int DOUT = 32;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  float* bh = reinterpret_cast<float*>(smem);   // W^T hi, K-major core matrices (N = 32 rows, K)
-  float* bl = bh + DOUT * K;                    // W^T lo
-  float* sP = bl + DOUT * K;                    // [128][TC_PS] transformed rows
-  int* s_rp = reinterpret_cast<int*>(sP + TC_ROWS * TC_PS);
-  const int rp_cap = a.n_pat * (KT_MAX_NODES + 1);
-  int* s_col = s_rp + ((rp_cap + 3) & ~3);
-  float* s_val = reinterpret_cast<float*>(s_col + MAXPNNZ);
-  uint8_t* s_mask = reinterpret_cast<uint8_t*>(s_val + MAXPNNZ);
-  __shared__ PatSmem P;
-  __shared__ double s_mean[KT_MAX_DIM], s_rstd[KT_MAX_DIM];
-  __shared__ __align__(8) uint64_t mma_bar;
-  __shared__ uint32_t tmem_slot;
-  __shared__ int64_t s_gptr[TC_ROWS + 1];  // row starts of the tile's graphs (tile-relative)
-  const int tid = threadIdx.x, warp = tid >> 5;
-
-  // ---- setup ---------------------------------------------------------------------------------
-  for (int e = tid; e < DOUT * K; e += TC_ROWS) {  // B = W^T: row n, column k
-    const int n = e / K, k = e - n * K;
-    const float v = k < DIN ? a.W[k * DOUT + n] : 0.0f;
-    const float h = tc::tf32_trunc(v);
-    const int off = tc::kmajor_offset(n, k, K) >> 2;
-    bh[off] = h;
-    bl[off] = v - h;
-  }
-  if (tid == 0) {
-    int rp = 0, nz = 0, mk = 0;
-    for (int p = 0; p < a.n_pat; ++p) {
-      P.n[p] = a.pat_n[p];
-      P.rp_off[p] = rp;
-      P.nz_off[p] = nz;
-      P.mask_off[p] = mk;
-      nz += a.pat_rp[rp + P.n[p]];
-      rp += P.n[p] + 1;
-      mk += P.n[p];
-    }
-    tc::mbar_init(&mma_bar, 1);
-  }
-  if (IN64)
-    for (int c = tid; c < DIN; c += TC_ROWS) {
-      s_mean[c] = a.fmean[c];
-      s_rstd[c] = 1.0 / a.fstd[c];
-    }
-  if (warp == 0) tc::tmem_alloc(&tmem_slot, 128);
-  __syncthreads();
-  {
-    int tot_rp = 0, tot_nz = 0, tot_mask = 0;
-    for (int p = 0; p < a.n_pat; ++p) {
-      tot_rp += P.n[p] + 1;
-      tot_mask += P.n[p];
-      tot_nz += a.pat_rp[P.rp_off[p] + P.n[p]];
-    }
-    for (int i = tid; i < tot_rp; i += TC_ROWS) s_rp[i] = a.pat_rp[i];
-    for (int i = tid; i < tot_nz; i += TC_ROWS) {
-      s_col[i] = a.pat_col[i];
-      s_val[i] = a.pat_val[i];
-    }
-    if (IN64 && a.pat_mask)
-      for (int i = tid; i < tot_mask; i += TC_ROWS) s_mask[i] = a.pat_mask[i];
-  }
-  tc::fence_async_smem();
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tmem = tmem_slot;
-  const uint32_t lane_addr = static_cast<uint32_t>((32 * warp) << 16);
-  const uint32_t T_AH = 0, T_AL = 32, T_D = 64;
-  const uint32_t idesc = tc::idesc_tf32(128, DOUT);
-  const bool masked = IN64 && a.pat_mask;
-  constexpr int esz = IN64 ? 8 : 4;
-  constexpr int NQ = DIN * esz / 16;  // 16-byte pieces per row
-
-  const int64_t n_tiles = (a.B + a.G - 1) / a.G;
-  float4 pf[NQ];
-  int64_t cur_r0 = 0;
-  int cur_rows = 0;
-  // row range of tile t and this thread's row (prefetch into registers)
-  auto load_tile = [&](int64_t t) {
-    const int64_t g0 = t * a.G;
-    const int64_t g1 = g0 + a.G < a.B ? g0 + a.G : a.B;
-    cur_r0 = tile_row0(a, g0);
-    cur_rows = static_cast<int>(tile_row0(a, g1) - cur_r0);
-    if (tid < cur_rows) {
-      const float4* src =
-          reinterpret_cast<const float4*>(static_cast<const unsigned char*>(a.in) + (cur_r0 + tid) * DIN * esz);
-#pragma unroll
-      for (int i = 0; i < NQ; ++i) pf[i] = __ldg(src + i);  // L1-allocating: a row's 16-B pieces share sectors
-    }
-  };
-  int64_t it = 0;
-  if (blockIdx.x < n_tiles) load_tile(blockIdx.x);
-  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
-    const int64_t g0 = t * a.G;
-    const int ng = static_cast<int>((g0 + a.G < a.B ? g0 + a.G : a.B) - g0);
-    const int64_t r0 = cur_r0;
-    const int rows = cur_rows;
-    // ---- 1. own row -> normalised fp32 -> hi / lo into TMEM ---------------------------------
-    float x[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) x[k] = 0.0f;
-    int my_g = -1, my_l = 0;
-    if (tid <= ng) s_gptr[tid] = tile_row0(a, g0 + tid) - r0;
-    __syncthreads();  // s_gptr ready; previous tile's sP reads done
-    if (tid < rows) {
-      my_g = 0;
-      while (my_g + 1 < ng && s_gptr[my_g + 1] <= tid) ++my_g;
-      my_l = tid - static_cast<int>(s_gptr[my_g]);
-      if constexpr (IN64) {
-        const int p = a.pat_id ? a.pat_id[g0 + my_g] : 0;
-        const bool on = !masked || s_mask[P.mask_off[p] + my_l];
-#pragma unroll
-        for (int i = 0; i < NQ; ++i) {
-          const double2 d = *reinterpret_cast<const double2*>(&pf[i]);
-          x[2 * i] = on ? static_cast<float>((d.x - s_mean[2 * i]) * s_rstd[2 * i]) : 0.0f;
-          x[2 * i + 1] = on ? static_cast<float>((d.y - s_mean[2 * i + 1]) * s_rstd[2 * i + 1]) : 0.0f;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < NQ; ++i) {
-          x[4 * i] = pf[i].x;
-          x[4 * i + 1] = pf[i].y;
-          x[4 * i + 2] = pf[i].z;
-          x[4 * i + 3] = pf[i].w;
-        }
-      }
-    }
-    {
-      float hi[K], lo[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        hi[k] = tc::tf32_trunc(x[k]);
-        lo[k] = x[k] - hi[k];
-      }
-#pragma unroll
-      for (int k0 = 0; k0 < K; k0 += 16) {
-        if (K - k0 >= 16) {
-          tc::tmem_st16(tmem + lane_addr + T_AH + k0, hi + k0);
-          tc::tmem_st16(tmem + lane_addr + T_AL + k0, lo + k0);
-        }
-      }
-      if constexpr (K % 16 == 8) {  // K = 8, 24, 40 ...: last 8 columns
-        float h16[16], l16[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          h16[k] = k < 8 ? hi[K - 8 + k] : 0.f;
-          l16[k] = k < 8 ? lo[K - 8 + k] : 0.f;
-        }
-        tc::tmem_st16(tmem + lane_addr + T_AH + K - 8, h16);
-        tc::tmem_st16(tmem + lane_addr + T_AL + K - 8, l16);
-      }
-      tc::tmem_wait_st();
-    }
-    // next tile's rows in flight while this tile computes
-    if (t + gridDim.x < n_tiles) load_tile(t + gridDim.x);
-    tc::tc_fence_before();
-    __syncthreads();
-    // ---- 2. P = X W on the tensor cores ------------------------------------------------------
-    if (warp == 0) {
-      tc::tc_fence_after();
-      if (tc::elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < K / 8; ++kk) {
-          tc::mma_tf32_ts(tmem + T_D, tmem + T_AH + 8 * kk, tc::kdesc(bh, K, kk), idesc, kk > 0);
-          tc::mma_tf32_ts(tmem + T_D, tmem + T_AH + 8 * kk, tc::kdesc(bl, K, kk), idesc, 1);
-          tc::mma_tf32_ts(tmem + T_D, tmem + T_AL + 8 * kk, tc::kdesc(bh, K, kk), idesc, 1);
-        }
-        tc::mma_commit(&mma_bar);
-      }
-      __syncwarp();
-    }
-    tc::mbar_wait(&mma_bar, static_cast<uint32_t>(it & 1));
-    __syncwarp();
-    tc::tc_fence_after();
-    {
-      float v[32];
-      tc::tmem_ld32(tmem + lane_addr + T_D, v);
-      tc::tmem_wait_ld();
-      float4* dst = reinterpret_cast<float4*>(sP + tid * TC_PS);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-    }
-    tc::tc_fence_before();
-    __syncthreads();
-    // ---- 3. out_r = ReLU(sum_j a_rj P_j) -> HBM ----------------------------------------------
-    if (tid < rows) {
-      const int p = a.pat_id ? a.pat_id[g0 + my_g] : 0;
-      const int* rp = s_rp + P.rp_off[p];
-      const int nz0 = P.nz_off[p];
-      const int base = static_cast<int>(s_gptr[my_g]);
-      float2 acc[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) acc[j] = make_float2(0.f, 0.f);
-      for (int e = rp[my_l]; e < rp[my_l + 1]; ++e) {
-        const float w = s_val[nz0 + e];
-        const float4* src = reinterpret_cast<const float4*>(sP + (base + s_col[nz0 + e]) * TC_PS);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float4 pv = src[j];
-          acc[2 * j] = ffma2s(w, make_float2(pv.x, pv.y), acc[2 * j]);
-          acc[2 * j + 1] = ffma2s(w, make_float2(pv.z, pv.w), acc[2 * j + 1]);
-        }
-      }
-      float4* out = reinterpret_cast<float4*>(a.out + (r0 + tid) * DOUT);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        float4 o = make_float4(acc[2 * j].x, acc[2 * j].y, acc[2 * j + 1].x, acc[2 * j + 1].y);
-        if (a.relu) o = make_float4(fmaxf(o.x, 0.f), fmaxf(o.y, 0.f), fmaxf(o.z, 0.f), fmaxf(o.w, 0.f));
-        __stcs(out + j, o);
-      }
-    }
-  }
-  tc::tc_fence_before();
-  __syncthreads();
-  if (warp == 0) {
-    tc::tc_fence_after();
-    tc::tmem_dealloc(tmem, 128);
-  }
-}
-
 
 // ---- pipelined tensor-core layer: TMA-staged tiles, aggregate-then-transform --------------------
 //
@@ -649,7 +411,7 @@ __global__ void __launch_bounds__(TC_ROWS, 4) gcn_layer_tc_kernel(LayerArgs a) {
 // -- so the row-per-thread reads and writes are bank-conflict free with no register
 // rotation (TMA undoes the swizzle on the way out).
 template <int DIN, bool IN64, int S, int OB, bool TM>
-__global__ void __launch_bounds__(TC_ROWS, 3)
+__global__ void __launch_bounds__(TC_ROWS, S == 1 ? 4 : 3)
     gcn_layer_pipe_kernel(LayerArgs a, int rp_cap, int nz_cap, const __grid_constant__ CUtensorMap tm_in,
                           const __grid_constant__ CUtensorMap tm_out) {
   constexpr int K = (DIN + 7) & ~7;
@@ -677,6 +439,7 @@ __global__ void __launch_bounds__(TC_ROWS, 3)
   __shared__ __align__(8) uint64_t mma_bar;
   __shared__ uint32_t tmem_slot;
   __shared__ int s_gptr[TC_ROWS + 1];
+  __shared__ float4 hub_s[TC_ROWS / 32][8];  // hub-row channel quads, per warp
   const int tid = threadIdx.x, warp = tid >> 5;
   (void)s_mean;
   (void)s_rstd;
@@ -786,10 +549,55 @@ __global__ void __launch_bounds__(TC_ROWS, 3)
   tc::tc_fence_after();
   const uint32_t tmem = tmem_slot;
   const uint32_t lane_addr = static_cast<uint32_t>((32 * warp) << 16);
-  const uint32_t T_AH = 0, T_AL = 32, T_D = 64;
+  const uint32_t T_AH = 0, T_AL = 32, T_D = 64;  // D double-buffered: T_D + 32 (it & 1)
   const uint32_t idesc = tc::idesc_tf32(128, DOUT);
 
-  int64_t it = 0;
+  // Epilogue of a tile whose MMA has completed: ReLU(D) -> output staging -> one bulk store.
+  // Runs one tile behind the aggregation, so tile t's MMA overlaps tile t-1's epilogue.
+  auto epilogue = [&](int64_t pit, int64_t pr0, int prows) {
+    float* ob = outb0 + (pit % OB) * (TC_ROWS * DOUT);
+    {
+      float v[32];
+      tc::tmem_ld32(tmem + lane_addr + T_D + 32 * static_cast<uint32_t>(pit & 1), v);
+      tc::tmem_wait_ld();
+      if (tid < prows) {
+        float4* dst = reinterpret_cast<float4*>(ob + tid * DOUT);
+        // rows are 128 B: store piece (q + r) % 8 at step q so that eight consecutive rows hit
+        // eight different bank groups; the registers are rotated to match (barrel shift)
+        const int orot = tid & 7;
+#pragma unroll
+        for (int sh = 1; sh < 8; sh <<= 1) {
+          if (!TM && (orot & sh)) {
+            float r[32];
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) r[4 * c + q] = v[4 * ((c + sh) & 7) + q];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) v[k] = r[k];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          if (a.relu) o = make_float4(fmaxf(o.x, 0.f), fmaxf(o.y, 0.f), fmaxf(o.z, 0.f), fmaxf(o.w, 0.f));
+          dst[TM ? (q ^ orot) : ((q + orot) & 7)] = o;
+        }
+      }
+    }
+    fence_proxy_async();
+    tc::tc_fence_before();
+    __syncthreads();  // (C) staging tile complete; TMEM D reads done
+    if (tid == 0) {
+      if constexpr (TM)
+        tma_store_2d(&tm_out, 0, static_cast<int>(pr0), ob);  // rows past the end are clipped
+      else
+        bulk_store(a.out + pr0 * DOUT, ob, static_cast<uint32_t>(prows) * DOUT * 4);
+    }
+  };
+
+  int64_t it = 0, prev_r0 = 0;
+  int prev_rows = 0;
   for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
     const int st = static_cast<int>(it % S);
     const int64_t g0 = t * a.G;
@@ -875,6 +683,42 @@ __global__ void __launch_bounds__(TC_ROWS, 3)
         hubs &= hubs - 1;
         const int h_lo = __shfl_sync(0xffffffffu, e_lo, src), h_hi = __shfl_sync(0xffffffffu, e_hi, src);
         const int h_base = __shfl_sync(0xffffffffu, base, src);
+        if constexpr (!IN64 && DIN == 32) {
+          // lane = (edge group eg, channel quad q): float4 partial sums over edges eg, eg + 4,
+          // ..., a fixed butterfly over the 4 edge groups, then the hub's lane reads the 8
+          // quads from a per-warp scratch -- 4 edge steps per lane instead of 13
+          const int q = lane & 7, eg = lane >> 3;
+          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int e = h_lo + eg; e < h_hi; e += 4) {
+            const int R = h_base + s_col[e];
+            const float w = s_val[e];
+            const float4 v = reinterpret_cast<const float4*>(tile + R * ROWB)[TM ? (q ^ (R & 7)) : q];
+            acc.x = fmaf(w, v.x, acc.x);
+            acc.y = fmaf(w, v.y, acc.y);
+            acc.z = fmaf(w, v.z, acc.z);
+            acc.w = fmaf(w, v.w, acc.w);
+          }
+#pragma unroll
+          for (int m = 8; m <= 16; m <<= 1) {
+            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, m);
+            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, m);
+            acc.z += __shfl_xor_sync(0xffffffffu, acc.z, m);
+            acc.w += __shfl_xor_sync(0xffffffffu, acc.w, m);
+          }
+          if (eg == 0) hub_s[warp][q] = acc;
+          __syncwarp();
+          if (lane == src)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 v = hub_s[warp][i];
+              y[4 * i] = v.x;
+              y[4 * i + 1] = v.y;
+              y[4 * i + 2] = v.z;
+              y[4 * i + 3] = v.w;
+            }
+          __syncwarp();
+          continue;
+        }
         float yc = 0.0f;
         if (lane < DIN)
           for (int e = h_lo; e < h_hi; ++e) {
@@ -895,6 +739,11 @@ __global__ void __launch_bounds__(TC_ROWS, 3)
           if (lane == src) y[k] = v;
         }
       }
+    }
+    if (it > 0) {  // MMA of the previous tile done: A free again, its D complete
+      tc::mbar_wait(&mma_bar, static_cast<uint32_t>((it - 1) & 1));
+      __syncwarp();
+      tc::tc_fence_after();
     }
     {
       float hi[K], lo[K];
@@ -937,57 +786,29 @@ __global__ void __launch_bounds__(TC_ROWS, 3)
       if (tc::elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < K / 8; ++kk) {
-          tc::mma_tf32_ts(tmem + T_D, tmem + T_AH + 8 * kk, tc::kdesc(bh, K, kk), idesc, kk > 0);
-          tc::mma_tf32_ts(tmem + T_D, tmem + T_AH + 8 * kk, tc::kdesc(bl, K, kk), idesc, 1);
-          tc::mma_tf32_ts(tmem + T_D, tmem + T_AL + 8 * kk, tc::kdesc(bh, K, kk), idesc, 1);
+          const uint32_t d = tmem + T_D + 32 * static_cast<uint32_t>(it & 1);
+          tc::mma_tf32_ts(d, tmem + T_AH + 8 * kk, tc::kdesc(bh, K, kk), idesc, kk > 0);
+          tc::mma_tf32_ts(d, tmem + T_AH + 8 * kk, tc::kdesc(bl, K, kk), idesc, 1);
+          tc::mma_tf32_ts(d, tmem + T_AL + 8 * kk, tc::kdesc(bh, K, kk), idesc, 1);
         }
         tc::mma_commit(&mma_bar);
       }
       __syncwarp();
     }
-    tc::mbar_wait(&mma_bar, static_cast<uint32_t>(it & 1));
+    // ---- 3. the previous tile's epilogue while this tile's MMA runs ---------------------------
+    if (it > 0) epilogue(it - 1, prev_r0, prev_rows);
+    prev_r0 = r0;
+    prev_rows = rows;
+  }
+  if (it > 0) {
+    if (tid == 0) {
+      if (OB == 1) bulk_wait_read0(); else bulk_wait_read1();
+    }
+    tc::mbar_wait(&mma_bar, static_cast<uint32_t>((it - 1) & 1));
     __syncwarp();
     tc::tc_fence_after();
-    // ---- 3. ReLU(D) -> output staging -> one bulk store -----------------------------------------
-    float* ob = outb0 + (it % OB) * (TC_ROWS * DOUT);
-    {
-      float v[32];
-      tc::tmem_ld32(tmem + lane_addr + T_D, v);
-      tc::tmem_wait_ld();
-      if (tid < rows) {
-        float4* dst = reinterpret_cast<float4*>(ob + tid * DOUT);
-        // rows are 128 B: store piece (q + r) % 8 at step q so that eight consecutive rows hit
-        // eight different bank groups; the registers are rotated to match (barrel shift)
-        const int orot = tid & 7;
-#pragma unroll
-        for (int sh = 1; sh < 8; sh <<= 1) {
-          if (!TM && (orot & sh)) {
-            float r[32];
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-#pragma unroll
-              for (int q = 0; q < 4; ++q) r[4 * c + q] = v[4 * ((c + sh) & 7) + q];
-#pragma unroll
-            for (int k = 0; k < 32; ++k) v[k] = r[k];
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-          if (a.relu) o = make_float4(fmaxf(o.x, 0.f), fmaxf(o.y, 0.f), fmaxf(o.z, 0.f), fmaxf(o.w, 0.f));
-          dst[TM ? (q ^ orot) : ((q + orot) & 7)] = o;
-        }
-      }
-    }
-    fence_proxy_async();
-    tc::tc_fence_before();
-    __syncthreads();  // (C) staging tile complete; TMEM D reads done
-    if (tid == 0) {
-      if constexpr (TM)
-        tma_store_2d(&tm_out, 0, static_cast<int>(r0), ob);  // rows past the end are clipped
-      else
-        bulk_store(a.out + r0 * DOUT, ob, static_cast<uint32_t>(rows) * DOUT * 4);
-    }
+    __syncthreads();  // (staging buffer free for every thread)
+    epilogue(it - 1, prev_r0, prev_rows);
   }
   if (tid == 0) bulk_wait0();
   tc::tc_fence_before();
@@ -1088,15 +909,16 @@ extern "C" int kt_gcn_layer(const void* in, int32_t in_f64, const double* fmean,
                      max_nodes <= agg::TC_ROWS &&
                      (reinterpret_cast<uintptr_t>(in) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
                      !(getenv("KT_AGG_FFMA") && getenv("KT_AGG_FFMA")[0] == '1');
-  const bool pipe_ok = tc_ok && !(getenv("KT_AGG_TC1") && getenv("KT_AGG_TC1")[0] == '1');
-  if (pipe_ok) {
+  if (tc_ok) {
     // TMA-staged tiles of whole graphs (<= 128 rows), three CTAs per SM
     a.G = agg::TC_ROWS / max_nodes;
     const int rp_cap = n_pat * (max_nodes + 1), nz_cap = pat_nnz;
     const size_t csr = ((static_cast<size_t>(rp_cap) + 3) & ~3) * 4 + ((static_cast<size_t>(nz_cap) + 3) & ~3) * 8 +
                        static_cast<size_t>(n_pat) * max_nodes + 16;
     const int64_t tiles = (B + a.G - 1) / a.G;
-    const int per_sm = 3;  // shared memory holds three CTAs per SM
+    const char* sob_env = getenv("KT_AGG_SOB");
+    const bool staged1 = d_in == 32 && nodes_per_graph > 0 && !(sob_env && sob_env[0] == '2');
+    const int per_sm = staged1 ? 4 : 3;  // CTAs per SM that shared memory holds
     const int tgrid = static_cast<int>(tiles < per_sm * kNumSMs ? tiles : per_sm * kNumSMs);
     CUtensorMap tm_in{}, tm_out{};
     auto plaunch = [&](auto kern, int K, int stage_bytes, int S, int OB, bool tm) {
@@ -1111,28 +933,17 @@ extern "C" int kt_gcn_layer(const void* in, int32_t in_f64, const double* fmean,
     } else if (nodes_per_graph > 0 && agg::tensor_maps(in, out, B * nodes_per_graph, a.G * nodes_per_graph,
                                                        &tm_in, &tm_out) &&
                !(getenv("KT_AGG_NOTM") && getenv("KT_AGG_NOTM")[0] == '1')) {
-      // (stages x output buffers 2x1, 3x1 and 2x2 measure the same, 72-73% of HBM peak)
-      plaunch(agg::gcn_layer_pipe_kernel<32, false, 2, 1, true>, 32, agg::TC_ROWS * 32 * 4, 2, 1, true);
+      // one input stage + one output tile (the epilogue already runs a tile behind the MMA),
+      // so four CTAs fit an SM: measured 0.77 of HBM peak against 0.75 for 2 x 1 at three
+      // CTAs per SM (2 x 2 and 3 x 1 drop to two CTAs per SM: 0.41); KT_AGG_SOB=21 for A/B
+      const char* sob = getenv("KT_AGG_SOB");
+      if (sob && sob[0] == '2' && sob[1] == '1')
+        plaunch(agg::gcn_layer_pipe_kernel<32, false, 2, 1, true>, 32, agg::TC_ROWS * 32 * 4, 2, 1, true);
+      else
+        plaunch(agg::gcn_layer_pipe_kernel<32, false, 1, 1, true>, 32, agg::TC_ROWS * 32 * 4, 1, 1, true);
     } else {
       plaunch(agg::gcn_layer_pipe_kernel<32, false, 3, 1, false>, 32, agg::TC_ROWS * 32 * 4, 3, 1, false);
     }
-  } else if (tc_ok) {
-    // tiles of whole graphs, <= 128 rows; 4 CTAs per SM (128 TMEM columns each)
-    a.G = agg::TC_ROWS / max_nodes;
-    const int K = (d_in + 7) & ~7;
-    const size_t tsm = 1024 + static_cast<size_t>(2 * 32 * K) * 4 + agg::TC_ROWS * agg::TC_PS * 4 +
-                       ((static_cast<size_t>(n_pat) * (KT_MAX_NODES + 1) + 3) & ~3) * 4 + agg::MAXPNNZ * 8 +
-                       static_cast<size_t>(n_pat) * KT_MAX_NODES + 64;
-    const int64_t tiles = (B + a.G - 1) / a.G;
-    const int tgrid = static_cast<int>(tiles < 4 * kNumSMs ? tiles : 4 * kNumSMs);
-    auto tlaunch = [&](auto kern) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsm));
-      kern<<<tgrid, agg::TC_ROWS, tsm, as_stream(stream)>>>(a);
-    };
-    if (d_in == 12)
-      tlaunch(agg::gcn_layer_tc_kernel<12, true>);
-    else
-      tlaunch(agg::gcn_layer_tc_kernel<32, false>);
   } else if (d_in == 12 && d_out == 32) {
     launch(agg::gcn_layer_kernel<12, 32>);
   } else if (d_in == 32 && d_out == 32) {

@@ -140,7 +140,7 @@ def test_streaming_errors(cuda_device, g_model):
         pm.aggregate_batch(torch.zeros((2, 3, 31), device="cuda"), m.agg)
 
 
-@pytest.mark.parametrize("variant", ["KT_AGG_NOTM", "KT_AGG_TC1", "KT_AGG_FFMA"])
+@pytest.mark.parametrize("variant", ["KT_AGG_NOTM", "KT_AGG_FFMA"])
 def test_layer_kernel_variants_agree(cuda_device, g_encode, g_model, monkeypatch, variant):
     """Every layer kernel gives the same H (fp32-level) on 50k super graphs: the default
     TMA-pipelined path (swizzled tensor maps for uniform graphs) against the 1-D bulk
