@@ -153,7 +153,7 @@ def hbm_peak():
 
 
 def load_traffic():
-    path = os.path.join(ROOT, "profiles", "r01_ncu_score.json")
+    path = os.path.join(ROOT, "profiles", "r02_ncu_score.json")
     try:
         with open(path) as f:
             d = json.load(f)
