@@ -59,6 +59,11 @@ class KernelSpec:
         if self.padding < 0:
             raise DomainError(f"padding must be non-negative, got {self.padding}")
 
+    def key_parts(self) -> tuple:
+        """Identity of the kernel for seeded draws (reference kernels.py:74-83)."""
+        return (self.op_type, self.input_size, self.in_channels, self.out_channels, self.kernel_size,
+                self.stride, self.padding)
+
     def signature(self) -> str:
         return "/".join(
             str(v)

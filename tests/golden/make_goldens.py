@@ -31,6 +31,8 @@ Everything is keyed by `rng_from` so reruns are byte-identical.  Outputs:
                  sgd_step at batch 512 mixed ops, raw and super, kink-free and unfiltered
   metatrain.npz  meta_train (meta.py:260-268): theta and CSV log, FO 6 steps / SO 3 steps
   rng.npz        raw rng_from streams for a set of keys (util.py:51-55)
+  hworacle.npz   the synthetic hardware oracle's measure() (oracle.py:142-241), all ops, two
+                 built-in platforms and a noise-free YAML profile
   dataset.npz    on that dataset: dataset_norms (meta.py:81-101) of the raw and the
                  augmented dataset_samples (harness.py:179-192), their labels and
                  kernel classes, grad (model.py:218) of an index-picked raw batch,
@@ -568,6 +570,31 @@ def rng_goldens():
     np.savez_compressed(os.path.join(OUT, "rng.npz"), **out)
 
 
+def hworacle_goldens():
+    """hworacle.npz: the reference's synthetic hardware oracle (oracle.py:142-241) on every op,
+    both built-in platforms and a noise-free YAML profile: measure() gflops / feasibility,
+    kernel_work_flops; configs as indices (sampled + edge cases)."""
+    from kerntune import oracle as ro
+
+    noiseless = ro.profile_from_yaml("name: flat\npeak_gflops: 5000\nl1_capacity: 8192\nshared_capacity: 65536\n"
+                                     "occupancy_knee: 64\nunroll_benefit: 0.2\ninfeasible_fraction: 0.0\n"
+                                     "noise_std_rel: 0.0\nseed: 7\n")
+    out = {}
+    for op in rk.OP_TYPES:
+        spec = spec_for(op)
+        space = rk.build_knob_space(spec)
+        idx = [rk.config_index(space, c) for c in rk.sample_configs(space, 48, rng_from("golden-hw", op))]
+        idx += [0, space.size - 1]
+        out[f"{op}/idx"] = np.array(idx, dtype=np.int64)
+        out[f"{op}/work"] = np.array(ro.kernel_work_flops(spec))
+        cfgs = [rk.index_config(space, i) for i in idx]
+        for tag, prof in (("A", ro.get_profile("platform-A")), ("B", ro.get_profile("platform-B")), ("flat", noiseless)):
+            ms = ro.batch_measure(spec, cfgs, prof, space)
+            out[f"{op}/{tag}/gflops"] = np.array([m.gflops for m in ms])
+            out[f"{op}/{tag}/feasible"] = np.array([m.feasible for m in ms])
+    np.savez_compressed(os.path.join(OUT, "hworacle.npz"), **out)
+
+
 def main():
     if sys.argv[1:] == ["ckpt"]:
         ckpt_golden()
@@ -580,6 +607,9 @@ def main():
         return
     if sys.argv[1:] == ["dataset"]:
         dataset_goldens()
+        return
+    if sys.argv[1:] == ["hworacle"]:
+        hworacle_goldens()
         return
     if sys.argv[1:] == ["rng"]:
         rng_goldens()
@@ -611,6 +641,7 @@ def main():
     baseline_goldens()
     metatrain_goldens(items, m)
     rng_goldens()
+    hworacle_goldens()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))
 
