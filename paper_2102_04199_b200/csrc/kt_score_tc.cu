@@ -73,6 +73,12 @@ using namespace kt::tc;
 #ifndef KT_R2
 #define KT_R2 1  // two R warpgroups, one per chunk parity
 #endif
+#ifndef KT_G2_UNROLL
+#define KT_G2_UNROLL 1  // GEMM2 issue loop unrolled over its two buffers
+#endif
+#ifndef KT_R_ISSUE
+#define KT_R_ISSUE 0  // 1: the R warpgroups issue their chunks' GEMM2 themselves (no separate MMA warp)
+#endif
 constexpr int WG_R = 2, WG_RO = WG_R + 1 + KT_R2, WG_MMA = WG_RO + 2;  // warpgroup of each role
 constexpr int NWG = WG_MMA + 1;
 constexpr int NT = 128 * NWG;  // (roles by warpgroup, see the header)
@@ -623,7 +629,37 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         __syncwarp();
         if (++c == C) c = 0;
       }
-    } else if (warp == 4 * WG_MMA + 1) {
+    } else if (warp == 4 * WG_MMA + 1 && !(KT_R2 && KT_R_ISSUE && !KT_DR)) {
+#if KT_G2_UNROLL
+      // unrolled over the two R / D2 buffers (NR == N2 == 2): buffer addresses are constants
+      static_assert(NR == 2 && N2 == 2, "GEMM2 unroll needs 2-deep R / D2 rings");
+      auto g2 = [&](int64_t q, int b, uint32_t ph) {
+        if ((tid & 31) == 0) TRACE(17, q);
+        mbar_wait(&S.r_full[b], ph);
+        mbar_wait(&S.d2_empty[b], ph ^ 1);
+        __syncwarp();
+        tc_fence_after();
+        if ((tid & 31) == 0) TRACE(18, q);
+        const uint32_t rh = tmem + T_R + 64 * b, rl = rh + 32, d = tmem + T_D2 + 32 * b;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            mma_tf32_ts(d, rh + 8 * kk, kdesc(S.b2h, 32, kk), id32, kk > 0);
+            mma_tf32_ts(d, rh + 8 * kk, kdesc(S.b2l, 32, kk), id32, 1);
+            mma_tf32_ts(d, rl + 8 * kk, kdesc(S.b2h, 32, kk), id32, 1);
+          }
+          mma_commit(&S.r_empty[b]);
+          mma_commit(&S.d2_full[b]);
+          TRACE(2, q);
+        }
+        __syncwarp();
+      };
+      uint32_t ph = 0;
+      for (int64_t q = 0; q < n_chunks; q += 2, ph ^= 1u) {
+        g2(q, 0, ph);
+        if (q + 1 < n_chunks) g2(q + 1, 1, ph);
+      }
+#else
       Ring<NR> rr;
       Ring<N2> r2;
       for (int64_t q = 0; q < n_chunks; ++q, rr.next(), r2.next()) {
@@ -646,6 +682,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         }
         __syncwarp();
       }
+#endif
     } else if (warp == 4 * WG_MMA + 2) {
       for (int64_t t = 0; t < my_tiles; ++t) {
         const uint32_t ph = static_cast<uint32_t>(t & 1);
@@ -733,8 +770,37 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       tmem_wait_st();
       if (g == 0) TRACE(16, q);
       tc_fence_before();
+#if KT_R2 && KT_R_ISSUE && !KT_DR
+      // GEMM2 of this chunk straight from the warpgroup that produced its operand: a named
+      // barrier over the 4 warps replaces the r_full hand-off to an MMA warp (whose wake-up and
+      // issue slots on a busy SMSP set the chunk cadence)
+      named_sync(1 + (wg - WG_R), 128);
+      if (g == 0) TRACE(6, q);
+      if (quad == 0) {
+        tc_fence_after();
+        role_wait<0>(&S.d2_empty[b], rr.ph ^ 1);  // readout of chunk q - 2 read D2[b]
+        __syncwarp();
+        tc_fence_after();
+        if ((tid & 31) == 0) TRACE(18, q);
+        const uint32_t id32 = idesc_tf32(128, 32);
+        const uint32_t rh = tmem + T_R + 64 * b, rl = rh + 32, d = tmem + T_D2 + 32 * b;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            mma_tf32_ts(d, rh + 8 * kk, kdesc(S.b2h, 32, kk), id32, kk > 0);
+            mma_tf32_ts(d, rh + 8 * kk, kdesc(S.b2l, 32, kk), id32, 1);
+            mma_tf32_ts(d, rl + 8 * kk, kdesc(S.b2h, 32, kk), id32, 1);
+          }
+          mma_commit(&S.r_empty[b]);
+          mma_commit(&S.d2_full[b]);
+          TRACE(2, q);
+        }
+        __syncwarp();
+      }
+#else
       warp_arrive(&S.r_full[b]);
       if (g == 0) TRACE(6, q);
+#endif
     }
   } else if (wg >= WG_RO && wg < WG_MMA) {
     setmaxnreg<REG_RO>();

@@ -90,10 +90,15 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase);
+
 // Blocking wait with a suspend-time hint: a thread whose phase is not complete is
 // parked by the hardware (woken on completion) instead of spinning through issue
-// slots its SMSP neighbours need.
+// slots its SMSP neighbours need.  KT_TEST_FIRST: probe with test_wait first.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+#if defined(KT_TEST_FIRST) && KT_TEST_FIRST
+  if (mbar_test(bar, phase)) return;
+#endif
 #if defined(KT_WAIT_HINT)
   // hardware-suspended wait: the thread parks until the phase completes (or the hint expires)
   asm volatile(
