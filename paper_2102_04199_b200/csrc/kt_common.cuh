@@ -35,14 +35,21 @@ inline int current_device() {
   return dev >= 0 && dev < kMaxDevices ? dev : 0;
 }
 struct SmemAttr {
-  size_t done[kMaxDevices] = {};
-  // raise the kernel's dynamic shared memory limit to `bytes` (once per device and size)
+  bool done[kMaxDevices] = {};
+  // lift the kernel's dynamic shared memory limit (once per device) to the sm_100 opt-in
+  // maximum, never to just `bytes`: several entry points launch the same kernel with
+  // their own SmemAttr, and a smaller limit set through one would fail another's launch
   template <class K>
   void ensure(K kernel, size_t bytes) {
     const int dev = current_device();
-    if (bytes > 48 * 1024 && bytes > done[dev]) {
-      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
-      done[dev] = bytes;
+    if (bytes > 48 * 1024 && !done[dev]) {
+      int optin = 227 * 1024;
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, kernel);
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           optin - static_cast<int>(fa.sharedSizeBytes));
+      done[dev] = true;
     }
   }
 };

@@ -642,7 +642,11 @@ fine_tune_cluster_kernel(kt_dims dims, int rc, const float* __restrict__ theta, 
   const Scratch S = carve(gb + 2 * P4, h, false);
   const int C = static_cast<int>(cl.num_blocks()), c = static_cast<int>(cl.block_rank());
   const int r0 = static_cast<int>(static_cast<int64_t>(n) * c / C), r1 = static_cast<int>(static_cast<int64_t>(n) * (c + 1) / C);
-  const int p0 = static_cast<int>(static_cast<int64_t>(h.P) * c / C), p1 = static_cast<int>(static_cast<int64_t>(h.P) * (c + 1) / C);
+  // parameter slices in whole float4 groups, so the distributed-shared-memory reduce and gather
+  // move 16 bytes per remote access with all of a thread's loads in flight together
+  const int G4 = P4 >> 2;
+  const int q0 = static_cast<int>(static_cast<int64_t>(G4) * c / C), q1 = static_cast<int>(static_cast<int64_t>(G4) * (c + 1) / C);
+  const int p0 = 4 * q0, p1 = 4 * q1 < h.P ? 4 * q1 : h.P;
   const int d0 = h.dim[0];
   for (int e = threadIdx.x; e < h.P; e += NT) th[e] = theta[e];
   __syncthreads();
@@ -655,10 +659,33 @@ fine_tune_cluster_kernel(kt_dims dims, int rc, const float* __restrict__ theta, 
     }
     if (threadIdx.x == 0) s_mse = part;
     cl.sync();  // every CTA's gradient share is complete
-    for (int e = p0 + static_cast<int>(threadIdx.x); e < p1; e += NT) {
-      float g = 0.0f;
-      for (int q = 0; q < C; ++q) g += cl.map_shared_rank(gb, q)[e];
-      th[e] -= alpha * g;
+    if (C == 8) {  // (the launch's cluster size for >= 64 rows: the peer loads unrolled)
+      for (int e4 = q0 + static_cast<int>(threadIdx.x); e4 < q1; e4 += NT) {
+        float4 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = reinterpret_cast<const float4*>(cl.map_shared_rank(gb, q))[e4];
+        float4 g = v[0];
+#pragma unroll
+        for (int q = 1; q < 8; ++q) {
+          g.x += v[q].x;
+          g.y += v[q].y;
+          g.z += v[q].z;
+          g.w += v[q].w;
+        }
+        float4* t = reinterpret_cast<float4*>(th) + e4;
+        float4 tv = *t;
+        tv.x -= alpha * g.x;
+        tv.y -= alpha * g.y;
+        tv.z -= alpha * g.z;
+        tv.w -= alpha * g.w;
+        *t = tv;
+      }
+    } else {
+      for (int e = p0 + static_cast<int>(threadIdx.x); e < p1; e += NT) {
+        float g = 0.0f;
+        for (int q = 0; q < C; ++q) g += cl.map_shared_rank(gb, q)[e];
+        th[e] -= alpha * g;
+      }
     }
     if (c == 0 && threadIdx.x == 0 && mse_out) {
       float m = 0.0f;
@@ -666,12 +693,13 @@ fine_tune_cluster_kernel(kt_dims dims, int rc, const float* __restrict__ theta, 
       mse_out[st] = m;
     }
     cl.sync();  // every slice updated
-    for (int q = 0; q < C; ++q) {
+    for (int q = 0; q < C; ++q) {  // the other slices, float4 groups, loads of all peers in flight
       if (q == c) continue;
-      const int a0 = static_cast<int>(static_cast<int64_t>(h.P) * q / C);
-      const int a1 = static_cast<int>(static_cast<int64_t>(h.P) * (q + 1) / C);
-      const float* src = cl.map_shared_rank(th, q);
-      for (int e = a0 + static_cast<int>(threadIdx.x); e < a1; e += NT) th[e] = src[e];
+      const int a0 = static_cast<int>(static_cast<int64_t>(G4) * q / C);
+      const int a1 = static_cast<int>(static_cast<int64_t>(G4) * (q + 1) / C);
+      const float4* src = reinterpret_cast<const float4*>(cl.map_shared_rank(th, q));
+      float4* dst = reinterpret_cast<float4*>(th);
+      for (int e4 = a0 + static_cast<int>(threadIdx.x); e4 < a1; e4 += NT) dst[e4] = src[e4];
     }
     __syncthreads();
   }
