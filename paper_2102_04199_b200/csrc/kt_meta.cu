@@ -78,16 +78,23 @@ __device__ __forceinline__ Scratch carve(float* p, const Head& h, bool hvp) {
   return Scratch{p, h.RC * h.HS, h.nh, hvp ? 1 : 0};
 }
 
+// Deterministic CTA sum: a fixed butterfly inside each warp, then warp 0 combines the warp
+// sums with the same butterfly (a fixed tree, so the result does not depend on timing).
 __device__ __forceinline__ float block_sum(float v, float* red) {
-  red[threadIdx.x] = v;
+  static_assert(NT % 32 == 0 && NT / 32 <= 32, "block_sum: whole warps, at most 32");
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+  if (lane == 0) red[w] = v;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    float s = 0.0f;
-    for (int i = 0; i < NT; ++i) s += red[i];  // fixed order
-    red[0] = s;
+  if (w == 0) {
+    float s = lane < NT / 32 ? red[lane] : 0.0f;
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+    if (lane == 0) red[NT / 32] = s;
   }
   __syncthreads();
-  const float s = red[0];
+  const float s = red[NT / 32];
   __syncthreads();
   return s;
 }
