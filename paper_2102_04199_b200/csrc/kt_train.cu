@@ -465,19 +465,32 @@ struct SubGroup {
 constexpr int FG = 4;
 
 __global__ void __launch_bounds__(CT * FG, 1)
-factor_cta_kernel(kt_dims dims, const float* __restrict__ params, const double* __restrict__ fmean,
+factor_cta_kernel(kt_dims dims_p, const float* __restrict__ params, const double* __restrict__ fmean,
                   const double* __restrict__ fstd, const double* __restrict__ feats, const uint8_t* __restrict__ mask,
                   const int64_t* __restrict__ node_ptr, int npg, int nmax, const int32_t* __restrict__ row_ptr,
                   const int32_t* __restrict__ col, const float* __restrict__ val, const int64_t* __restrict__ gidx,
-                  const float* __restrict__ y, int64_t nb, float inv_b, int head_only, int D, FactorLayout FL,
+                  const float* __restrict__ y, int64_t nb, float inv_b, int head_only, int D, FactorLayout FL_p,
                   float* __restrict__ recs, float* __restrict__ pg_sq) {
   extern __shared__ __align__(16) float sm[];
+  // the dims / record layout / slab pointer tables are indexed by run-time layer numbers: kept
+  // in shared memory (as kernel parameters or locals they would be copied to the stack)
+  __shared__ kt_dims dims_s;
+  __shared__ FactorLayout fl_s;
+  __shared__ Slab slab_s[FG];
+  if (threadIdx.x == 0) {
+    dims_s = dims_p;
+    fl_s = FL_p;
+  }
+  __syncthreads();
+  const kt_dims& dims = dims_s;
+  const FactorLayout& FL = fl_s;
   const int P = dims.n_params;
   float* Ps = sm;
   for (int e = threadIdx.x; e < P; e += CT * FG) Ps[e] = params[e];
-  __syncthreads();
   const int grp = threadIdx.x / CT;
-  const Slab S = carve(sm + ((P + 3) & ~3) + grp * slab_floats(dims, nmax, D), dims, nmax, D);
+  if (threadIdx.x % CT == 0) slab_s[grp] = carve(sm + ((P + 3) & ~3) + grp * slab_floats(dims, nmax, D), dims, nmax, D);
+  __syncthreads();
+  const Slab& S = slab_s[grp];
   const SubGroup G{static_cast<int>(threadIdx.x) - grp * CT, CT, grp};
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * FG + grp; i < nb; i += static_cast<int64_t>(gridDim.x) * FG) {
     const int64_t g = gidx ? gidx[i] : i;

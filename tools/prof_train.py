@@ -21,13 +21,14 @@ corpus = bench.synthetic_corpus(entries)
 fn, ln = pmeta.dataset_norms(corpus)
 m = pm.model_from_flat(m._flat, m, feature_norm=fn, label_norm=ln)
 what = sys.argv[1:] or ["pretrain", "maml", "fine_tune", "aggregate"]
+N = int(__import__("os").environ.get("PROF_STEPS", "5"))  # timed steps (more for A/B timing runs)
 if "pretrain" in what:
-    print(bench.bench_pretrain_step(m, bench.synthetic_corpus(entries, ("conv2d", "winograd", "depthwise")), 5, 3))
+    print(bench.bench_pretrain_step(m, bench.synthetic_corpus(entries, ("conv2d", "winograd", "depthwise")), N, 3))
 if "maml" in what:
-    print(bench.bench_maml(m, corpus, 5, 3))
-    print(bench.bench_maml(m, corpus, 5, 3, first_order=False))
+    print(bench.bench_maml(m, corpus, N, 3))
+    print(bench.bench_maml(m, corpus, N, 3, first_order=False))
 if "fine_tune" in what:
-    print(bench.bench_fine_tune(m, corpus, reps=5))
+    print(bench.bench_fine_tune(m, corpus, reps=N))
 if "aggregate" in what:
     print(bench.bench_aggregate(m, reps=2))
 torch.cuda.synchronize()
