@@ -39,7 +39,9 @@ def _compile(src: pathlib.Path, verbose: bool) -> tuple:
     deps = [src] + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "kerntune_b200.h"]
     if out.exists() and all(out.stat().st_mtime >= d.stat().st_mtime for d in deps):
         return src.name, ""
-    cmd = [nvcc(), *ARCH, *FLAGS, "-c", str(src), "-o", str(out)]
+    # KT_NVCC_DEFS: extra -D switches for A/B builds of the compile-time variants
+    defs = os.environ.get("KT_NVCC_DEFS", "").split()
+    cmd = [nvcc(), *ARCH, *FLAGS, *defs, "-c", str(src), "-o", str(out)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stderr}")

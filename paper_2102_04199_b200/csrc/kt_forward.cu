@@ -135,6 +135,7 @@ int kt_embed_csr(const kt_dims* dims, const float* params, const double* fmean, 
   int D = dims->F;
   for (int i = 1; i <= dims->n_gcn; ++i) D = D > dims->gcn[i] ? D : dims->gcn[i];
   D = (D + 3) & ~3;
+  if (D % 32 == 0) D += 4;  // (bank spread for the 4-wide dense, as kt_grad's row_stride)
   if (B <= kNumSMs) {
     const size_t smem1 = sizeof(float) * (2 * max_nodes * D + 4 * KT_MAX_DIM);
     static SmemAttr attr1;

@@ -11,6 +11,16 @@
 
 #include "kt_common.cuh"
 
+#ifndef KT_VEC_CSR
+#define KT_VEC_CSR 1
+#endif
+#ifndef KT_VEC_DENSE
+#define KT_VEC_DENSE 1
+#endif
+#ifndef KT_DPAD
+#define KT_DPAD 1
+#endif
+
 namespace kt {
 
 struct WarpGroup {
@@ -70,10 +80,34 @@ __device__ __forceinline__ void load_features(const Grp& G, const GraphView& v, 
   }
 }
 
+__device__ __forceinline__ bool aligned16(const void* a, const void* b) {
+  return ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
+}
+__device__ __forceinline__ void fma4(float w, const float4& x, float4& acc) {
+  acc.x = fmaf(w, x.x, acc.x);
+  acc.y = fmaf(w, x.y, acc.y);
+  acc.z = fmaf(w, x.z, acc.z);
+  acc.w = fmaf(w, x.w, acc.w);
+}
+
 // T (n x din) <- A_hat H   (A_hat symmetric, so A_hat^T products use the same routine)
+// Width a multiple of 4: a thread owns a channel quad (16-byte row pieces, the CSR entries
+// read once per quad); the per-channel edge order is the same either way.
 template <class Grp>
 __device__ __forceinline__ void csr_aggregate(const Grp& G, const GraphView& v, const float* Hs, float* Ts,
                                               int din, int D) {
+  if (KT_VEC_CSR && (din & 3) == 0 && (D & 3) == 0 && aligned16(Hs, Ts)) {
+    const int q4 = din >> 2;
+    for (int e = G.r; e < v.n * q4; e += G.n) {
+      const int r = e / q4, c = 4 * (e - r * q4);
+      const int64_t b = v.row_ptr[v.rp_base + r], end = v.row_ptr[v.rp_base + r + 1];
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int64_t q = b; q < end; ++q)
+        fma4(v.val[q], *reinterpret_cast<const float4*>(Hs + (v.col[q] - v.col_base) * D + c), acc);
+      *reinterpret_cast<float4*>(Ts + r * D + c) = acc;
+    }
+    return;
+  }
   for (int e = G.r; e < v.n * din; e += G.n) {
     const int r = e / din, c = e - (e / din) * din;
     const int64_t b = v.row_ptr[v.rp_base + r], end = v.row_ptr[v.rp_base + r + 1];
@@ -83,10 +117,24 @@ __device__ __forceinline__ void csr_aggregate(const Grp& G, const GraphView& v, 
   }
 }
 
-// Out (n x dout) <- T W (+ optional ReLU); W row-major (din x dout).
+// Out (n x dout) <- T W (+ optional ReLU); W row-major (din x dout).  Width a multiple of 4:
+// a thread owns four adjacent outputs of a row (one 16-byte W load per k, k order unchanged).
 template <class Grp>
 __device__ __forceinline__ void dense(const Grp& G, const float* Ts, const float* __restrict__ W, float* Out, int n,
                                       int din, int dout, int D, bool relu_out) {
+  if (KT_VEC_DENSE && (dout & 3) == 0 && (D & 3) == 0 && aligned16(W, Out)) {
+    const int q4 = dout >> 2;
+    for (int e = G.r; e < n * q4; e += G.n) {
+      const int r = e / q4, c = 4 * (e - r * q4);
+      const float* t = Ts + r * D;
+      const float* w = W + c;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int k = 0; k < din; ++k) fma4(t[k], *reinterpret_cast<const float4*>(w + k * dout), acc);
+      if (relu_out) acc = make_float4(fmaxf(acc.x, 0.f), fmaxf(acc.y, 0.f), fmaxf(acc.z, 0.f), fmaxf(acc.w, 0.f));
+      *reinterpret_cast<float4*>(Out + r * D + c) = acc;
+    }
+    return;
+  }
   for (int e = G.r; e < n * dout; e += G.n) {
     const int r = e / dout, c = e - (e / dout) * dout;
     float acc = 0.0f;

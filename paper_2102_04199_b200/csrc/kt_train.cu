@@ -163,15 +163,22 @@ __device__ float graph_grad(const Grp& G, const kt_dims& dims, const float* P, c
 constexpr int WARPS = 4;
 
 __global__ void __launch_bounds__(WARPS * 32)
-pergraph_kernel(kt_dims dims, const float* __restrict__ params, const double* __restrict__ fmean,
+pergraph_kernel(kt_dims dims_p, const float* __restrict__ params, const double* __restrict__ fmean,
                 const double* __restrict__ fstd, const double* __restrict__ feats, const uint8_t* __restrict__ mask,
                 const int64_t* __restrict__ node_ptr, int npg, int nmax, const int32_t* __restrict__ row_ptr,
                 const int32_t* __restrict__ col, const float* __restrict__ val, const int64_t* __restrict__ gidx,
                 const float* __restrict__ y, int64_t b0, int64_t nb, float inv_b, int head_only, int D,
                 float* __restrict__ pg_grad, float* __restrict__ pg_sq) {
   extern __shared__ __align__(16) float sm[];
+  __shared__ kt_dims dims_s;  // (run-time indexed tables: shared memory, not the stack)
+  __shared__ Slab slab_s[WARPS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const Slab S = carve(sm + warp * slab_floats(dims, nmax, D), dims, nmax, D);
+  if (threadIdx.x == 0) dims_s = dims_p;
+  __syncthreads();
+  const kt_dims& dims = dims_s;
+  if (lane == 0) slab_s[warp] = carve(sm + warp * slab_floats(dims, nmax, D), dims, nmax, D);
+  __syncthreads();
+  const Slab& S = slab_s[warp];
   const WarpGroup W{lane};
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * WARPS + warp; i < nb;
        i += static_cast<int64_t>(gridDim.x) * WARPS) {
@@ -196,7 +203,7 @@ pergraph_kernel(kt_dims dims, const float* __restrict__ params, const double* __
 constexpr int CT = KT_GRAD_CT;
 
 __global__ void __launch_bounds__(CT)
-pergraph_cta_kernel(kt_dims dims, const float* __restrict__ params, const double* __restrict__ fmean,
+pergraph_cta_kernel(kt_dims dims_p, const float* __restrict__ params, const double* __restrict__ fmean,
                     const double* __restrict__ fstd, const double* __restrict__ feats,
                     const uint8_t* __restrict__ mask, const int64_t* __restrict__ node_ptr, int npg, int nmax,
                     const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
@@ -204,9 +211,15 @@ pergraph_cta_kernel(kt_dims dims, const float* __restrict__ params, const double
                     int64_t b0, int64_t nb, float inv_b, int head_only, int D, float* __restrict__ pg_grad,
                     float* __restrict__ pg_sq) {
   extern __shared__ __align__(16) float sm[];
+  __shared__ kt_dims dims_s;  // (run-time indexed tables: shared memory, not the stack)
+  __shared__ Slab slab_s;
+  if (threadIdx.x == 0) dims_s = dims_p;
+  __syncthreads();
+  const kt_dims& dims = dims_s;
   const int P = dims.n_params;
   float* Ps = sm;
-  const Slab S = carve(sm + ((P + 3) & ~3), dims, nmax, D);
+  if (threadIdx.x == 0) slab_s = carve(sm + ((P + 3) & ~3), dims, nmax, D);
+  const Slab& S = slab_s;
   const CtaGroup G{static_cast<int>(threadIdx.x), CT};
   for (int e = threadIdx.x; e < P; e += CT) Ps[e] = params[e];
   __syncthreads();
@@ -276,17 +289,24 @@ __global__ void sgd_kernel(const float* __restrict__ p, const float* __restrict_
 // Sequential batch-1 SGD (meta.pretrain's inner loop): one CTA, params in smem.
 template <int NTP>
 __global__ void __launch_bounds__(NTP)
-pretrain_sgd_kernel(kt_dims dims, float* __restrict__ params, const double* __restrict__ fmean,
+pretrain_sgd_kernel(kt_dims dims_p, float* __restrict__ params, const double* __restrict__ fmean,
                     const double* __restrict__ fstd, const double* __restrict__ feats,
                     const uint8_t* __restrict__ mask, const int64_t* __restrict__ node_ptr, int npg, int nmax,
                     const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
                     const float* __restrict__ val, const int64_t* __restrict__ order, const float* __restrict__ y,
                     int64_t n_steps, float gamma, int D) {
   extern __shared__ __align__(16) float sm[];
+  __shared__ kt_dims dims_s;  // (run-time indexed tables: shared memory, not the stack)
+  __shared__ Slab slab_s;
+  if (threadIdx.x == 0) dims_s = dims_p;
+  __syncthreads();
+  const kt_dims& dims = dims_s;
   const int P = dims.n_params;
   float* Ps = sm;
   float* Gs = Ps + ((P + 3) & ~3);
-  const Slab S = carve(Gs + ((P + 3) & ~3), dims, nmax, D);
+  if (threadIdx.x == 0) slab_s = carve(Gs + ((P + 3) & ~3), dims, nmax, D);
+  __syncthreads();
+  const Slab& S = slab_s;
   const CtaGroup C{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)};
   for (int i = C.r; i < P; i += C.n) Ps[i] = params[i];
   C.sync();
@@ -344,10 +364,18 @@ inline FactorLayout factor_layout(const kt_dims& d, int nmax) {
   return f;
 }
 
+// Transposed GCN weights W_l^T (dout x din) for layers l >= 1, consecutive in shared memory.
+__host__ __device__ inline int wt_offset(const kt_dims& d, int l) {
+  int o = 0;
+  for (int j = 1; j < l; ++j) o += d.gcn[j] * d.gcn[j + 1];
+  return o;
+}
+__host__ __device__ inline int wt_floats(const kt_dims& d) { return (wt_offset(d, d.n_gcn) + 3) & ~3; }
+
 // Forward with caches + reverse pass for one graph (the arithmetic of graph_grad), writing
 // the gradient factors to rec; returns the squared error.
 template <class Grp>
-__device__ float graph_factors(const Grp& G, const kt_dims& dims, const float* P, const GraphView& v,
+__device__ float graph_factors(const Grp& G, const kt_dims& dims, const float* P, const float* WT, const GraphView& v,
                                const double* feats, const double* fmean, const double* fstd, float y, float inv_b,
                                bool head_only, const Slab& S, const FactorLayout& FL, float* rec, int D) {
   const int L = dims.n_gcn, nh = dims.n_head, n = v.n, nmax = FL.nmax;
@@ -444,7 +472,8 @@ __device__ float graph_factors(const Grp& G, const kt_dims& dims, const float* P
     }
     G.sync();
     if (l > 0) {
-      dense_t(G, S.t0, P + dims.off_gcn[l], S.t1, n, din, dout, D);
+      // dZ W^T as a plain dense product with the transposed weights (staged once per CTA)
+      dense(G, S.t0, WT + wt_offset(dims, l), S.t1, n, dout, din, D, false);
       G.sync();
       csr_aggregate(G, v, S.t1, S.t0, din, D);
       G.sync();
@@ -486,16 +515,26 @@ factor_cta_kernel(kt_dims dims_p, const float* __restrict__ params, const double
   const FactorLayout& FL = fl_s;
   const int P = dims.n_params;
   float* Ps = sm;
+  float* WT = Ps + ((P + 3) & ~3);
   for (int e = threadIdx.x; e < P; e += CT * FG) Ps[e] = params[e];
+  for (int l = 1; l < dims.n_gcn; ++l) {
+    const int din = dims.gcn[l], dout = dims.gcn[l + 1];
+    float* wt = WT + wt_offset(dims, l);
+    for (int e = threadIdx.x; e < din * dout; e += CT * FG) {
+      const int k = e / dout, c = e - k * dout;
+      wt[c * din + k] = params[dims.off_gcn[l] + e];
+    }
+  }
   const int grp = threadIdx.x / CT;
-  if (threadIdx.x % CT == 0) slab_s[grp] = carve(sm + ((P + 3) & ~3) + grp * slab_floats(dims, nmax, D), dims, nmax, D);
+  if (threadIdx.x % CT == 0)
+    slab_s[grp] = carve(WT + wt_floats(dims) + grp * slab_floats(dims, nmax, D), dims, nmax, D);
   __syncthreads();
   const Slab& S = slab_s[grp];
   const SubGroup G{static_cast<int>(threadIdx.x) - grp * CT, CT, grp};
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * FG + grp; i < nb; i += static_cast<int64_t>(gridDim.x) * FG) {
     const int64_t g = gidx ? gidx[i] : i;
     const GraphView v = graph_view(g, node_ptr, npg, row_ptr, col, val, mask);
-    const float sq = graph_factors(G, dims, Ps, v, feats, fmean, fstd, y[i], inv_b, head_only != 0, S, FL,
+    const float sq = graph_factors(G, dims, Ps, WT, v, feats, fmean, fstd, y[i], inv_b, head_only != 0, S, FL,
                                    recs + i * FL.rec, D);
     if (G.r == 0) pg_sq[i] = sq;
     G.sync();
@@ -630,7 +669,10 @@ constexpr int FACTOR_GPC = 4;  // graphs per phase-B chunk (CTA)
 static int row_stride(const kt_dims& d) {
   int D = d.F;
   for (int i = 1; i <= d.n_gcn; ++i) D = D > d.gcn[i] ? D : d.gcn[i];
-  return (D + 3) & ~3;
+  D = (D + 3) & ~3;
+  // rows of a multiple of 32 words would put every row's word k in one bank (the 4-wide
+  // dense reads t[k] of four rows per warp): pad by one 16-byte piece
+  return KT_DPAD && D % 32 == 0 ? D + 4 : D;
 }
 
 static int64_t chunk_of(int64_t B) { return B < 8192 ? B : 8192; }
@@ -680,23 +722,24 @@ int kt_grad(const kt_dims* dims, const float* params, const double* fmean, const
   double* sq_acc = acc + P;
   double* part = reinterpret_cast<double*>(reinterpret_cast<uintptr_t>(sq_acc + 2 + 7) & ~uintptr_t(63));
   const float inv_b = static_cast<float>(1.0 / static_cast<double>(B));
-  if (B <= kNumSMs * 8 && !(getenv("KT_GRAD_ROWS") && getenv("KT_GRAD_ROWS")[0] == '1')) {
+  const train::FactorLayout FL = train::factor_layout(*dims, max_nodes);
+  const size_t csm = sizeof(float) * (((P + 3) & ~3) + train::wt_floats(*dims) +
+                                      train::FG * train::slab_floats(*dims, max_nodes, D));
+  const size_t rsm = sizeof(float) * train::FACTOR_GPC * FL.rec;
+  // factored path when its CTAs fit shared memory (large graphs / models: the row path)
+  if (B <= kNumSMs * 8 && csm <= 220 * 1024 && rsm <= 220 * 1024 &&
+      !(getenv("KT_GRAD_ROWS") && getenv("KT_GRAD_ROWS")[0] == '1')) {
     // factored path: per-graph gradient factors, then fixed-order fp64 contractions
-    const train::FactorLayout FL = train::factor_layout(*dims, max_nodes);
     const train::Segments SG = train::factor_segments(*dims, FL, B, train::FACTOR_GPC);
     float* recs = static_cast<float*>(workspace);
     float* fsq = recs + B * FL.rec;
     double* part = reinterpret_cast<double*>(reinterpret_cast<uintptr_t>(fsq + B + 15) & ~uintptr_t(63));
-    const size_t csm = sizeof(float) * (((P + 3) & ~3) + train::FG * train::slab_floats(*dims, max_nodes, D));
-    KT_REQUIRE(csm <= 220 * 1024, KT_E_UNSUPPORTED, "kt_grad: model too large for shared memory");
     static SmemAttr fsm_attr;
     fsm_attr.ensure(train::factor_cta_kernel, csm);
     const int64_t fcta = (B + train::FG - 1) / train::FG;
     train::factor_cta_kernel<<<(int)(fcta < kNumSMs ? fcta : kNumSMs), train::CT * train::FG, csm, st>>>(*dims, params, fmean, fstd, feats, mask, node_ptr,
                                                               nodes_per_graph, max_nodes, row_ptr, col, val,
                                                               graph_idx, y, B, inv_b, head_only, D, FL, recs, fsq);
-    const size_t rsm = sizeof(float) * train::FACTOR_GPC * FL.rec;
-    KT_REQUIRE(rsm <= 220 * 1024, KT_E_UNSUPPORTED, "kt_grad: graph records too large for shared memory");
     static SmemAttr rsm_attr;
     rsm_attr.ensure(train::factor_reduce_kernel, rsm);
     train::factor_reduce_kernel<<<SG.nch, train::FRT, rsm, st>>>(recs, FL.rec, B, SG, part);
