@@ -577,10 +577,40 @@ factor_reduce_kernel(const float* __restrict__ recs, int rec, int64_t nb, Segmen
     for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = __ldcs(src + i);
   }
   __syncthreads();
+  // the work items of every segment in one index space (item = an output quad of a 4-wide
+  // segment, else one output), so the threads run the segments side by side
+  int base = 0;
   for (int k = 0; k < SG.n; ++k) {
     const Segment sg = SG.s[k];
     double* out = part + SG.part_off[k] + static_cast<int64_t>(ch) * sg.n_out;
-    for (int o = threadIdx.x; o < sg.n_out; o += blockDim.x) {
+    const bool quad = sg.din > 0 && (sg.dout & 3) == 0 && ((sg.b_off | rec) & 3) == 0;
+    const int items = quad ? sg.n_out >> 2 : sg.n_out;
+    const int first = ((static_cast<int>(threadIdx.x) - base) % FRT + FRT) % FRT;  // this thread's first item
+    base += items;
+    if (quad) {
+      // four adjacent outputs per thread (16-byte B reads, four independent chains); each
+      // output's arithmetic and order are those of the scalar loop below
+      const int q4 = sg.dout >> 2, n4 = items;
+      for (int o4 = first; o4 < n4; o4 += FRT) {
+        const int a = o4 / q4, c = 4 * (o4 - a * q4);
+        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+        for (int g = 0; g < ng; ++g) {
+          const float* A = rs + g * rec + sg.a_off + a;
+          const float* Bm = rs + g * rec + sg.b_off + c;
+          float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int r = 0; r < sg.rows; ++r) fma4(A[r * sg.din], *reinterpret_cast<const float4*>(Bm + r * sg.dout), s4);
+          acc0 += static_cast<double>(s4.x);
+          acc1 += static_cast<double>(s4.y);
+          acc2 += static_cast<double>(s4.z);
+          acc3 += static_cast<double>(s4.w);
+        }
+        double2* o2 = reinterpret_cast<double2*>(out + 4 * o4);
+        o2[0] = make_double2(acc0, acc1);
+        o2[1] = make_double2(acc2, acc3);
+      }
+      continue;
+    }
+    for (int o = first; o < sg.n_out; o += FRT) {
       // per graph: an fp32 dot over its rows (as each graph's own gradient row was formed
       // before); across the chunk's graphs: fp64, in batch order
       double acc = 0.0;
@@ -601,16 +631,15 @@ factor_reduce_kernel(const float* __restrict__ recs, int rec, int64_t nb, Segmen
   }
 }
 
-// One warp per parameter: lane l sums chunks l, l + 32, ... in order, then a fixed
-// butterfly combines the lanes (deterministic); then the update and the loss.
+// Eight lanes per parameter: lane j sums chunks j, j + 8, ... in order (fp64), a fixed
+// three-step butterfly combines them, then the update; warp 0 of CTA 0 also sums the loss.
 __global__ void __launch_bounds__(256)
 factor_finalize_kernel(const double* __restrict__ part, Segments SG, int P, int head_only, int off_head,
                        const float* __restrict__ pg_sq, int64_t nb, double inv_b, float* __restrict__ grad_out,
                        double* __restrict__ loss_out, const float* __restrict__ params, float lr,
                        float* __restrict__ new_params) {
-  const int lane = threadIdx.x & 31;
-  const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (p < P) {
+  const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 3, j = threadIdx.x & 7;
+  if (p < P) {  // (P is uniform per 8-lane group: the group is all in or all out)
     int k = 0;
 #pragma unroll 1
     while (k + 1 < SG.n && SG.s[k + 1].p_off <= p) ++k;
@@ -618,11 +647,14 @@ factor_finalize_kernel(const double* __restrict__ part, Segments SG, int P, int 
     double s = 0.0;
     if (!(head_only && p < off_head)) {
       const double* q = part + SG.part_off[k] + o;
-      for (int c = lane; c < SG.nch; c += 32) s += q[static_cast<int64_t>(c) * n_out];
+#pragma unroll 4
+      for (int c = j; c < SG.nch; c += 8) s += __ldcs(q + static_cast<int64_t>(c) * n_out);
     }
-#pragma unroll
-    for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
-    if (lane == 0) {
+    const unsigned gm = 0xFFu << (threadIdx.x & 24);
+    s += __shfl_xor_sync(gm, s, 1);
+    s += __shfl_xor_sync(gm, s, 2);
+    s += __shfl_xor_sync(gm, s, 4);
+    if (j == 0) {
       const float g = static_cast<float>(s);
       if (grad_out) grad_out[p] = g;
       if (new_params) new_params[p] = params[p] - lr * g;
@@ -743,7 +775,7 @@ int kt_grad(const kt_dims* dims, const float* params, const double* fmean, const
     static SmemAttr rsm_attr;
     rsm_attr.ensure(train::factor_reduce_kernel, rsm);
     train::factor_reduce_kernel<<<SG.nch, train::FRT, rsm, st>>>(recs, FL.rec, B, SG, part);
-    train::factor_finalize_kernel<<<(P + 7) / 8, 256, 0, st>>>(part, SG, P, head_only, dims->off_head, fsq, B,
+    train::factor_finalize_kernel<<<(P + 31) / 32, 256, 0, st>>>(part, SG, P, head_only, dims->off_head, fsq, B,
                                                                    1.0 / static_cast<double>(B), grad_out, loss_out,
                                                                    params, lr, new_params);
     note_launches(3);
