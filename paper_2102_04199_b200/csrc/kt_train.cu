@@ -457,6 +457,28 @@ __device__ float graph_factors(const Grp& G, const kt_dims& dims, const float* P
   G.sync();
   for (int l = L - 1; l >= 0; --l) {
     const int din = dims.gcn[l], dout = dims.gcn[l + 1];
+    if (((din | dout | FL.ft[l] | FL.fa[l] | D) & 3) == 0) {  // the same, in 16-byte pieces
+      const int q4 = dout >> 2;
+      for (int e = G.r; e < nmax * q4; e += G.n) {
+        const int r = e / q4, c = 4 * (e - r * q4);
+        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r < n) {
+          const float4 h = *reinterpret_cast<const float4*>(S.H[l + 1] + r * D + c);
+          float4* tp = reinterpret_cast<float4*>(S.t0 + r * D + c);
+          const float4 d = *tp;
+          t = make_float4(h.x > 0.0f ? d.x : 0.0f, h.y > 0.0f ? d.y : 0.0f, h.z > 0.0f ? d.z : 0.0f,
+                          h.w > 0.0f ? d.w : 0.0f);
+          *tp = t;
+        }
+        *reinterpret_cast<float4*>(rec + FL.ft[l] + r * dout + c) = t;
+      }
+      const int a4 = din >> 2;
+      for (int e = G.r; e < nmax * a4; e += G.n) {
+        const int r = e / a4, a = 4 * (e - r * a4);
+        *reinterpret_cast<float4*>(rec + FL.fa[l] + r * din + a) =
+            r < n ? *reinterpret_cast<const float4*>(S.AH[l] + r * D + a) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    } else {
     for (int e = G.r; e < nmax * dout; e += G.n) {  // masked delta rows (zero padding rows)
       const int r = e / dout, c = e - (e / dout) * dout;
       float t = 0.0f;
@@ -469,6 +491,7 @@ __device__ float graph_factors(const Grp& G, const kt_dims& dims, const float* P
     for (int e = G.r; e < nmax * din; e += G.n) {
       const int r = e / din, a = e - (e / din) * din;
       rec[FL.fa[l] + e] = r < n ? S.AH[l][r * D + a] : 0.0f;
+    }
     }
     G.sync();
     if (l > 0) {
@@ -696,7 +719,10 @@ inline int64_t factor_partials(const Segments& SG) {
   return t;
 }
 
-constexpr int FACTOR_GPC = 4;  // graphs per phase-B chunk (CTA)
+#ifndef KT_FACTOR_GPC
+#define KT_FACTOR_GPC 4
+#endif
+constexpr int FACTOR_GPC = KT_FACTOR_GPC;  // graphs per phase-B chunk (CTA)
 
 static int row_stride(const kt_dims& d) {
   int D = d.F;
