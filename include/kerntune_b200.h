@@ -242,6 +242,16 @@ int kt_gp_ucb(const double* mean, const double* cov, int32_t P, double noise, do
 int kt_sa_propose(const int32_t* cur, int32_t n_chains, int32_t n_knobs, const int32_t* cards,
                   const int64_t* mult, const int32_t* knob, const uint8_t* nudge, const int32_t* delta,
                   const int32_t* resample, int32_t* nxt, int64_t* nxt_idx, void* stream);
+/* The per-step random draws of sa_explore (search.py:233-237: integers(0, n_knobs),
+ * random() < 0.5, integers(0, 2) * 2 - 1, integers(0, cards[knob]), random(), each of
+ * size n_chains) for n_steps steps, reproducing numpy's Generator(PCG64) stream bit for
+ * bit (dependency: numpy's PCG64 + bounded-integer algorithms).  pcg = {state_hi,
+ * state_lo, inc_hi, inc_lo} of bit_generator.state; pcg / has_uint32 / uinteger are
+ * advanced in place to the state numpy would hold after the same calls.  Host memory;
+ * outputs (n_steps, n_chains) row-major.  Host-side: no GPU work. */
+int kt_sa_draws(uint64_t* pcg, int32_t* has_uint32, uint32_t* uinteger, int32_t n_steps, int32_t n_chains,
+                int32_t n_knobs, const int32_t* cards, int32_t* knob, uint8_t* nudge, int32_t* delta,
+                int32_t* resample, double* u);
 /* Metropolis acceptance (search.py:246-251) in fp64: accept if e_new >= energy or
  * u < exp(min((e_new - energy) / temp, 0)); accepted chains copy nxt into cur and
  * e_new into energy. */

@@ -404,11 +404,20 @@ class DeviceAnnealer:
         self.cards = torch.from_numpy(self.cards_np.astype(np.int32)).to(dev)
         self.mult = torch.from_numpy(_space_multipliers(space)).to(dev)
         steps, n, nk = sched.steps_per_round, n_chains, self.nk
-        self.knob = torch.empty((steps, n), dtype=torch.int32, device=dev)
-        self.nudge = torch.empty((steps, n), dtype=torch.uint8, device=dev)
-        self.delta = torch.empty((steps, n), dtype=torch.int32, device=dev)
-        self.resample = torch.empty((steps, n), dtype=torch.int32, device=dev)
-        self.u = torch.empty((steps, n), dtype=torch.float64, device=dev)
+        # the step draws (u, knob, delta, resample, nudge) as views of one byte buffer, host
+        # (pinned) and device, so a call uploads them with one copy
+        sn = steps * n
+        nbytes = 8 * sn + 3 * 4 * sn + sn
+        self.draws_host = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+        self.draws_dev = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+
+        def views(buf):
+            u = buf[: 8 * sn].view(torch.float64).view(steps, n)
+            i32 = buf[8 * sn: 20 * sn].view(torch.int32).view(3, steps, n)
+            return i32[0], buf[20 * sn:].view(steps, n), i32[1], i32[2], u
+
+        self.knob, self.nudge, self.delta, self.resample, self.u = views(self.draws_dev)
+        self.host_draws = tuple(t.numpy() for t in views(self.draws_host))
         self.cur = torch.empty((n, nk), dtype=torch.int32, device=dev)
         self.nxt = torch.empty((n, nk), dtype=torch.int32, device=dev)
         self.energy = torch.empty(n, dtype=torch.float64, device=dev)
@@ -443,22 +452,10 @@ class DeviceAnnealer:
 
     def explore(self, starts: list, rng) -> dict:
         steps, n = self.sched.steps_per_round, self.n
-        knob = np.empty((steps, n), dtype=np.int32)
-        nudge = np.empty((steps, n), dtype=np.uint8)
-        delta = np.empty((steps, n), dtype=np.int32)
-        resample = np.empty((steps, n), dtype=np.int32)
-        u = np.empty((steps, n), dtype=np.float64)
-        for s in range(steps):  # search.py:233-237, same calls in the same order
-            k = rng.integers(0, self.nk, size=n)
-            knob[s] = k
-            nudge[s] = rng.random(n) < 0.5
-            delta[s] = rng.integers(0, 2, size=n) * 2 - 1
-            resample[s] = rng.integers(0, self.cards_np[k])
-            u[s] = rng.random(n)
+        knob, nudge, delta, resample, u = self.host_draws
+        sa_draws(rng, self.cards_np, knob, nudge, delta, resample, u)
         with torch.cuda.device(self.dev):
-            for dst, src in ((self.knob, knob), (self.nudge, nudge), (self.delta, delta),
-                             (self.resample, resample), (self.u, u)):
-                dst.copy_(torch.from_numpy(src), non_blocking=False)
+            self.draws_dev.copy_(self.draws_host)  # one copy: the five draw arrays are views of one buffer
             start_idx = np.array(starts, dtype=np.int64)
             self.hist_idx[0].copy_(torch.from_numpy(start_idx))
             choices = np.zeros((n, self.nk), dtype=np.int64)
@@ -478,14 +475,52 @@ class DeviceAnnealer:
                 self.graph = g
             self.graph.replay()
             hi = self.hist_idx.cpu().numpy().reshape(-1)
-            hz = self.hist_z.double().cpu().numpy().reshape(-1)
-        history: dict = {}
-        for i, e in zip(hi, hz):  # insertion order: starts, then each step's chains
-            history[int(i)] = float(e)
-        return history
+            hz = self.hist_z.cpu().numpy().reshape(-1).astype(np.float64)
+        # insertion order: starts, then each step's chains (a revisit keeps its first
+        # position and takes the later score, as the reference's dict assignment does)
+        return dict(zip(hi.tolist(), hz.tolist()))
 
 
 _ANNEALERS: dict = {}
+
+
+def _draws_python(rng, cards, knob, nudge, delta, resample, u) -> None:
+    for s in range(knob.shape[0]):  # search.py:233-237, same calls in the same order
+        k = rng.integers(0, len(cards), size=knob.shape[1])
+        knob[s] = k
+        nudge[s] = rng.random(knob.shape[1]) < 0.5
+        delta[s] = rng.integers(0, 2, size=knob.shape[1]) * 2 - 1
+        resample[s] = rng.integers(0, cards[k])
+        u[s] = rng.random(knob.shape[1])
+
+
+def sa_draws(rng, cards, knob, nudge, delta, resample, u) -> None:
+    """Fill the (steps, chains) draw arrays with sa_explore's per-step Generator calls
+    (search.py:233-237) and leave `rng` where those calls would leave it.  A PCG64
+    Generator (numpy's default, the reference's rng_from) is drawn natively from its
+    state (kt_sa_draws, bit-exact with numpy); any other bit generator goes through
+    the Generator calls themselves."""
+    st = rng.bit_generator.state
+    cards = np.asarray(cards, dtype=np.int64)
+    if st.get("bit_generator") != "PCG64" or cards.max() >= 2**31:
+        _draws_python(rng, cards, knob, nudge, delta, resample, u)
+        return
+    m64 = (1 << 64) - 1
+    s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+    pcg = np.array([s >> 64, s & m64, inc >> 64, inc & m64], dtype=np.uint64)
+    has = np.array([st["has_uint32"]], dtype=np.int32)
+    ui = np.array([st["uinteger"]], dtype=np.uint32)
+    c32 = np.ascontiguousarray(cards, dtype=np.int32)
+    for a, dt in ((knob, np.int32), (nudge, np.uint8), (delta, np.int32), (resample, np.int32), (u, np.float64)):
+        if a.dtype != dt or not a.flags.c_contiguous or a.shape != knob.shape:
+            raise DomainError("sa_draws: draw arrays must be C-contiguous (steps, chains) of the documented dtypes")
+    lib = _lib.load()
+    p = lambda a: a.ctypes.data  # noqa: E731
+    _lib.check(lib.kt_sa_draws(p(pcg), p(has), p(ui), knob.shape[0], knob.shape[1], len(cards), p(c32), p(knob),
+                               p(nudge), p(delta), p(resample), p(u)), "sa draws")
+    rng.bit_generator.state = {"bit_generator": "PCG64",
+                               "state": {"state": (int(pcg[0]) << 64) | int(pcg[1]), "inc": inc},
+                               "has_uint32": int(has[0]), "uinteger": int(ui[0])}
 
 
 def _sa_explore_host(predict, space: KnobSpace, sched: SaSchedule, starts: list, rng) -> dict:
