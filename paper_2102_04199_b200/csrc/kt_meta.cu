@@ -251,8 +251,50 @@ __device__ float head_pass_scalar(const Head& h, const float* th, const float* v
 }
 
 
+#ifdef KT_META_TRACE
+__device__ long long g_mt[512];
+__device__ int g_mt_n;
+#define MT()                                                                   \
+  do {                                                                         \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && g_mt_n < 255) {                 \
+      g_mt[2 * g_mt_n] = __LINE__;                                             \
+      g_mt[2 * g_mt_n + 1] = clock64();                                        \
+      ++g_mt_n;                                                                \
+    }                                                                          \
+  } while (0)
+extern "C" int kt_meta_trace_read(void* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_mt, sizeof(g_mt)));
+}
+#else
+#define MT() \
+  do {       \
+  } while (0)
+#endif
+
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ float ks_sum(float v, int ks, unsigned gm) {
+  for (int o = 1; o < ks; o <<= 1) v += __shfl_xor_sync(gm, v, o);
+  return v;
+}
+// dst[0..n) = src (+ scale * add): 16-byte pieces with every load of a thread in flight
+// (n multiple of 4 and 16-byte aligned pointers; the tail in scalars otherwise)
+__device__ __forceinline__ void vcopy(float* dst, const float* src, int n, const float* add = nullptr,
+                                      float scale = 0.0f) {
+  const bool al = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) |
+                    reinterpret_cast<uintptr_t>(add)) & 15) == 0;
+  const int n4 = al ? n >> 2 : 0;
+#pragma unroll 4
+  for (int e = threadIdx.x; e < n4; e += NT) {
+    float4 v = ld4(src + 4 * e);
+    if (add) {
+      const float4 a = ld4(add + 4 * e);
+      v = make_float4(v.x - scale * a.x, v.y - scale * a.y, v.z - scale * a.z, v.w - scale * a.w);
+    }
+    st4(dst + 4 * e, v);
+  }
+  for (int e = 4 * n4 + threadIdx.x; e < n; e += NT) dst[e] = add ? src[e] - scale * add[e] : src[e];
+}
 
 // Register-tiled pass (all hidden widths and the input width multiples of 4,
 // single-output last layer): same arithmetic contract as head_pass_scalar.
@@ -265,7 +307,8 @@ __device__ float head_pass_tiled(const Head& h, const float* th, const float* v,
   const int nh = h.nh, HS = h.HS, RC = h.RC;
   const bool hvp = v != nullptr;
   const int tid = threadIdx.x;
-  for (int e = tid; e < h.P; e += NT) out[e] = 0.0f;
+  for (int e = tid; e < (h.P >> 2); e += NT) st4(out + 4 * e, make_float4(0.f, 0.f, 0.f, 0.f));
+  for (int e = (h.P & ~3) + tid; e < h.P; e += NT) out[e] = 0.0f;
   float sq_local = 0.0f;
   const float two_n = 2.0f / static_cast<float>(n_norm);
   for (int r0 = 0; r0 < n; r0 += RC) {
@@ -287,6 +330,7 @@ __device__ float head_pass_tiled(const Head& h, const float* th, const float* v,
       }
     }
     __syncthreads();
+    MT();
     // ---- forward
     for (int i = 0; i < nh; ++i) {
       const int din = h.dim[i], dout = h.dim[i + 1];
@@ -296,16 +340,23 @@ __device__ float head_pass_tiled(const Head& h, const float* th, const float* v,
       float* __restrict__ Zi = S.Z(i);
       float* __restrict__ An = S.A(i + 1);
       const bool last = i == nh - 1;
-      if (last) {  // dout == 1: one thread per row
-        for (int r = tid; r < nr2; r += NT) {
-          float acc = b[0], t = hvp ? v[h.ob[i]] : 0.0f;
-          for (int k = 0; k < din; ++k) {
+      if (last) {  // dout == 1: eight adjacent lanes per row, k strided by 8, fixed xor tree
+        for (int e = tid; e < 8 * nr2; e += NT) {
+          const int r = e >> 3, j = e & 7;
+          const unsigned gm = 0xFFu << (tid & 24);
+          float acc = 0.0f, t = 0.0f;
+          for (int k = j; k < din; k += 8) {
             acc = fmaf(Ai[r * HS + k], W[k], acc);
             if (hvp) t = fmaf(S.TA(i)[r * HS + k], W[k], fmaf(Ai[r * HS + k], v[h.ow[i] + k], t));
           }
-          Zi[r * HS] = acc;
-          An[r * HS] = acc;
-          if (hvp) S.TA(i + 1)[r * HS] = t;
+          acc = ks_sum(acc, 8, gm);
+          if (hvp) t = ks_sum(t, 8, gm);
+          if (j == 0) {
+            acc += b[0];
+            Zi[r * HS] = acc;
+            An[r * HS] = acc;
+            if (hvp) S.TA(i + 1)[r * HS] = t + v[h.ob[i]];
+          }
         }
       } else {
         const int ncg = dout >> 2;
@@ -350,6 +401,7 @@ __device__ float head_pass_tiled(const Head& h, const float* th, const float* v,
         }
       }
       __syncthreads();
+      MT();
     }
     // ---- output deltas; the pad row (if any) gets zero deltas
     {
@@ -369,6 +421,7 @@ __device__ float head_pass_tiled(const Head& h, const float* th, const float* v,
       }
     }
     __syncthreads();
+    MT();
     // ---- backward
     int cur = 0;
     for (int i = nh - 1; i >= 0; --i) {
@@ -390,6 +443,7 @@ __device__ float head_pass_tiled(const Head& h, const float* th, const float* v,
           }
         }
         __syncthreads();
+        MT();
       }
       float* gw = out + h.ow[i];
       if (last) {  // dout == 1: gW[k] += sum_r A[r][k] dz[r]
@@ -460,7 +514,12 @@ __device__ float head_pass_tiled(const Head& h, const float* th, const float* v,
               }
             }
           } else {
-            for (int c = 0; c < dout; c += 4) {
+            // rows k..k+3 of W are read at column c: threads on consecutive k quads start at
+            // different column quads (rotated, fixed order per output) so their 16-byte reads
+            // spread over the banks instead of all hitting column c's
+            const int crot = k % dout;
+            for (int cc = 0; cc < dout; cc += 4) {
+              const int c = cc + crot < dout ? cc + crot : cc + crot - dout;
               const float4 d0 = ld4(da + r * HS + c), d1 = ld4(da + (r + 1) * HS + c);
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
@@ -487,6 +546,7 @@ __device__ float head_pass_tiled(const Head& h, const float* th, const float* v,
         }
       }
       __syncthreads();
+      MT();
       cur ^= 1;
     }
   }
@@ -526,6 +586,7 @@ maml_task_kernel(kt_dims dims, int rc, const float* __restrict__ theta, TaskSet 
   extern __shared__ __align__(16) float sm[];
   pdl_launch_dependents();  // task_sum may launch now and wait for this grid
   pdl_wait();               // theta: the previous step's update
+  MT();
   const Head h = head_of(dims, rc);
   const int P4 = (h.P + 3) & ~3;
   float* th = sm;             // current theta_k
@@ -537,8 +598,9 @@ maml_task_kernel(kt_dims dims, int rc, const float* __restrict__ theta, TaskSet 
   if (t >= T) return;
   const int64_t s0 = ts.s_off[t], ns = ts.s_off[t + 1] - s0;
   const int64_t q0 = ts.q_off[t], nq = ts.q_off[t + 1] - q0;
-  for (int e = threadIdx.x; e < h.P; e += NT) th[e] = theta[e];
+  vcopy(th, theta, h.P);
   __syncthreads();
+  MT();
   float ls0 = 0.0f;
   float* cur = th;
   float* nxt = th1;
@@ -548,25 +610,32 @@ maml_task_kernel(kt_dims dims, int rc, const float* __restrict__ theta, TaskSet 
     const float ls = head_pass(h, cur, nullptr, ts.u, ts.s_idx + s0, ts.y, static_cast<int>(ns), gb, S);
     if (k == 0) ls0 = ls;
     __syncthreads();
-    for (int e = threadIdx.x; e < h.P; e += NT) nxt[e] = cur[e] - alpha * gb[e];
+    MT();
+    vcopy(nxt, cur, h.P, gb, alpha);
     __syncthreads();
+    MT();
     float* tmp = cur; cur = nxt; nxt = tmp;
   }
   const float lq = head_pass(h, cur, nullptr, ts.u, ts.q_idx + q0, ts.y, static_cast<int>(nq), vb, S);
   __syncthreads();
+  MT();
   if (!first_order) {
     for (int k = inner_steps - 1; k >= 0; --k) {
       // theta_k -> nxt
       for (int e = threadIdx.x; e < h.P; e += NT)
         nxt[e] = inner_steps > 1 ? theta_ws[(static_cast<int64_t>(t) * inner_steps + k) * h.P + e] : theta[e];
       __syncthreads();
+      MT();
       head_pass(h, nxt, vb, ts.u, ts.s_idx + s0, ts.y, static_cast<int>(ns), gb, S);
       __syncthreads();
-      for (int e = threadIdx.x; e < h.P; e += NT) vb[e] -= alpha * gb[e];
+      MT();
+      vcopy(vb, vb, h.P, gb, alpha);
       __syncthreads();
+      MT();
     }
   }
-  for (int e = threadIdx.x; e < h.P; e += NT) g_out[static_cast<int64_t>(t) * h.P + e] = vb[e];
+  vcopy(g_out + static_cast<int64_t>(t) * h.P, vb, h.P);
+  MT();
   if (threadIdx.x == 0) {
     loss_out[2 * t] = ls0;
     loss_out[2 * t + 1] = lq;
@@ -611,9 +680,11 @@ head_kernel(kt_dims dims, int rc, const float* __restrict__ theta, const float* 
     if (hvp) vb[e] = v[e];
   }
   __syncthreads();
+  MT();
   if (steps <= 0) {  // single evaluation: grad (or hvp) -> out
     const float mse = head_pass(h, th, hvp ? vb : nullptr, u, nullptr, y, n, gb, S);
     __syncthreads();
+    MT();
     for (int e = threadIdx.x; e < h.P; e += NT) out[e] = gb[e];
     if (threadIdx.x == 0 && mse_out) mse_out[0] = mse;
     return;
@@ -621,7 +692,8 @@ head_kernel(kt_dims dims, int rc, const float* __restrict__ theta, const float* 
   for (int s = 0; s < steps; ++s) {  // fine_tune_embedded: theta -= alpha * grad, `steps` times
     const float mse = head_pass(h, th, nullptr, u, nullptr, y, n, gb, S);
     __syncthreads();
-    for (int e = threadIdx.x; e < h.P; e += NT) th[e] -= alpha * gb[e];
+    MT();
+    vcopy(th, th, h.P, gb, alpha);
     if (threadIdx.x == 0 && mse_out) mse_out[s] = mse;
     __syncthreads();
   }
