@@ -307,13 +307,13 @@ __device__ float head_pass_tiled(const Head& h, const float* th, const float* v,
   const int nh = h.nh, HS = h.HS, RC = h.RC;
   const bool hvp = v != nullptr;
   const int tid = threadIdx.x;
-  for (int e = tid; e < (h.P >> 2); e += NT) st4(out + 4 * e, make_float4(0.f, 0.f, 0.f, 0.f));
-  for (int e = (h.P & ~3) + tid; e < h.P; e += NT) out[e] = 0.0f;
+  // (no zero pass: the first row chunk writes every gradient element, later chunks add)
   float sq_local = 0.0f;
   const float two_n = 2.0f / static_cast<float>(n_norm);
   for (int r0 = 0; r0 < n; r0 += RC) {
     const int nr = n - r0 < RC ? n - r0 : RC;
     const int nr2 = (nr + 1) & ~1;  // rows padded to pairs (pad row is zero)
+    const bool first = r0 == 0;
     __syncthreads();
     {
       const int d4 = h.dim[0] >> 2;
@@ -434,21 +434,11 @@ __device__ float head_pass_tiled(const Head& h, const float* th, const float* v,
       const float* __restrict__ Zi = S.Z(i);
       const float* __restrict__ Ai = S.A(i);
       const float* __restrict__ TAi = hvp ? S.TA(i) : nullptr;
-      if (!last) {  // dz = da * (z > 0)
-        for (int e = tid; e < nr2 * dout; e += NT) {
-          const int r = e / dout, c = e - r * dout;
-          if (!(Zi[r * HS + c] > 0.0f)) {
-            da[r * HS + c] = 0.0f;
-            if (hvp) tda[r * HS + c] = 0.0f;
-          }
-        }
-        __syncthreads();
-        MT();
-      }
+      // (layers below the last: da arrives already masked by (z > 0), see the propagate)
       float* gw = out + h.ow[i];
       if (last) {  // dout == 1: gW[k] += sum_r A[r][k] dz[r]
         for (int k = tid; k < din; k += NT) {
-          float acc = gw[k];
+          float acc = first ? 0.0f : gw[k];
           for (int r = 0; r < nr; ++r)
             acc = hvp ? fmaf(TAi[r * HS + k], da[r * HS], fmaf(Ai[r * HS + k], tda[r * HS], acc))
                       : fmaf(Ai[r * HS + k], da[r * HS], acc);
@@ -460,7 +450,7 @@ __device__ float head_pass_tiled(const Head& h, const float* th, const float* v,
           const int c = (it % ncg) * 4, k = (it / ncg) * 4;
           float4 g[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) g[j] = ld4(gw + (k + j) * dout + c);
+          for (int j = 0; j < 4; ++j) g[j] = first ? make_float4(0.f, 0.f, 0.f, 0.f) : ld4(gw + (k + j) * dout + c);
           for (int r = 0; r < nr; ++r) {
             const float4 a = ld4(Ai + r * HS + k);
             const float4 d = ld4(da + r * HS + c);
@@ -489,7 +479,7 @@ __device__ float head_pass_tiled(const Head& h, const float* th, const float* v,
         }
       }
       for (int c = tid; c < dout; c += NT) {
-        float acc = out[h.ob[i] + c];
+        float acc = first ? 0.0f : out[h.ob[i] + c];
         const float* src = hvp ? tda : da;
         for (int r = 0; r < nr; ++r) acc += src[r * HS + c];
         out[h.ob[i] + c] = acc;
@@ -536,6 +526,15 @@ __device__ float head_pass_tiled(const Head& h, const float* th, const float* v,
                 }
               }
             }
+          }
+          // dz of layer i - 1 = da' * (z_{i-1} > 0), applied here (no separate masking phase)
+          const float* Zp = S.Z(i - 1);
+          const float4 z0 = ld4(Zp + r * HS + k), z1 = ld4(Zp + (r + 1) * HS + k);
+          const float m0[4] = {z0.x, z0.y, z0.z, z0.w}, m1[4] = {z1.x, z1.y, z1.z, z1.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (!(m0[j] > 0.0f)) a[0][j] = t[0][j] = 0.0f;
+            if (!(m1[j] > 0.0f)) a[1][j] = t[1][j] = 0.0f;
           }
           st4(dn + r * HS + k, make_float4(a[0][0], a[0][1], a[0][2], a[0][3]));
           st4(dn + (r + 1) * HS + k, make_float4(a[1][0], a[1][1], a[1][2], a[1][3]));
