@@ -272,6 +272,28 @@ extern "C" int kt_meta_trace_read(void* host) {
 #endif
 
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ uint32_t sa32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// global -> shared bulk copy (bytes % 16 == 0, 16-byte aligned), completion on bar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   sa32(dst)),
+               "l"(src), "r"(bytes), "r"(sa32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t ph) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(sa32(bar)), "r"(ph)
+        : "memory");
+}
 __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
 __device__ __forceinline__ float ks_sum(float v, int ks, unsigned gm) {
   for (int o = 1; o < ks; o <<= 1) v += __shfl_xor_sync(gm, v, o);
@@ -301,9 +323,27 @@ __device__ __forceinline__ void vcopy(float* dst, const float* src, int n, const
 //   forward   2 rows x 4 cols per thread, float4 weight loads
 //   dW        4 x 4 (k, c) tile per thread, float4 row loads, summed over the chunk rows in order
 //   propagate 2 rows x 4 k per thread, float4 loads along c
+// Rows r0 .. r0 + nr of u (through ridx) into A(0), padded to a pair with a zero row.
+__device__ __forceinline__ void load_rows(const Head& h, const float* u, const int64_t* ridx, int r0, int nr,
+                                          const Scratch& S, bool hvp) {
+  const int d4 = h.dim[0] >> 2, nr2 = (nr + 1) & ~1, HS = h.HS;
+  float* A0 = S.A(0);
+  for (int e = threadIdx.x; e < nr2 * d4; e += NT) {
+    const int r = e / d4, c = (e - r * d4) * 4;
+    float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r < nr) {
+      const int64_t row = ridx ? ridx[r0 + r] : r0 + r;
+      val = *reinterpret_cast<const float4*>(u + row * h.dim[0] + c);
+    }
+    st4(A0 + r * HS + c, val);
+    if (hvp) st4(S.TA(0) + r * HS + c, make_float4(0.f, 0.f, 0.f, 0.f));
+  }
+}
+
+// a0_ready: the caller already loaded the first row chunk (load_rows) and synchronised
 __device__ float head_pass_tiled(const Head& h, const float* th, const float* v, const float* u,
                                  const int64_t* ridx, const float* y, int n, float* out, const Scratch& S,
-                                 int n_norm) {
+                                 int n_norm, bool a0_ready = false) {
   const int nh = h.nh, HS = h.HS, RC = h.RC;
   const bool hvp = v != nullptr;
   const int tid = threadIdx.x;
@@ -315,21 +355,10 @@ __device__ float head_pass_tiled(const Head& h, const float* th, const float* v,
     const int nr2 = (nr + 1) & ~1;  // rows padded to pairs (pad row is zero)
     const bool first = r0 == 0;
     __syncthreads();
-    {
-      const int d4 = h.dim[0] >> 2;
-      float* A0 = S.A(0);
-      for (int e = tid; e < nr2 * d4; e += NT) {
-        const int r = e / d4, c = (e - r * d4) * 4;
-        float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (r < nr) {
-          const int64_t row = ridx ? ridx[r0 + r] : r0 + r;
-          val = *reinterpret_cast<const float4*>(u + row * h.dim[0] + c);
-        }
-        st4(A0 + r * HS + c, val);
-        if (hvp) st4(S.TA(0) + r * HS + c, make_float4(0.f, 0.f, 0.f, 0.f));
-      }
+    if (!(first && a0_ready)) {
+      load_rows(h, u, ridx, r0, nr, S, hvp);
+      __syncthreads();
     }
-    __syncthreads();
     MT();
     // ---- forward
     for (int i = 0; i < nh; ++i) {
@@ -563,9 +592,10 @@ __device__ __forceinline__ bool tiled_ok(const Head& h) {
 // n rows; the loss is the mean over n_norm rows (n_norm = n unless the rows are one
 // share of a larger batch split over a cluster)
 __device__ float head_pass(const Head& h, const float* th, const float* v, const float* u, const int64_t* ridx,
-                           const float* y, int n, float* out, const Scratch& S, int n_norm = 0) {
+                           const float* y, int n, float* out, const Scratch& S, int n_norm = 0,
+                           bool a0_ready = false) {
   if (n_norm <= 0) n_norm = n;
-  return tiled_ok(h) ? head_pass_tiled(h, th, v, u, ridx, y, n, out, S, n_norm)
+  return tiled_ok(h) ? head_pass_tiled(h, th, v, u, ridx, y, n, out, S, n_norm, a0_ready)
                      : head_pass_scalar(h, th, v, u, ridx, y, n, out, S, n_norm);
 }
 
@@ -597,8 +627,23 @@ maml_task_kernel(kt_dims dims, int rc, const float* __restrict__ theta, TaskSet 
   if (t >= T) return;
   const int64_t s0 = ts.s_off[t], ns = ts.s_off[t + 1] - s0;
   const int64_t q0 = ts.q_off[t], nq = ts.q_off[t + 1] - q0;
-  vcopy(th, theta, h.P);
+  // theta: one bulk copy (TMA engine) while the threads stage the support set's first rows
+  __shared__ __align__(8) uint64_t tbar;
+  const bool bulk = (reinterpret_cast<uintptr_t>(theta) & 15) == 0;
+  const uint32_t tb = static_cast<uint32_t>(h.P * 4) & ~15u;
+  if (threadIdx.x == 0 && bulk) {
+    mbar_init1(&tbar);
+    bulk_g2s(th, theta, tb, &tbar);
+  }
+  if (bulk) {
+    for (int e = static_cast<int>(tb >> 2) + threadIdx.x; e < h.P; e += NT) th[e] = theta[e];
+  } else {
+    vcopy(th, theta, h.P);
+  }
+  const bool pre = tiled_ok(h);
+  if (pre) load_rows(h, ts.u, ts.s_idx + s0, 0, static_cast<int>(ns < h.RC ? ns : h.RC), S, false);
   __syncthreads();
+  if (bulk) mbar_wait_parity(&tbar, 0);
   MT();
   float ls0 = 0.0f;
   float* cur = th;
@@ -606,7 +651,7 @@ maml_task_kernel(kt_dims dims, int rc, const float* __restrict__ theta, TaskSet 
   for (int k = 0; k < inner_steps; ++k) {
     if (!first_order && inner_steps > 1)
       for (int e = threadIdx.x; e < h.P; e += NT) theta_ws[(static_cast<int64_t>(t) * inner_steps + k) * h.P + e] = cur[e];
-    const float ls = head_pass(h, cur, nullptr, ts.u, ts.s_idx + s0, ts.y, static_cast<int>(ns), gb, S);
+    const float ls = head_pass(h, cur, nullptr, ts.u, ts.s_idx + s0, ts.y, static_cast<int>(ns), gb, S, 0, pre && k == 0);
     if (k == 0) ls0 = ls;
     __syncthreads();
     MT();
