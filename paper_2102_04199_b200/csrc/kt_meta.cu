@@ -340,10 +340,14 @@ __device__ __forceinline__ void load_rows(const Head& h, const float* u, const i
   }
 }
 
-// a0_ready: the caller already loaded the first row chunk (load_rows) and synchronised
+// a0_ready: the caller already loaded the first row chunk (load_rows) and synchronised.
+// upd (single row chunk only, n <= RC): out receives upd - ualpha * gradient, the SGD step
+// fused into the gradient's only write (upd may be th itself: each element is read once,
+// by the thread that writes it, after the pass's last read of th)
 __device__ float head_pass_tiled(const Head& h, const float* th, const float* v, const float* u,
                                  const int64_t* ridx, const float* y, int n, float* out, const Scratch& S,
-                                 int n_norm, bool a0_ready = false) {
+                                 int n_norm, bool a0_ready = false, const float* upd = nullptr,
+                                 float ualpha = 0.0f) {
   const int nh = h.nh, HS = h.HS, RC = h.RC;
   const bool hvp = v != nullptr;
   const int tid = threadIdx.x;
@@ -471,7 +475,7 @@ __device__ float head_pass_tiled(const Head& h, const float* th, const float* v,
           for (int r = 0; r < nr; ++r)
             acc = hvp ? fmaf(TAi[r * HS + k], da[r * HS], fmaf(Ai[r * HS + k], tda[r * HS], acc))
                       : fmaf(Ai[r * HS + k], da[r * HS], acc);
-          gw[k] = acc;
+          gw[k] = upd ? upd[gw - out + k] - ualpha * acc : acc;
         }
       } else {
         const int ncg = dout >> 2;
@@ -504,14 +508,21 @@ __device__ float head_pass_tiled(const Head& h, const float* th, const float* v,
             }
           }
 #pragma unroll
-          for (int j = 0; j < 4; ++j) st4(gw + (k + j) * dout + c, g[j]);
+          for (int j = 0; j < 4; ++j) {
+            float4 o = g[j];
+            if (upd) {
+              const float4 b = ld4(upd + (gw - out) + (k + j) * dout + c);
+              o = make_float4(b.x - ualpha * o.x, b.y - ualpha * o.y, b.z - ualpha * o.z, b.w - ualpha * o.w);
+            }
+            st4(gw + (k + j) * dout + c, o);
+          }
         }
       }
       for (int c = tid; c < dout; c += NT) {
         float acc = first ? 0.0f : out[h.ob[i] + c];
         const float* src = hvp ? tda : da;
         for (int r = 0; r < nr; ++r) acc += src[r * HS + c];
-        out[h.ob[i] + c] = acc;
+        out[h.ob[i] + c] = upd ? upd[h.ob[i] + c] - ualpha * acc : acc;
       }
       if (i > 0) {  // da' = dz W^T ; tda' = tdz W^T + dz vW^T   (2 rows x 4 k per thread)
         const float* __restrict__ W = th + h.ow[i];
@@ -593,9 +604,9 @@ __device__ __forceinline__ bool tiled_ok(const Head& h) {
 // share of a larger batch split over a cluster)
 __device__ float head_pass(const Head& h, const float* th, const float* v, const float* u, const int64_t* ridx,
                            const float* y, int n, float* out, const Scratch& S, int n_norm = 0,
-                           bool a0_ready = false) {
+                           bool a0_ready = false, const float* upd = nullptr, float ualpha = 0.0f) {
   if (n_norm <= 0) n_norm = n;
-  return tiled_ok(h) ? head_pass_tiled(h, th, v, u, ridx, y, n, out, S, n_norm, a0_ready)
+  return tiled_ok(h) ? head_pass_tiled(h, th, v, u, ridx, y, n, out, S, n_norm, a0_ready, upd, ualpha)
                      : head_pass_scalar(h, th, v, u, ridx, y, n, out, S, n_norm);
 }
 
@@ -651,13 +662,18 @@ maml_task_kernel(kt_dims dims, int rc, const float* __restrict__ theta, TaskSet 
   for (int k = 0; k < inner_steps; ++k) {
     if (!first_order && inner_steps > 1)
       for (int e = threadIdx.x; e < h.P; e += NT) theta_ws[(static_cast<int64_t>(t) * inner_steps + k) * h.P + e] = cur[e];
-    const float ls = head_pass(h, cur, nullptr, ts.u, ts.s_idx + s0, ts.y, static_cast<int>(ns), gb, S, 0, pre && k == 0);
+    // one row chunk: the pass writes nxt = cur - alpha * grad directly
+    const bool fused = pre && ns <= h.RC;
+    const float ls = head_pass(h, cur, nullptr, ts.u, ts.s_idx + s0, ts.y, static_cast<int>(ns), fused ? nxt : gb,
+                               S, 0, pre && k == 0, fused ? cur : nullptr, alpha);
     if (k == 0) ls0 = ls;
     __syncthreads();
     MT();
-    vcopy(nxt, cur, h.P, gb, alpha);
-    __syncthreads();
-    MT();
+    if (!fused) {
+      vcopy(nxt, cur, h.P, gb, alpha);
+      __syncthreads();
+      MT();
+    }
     float* tmp = cur; cur = nxt; nxt = tmp;
   }
   const float lq = head_pass(h, cur, nullptr, ts.u, ts.q_idx + q0, ts.y, static_cast<int>(nq), vb, S);
