@@ -147,6 +147,16 @@ int kt_score_indices_ex(const kt_spec_table* tab, const kt_dims* dims, const flo
                         const int64_t* idx, const uint32_t* idx32, int64_t idx_base, int64_t B,
                         float* z_out, float* u_out, uint64_t* keys_out, uint32_t* key_hist,
                         int32_t* err_flag, void* stream);
+/* kt_score_indices_ex with launch flags.  KT_SCORE_PARAMS_STABLE: the caller guarantees
+ * that the kernel immediately before this launch on the stream does not write params
+ * (e.g. the annealing steps after the first in one CUDA graph), so the operand staging
+ * may overlap that kernel under programmatic dependent launch; indices, outputs and the
+ * rest still wait for it. */
+#define KT_SCORE_PARAMS_STABLE 1
+int kt_score_indices_flags(const kt_spec_table* tab, const kt_dims* dims, const float* params,
+                           const int64_t* idx, const uint32_t* idx32, int64_t idx_base, int64_t B,
+                           float* z_out, float* u_out, uint64_t* keys_out, uint32_t* key_hist,
+                           int32_t* err_flag, int32_t flags, void* stream);
 /* Same contract as kt_score_indices on the FP32 FMA pipe (FFMA2 register tiles) instead
  * of tcgen05 3xTF32 tensor cores; kept as the second, independent implementation the
  * parity tests hold the tensor-core kernel against. */

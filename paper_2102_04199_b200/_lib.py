@@ -118,6 +118,8 @@ _SIGS = {
     "kt_sweep_host": (ctypes.c_int, [vp, ctypes.POINTER(Dims), vp, vp, i32, i64, vp, vp, i32, vp, vp, vp, vp, vp,
                                      i64, vp, vp]),
     "kt_score_indices_ex": (ctypes.c_int, [vp, ctypes.POINTER(Dims), vp, vp, vp, i64, i64, vp, vp, vp, vp, vp, vp]),
+    "kt_score_indices_flags": (ctypes.c_int, [vp, ctypes.POINTER(Dims), vp, vp, vp, i64, i64, vp, vp, vp, vp, vp, i32,
+                                              vp]),
     "kt_topk_keys": (ctypes.c_int, [vp, i64, i32, i32, vp, vp, vp, i64, vp]),
     "kt_topk_key_hist": (vp, [vp]),
     "kt_gp_gram": (ctypes.c_int, [vp, i32, vp, i32, i32, vp, vp, vp]),

@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(NT, 1)
 score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float* __restrict__ params,
                 const int64_t* __restrict__ idx, const uint32_t* __restrict__ idx32, int64_t idx_base, int64_t B,
                 float* __restrict__ z_out, float* __restrict__ u_out, unsigned long long* __restrict__ keys_out,
-                unsigned int* __restrict__ key_hist, int32_t* __restrict__ err) {
+                unsigned int* __restrict__ key_hist, int32_t* __restrict__ err, int flags) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const kt_spec_table& T = *tab;
@@ -517,9 +517,14 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
   if (threadIdx.x == 0) TRACE(28, 0);  // table prologue done
   // PDL: everything above reads only the constant spec table.  The parameters, indices,
   // outputs and key_hist belong to the stream order from here on (a predecessor may write
-  // the parameters, e.g. kt_maml_step / kt_sgd in place).
-  pdl_wait();
-  pdl_launch_dependents();
+  // the parameters, e.g. kt_maml_step / kt_sgd in place) -- unless the caller vouches that
+  // the preceding kernel leaves the parameters alone (KT_SCORE_PARAMS_STABLE): then the
+  // operand staging below overlaps it too and only the indices wait.
+  const bool params_stable = (flags & KT_SCORE_PARAMS_STABLE) != 0;
+  if (!params_stable) {
+    pdl_wait();
+    pdl_launch_dependents();
+  }
 
   // ---- setup, part 2: operands from the parameters --------------------------------
   {
@@ -562,10 +567,16 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (params_stable) {
+    pdl_wait();
+    pdl_launch_dependents();
+  }
   if (threadIdx.x == 0) TRACE(30, 0);  // operand prologue done
   const uint32_t tmem = S.tmem_base;
   const int64_t n_tiles = (B + GT - 1) / GT;
   const int64_t my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // one tile per CTA (small batches): the head's waits are on the critical path, no sleeping
+  const bool one_tile = my_tiles <= 1;
   const int C = n_loops;  // chunks per tile
   const int64_t n_chunks = my_tiles * C;
   const uint64_t size = T.space_size;
@@ -688,7 +699,10 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         const uint32_t ph = static_cast<uint32_t>(t & 1);
         // GEMM3: U (TMEM) x H0 into the head accumulator, once the head warps have read
         // D4 of the previous tile out of it
-        mbar_wait_sleep<KT_HEAD_SLEEP>(&S.u_full, ph);
+        if (one_tile)
+          mbar_wait(&S.u_full, ph);
+        else
+          mbar_wait_sleep<KT_HEAD_SLEEP>(&S.u_full, ph);
         wait_bar(&S.d4_empty, ph ^ 1);
         const uint32_t ah = tmem + T_Z, al = ah + 64;
         if (elect_one()) {
@@ -703,7 +717,10 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         }
         __syncwarp();
         // GEMM4: Z1 (TMEM, written over U) x H1, same accumulator (the head warps have read D3)
-        mbar_wait_sleep<64>(&S.z_full, ph);
+        if (one_tile)
+          mbar_wait(&S.z_full, ph);
+        else
+          mbar_wait_sleep<64>(&S.z_full, ph);
         __syncwarp();
         tc_fence_after();
         if (elect_one()) {
@@ -910,7 +927,10 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     const bool tr = g == 0;
     for (int64_t ti = 0; ti < my_tiles; ++ti) {
       const uint32_t ph = static_cast<uint32_t>(ti & 1);
-      mbar_wait_sleep<KT_HEAD_SLEEP>(&S.d3_full, ph);
+      if (one_tile)
+        mbar_wait(&S.d3_full, ph);
+      else
+        mbar_wait_sleep<KT_HEAD_SLEEP>(&S.d3_full, ph);
       __syncwarp();
       if (tr) TRACE(10, ti);
       tc_fence_after();
@@ -930,7 +950,10 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       tmem_wait_st();
       tc_fence_before();
       warp_arrive(&S.z_full);
-      mbar_wait_sleep<KT_HEAD_SLEEP>(&S.d4_full, ph);
+      if (one_tile)
+        mbar_wait(&S.d4_full, ph);
+      else
+        mbar_wait_sleep<KT_HEAD_SLEEP>(&S.d4_full, ph);
       __syncwarp();
       if (tr) TRACE(11, ti);
       tc_fence_after();
@@ -986,10 +1009,10 @@ static bool default_dims_tc(const kt_dims& d) {
 
 }  // namespace kt
 
-extern "C" int kt_score_indices_ex(const kt_spec_table* tab, const kt_dims* dims, const float* params,
-                                   const int64_t* idx, const uint32_t* idx32, int64_t idx_base, int64_t B,
-                                   float* z_out, float* u_out, uint64_t* keys_out, uint32_t* key_hist,
-                                   int32_t* err_flag, void* stream) {
+extern "C" int kt_score_indices_flags(const kt_spec_table* tab, const kt_dims* dims, const float* params,
+                                      const int64_t* idx, const uint32_t* idx32, int64_t idx_base, int64_t B,
+                                      float* z_out, float* u_out, uint64_t* keys_out, uint32_t* key_hist,
+                                      int32_t* err_flag, int32_t flags, void* stream) {
   using namespace kt;
   KT_REQUIRE(tab && dims && params && z_out && err_flag, KT_E_ARG, "kt_score_indices: null pointer");
   KT_REQUIRE(B > 0, KT_E_EMPTY, "kt_score_indices: empty batch");
@@ -1003,10 +1026,19 @@ extern "C" int kt_score_indices_ex(const kt_spec_table* tab, const kt_dims* dims
   const cudaError_t e =
       launch_pdl(tcs::score_tc_kernel, dim3(grid), dim3(tcs::NT), static_cast<size_t>(smem), as_stream(stream), tab,
                  *dims, params, idx, idx32, idx_base, B, z_out, u_out,
-                 reinterpret_cast<unsigned long long*>(keys_out), keys_out ? key_hist : nullptr, err_flag);
+                 reinterpret_cast<unsigned long long*>(keys_out), keys_out ? key_hist : nullptr, err_flag,
+                 static_cast<int>(flags));
   KT_REQUIRE(e == cudaSuccess, KT_E_CUDA, "kt_score_indices: %s", cudaGetErrorString(e));
   note_launches(1);
   return check_launch("kt_score_indices");
+}
+
+extern "C" int kt_score_indices_ex(const kt_spec_table* tab, const kt_dims* dims, const float* params,
+                                   const int64_t* idx, const uint32_t* idx32, int64_t idx_base, int64_t B,
+                                   float* z_out, float* u_out, uint64_t* keys_out, uint32_t* key_hist,
+                                   int32_t* err_flag, void* stream) {
+  return kt_score_indices_flags(tab, dims, params, idx, idx32, idx_base, B, z_out, u_out, keys_out, key_hist,
+                                err_flag, 0, stream);
 }
 
 extern "C" int kt_score_indices(const kt_spec_table* tab, const kt_dims* dims, const float* params,

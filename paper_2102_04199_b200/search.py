@@ -432,9 +432,12 @@ class DeviceAnnealer:
         self.graph = None
 
     def _score(self, i, st):
+        # after the first score the preceding kernel is kt_sa_propose, which leaves the
+        # parameters alone: the scorer may stage its operands under it (PDL)
         p = _lib.ptr
-        _lib.check(self.lib.kt_score_indices(p(self.tab), self.dims, p(self.flat), p(self.hist_idx[i]), 0, self.n,
-                                             p(self.hist_z[i]), None, p(self.err), st), "sa score")
+        _lib.check(self.lib.kt_score_indices_flags(p(self.tab), self.dims, p(self.flat), p(self.hist_idx[i]), None, 0,
+                                                   self.n, p(self.hist_z[i]), None, None, None, p(self.err),
+                                                   1 if i > 0 else 0, st), "sa score")
 
     def _steps(self):
         p = _lib.ptr
