@@ -68,10 +68,13 @@ struct Scratch {
   __device__ __forceinline__ float* TA(int i) const { return base + (2 * nh + 1 + i) * blk; }
   __device__ __forceinline__ float* D(int j) const { return base + ((hvp ? 3 * nh + 2 : 2 * nh + 1) + j) * blk; }
   __device__ __forceinline__ float* red() const { return base + ((hvp ? 3 * nh + 2 : 2 * nh + 1) + (hvp ? 4 : 2)) * blk; }
+  // reduction-split partial sums, slice s (KS_MAX slices of a row chunk)
+  __device__ __forceinline__ float* part(int s) const { return red() + NT + s * blk; }
 };
 
+constexpr int KS_MAX = 4;  // reduction slices of the split forward / propagate (warp-level split)
 __host__ __device__ inline int scratch_floats(const Head& h, bool hvp) {
-  return ((h.nh + 1) + h.nh + (hvp ? h.nh + 1 : 0) + (hvp ? 4 : 2)) * h.RC * h.HS + NT;
+  return ((h.nh + 1) + h.nh + (hvp ? h.nh + 1 : 0) + (hvp ? 4 : 2) + KS_MAX) * h.RC * h.HS + NT;
 }
 
 __device__ __forceinline__ Scratch carve(float* p, const Head& h, bool hvp) {
@@ -295,6 +298,12 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t ph) {
         : "memory");
 }
 __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+#ifndef KT_HEAD_WSPLIT
+#define KT_HEAD_WSPLIT 1
+#endif
+// work items of a 2-row x 4-column tiling of an (nr2 x width) block, rounded up to whole warps
+// (each warp then works on one reduction slice)
+__device__ __forceinline__ int ncg_items(int width, int nr2) { return (((width >> 2) * (nr2 >> 1)) + 31) & ~31; }
 __device__ __forceinline__ float ks_sum(float v, int ks, unsigned gm) {
   for (int o = 1; o < ks; o <<= 1) v += __shfl_xor_sync(gm, v, o);
   return v;
@@ -390,6 +399,40 @@ __device__ float head_pass_tiled(const Head& h, const float* th, const float* v,
             An[r * HS] = acc;
             if (hvp) S.TA(i + 1)[r * HS] = t + v[h.ob[i]];
           }
+        }
+      } else if (!hvp && KT_HEAD_WSPLIT && (ncg_items(dout, nr2) * KS_MAX <= NT) && din % (4 * KS_MAX) == 0) {
+        // few rows: the k range is split over KS_MAX thread slices (a warp's lanes share a
+        // slice, so their W reads stay row-contiguous), partial sums go to shared memory, and
+        // a second phase adds them in slice order, then the bias and the ReLU
+        const int ncg = dout >> 2, items = ncg * (nr2 >> 1), ip = ncg_items(dout, nr2), kl = din / KS_MAX;
+        for (int it = tid; it < ip * KS_MAX; it += NT) {
+          const int sl = it / ip, item = it - sl * ip;
+          if (item >= items) continue;
+          const int c = (item % ncg) * 4, r = (item / ncg) * 2;
+          float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+          const float* x0 = Ai + r * HS;
+          const float* x1 = x0 + HS;
+#pragma unroll 4
+          for (int k = sl * kl; k < (sl + 1) * kl; ++k) {
+            const float4 w = ld4(W + k * dout + c);
+            const float p = x0[k], q = x1[k];
+            a0.x = fmaf(p, w.x, a0.x); a0.y = fmaf(p, w.y, a0.y); a0.z = fmaf(p, w.z, a0.z); a0.w = fmaf(p, w.w, a0.w);
+            a1.x = fmaf(q, w.x, a1.x); a1.y = fmaf(q, w.y, a1.y); a1.z = fmaf(q, w.z, a1.z); a1.w = fmaf(q, w.w, a1.w);
+          }
+          st4(S.part(sl) + r * HS + c, a0);
+          st4(S.part(sl) + (r + 1) * HS + c, a1);
+        }
+        __syncthreads();
+        for (int e = tid; e < nr2 * ncg; e += NT) {
+          const int r = e / ncg, c = (e - r * ncg) * 4;
+          float4 a = ld4(b + c);
+#pragma unroll
+          for (int sl = 0; sl < KS_MAX; ++sl) {
+            const float4 q = ld4(S.part(sl) + r * HS + c);
+            a = make_float4(a.x + q.x, a.y + q.y, a.z + q.z, a.w + q.w);
+          }
+          st4(Zi + r * HS + c, a);
+          st4(An + r * HS + c, make_float4(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f), fmaxf(a.z, 0.f), fmaxf(a.w, 0.f)));
         }
       } else {
         const int ncg = dout >> 2;
@@ -524,7 +567,47 @@ __device__ float head_pass_tiled(const Head& h, const float* th, const float* v,
         for (int r = 0; r < nr; ++r) acc += src[r * HS + c];
         out[h.ob[i] + c] = upd ? upd[h.ob[i] + c] - ualpha * acc : acc;
       }
-      if (i > 0) {  // da' = dz W^T ; tda' = tdz W^T + dz vW^T   (2 rows x 4 k per thread)
+      const bool wsplit = i > 0 && !last && !hvp && KT_HEAD_WSPLIT &&
+                          ncg_items(din, nr2) * KS_MAX <= NT && dout % (4 * KS_MAX) == 0;
+      if (wsplit) {  // da' = dz W^T with the column range split over KS_MAX thread slices
+        const float* __restrict__ W = th + h.ow[i];
+        const int nkg = din >> 2, items = nkg * (nr2 >> 1), ip = ncg_items(din, nr2), cl = dout / KS_MAX;
+        for (int it = tid; it < ip * KS_MAX; it += NT) {
+          const int sl = it / ip, item = it - sl * ip;
+          if (item >= items) continue;
+          const int k = (item % nkg) * 4, r = (item / nkg) * 2;
+          float a[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+          const int crot = k % cl;  // rotated start inside the slice (bank spread, fixed order)
+          for (int cc = 0; cc < cl; cc += 4) {
+            const int c = sl * cl + (cc + crot < cl ? cc + crot : cc + crot - cl);
+            const float4 d0 = ld4(da + r * HS + c), d1 = ld4(da + (r + 1) * HS + c);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float4 w = ld4(W + (k + j) * dout + c);
+              a[0][j] += d0.x * w.x + d0.y * w.y + d0.z * w.z + d0.w * w.w;
+              a[1][j] += d1.x * w.x + d1.y * w.y + d1.z * w.z + d1.w * w.w;
+            }
+          }
+          st4(S.part(sl) + r * HS + k, make_float4(a[0][0], a[0][1], a[0][2], a[0][3]));
+          st4(S.part(sl) + (r + 1) * HS + k, make_float4(a[1][0], a[1][1], a[1][2], a[1][3]));
+        }
+        __syncthreads();
+        // slice sums in order, then dz of layer i - 1 = da' * (z_{i-1} > 0)
+        const float* Zp = S.Z(i - 1);
+        for (int e = tid; e < nr2 * nkg; e += NT) {
+          const int r = e / nkg, k = (e - r * nkg) * 4;
+          float4 a = ld4(S.part(0) + r * HS + k);
+#pragma unroll
+          for (int sl = 1; sl < KS_MAX; ++sl) {
+            const float4 q = ld4(S.part(sl) + r * HS + k);
+            a = make_float4(a.x + q.x, a.y + q.y, a.z + q.z, a.w + q.w);
+          }
+          const float4 z = ld4(Zp + r * HS + k);
+          st4(dn + r * HS + k, make_float4(z.x > 0.f ? a.x : 0.f, z.y > 0.f ? a.y : 0.f, z.z > 0.f ? a.z : 0.f,
+                                           z.w > 0.f ? a.w : 0.f));
+        }
+      }
+      if (i > 0 && !wsplit) {  // da' = dz W^T ; tda' = tdz W^T + dz vW^T   (2 rows x 4 k per thread)
         const float* __restrict__ W = th + h.ow[i];
         const float* __restrict__ vW = hvp ? v + h.ow[i] : nullptr;
         const int nkg = din >> 2;
