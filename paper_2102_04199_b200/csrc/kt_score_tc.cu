@@ -128,7 +128,10 @@ constexpr int TAB = 448;
 #define KT_SLEEP_ENC 0
 #endif
 #ifndef KT_HEAD_SLEEP
-#define KT_HEAD_SLEEP 256  // ns between probes of the head warpgroup's (long) waits
+#define KT_HEAD_SLEEP 256  // ns between probes of the head warpgroup's (long) waits (0: hardware wait)
+#endif
+#ifndef KT_HEAD_SLEEP_Z
+#define KT_HEAD_SLEEP_Z 64  // the head MMA warp's wait for Z1
 #endif
 
 // TMEM column map (512 allocated)
@@ -702,7 +705,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         if (one_tile)
           mbar_wait(&S.u_full, ph);
         else
-          mbar_wait_sleep<KT_HEAD_SLEEP>(&S.u_full, ph);
+          role_wait<KT_HEAD_SLEEP>(&S.u_full, ph);
         wait_bar(&S.d4_empty, ph ^ 1);
         const uint32_t ah = tmem + T_Z, al = ah + 64;
         if (elect_one()) {
@@ -720,7 +723,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         if (one_tile)
           mbar_wait(&S.z_full, ph);
         else
-          mbar_wait_sleep<64>(&S.z_full, ph);
+          role_wait<KT_HEAD_SLEEP_Z>(&S.z_full, ph);
         __syncwarp();
         tc_fence_after();
         if (elect_one()) {
@@ -930,7 +933,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       if (one_tile)
         mbar_wait(&S.d3_full, ph);
       else
-        mbar_wait_sleep<KT_HEAD_SLEEP>(&S.d3_full, ph);
+        role_wait<KT_HEAD_SLEEP>(&S.d3_full, ph);
       __syncwarp();
       if (tr) TRACE(10, ti);
       tc_fence_after();
@@ -953,7 +956,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       if (one_tile)
         mbar_wait(&S.d4_full, ph);
       else
-        mbar_wait_sleep<KT_HEAD_SLEEP>(&S.d4_full, ph);
+        role_wait<KT_HEAD_SLEEP>(&S.d4_full, ph);
       __syncwarp();
       if (tr) TRACE(11, ti);
       tc_fence_after();
