@@ -262,6 +262,20 @@ int kt_sa_propose(const int32_t* cur, int32_t n_chains, int32_t n_knobs, const i
 int kt_sa_draws(uint64_t* pcg, int32_t* has_uint32, uint32_t* uinteger, int32_t n_steps, int32_t n_chains,
                 int32_t n_knobs, const int32_t* cards, int32_t* knob, uint8_t* nudge, int32_t* delta,
                 int32_t* resample, double* u);
+/* The whole of sa_explore's annealing loop (search.py:228-252) in one launch of the fused
+ * scorer on one CTA: tile t holds the n_chains (<= 128) configurations of step t; the
+ * encode warps propose step t's neighbours from the accepted chain state with
+ * kt_sa_propose's rule once the head has run kt_sa_accept's Metropolis test on step
+ * t - 1's scores.  Draws (n_steps, n_chains) and temps (n_steps) as kt_sa_draws / the
+ * schedule give them; cur0 (n_chains, n_knobs) the starting choices; hist_idx row 0 holds
+ * the starts on input; hist_idx / hist_z ((n_steps + 1) x n_chains) receive every
+ * evaluated configuration and score, the trajectory the per-step kernels produce.
+ * cards / mult are host arrays; the rest device memory.  Default dims only. */
+int kt_sa_run(const kt_spec_table* tab, const kt_dims* dims, const float* params, int32_t n_chains,
+              int32_t n_knobs, const int32_t* cards, const int64_t* mult, int32_t n_steps,
+              const int32_t* knob, const uint8_t* nudge, const int32_t* delta, const int32_t* resample,
+              const double* u, const double* temps, const int32_t* cur0, int64_t* hist_idx, float* hist_z,
+              int32_t* err_flag, void* stream);
 /* Metropolis acceptance (search.py:246-251) in fp64: accept if e_new >= energy or
  * u < exp(min((e_new - energy) / temp, 0)); accepted chains copy nxt into cur and
  * e_new into energy. */

@@ -130,6 +130,8 @@ _SIGS = {
     "kt_sa_propose": (ctypes.c_int, [vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "kt_sa_accept": (ctypes.c_int, [i32, i32, vp, vp, f64, vp, vp, vp, vp]),
     "kt_sa_draws": (ctypes.c_int, [vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
+    "kt_sa_run": (ctypes.c_int, [vp, ctypes.POINTER(Dims), vp, i32, i32, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp,
+                                 vp, vp, vp]),
     "kt_topk_workspace_bytes": (i64, [i64, i32]),
     "kt_topk": (ctypes.c_int, [vp, vp, i64, i64, vp, i64, i32, vp, vp, vp, i64, vp]),
     "kt_topk_merge": (ctypes.c_int, [vp, vp, i64, i32, vp, vp, vp, i64, vp]),

@@ -151,6 +151,26 @@ constexpr uint32_t T_D34 = T_D2 + 32 * N2;   // head accumulator: D3, then D4 (6
 constexpr uint32_t T_Z = T_D34 + 64;         // head A operand, U then Z1 = ReLU(D3 + b0): hi at T_Z, lo at +64
 static_assert(T_Z + 128 <= 512, "TMEM budget: 512 columns");
 
+// Annealing mode (kt_sa_run, sa_explore search.py:202-254): one CTA, tile t = the chains'
+// configurations of step t (lane g = chain g).  The encode warps propose step t's
+// neighbours (kt_sa_propose's rule) once the head has accepted step t-1, and the head
+// applies the Metropolis test (kt_sa_accept's fp64 arithmetic) to each tile's scores: the
+// whole exploration is one launch, the scorer's prologue paid once.  n_steps == 0: off.
+struct SaArgs {
+  int n_steps, n_chains, n_knobs;
+  int cards[KT_MAX_KNOBS];
+  long long mult[KT_MAX_KNOBS];
+  const int32_t* knob;    // (n_steps, n_chains) draws, the reference's order (search.py:233-237)
+  const uint8_t* nudge;
+  const int32_t* delta;
+  const int32_t* resample;
+  const double* u;
+  const double* temps;    // (n_steps,) temperature of each step
+  const int32_t* cur0;    // (n_chains, n_knobs) starting choices
+  int64_t* hist_idx;      // (n_steps + 1, n_chains): row 0 = the starts (input), then each step's proposals
+  float* hist_z;          // (n_steps + 1, n_chains) scores
+};
+
 struct __align__(1024) Smem {
   float b1h[KT_MAX_LOOPS][32 * XK], b1l[KT_MAX_LOOPS][32 * XK];  // B_k^T (N=32, K=8) per loop row
   float b2h[32 * 32], b2l[32 * 32];  // W2^T
@@ -181,6 +201,11 @@ struct __align__(1024) Smem {
   uint64_t x_full[XS], x_empty[XS];
   uint64_t d1_full[N1], d1_empty[N1], r_full[NR], r_empty[NR], d2_full[N2], d2_empty[N2];
   uint64_t u_full, uz_empty, z_full, d3_full, d4_full, d4_empty, v_free[4];
+  uint64_t acc_done;                            // annealing: the head has accepted a step
+  int32_t sa_cur[GT][KT_MAX_KNOBS], sa_nxt[GT][KT_MAX_KNOBS];
+  double sa_energy[GT];
+  long long sa_mult[KT_MAX_KNOBS];
+  int sa_cards[KT_MAX_KNOBS];
   uint32_t tmem_base;
 };
 
@@ -290,7 +315,33 @@ struct EncodeCtx {
   uint32_t tmem, lane;
   int g;
   double m6, r6, m7, r7;  // touched-derived slots: fp64 (x - mean) * (1 / std)
+  const SaArgs* sa;       // annealing mode (n_steps > 0), else unused
 };
+
+// Annealing mode: chain g's configuration for tile ti -- the start (ti = 0), else the
+// neighbour of step ti - 1 proposed from the accepted chain state (kt_sa_propose's rule,
+// search.py:232-241), recorded in the history.
+__device__ __forceinline__ int64_t sa_propose(Smem& S, const EncodeCtx& X, int64_t ti) {
+  const SaArgs& A = *X.sa;
+  const int g = X.g, n = A.n_chains;
+  if (ti > 0) mbar_wait(&S.acc_done, static_cast<uint32_t>((ti - 1) & 1));
+  if (g >= n) return INT64_MIN;
+  if (ti == 0) return A.hist_idx[g];
+  const int64_t o = (ti - 1) * n + g;
+  const int kn = A.knob[o];
+  int64_t id = 0;
+  for (int j = 0; j < A.n_knobs; ++j) {
+    int v = S.sa_cur[g][j];
+    if (j == kn) {
+      const int stepped = min(max(v + A.delta[o], 0), S.sa_cards[j] - 1);
+      v = A.nudge[o] ? stepped : A.resample[o];
+    }
+    S.sa_nxt[g][j] = v;
+    id += static_cast<int64_t>(v) * S.sa_mult[j];
+  }
+  A.hist_idx[ti * n + g] = id;
+  return id;
+}
 
 // A tile's per-graph encode state: the config index, the unroll knobs, the axes' table
 // entries and extents, and the running touched / log2 touched.
@@ -429,12 +480,13 @@ __device__ __forceinline__ void encode_loop(Smem& S, const EncodeCtx& X) {
     cur.one = nxt.one;
   }
 #else
-  int64_t v_next = index_of(0);
+  const bool sa = X.sa->n_steps > 0;
+  int64_t v_next = sa ? 0 : index_of(0);
   for (int64_t ti = 0; ti < X.my_tiles; ++ti) {
     EncodeTile<NA> st;
     if (X.g == 0) TRACE(24, ti);
-    encode_prepare<NA>(S, X, ti, v_next, st);
-    v_next = index_of(ti + 1);  // next tile's index load in flight during this tile
+    encode_prepare<NA>(S, X, ti, sa ? sa_propose(S, X, ti) : v_next, st);
+    if (!sa) v_next = index_of(ti + 1);  // next tile's index load in flight during this tile
     if (X.g == 0) TRACE(26, ti);
 #pragma unroll
     for (int c = 0; c < C; ++c) encode_row<NA>(S, X, st, c, 0);
@@ -451,7 +503,8 @@ __global__ void __launch_bounds__(NT, 1)
 score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float* __restrict__ params,
                 const int64_t* __restrict__ idx, const uint32_t* __restrict__ idx32, int64_t idx_base, int64_t B,
                 float* __restrict__ z_out, float* __restrict__ u_out, unsigned long long* __restrict__ keys_out,
-                unsigned int* __restrict__ key_hist, int32_t* __restrict__ err, int flags) {
+                unsigned int* __restrict__ key_hist, int32_t* __restrict__ err, int flags,
+                const __grid_constant__ SaArgs sa) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const kt_spec_table& T = *tab;
@@ -501,11 +554,21 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     mbar_init(&S.d3_full, 1);
     mbar_init(&S.d4_full, 1);
     mbar_init(&S.d4_empty, 4);
+    mbar_init(&S.acc_done, 4);
     for (int i = 0; i < 4; ++i) mbar_init(&S.v_free[i], 4);
   }
   if (warp == 4 * WG_MMA) tmem_alloc(&S.tmem_base, 512);
   if (key_hist)
     for (int i = tid; i < 2048; i += NT) S.khist[i] = 0;
+  const bool sa_mode = sa.n_steps > 0;
+  if (sa_mode) {
+    if (tid < sa.n_knobs) {
+      S.sa_cards[tid] = sa.cards[tid];
+      S.sa_mult[tid] = sa.mult[tid];
+    }
+    // (the starting choices are the kernel's input, not written by the stream's predecessor)
+    for (int e = tid; e < sa.n_chains * sa.n_knobs; e += NT) S.sa_cur[e / sa.n_knobs][e % sa.n_knobs] = sa.cur0[e];
+  }
   __syncthreads();
   // per-choice tables, one flat pass over every axis' entries (loads independent across threads)
   for (int e = tid; e < S.tab_off[na]; e += NT) {
@@ -578,8 +641,9 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
   const uint32_t tmem = S.tmem_base;
   const int64_t n_tiles = (B + GT - 1) / GT;
   const int64_t my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  // one tile per CTA (small batches): the head's waits are on the critical path, no sleeping
-  const bool one_tile = my_tiles <= 1;
+  // one tile per CTA (small batches) or annealing (every tile waits on the previous one's
+  // head): the head's waits are on the critical path, no sleeping
+  const bool one_tile = my_tiles <= 1 || sa_mode;
   const int C = n_loops;  // chunks per tile
   const int64_t n_chunks = my_tiles * C;
   const uint64_t size = T.space_size;
@@ -593,7 +657,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     // IEEE (x - mean) / std of model.py:108-112 before the single cast to fp32
     const double m6 = T.fmean[6], r6 = 1.0 / T.fstd[6], m7 = T.fmean[7], r7 = 1.0 / T.fstd[7];
     const EncodeCtx X{idx, idx32, idx_base, B, my_tiles, size, err, tmem,
-                      static_cast<uint32_t>((g & ~31) << 16), g, m6, r6, m7, r7};
+                      static_cast<uint32_t>((g & ~31) << 16), g, m6, r6, m7, r7, &sa};
     switch (na) {  // (kernels.py: 4 axes for 1-D ops, 5 depthwise, 6 the 2-D ops)
       case 6: encode_loop<6>(S, X); break;
       case 5: encode_loop<5>(S, X); break;
@@ -974,6 +1038,29 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       }
       tc_fence_before();
       warp_arrive(&S.d4_empty);
+      if (sa_mode) {  // history, then the Metropolis test of step ti - 1 (kt_sa_accept, search.py:246-251)
+        const int n = sa.n_chains;
+        if (g < n) {
+          const bool ok = v >= 0 && static_cast<uint64_t>(v) < size;
+          const float zf = ok ? (b3 + acc0) + acc1 : __int_as_float(0x7fc00000);
+          sa.hist_z[ti * n + g] = zf;
+          const double en = static_cast<double>(zf);
+          if (ti == 0) {
+            S.sa_energy[g] = en;
+          } else {
+            const int64_t o = (ti - 1) * n + g;
+            const double eo = S.sa_energy[g];
+            const double pr = exp(fmin((en - eo) / sa.temps[ti - 1], 0.0));
+            if ((en >= eo) || (sa.u[o] < pr)) {
+              for (int j = 0; j < sa.n_knobs; ++j) S.sa_cur[g][j] = S.sa_nxt[g][j];
+              S.sa_energy[g] = en;
+            }
+          }
+        }
+        warp_arrive(&S.acc_done);
+        if (tr) TRACE(12, ti);
+        continue;
+      }
       const int64_t gi = (blockIdx.x + ti * gridDim.x) * GT + g;
       if (gi < B) {
         const bool ok = v >= 0 && static_cast<uint64_t>(v) < size;
@@ -1030,7 +1117,7 @@ extern "C" int kt_score_indices_flags(const kt_spec_table* tab, const kt_dims* d
       launch_pdl(tcs::score_tc_kernel, dim3(grid), dim3(tcs::NT), static_cast<size_t>(smem), as_stream(stream), tab,
                  *dims, params, idx, idx32, idx_base, B, z_out, u_out,
                  reinterpret_cast<unsigned long long*>(keys_out), keys_out ? key_hist : nullptr, err_flag,
-                 static_cast<int>(flags));
+                 static_cast<int>(flags), tcs::SaArgs{});
   KT_REQUIRE(e == cudaSuccess, KT_E_CUDA, "kt_score_indices: %s", cudaGetErrorString(e));
   note_launches(1);
   return check_launch("kt_score_indices");
@@ -1049,4 +1136,49 @@ extern "C" int kt_score_indices(const kt_spec_table* tab, const kt_dims* dims, c
                                 float* u_out, int32_t* err_flag, void* stream) {
   return kt_score_indices_ex(tab, dims, params, idx, nullptr, idx_base, B, z_out, u_out, nullptr, nullptr, err_flag,
                              stream);
+}
+
+extern "C" int kt_sa_run(const kt_spec_table* tab, const kt_dims* dims, const float* params, int32_t n_chains,
+                         int32_t n_knobs, const int32_t* cards, const int64_t* mult, int32_t n_steps,
+                         const int32_t* knob, const uint8_t* nudge, const int32_t* delta, const int32_t* resample,
+                         const double* u, const double* temps, const int32_t* cur0, int64_t* hist_idx,
+                         float* hist_z, int32_t* err_flag, void* stream) {
+  using namespace kt;
+  KT_REQUIRE(tab && dims && params && cards && mult && knob && nudge && delta && resample && u && temps && cur0 &&
+                 hist_idx && hist_z && err_flag,
+             KT_E_ARG, "kt_sa_run: null pointer");
+  KT_REQUIRE(n_chains >= 1 && n_chains <= tcs::GT, KT_E_SHAPE, "kt_sa_run: 1..%d chains", tcs::GT);
+  KT_REQUIRE(n_knobs >= 1 && n_knobs <= KT_MAX_KNOBS, KT_E_SHAPE, "kt_sa_run: 1..%d knobs", KT_MAX_KNOBS);
+  KT_REQUIRE(n_steps >= 1, KT_E_EMPTY, "kt_sa_run: no steps");
+  KT_REQUIRE(default_dims_tc(*dims), KT_E_UNSUPPORTED, "kt_sa_run: fused scorer needs the default dims");
+  tcs::SaArgs a{};
+  a.n_steps = n_steps;
+  a.n_chains = n_chains;
+  a.n_knobs = n_knobs;
+  for (int j = 0; j < n_knobs; ++j) {
+    KT_REQUIRE(cards[j] >= 1, KT_E_RANGE, "kt_sa_run: empty knob %d", j);
+    a.cards[j] = cards[j];
+    a.mult[j] = static_cast<long long>(mult[j]);
+  }
+  a.knob = knob;
+  a.nudge = nudge;
+  a.delta = delta;
+  a.resample = resample;
+  a.u = u;
+  a.temps = temps;
+  a.cur0 = cur0;
+  a.hist_idx = hist_idx;
+  a.hist_z = hist_z;
+  static SmemAttr attr;
+  const int smem = static_cast<int>(sizeof(tcs::Smem));
+  attr.ensure(tcs::score_tc_kernel, static_cast<size_t>(smem));
+  const int64_t B = static_cast<int64_t>(n_steps + 1) * tcs::GT;  // one tile per step, one CTA
+  const cudaError_t e =
+      launch_pdl(tcs::score_tc_kernel, dim3(1), dim3(tcs::NT), static_cast<size_t>(smem), as_stream(stream), tab,
+                 *dims, params, static_cast<const int64_t*>(nullptr), static_cast<const uint32_t*>(nullptr),
+                 int64_t{0}, B, hist_z, static_cast<float*>(nullptr), static_cast<unsigned long long*>(nullptr),
+                 static_cast<unsigned int*>(nullptr), err_flag, 0, a);
+  KT_REQUIRE(e == cudaSuccess, KT_E_CUDA, "kt_sa_run: %s", cudaGetErrorString(e));
+  note_launches(1);
+  return check_launch("kt_sa_run");
 }

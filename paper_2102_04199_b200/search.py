@@ -382,12 +382,15 @@ def draw_unvisited(space: KnobSpace, visited: set, count: int, rng) -> list:
 class DeviceAnnealer:
     """sa_explore's chains on the GPU for one CostModelPredictor.
 
-    Every step is kt_sa_propose -> fused scorer -> kt_sa_accept on device-resident
-    chain state; the per-step random draws come from the caller's Generator in the
-    reference's order (they never depend on the predictions), and the whole
-    step sequence is captured once into a CUDA graph and replayed."""
+    The per-step random draws come from the caller's Generator in the reference's order
+    (they never depend on the predictions: kt_sa_draws).  engine "fused" (default, up to
+    128 chains): the whole annealing loop is one kt_sa_run launch -- the fused scorer on
+    one CTA proposes, scores and accepts step after step.  engine "steps": every step is
+    kt_sa_propose -> scorer -> kt_sa_accept on device-resident chain state, the step
+    sequence captured once into a CUDA graph and replayed.  Both give the reference
+    loop's history."""
 
-    def __init__(self, predictor: CostModelPredictor, sched: SaSchedule, n_chains: int):
+    def __init__(self, predictor: CostModelPredictor, sched: SaSchedule, n_chains: int, engine: str | None = None):
         m, space = predictor.m, predictor.space
         if not _default_model(m) or space.size >= 2**32:
             raise DomainError("device annealing needs the default model dims and a space < 2^32")
@@ -430,6 +433,23 @@ class DeviceAnnealer:
             self.temps.append(t)
             t = max(t * sched.cooling, 1e-9)
         self.graph = None
+        import os
+
+        engine = engine or os.environ.get("KT_SA_ENGINE", "fused")
+        if engine not in ("fused", "steps"):
+            raise DomainError(f"unknown annealing engine {engine!r}")
+        self.engine = "fused" if engine == "fused" and n_chains <= 128 else "steps"
+        self.temps_dev = torch.tensor(self.temps, dtype=torch.float64, device=dev)
+        self.cards_h = np.ascontiguousarray(self.cards_np, dtype=np.int32)
+        self.mult_h = np.ascontiguousarray(_space_multipliers(space), dtype=np.int64)
+
+    def _run_fused(self):
+        p = _lib.ptr
+        _lib.check(self.lib.kt_sa_run(p(self.tab), self.dims, p(self.flat), self.n, self.nk, self.cards_h.ctypes.data,
+                                      self.mult_h.ctypes.data, self.sched.steps_per_round, p(self.knob),
+                                      p(self.nudge), p(self.delta), p(self.resample), p(self.u), p(self.temps_dev),
+                                      p(self.cur), p(self.hist_idx), p(self.hist_z), p(self.err),
+                                      _lib.stream_handle(self.dev)), "sa run")
 
     def _score(self, i, st):
         # after the first score the preceding kernel is kt_sa_propose, which leaves the
@@ -467,7 +487,9 @@ class DeviceAnnealer:
                 choices[:, j] = rest % self.cards_np[j]
                 rest //= self.cards_np[j]
             self.cur.copy_(torch.from_numpy(choices.astype(np.int32)))
-            if self.graph is None:
+            if self.engine == "fused":
+                self._run_fused()
+            elif self.graph is None:
                 self._steps()  # eager first run (kernel attributes set outside capture)
                 torch.cuda.synchronize(self.dev)
                 self.hist_idx[0].copy_(torch.from_numpy(start_idx))
@@ -476,7 +498,8 @@ class DeviceAnnealer:
                 with torch.cuda.graph(g):
                     self._steps()
                 self.graph = g
-            self.graph.replay()
+            if self.engine == "steps":
+                self.graph.replay()
             hi = self.hist_idx.cpu().numpy().reshape(-1)
             hz = self.hist_z.cpu().numpy().reshape(-1).astype(np.float64)
         # insertion order: starts, then each step's chains (a revisit keeps its first
