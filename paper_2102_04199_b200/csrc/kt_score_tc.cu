@@ -324,17 +324,20 @@ struct EncodeCtx {
 __device__ __forceinline__ int64_t sa_propose(Smem& S, const EncodeCtx& X, int64_t ti) {
   const SaArgs& A = *X.sa;
   const int g = X.g, n = A.n_chains;
+  // the step's draws are inputs: loaded before waiting for the previous step's acceptance
+  const int64_t o = (ti - 1) * n + g;
+  const bool mine = ti > 0 && g < n;
+  const int kn = mine ? A.knob[o] : 0, dl = mine ? A.delta[o] : 0, rs = mine ? A.resample[o] : 0;
+  const bool nd = mine && A.nudge[o];
   if (ti > 0) mbar_wait(&S.acc_done, static_cast<uint32_t>((ti - 1) & 1));
   if (g >= n) return INT64_MIN;
   if (ti == 0) return A.hist_idx[g];
-  const int64_t o = (ti - 1) * n + g;
-  const int kn = A.knob[o];
   int64_t id = 0;
   for (int j = 0; j < A.n_knobs; ++j) {
     int v = S.sa_cur[g][j];
     if (j == kn) {
-      const int stepped = min(max(v + A.delta[o], 0), S.sa_cards[j] - 1);
-      v = A.nudge[o] ? stepped : A.resample[o];
+      const int stepped = min(max(v + dl, 0), S.sa_cards[j] - 1);
+      v = nd ? stepped : rs;
     }
     S.sa_nxt[g][j] = v;
     id += static_cast<int64_t>(v) * S.sa_mult[j];
@@ -994,6 +997,12 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     const bool tr = g == 0;
     for (int64_t ti = 0; ti < my_tiles; ++ti) {
       const uint32_t ph = static_cast<uint32_t>(ti & 1);
+      // annealing: this step's uniform and temperature, loaded ahead of the scores
+      double sa_u = 0.0, sa_t = 1.0;
+      if (sa_mode && ti > 0 && g < sa.n_chains) {
+        sa_u = sa.u[(ti - 1) * sa.n_chains + g];
+        sa_t = sa.temps[ti - 1];
+      }
       if (one_tile)
         mbar_wait(&S.d3_full, ph);
       else
@@ -1048,10 +1057,9 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
           if (ti == 0) {
             S.sa_energy[g] = en;
           } else {
-            const int64_t o = (ti - 1) * n + g;
             const double eo = S.sa_energy[g];
-            const double pr = exp(fmin((en - eo) / sa.temps[ti - 1], 0.0));
-            if ((en >= eo) || (sa.u[o] < pr)) {
+            const double pr = exp(fmin((en - eo) / sa_t, 0.0));
+            if ((en >= eo) || (sa_u < pr)) {
               for (int j = 0; j < sa.n_knobs; ++j) S.sa_cur[g][j] = S.sa_nxt[g][j];
               S.sa_energy[g] = en;
             }
