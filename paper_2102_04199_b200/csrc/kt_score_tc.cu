@@ -86,7 +86,22 @@ constexpr int NT = 128 * NWG;  // (roles by warpgroup, see the header)
 // registers per lane; the launch gives each REG_BASE, the roles rebalance them
 constexpr int REG_BASE = (512 / NWG) & ~7;
 #if KT_R2
-constexpr int REG_HEAD = 64, REG_ENC = 80, REG_R = 56, REG_RO = 96, REG_MMA = 56;
+#ifndef KT_REG_HEAD
+#define KT_REG_HEAD 64
+#endif
+#ifndef KT_REG_ENC
+#define KT_REG_ENC 80
+#endif
+#ifndef KT_REG_R
+#define KT_REG_R 56
+#endif
+#ifndef KT_REG_RO
+#define KT_REG_RO 96
+#endif
+#ifndef KT_REG_MMA
+#define KT_REG_MMA 56
+#endif
+constexpr int REG_HEAD = KT_REG_HEAD, REG_ENC = KT_REG_ENC, REG_R = KT_REG_R, REG_RO = KT_REG_RO, REG_MMA = KT_REG_MMA;
 #else
 constexpr int REG_HEAD = 72, REG_ENC = 80, REG_R = 56, REG_RO = 104, REG_MMA = 64;
 #endif
@@ -283,6 +298,19 @@ __device__ __forceinline__ void store_operand(const OperandRegs<N, K>& r, float*
   for (int i = 0; i < IT; ++i) {
     const int e = tid + i * NT, k = e / N, n = e - k * N;
     if (e < N * K) store_split(hi, lo, kmajor_offset(n, k, K) >> 2, r.v[i]);
+  }
+}
+
+// 16 values -> v = hi (truncated tf32, in place), lo = exact remainder
+__device__ __forceinline__ void split16_inplace(float* v, float* lo) {
+#pragma unroll
+  for (int j = 0; j < 16; j += 2) {
+    const float2 t = make_float2(tf32_trunc(v[j]), tf32_trunc(v[j + 1]));
+    const float2 l = fsub2(make_float2(v[j], v[j + 1]), t);
+    v[j] = t.x;
+    v[j + 1] = t.y;
+    lo[j] = l.x;
+    lo[j + 1] = l.y;
   }
 }
 
@@ -847,10 +875,10 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       if (g == 0) TRACE(14, q);
       tc_fence_after();
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float hi[16], lo[16];
-        split16(v + 16 * h, hi, lo);
-        tmem_st16(tmem + lane + T_R + 64 * b + 16 * h, hi);
+      for (int h = 0; h < 2; ++h) {  // hi in place (v), lo alongside: 48 live values, not 64
+        float lo[16];
+        split16_inplace(v + 16 * h, lo);
+        tmem_st16(tmem + lane + T_R + 64 * b + 16 * h, v + 16 * h);
         tmem_st16(tmem + lane + T_R + 64 * b + 32 + 16 * h, lo);
       }
       if (g == 0) TRACE(15, q);
