@@ -87,7 +87,7 @@ constexpr int NT = 128 * NWG;  // (roles by warpgroup, see the header)
 constexpr int REG_BASE = (512 / NWG) & ~7;
 #if KT_R2
 #ifndef KT_REG_HEAD
-#define KT_REG_HEAD 64
+#define KT_REG_HEAD 48
 #endif
 #ifndef KT_REG_ENC
 #define KT_REG_ENC 80
@@ -96,7 +96,7 @@ constexpr int REG_BASE = (512 / NWG) & ~7;
 #define KT_REG_R 56
 #endif
 #ifndef KT_REG_RO
-#define KT_REG_RO 96
+#define KT_REG_RO 104
 #endif
 #ifndef KT_REG_MMA
 #define KT_REG_MMA 56
