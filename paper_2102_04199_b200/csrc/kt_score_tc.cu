@@ -1187,6 +1187,7 @@ extern "C" int kt_sa_run(const kt_spec_table* tab, const kt_dims* dims, const fl
   KT_REQUIRE(n_knobs >= 1 && n_knobs <= KT_MAX_KNOBS, KT_E_SHAPE, "kt_sa_run: 1..%d knobs", KT_MAX_KNOBS);
   KT_REQUIRE(n_steps >= 1, KT_E_EMPTY, "kt_sa_run: no steps");
   KT_REQUIRE(default_dims_tc(*dims), KT_E_UNSUPPORTED, "kt_sa_run: fused scorer needs the default dims");
+  KT_REQUIRE(!KT_ENC_PIPE, KT_E_UNSUPPORTED, "kt_sa_run: not built for the KT_ENC_PIPE encode variant");
   tcs::SaArgs a{};
   a.n_steps = n_steps;
   a.n_chains = n_chains;
