@@ -915,13 +915,32 @@ fine_tune_cluster_kernel(kt_dims dims, int rc, const float* __restrict__ theta, 
       mse_out[st] = m;
     }
     cl.sync();  // every slice updated
-    for (int q = 0; q < C; ++q) {  // the other slices, float4 groups, loads of all peers in flight
-      if (q == c) continue;
-      const int a0 = static_cast<int>(static_cast<int64_t>(G4) * q / C);
-      const int a1 = static_cast<int>(static_cast<int64_t>(G4) * (q + 1) / C);
-      const float4* src = reinterpret_cast<const float4*>(cl.map_shared_rank(th, q));
-      float4* dst = reinterpret_cast<float4*>(th);
-      for (int e4 = a0 + static_cast<int>(threadIdx.x); e4 < a1; e4 += NT) dst[e4] = src[e4];
+    if (C == 8) {  // the other slices: every peer's load issued before any store (DSMEM latency once)
+      const int smax = (G4 + C - 1) / C;
+      for (int base = 0; base < smax; base += NT) {
+        float4 v[8];
+        int at[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int a0 = static_cast<int>(static_cast<int64_t>(G4) * q / C);
+          const int a1 = static_cast<int>(static_cast<int64_t>(G4) * (q + 1) / C);
+          const int e4 = a0 + base + static_cast<int>(threadIdx.x);
+          at[q] = q != c && e4 < a1 ? e4 : -1;
+          if (at[q] >= 0) v[q] = reinterpret_cast<const float4*>(cl.map_shared_rank(th, q))[e4];
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (at[q] >= 0) reinterpret_cast<float4*>(th)[at[q]] = v[q];
+      }
+    } else {
+      for (int q = 0; q < C; ++q) {  // the other slices, float4 groups
+        if (q == c) continue;
+        const int a0 = static_cast<int>(static_cast<int64_t>(G4) * q / C);
+        const int a1 = static_cast<int>(static_cast<int64_t>(G4) * (q + 1) / C);
+        const float4* src = reinterpret_cast<const float4*>(cl.map_shared_rank(th, q));
+        float4* dst = reinterpret_cast<float4*>(th);
+        for (int e4 = a0 + static_cast<int>(threadIdx.x); e4 < a1; e4 += NT) dst[e4] = src[e4];
+      }
     }
     __syncthreads();
   }
