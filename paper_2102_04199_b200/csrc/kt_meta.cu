@@ -871,16 +871,21 @@ fine_tune_cluster_kernel(kt_dims dims, int rc, const float* __restrict__ theta, 
   const int p0 = 4 * q0, p1 = 4 * q1 < h.P ? 4 * q1 : h.P;
   const int d0 = h.dim[0];
   for (int e = threadIdx.x; e < h.P; e += NT) th[e] = theta[e];
+  // this CTA's rows never change across the steps: staged once when they fit one row chunk
+  const bool rows_once = tiled_ok(h) && r1 > r0 && r1 - r0 <= h.RC;
+  if (rows_once) load_rows(h, u + static_cast<int64_t>(r0) * d0, nullptr, 0, r1 - r0, S, false);
   __syncthreads();
   for (int st = 0; st < steps; ++st) {
     float part = 0.0f;
     if (r1 > r0) {
-      part = head_pass(h, th, nullptr, u + static_cast<int64_t>(r0) * d0, nullptr, y + r0, r1 - r0, gb, S, n);
+      part = head_pass(h, th, nullptr, u + static_cast<int64_t>(r0) * d0, nullptr, y + r0, r1 - r0, gb, S, n, rows_once);
     } else {
       for (int e = threadIdx.x; e < h.P; e += NT) gb[e] = 0.0f;
     }
     if (threadIdx.x == 0) s_mse = part;
+    MT();
     cl.sync();  // every CTA's gradient share is complete
+    MT();
     if (C == 8) {  // (the launch's cluster size for >= 64 rows: the peer loads unrolled)
       for (int e4 = q0 + static_cast<int>(threadIdx.x); e4 < q1; e4 += NT) {
         float4 v[8];
@@ -901,6 +906,11 @@ fine_tune_cluster_kernel(kt_dims dims, int rc, const float* __restrict__ theta, 
         tv.z -= alpha * g.z;
         tv.w -= alpha * g.w;
         *t = tv;
+        // pushed into every peer's copy too (their slice c is read only after the next cluster
+        // barrier and written only here), so no gather pass follows
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q != c) reinterpret_cast<float4*>(cl.map_shared_rank(th, q))[e4] = tv;
       }
     } else {
       for (int e = p0 + static_cast<int>(threadIdx.x); e < p1; e += NT) {
@@ -914,25 +924,10 @@ fine_tune_cluster_kernel(kt_dims dims, int rc, const float* __restrict__ theta, 
       for (int q = 0; q < C; ++q) m += *cl.map_shared_rank(&s_mse, q);
       mse_out[st] = m;
     }
+    MT();
     cl.sync();  // every slice updated
-    if (C == 8) {  // the other slices: every peer's load issued before any store (DSMEM latency once)
-      const int smax = (G4 + C - 1) / C;
-      for (int base = 0; base < smax; base += NT) {
-        float4 v[8];
-        int at[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int a0 = static_cast<int>(static_cast<int64_t>(G4) * q / C);
-          const int a1 = static_cast<int>(static_cast<int64_t>(G4) * (q + 1) / C);
-          const int e4 = a0 + base + static_cast<int>(threadIdx.x);
-          at[q] = q != c && e4 < a1 ? e4 : -1;
-          if (at[q] >= 0) v[q] = reinterpret_cast<const float4*>(cl.map_shared_rank(th, q))[e4];
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (at[q] >= 0) reinterpret_cast<float4*>(th)[at[q]] = v[q];
-      }
-    } else {
+    MT();
+    if (C != 8) {  // (C == 8: the peers pushed their slices during the reduce)
       for (int q = 0; q < C; ++q) {  // the other slices, float4 groups
         if (q == c) continue;
         const int a0 = static_cast<int>(static_cast<int64_t>(G4) * q / C);
