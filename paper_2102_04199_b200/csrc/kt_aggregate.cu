@@ -439,7 +439,7 @@ constexpr int TC_ROWS = 128;
 // swizzle instead of 1-D copies -- 16-byte piece c of tile row R sits at piece c ^ (R & 7)
 // -- so the row-per-thread reads and writes are bank-conflict free with no register
 // rotation (TMA undoes the swizzle on the way out).
-template <int DIN, bool IN64, int S, int OB, bool TM>
+template <int DIN, bool IN64, int S, int OB, bool TM, bool PF = false>  // PF: the L2 prefetch is compiled in
 __global__ void __launch_bounds__(TC_ROWS, S == 1 ? 4 : 3)
     gcn_layer_pipe_kernel(LayerArgs a, int rp_cap, int nz_cap, const __grid_constant__ CUtensorMap tm_in,
                           const __grid_constant__ CUtensorMap tm_out) {
@@ -531,7 +531,8 @@ __global__ void __launch_bounds__(TC_ROWS, S == 1 ? 4 : 3)
     for (int st = 0; st < S; ++st)
       if (blockIdx.x + static_cast<int64_t>(st) * gridDim.x < n_tiles)
         issue_load(blockIdx.x + static_cast<int64_t>(st) * gridDim.x, st);
-    for (int p = 0; p < a.l2pf; ++p) issue_prefetch(blockIdx.x + static_cast<int64_t>(S + p) * gridDim.x);
+    if constexpr (PF)
+      for (int p = 0; p < a.l2pf; ++p) issue_prefetch(blockIdx.x + static_cast<int64_t>(S + p) * gridDim.x);
   }
   if (IN64)
     for (int c = tid; c < DIN; c += TC_ROWS) {
@@ -823,7 +824,8 @@ __global__ void __launch_bounds__(TC_ROWS, S == 1 ? 4 : 3)
       tc::tc_fence_after();
       if (tid == 0 && t + static_cast<int64_t>(S) * gridDim.x < n_tiles) {
         issue_load(t + static_cast<int64_t>(S) * gridDim.x, st);
-        if (a.l2pf > 0) issue_prefetch(t + static_cast<int64_t>(S + a.l2pf) * gridDim.x);
+        if constexpr (PF)
+          if (a.l2pf > 0) issue_prefetch(t + static_cast<int64_t>(S + a.l2pf) * gridDim.x);
       }
       __syncwarp();
       if (tc::elect_one()) {
@@ -987,9 +989,9 @@ extern "C" int kt_gcn_layer(const void* in, int32_t in_f64, const double* fmean,
       // CTAs per SM (2 x 2 and 3 x 1 drop to two CTAs per SM: 0.41); KT_AGG_SOB=21 for A/B
       const char* sob = getenv("KT_AGG_SOB");
       if (sob && sob[0] == '2' && sob[1] == '1')
-        plaunch(agg::gcn_layer_pipe_kernel<32, false, 2, 1, true>, 32, agg::TC_ROWS * 32 * 4, 2, 1, true);
+        plaunch(agg::gcn_layer_pipe_kernel<32, false, 2, 1, true, true>, 32, agg::TC_ROWS * 32 * 4, 2, 1, true);
       else
-        plaunch(agg::gcn_layer_pipe_kernel<32, false, 1, 1, true>, 32, agg::TC_ROWS * 32 * 4, 1, 1, true);
+        plaunch(agg::gcn_layer_pipe_kernel<32, false, 1, 1, true, true>, 32, agg::TC_ROWS * 32 * 4, 1, 1, true);
     } else {
       plaunch(agg::gcn_layer_pipe_kernel<32, false, 3, 1, false>, 32, agg::TC_ROWS * 32 * 4, 3, 1, false);
     }
