@@ -446,7 +446,8 @@ def bench_sa(m, reps=20):
     ms = 1e3 * (time.perf_counter() - t0) / reps
     return {"metric": "sa_explore call (16 chains x 128 steps)", "value": ms, "unit": "ms/call",
             "higher_is_better": False, "graphs_per_s": 16 * 129 / (ms / 1e3),
-            "config": "SaSchedule defaults, conv2d bench spec, super layout; wall clock incl. host RNG draws"}
+            "config": "SaSchedule defaults, conv2d bench spec, super layout; wall clock incl. the step draws "
+                      "(native PCG64, kt_sa_draws) and one kt_sa_run launch (propose / score / accept fused)"}
 
 
 def bench_predict(m, n=4096, reps=50):
