@@ -126,9 +126,6 @@ constexpr int NR = 2;     // R buffers
 #endif
 constexpr int N2 = 2;     // D2 buffers
 constexpr int TAB = 448;
-#ifndef KT_HEAD_PREP
-#define KT_HEAD_PREP 1  // the head warpgroup extracts the digits / table entries two tiles ahead
-#endif
 #ifndef KT_ENC_PIPE
 #define KT_ENC_PIPE 0
 #endif
@@ -220,13 +217,6 @@ struct __align__(1024) Smem {
   uint64_t d1_full[N1], d1_empty[N1], r_full[NR], r_empty[NR], d2_full[N2], d2_empty[N2];
   uint64_t u_full, uz_empty, z_full, d3_full, d4_full, d4_empty, v_free[4];
   uint64_t acc_done;                            // annealing: the head has accepted a step
-  // tiles prepared by the head warpgroup for the encode (KT_HEAD_PREP), two slots
-  uint64_t pre_full[2], pre_empty[2];
-  int pre_e[2][KT_MAX_AXES][GT];
-  int2 pre_oi[2][KT_MAX_AXES][GT];
-  int pre_autov[2][GT];
-  float pre_one[2][GT];
-  unsigned char pre_unr[2][GT];
   int32_t sa_cur[GT][KT_MAX_KNOBS], sa_nxt[GT][KT_MAX_KNOBS];
   double sa_energy[GT];
   long long sa_mult[KT_MAX_KNOBS];
@@ -416,48 +406,6 @@ __device__ __forceinline__ void encode_prepare(Smem& S, const EncodeCtx& X, int6
   st.lt = 0.0;
 }
 
-// KT_HEAD_PREP: the head warpgroup (idle for most of a tile) does encode_prepare's index
-// decode for tile ti two tiles ahead and leaves the per-graph results in a shared slot.
-template <int NA>
-__device__ __forceinline__ void head_prepare(Smem& S, const EncodeCtx& X, int64_t ti, int64_t v64) {
-  const int slot = static_cast<int>(ti & 1);
-  mbar_wait(&S.pre_empty[slot], static_cast<uint32_t>(((ti >> 1) & 1) ^ 1));  // encode read tile ti - 2
-  const bool ok = v64 >= 0 && static_cast<uint64_t>(v64) < X.size;
-  S.vtile[ti & 3][X.g] = v64;  // (the head's own ring: it reads the slot back at tile ti)
-  if (v64 != INT64_MIN && !ok) atomicOr(X.err, 1);
-  const uint32_t v = ok ? static_cast<uint32_t>(v64) : 0u;
-  const int autov = S.auto_knob >= 0 ? S.auto_vals[knob_digit(S, v, 6)] : 0;
-  const int expl = S.expl_knob >= 0 ? S.expl_vals[knob_digit(S, v, 7)] : 0;
-  S.pre_autov[slot][X.g] = autov;
-  S.pre_unr[slot][X.g] = expl != 0 && autov > 0;
-  S.pre_one[slot][X.g] = ok ? 1.0f : 0.0f;
-#pragma unroll
-  for (int a = 0; a < NA; ++a) {
-    const int e = S.tab_off[a] + (S.axis_knob[a] >= 0 ? knob_digit(S, v, a) : 0);
-    S.pre_e[slot][a][X.g] = e;
-    S.pre_oi[slot][a][X.g] = S.oi[e];
-  }
-  warp_arrive(&S.pre_full[slot]);
-}
-// The encode side: tile ti's prepared fields out of the shared slot.
-template <int NA>
-__device__ __forceinline__ void encode_take(Smem& S, const EncodeCtx& X, int64_t ti, EncodeTile<NA>& st) {
-  const int slot = static_cast<int>(ti & 1);
-  mbar_wait(&S.pre_full[slot], static_cast<uint32_t>((ti >> 1) & 1));
-  st.autov = S.pre_autov[slot][X.g];
-  st.unr_on = S.pre_unr[slot][X.g] != 0;
-  st.one = S.pre_one[slot][X.g];
-#pragma unroll
-  for (int a = 0; a < NA; ++a) {
-    st.e[a] = S.pre_e[slot][a][X.g];
-    st.oi[a] = S.pre_oi[slot][a][X.g];
-  }
-  st.t = 1.0;
-  st.lt = 0.0;
-  __syncwarp();
-  warp_arrive(&S.pre_empty[slot]);
-}
-
 // Feature row c (loop k = 2 NA - 1 - c, innermost first) of a tile into S.xstage[buf][c].
 // touched -- the product of the extents of the loops inside loop k, multiplied innermost
 // outward as np.cumprod(e[::-1]) does -- accumulates exactly in fp64, and log2(touched)
@@ -564,17 +512,12 @@ __device__ __forceinline__ void encode_loop(Smem& S, const EncodeCtx& X) {
   }
 #else
   const bool sa = X.sa->n_steps > 0;
-  const bool from_head = KT_HEAD_PREP && !sa;
-  int64_t v_next = sa || from_head ? 0 : index_of(0);
+  int64_t v_next = sa ? 0 : index_of(0);
   for (int64_t ti = 0; ti < X.my_tiles; ++ti) {
     EncodeTile<NA> st;
     if (X.g == 0) TRACE(24, ti);
-    if (from_head) {
-      encode_take<NA>(S, X, ti, st);
-    } else {
-      encode_prepare<NA>(S, X, ti, sa ? sa_propose(S, X, ti) : v_next, st);
-      if (!sa) v_next = index_of(ti + 1);  // next tile's index load in flight during this tile
-    }
+    encode_prepare<NA>(S, X, ti, sa ? sa_propose(S, X, ti) : v_next, st);
+    if (!sa) v_next = index_of(ti + 1);  // next tile's index load in flight during this tile
     if (X.g == 0) TRACE(26, ti);
 #pragma unroll
     for (int c = 0; c < C; ++c) encode_row<NA>(S, X, st, c, 0);
@@ -643,10 +586,6 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     mbar_init(&S.d4_full, 1);
     mbar_init(&S.d4_empty, 4);
     mbar_init(&S.acc_done, 4);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&S.pre_full[i], 4);
-      mbar_init(&S.pre_empty[i], 4);
-    }
     for (int i = 0; i < 4; ++i) mbar_init(&S.v_free[i], 4);
   }
   if (warp == 4 * WG_MMA) tmem_alloc(&S.tmem_base, 512);
@@ -1084,32 +1023,8 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     const uint32_t lane = static_cast<uint32_t>((32 * quad) << 16);
     const float b3 = params[dims.off_hb[2]];
     const bool tr = g == 0;
-    // KT_HEAD_PREP: this warpgroup decodes the encode's tiles two ahead (it idles most of a tile)
-    const bool prep_here = KT_HEAD_PREP && !sa_mode;
-    const EncodeCtx HX{idx, idx32, idx_base, B, my_tiles, size, err, tmem, lane, g, 0.0, 0.0, 0.0, 0.0, &sa};
-    auto prep = [&](int64_t pt) {
-      if (pt >= my_tiles) return;
-      const int64_t gi = (blockIdx.x + pt * gridDim.x) * GT + g;
-      const int64_t v64 = gi >= B ? INT64_MIN
-                          : idx32 ? static_cast<int64_t>(idx32[gi])
-                          : idx   ? __ldcs(idx + gi)
-                                  : idx_base + gi;
-      switch (na) {
-        case 6: head_prepare<6>(S, HX, pt, v64); break;
-        case 5: head_prepare<5>(S, HX, pt, v64); break;
-        case 4: head_prepare<4>(S, HX, pt, v64); break;
-        case 3: head_prepare<3>(S, HX, pt, v64); break;
-        case 2: head_prepare<2>(S, HX, pt, v64); break;
-        default: head_prepare<1>(S, HX, pt, v64); break;
-      }
-    };
-    if (prep_here) {
-      prep(0);
-      prep(1);
-    }
     for (int64_t ti = 0; ti < my_tiles; ++ti) {
       const uint32_t ph = static_cast<uint32_t>(ti & 1);
-      if (prep_here) prep(ti + 2);
       // annealing: this step's uniform and temperature, loaded ahead of the scores
       double sa_u = 0.0, sa_t = 1.0;
       if (sa_mode && ti > 0 && g < sa.n_chains) {
