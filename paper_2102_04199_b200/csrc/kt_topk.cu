@@ -23,7 +23,6 @@
 // (kt_score_indices_ex keys_out / key_hist), so a sweep step reads its keys once for
 // the second digit and once for the gather.
 #include <cooperative_groups.h>
-#include <cstdlib>
 
 #include "kt_common.cuh"
 
@@ -274,8 +273,6 @@ static int run(const Src& src_in, int k, int hist_ready, int64_t* top_idx, float
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel, NT, smem);
     if (per_sm < 1) per_sm = 1;
     if (per_sm > 2) per_sm = 2;
-    const char* cap = getenv("KT_TOPK_PER_SM");  // (A/B: CTAs per SM)
-    if (cap && atoi(cap) >= 1 && atoi(cap) < per_sm) per_sm = atoi(cap);
   }
   const int64_t want = (src.B + NT - 1) / NT;
   const int grid = static_cast<int>(want < per_sm * kNumSMs ? want : per_sm * kNumSMs);
