@@ -17,6 +17,7 @@ from paper_2102_04199_b200 import graphs as pg
 from paper_2102_04199_b200 import kernels as pk
 from paper_2102_04199_b200 import meta as pmeta
 from paper_2102_04199_b200 import model as pm
+from paper_2102_04199_b200.util import rng_from
 from tests._shared import device_model, head_shapes, oracle_params, spec_of
 
 pytestmark = pytest.mark.gpu
@@ -183,6 +184,23 @@ def test_fine_tune_matches_reference(cuda_device, g_model, g_meta, super_samples
     assert_params_close(pm.head_to_vec(m2.head).cpu().numpy(), g_meta["ft/theta"])
     assert torch.equal(pm.flat_params(m2)[: pm.dims_of(m).off_head], pm.flat_params(m)[: pm.dims_of(m).off_head])
     assert pmeta.fine_tune(m, [], 0.01, 5) is m
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [1, 7, 16, 40, 64, 100, 130, 257])
+def test_fine_tune_embedded_row_counts_match_oracle(cuda_device, g_model, n):
+    """kt_fine_tune at every launch shape (one CTA below 16 rows, clusters of 4 / 8 CTAs
+    above, rows staged once when they fit a chunk, slices pushed to the peers) against the
+    fp64 oracle restatement of fine_tune_embedded (meta.py:274-282)."""
+    m = device_model(g_model)
+    p = oracle_params(g_model)
+    rng = rng_from("ft-rows", n)
+    u = np.abs(rng.normal(size=(n, 64)))
+    y = rng.normal(size=n)
+    theta = ko.head_to_vec(p["head_w"], p["head_b"])
+    want = ko.fine_tune_embedded(theta, head_shapes(p), u, y, 0.01, 6)
+    got = pm.head_to_vec(pmeta.fine_tune_embedded(m, u, y, 0.01, 6).head).cpu().numpy()
+    assert_params_close(got, want, rtol=1e-5)
 
 
 def test_inner_adapt_alpha_zero_identity(cuda_device, g_model, super_samples):
