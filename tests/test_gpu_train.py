@@ -158,6 +158,40 @@ def test_meta_step_matches_reference(cuda_device, g_model, g_meta, super_samples
     assert_params_close(pm.head_to_vec(m3.head).cpu().numpy(), g_meta[f"{order}/theta3"])
 
 
+@pytest.mark.parametrize("order", ["fo", "so"])
+@pytest.mark.parametrize("ns,nq,inner", [(1, 1, 1), (6, 6, 1), (8, 8, 2), (9, 3, 1), (20, 13, 2), (33, 17, 1)])
+def test_maml_task_shapes_match_oracle(cuda_device, g_model, order, ns, nq, inner):
+    """kt_maml_tasks over support / query sets that fit one row chunk (staged rows, the inner
+    SGD step fused into the gradient write) and sets spanning several chunks, one and two inner
+    steps, first and second order, against the fp64 oracle of maml_outer_grad (meta.py:167-257)."""
+    m = device_model(g_model)
+    p = oracle_params(g_model)
+    rng = rng_from("maml-shapes", ns, nq, inner, order)
+    T = 5
+    n_rows = T * (ns + nq)
+    u = np.abs(rng.normal(size=(n_rows, 64))).astype(np.float32)
+    y = rng.normal(size=n_rows).astype(np.float32)
+    perm = rng.permutation(n_rows)
+    tasks, s_idx, q_idx = [], [], []
+    for t in range(T):
+        rows = perm[t * (ns + nq):(t + 1) * (ns + nq)]
+        s, q = rows[:ns], rows[ns:]
+        s_idx += list(s)
+        q_idx += list(q)
+        tasks.append((u[s].astype(np.float64), y[s].astype(np.float64), u[q].astype(np.float64),
+                      y[q].astype(np.float64)))
+    cfg = pmeta.MetaConfig(alpha=0.01, beta=0.001, inner_steps=inner, first_order=order == "fo")
+    theta = ko.head_to_vec(p["head_w"], p["head_b"])
+    want, sl, ql = ko.meta_step_embedded(theta, head_shapes(p), tasks, cfg.alpha, cfg.beta, inner, order == "fo")
+    dev = cuda_device
+    t64 = lambda a: torch.tensor(np.asarray(a, dtype=np.int64), device=dev)  # noqa: E731
+    g_sum, stats = pmeta.maml_sum(m, torch.from_numpy(u).to(dev), torch.from_numpy(y).to(dev),
+                                  t64(np.arange(T + 1) * ns), t64(s_idx), t64(np.arange(T + 1) * nq), t64(q_idx), cfg)
+    got = pm.head_to_vec(m.head).cpu().numpy().astype(np.float64) - cfg.beta * g_sum.cpu().numpy()
+    assert_params_close(got, want, rtol=1e-5)
+    np.testing.assert_allclose(stats.cpu().numpy() / T, [sl, ql], rtol=1e-4)
+
+
 def test_meta_step_reductions(cuda_device, g_model, g_meta, super_samples):
     m = device_model(g_model)
     tasks = [pmeta.MetaTask([super_samples[i] for i in s], [super_samples[i] for i in q], [])
