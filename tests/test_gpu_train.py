@@ -25,7 +25,12 @@ OPS = pk.OP_TYPES
 TEMPLATE = pg.build_super_template(OPS)
 
 
-def assert_grad_close(got, want, rtol=1e-4):
+def assert_grad_close(got, want, rtol=1e-4, elem_rtol=None):
+    """Per-tensor norm-wise rel <= rtol, and element-wise rel <= elem_rtol (default rtol) above a
+    1e-3 * max floor.  The element-wise 1e-4 bar is for kink-free batches: on an
+    arbitrary batch a ReLU / max-routing decision within fp32 reach of flipping, or fp32
+    cancellation in a batch sum, moves single entries further."""
+    elem_rtol = rtol if elem_rtol is None else elem_rtol
     got = np.asarray(got, dtype=np.float64).ravel()
     want = np.asarray(want, dtype=np.float64).ravel()
     scale = np.linalg.norm(want)
@@ -36,7 +41,7 @@ def assert_grad_close(got, want, rtol=1e-4):
     floor = 1e-3 * np.abs(want).max()
     big = np.abs(want) > floor
     rel = np.abs(got[big] - want[big]) / np.abs(want[big])
-    assert rel.max() <= rtol, f"element-wise rel {rel.max():.2e}"
+    assert rel.max() <= elem_rtol, f"element-wise rel {rel.max():.2e}"
 
 
 def assert_params_close(got, want, rtol=1e-5):
@@ -111,6 +116,29 @@ def test_grad_super_batch_vs_oracle(cuda_device, g_model, super_samples):
     for a, b in zip(g.gcn + [g.agg] + g.head_weights + g.head_biases,
                     rg["gcn"] + [rg["agg"]] + rg["head_w"] + rg["head_b"]):
         assert_grad_close(a.cpu().numpy(), b)
+
+
+@pytest.mark.parametrize("layout", ["raw", "super"])
+@pytest.mark.parametrize("b", [1, 5, 131, 1200])
+def test_grad_batch_sizes_vs_oracle(cuda_device, g_model, raw_samples, super_samples, layout, b):
+    """kt_grad's launch shapes: factored path with 4-graph CTAs and a partial last CTA (1, 5,
+    131 graphs) and the per-graph-row path above 8 x 148 graphs (1,200, samples repeated),
+    raw-segmented and super layouts, against the oracle's batch gradient."""
+    m = device_model(g_model)
+    p = oracle_params(g_model)
+    pool = raw_samples if layout == "raw" else super_samples
+    pick = rng_from("grad-b", b, layout).integers(0, len(pool), b)
+    batch = [(pool[int(j)].graph, pool[int(j)].label_gflops) for j in pick]
+    loss, g = pm.grad(m, batch)
+    trip = []
+    for gr, _ in batch:
+        t = pg.graph_to_tensors(gr)
+        trip.append((t.feature_matrix, t.normalized_adjacency, t.feature_mask))
+    rl, rg = ko.grad(p, trip, [lab for _, lab in batch])
+    assert abs(loss - rl) <= 1e-5 * rl
+    for a, r in zip(g.gcn + [g.agg] + g.head_weights + g.head_biases,
+                    rg["gcn"] + [rg["agg"]] + rg["head_w"] + rg["head_b"]):
+        assert_grad_close(a.cpu().numpy(), r, elem_rtol=1e-3)  # (random batches, not kink-free)
 
 
 def test_sgd_step_matches_reference(cuda_device, g_model, g_grad, raw_samples):
