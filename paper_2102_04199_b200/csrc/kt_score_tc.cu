@@ -597,8 +597,6 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       S.sa_cards[tid] = sa.cards[tid];
       S.sa_mult[tid] = sa.mult[tid];
     }
-    // (the starting choices are the kernel's input, not written by the stream's predecessor)
-    for (int e = tid; e < sa.n_chains * sa.n_knobs; e += NT) S.sa_cur[e / sa.n_knobs][e % sa.n_knobs] = sa.cur0[e];
   }
   __syncthreads();
   // per-choice tables, one flat pass over every axis' entries (loads independent across threads)
@@ -667,6 +665,10 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
   if (params_stable) {
     pdl_wait();
     pdl_launch_dependents();
+  }
+  if (sa_mode) {  // the starting choices, after the programmatic wait (a predecessor may write them)
+    for (int e = tid; e < sa.n_chains * sa.n_knobs; e += NT) S.sa_cur[e / sa.n_knobs][e % sa.n_knobs] = sa.cur0[e];
+    __syncthreads();
   }
   if (threadIdx.x == 0) TRACE(30, 0);  // operand prologue done
   const uint32_t tmem = S.tmem_base;
