@@ -40,3 +40,16 @@ for _ in range(reps):
     tf += t1 - t0
     tb += t2 - t1
 print({"gp_fit_ms": 1e3 * tf / reps, "bo_propose_ms": 1e3 * tb / reps})
+
+if len(sys.argv) > 1 and sys.argv[1] == "--cprofile":
+    import cProfile
+    import pstats
+
+    def rounds():
+        for _ in range(10):
+            s = ps.gp_fit(ps.GpSurrogate(x=x, y=y, noise_variance=1e-4), select_lengthscale=True)
+            ps.bo_propose_batch(s, space, batch, 2.0, pool, visited, rng_from("bench-gp-bo"), pool=pool_cfgs)
+        torch.cuda.synchronize()
+
+    cProfile.run("rounds()", "/tmp/gp.prof")
+    pstats.Stats("/tmp/gp.prof").sort_stats("tottime").print_stats(18)
