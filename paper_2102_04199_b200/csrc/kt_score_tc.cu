@@ -29,19 +29,22 @@
 // a deterministic function of the features, so equal features still score equal.  GEMM1
 // is one K-step instead of two and an X slot is 16 TMEM columns instead of 32.
 //
-// Warp roles (768 threads = 6 warpgroups, 1 CTA / SM, 512 TMEM columns; registers
-// rebalanced per warpgroup with setmaxnreg):
+// Warp roles (896 threads = 7 warpgroups with the default KT_R2, 1 CTA / SM, 512 TMEM
+// columns; registers rebalanced per warpgroup with setmaxnreg, which ptxas also takes as
+// each region's compile-time budget):
 //   WG 0 (warps 0-3)    head: thread = TMEM lane = graph; per tile ReLU(D3 + b0) -> Z1
 //                       (TMEM, hi / lo), then ReLU(D4 + b1) . w3 + b3 -> score, top-k key
 //   WG 1 (warps 4-7)    encode: thread = graph; per row the axis' knob digit straight from
 //                       the index (two magic-number divisions), then the folded operand
 //                       row (fp64 touched / log2 / z-norm, host tables for the rest),
 //                       hi/lo split, tcgen05.st into an X slot
-//   WG 2 (warps 8-11)   R: thread = TMEM lane = graph; ReLU(D1) split hi/lo into R (TMEM)
-//   WG 3-4 (12-19)      readout, two warps per lane quadrant, 16 channels each: running
+//   WG 2-3 (8-15)       R: thread = TMEM lane = graph; ReLU(D1) split hi/lo into R (TMEM),
+//                       one warpgroup per chunk parity
+//   WG 4-5 (16-23)      readout, two warps per lane quadrant, 16 channels each: running
 //                       sum / ReLU-sum / max over the chunks; at a tile's end U -> TMEM
-//   WG 5 (warps 20-22)  MMA issue, one stream each: GEMM1s, GEMM2s, head GEMMs (one
+//   WG 6 (warps 24-26)  MMA issue, one stream each: GEMM1s, GEMM2s, head GEMMs (one
 //                       elected lane issues; each waits only on its own operand barriers)
+// kt_sa_run runs the same kernel in annealing mode (one CTA, a tile per step; see SaArgs).
 // The head warps run a tile's head while the readout warps stream the next tile, so no
 // stage of the chunk pipeline ever waits for the head epilogue.
 #include "kt_encode.cuh"
