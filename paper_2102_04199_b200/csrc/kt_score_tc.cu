@@ -149,7 +149,7 @@ constexpr int TAB = 448;
 #define KT_HEAD_SLEEP 128  // ns between probes of the head warpgroup's (long) waits (0: hardware wait)
 #endif
 #ifndef KT_HEAD_SLEEP_Z
-#define KT_HEAD_SLEEP_Z 64  // the head MMA warp's wait for Z1
+#define KT_HEAD_SLEEP_Z 128  // the head MMA warp's wait for Z1
 #endif
 
 // TMEM column map (512 allocated)
