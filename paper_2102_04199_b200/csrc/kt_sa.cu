@@ -117,6 +117,9 @@ extern "C" int kt_sa_draws(uint64_t* pcg, int32_t* has_uint32, uint32_t* uintege
   KT_REQUIRE(n_steps >= 0 && n_chains >= 0, KT_E_SHAPE, "kt_sa_draws: negative size");
   KT_REQUIRE(n_knobs > 0 && n_knobs <= KT_MAX_KNOBS, KT_E_SHAPE, "kt_sa_draws: 1..%d knobs", KT_MAX_KNOBS);
   for (int j = 0; j < n_knobs; ++j) KT_REQUIRE(cards[j] >= 1, KT_E_RANGE, "kt_sa_draws: empty knob %d", j);
+  // PCG64's increment is odd (numpy's always is); an even one can cycle on a fixed point,
+  // where the bounded draws' rejection loop would never end
+  KT_REQUIRE((pcg[3] & 1u) == 1u, KT_E_ARG, "kt_sa_draws: not a PCG64 state (even increment)");
   kt::sa::Pcg64 g;
   g.state = (static_cast<unsigned __int128>(pcg[0]) << 64) | pcg[1];
   g.inc = (static_cast<unsigned __int128>(pcg[2]) << 64) | pcg[3];

@@ -73,3 +73,25 @@ def test_missing_library_fails_loudly(tmp_path):
 
     with pytest.raises(NumericError):
         _lib.load(tmp_path / "libkerntune_b200.so")
+
+
+def test_host_side_entry_points_validate_arguments(lib):
+    """kt_sa_draws is host-side (no GPU): its argument checks return the documented codes."""
+    import ctypes
+
+    import numpy as np
+
+    pcg = np.array([0, 12345, 0, 6789], dtype=np.uint64)  # (odd increment: a valid PCG64 state)
+    has = np.zeros(1, dtype=np.int32)
+    ui = np.zeros(1, dtype=np.uint32)
+    out = [np.zeros((2, 3), dtype=dt) for dt in (np.int32, np.uint8, np.int32, np.int32, np.float64)]
+    p = lambda a: a.ctypes.data  # noqa: E731
+    cards = np.array([3, 0], dtype=np.int32)
+    assert lib.kt_sa_draws(None, p(has), p(ui), 2, 3, 2, p(cards), *map(p, out)) == 7  # KT_E_ARG
+    assert lib.kt_sa_draws(p(pcg), p(has), p(ui), 2, 3, 0, p(cards), *map(p, out)) == 1  # KT_E_SHAPE
+    assert lib.kt_sa_draws(p(pcg), p(has), p(ui), 2, 3, 2, p(cards), *map(p, out)) == 3  # KT_E_RANGE (empty knob)
+    assert b"empty knob" in ctypes.string_at(lib.kt_last_error())
+    cards[1] = 4
+    even = np.array([0, 12345, 0, 6788], dtype=np.uint64)
+    assert lib.kt_sa_draws(p(even), p(has), p(ui), 2, 3, 2, p(cards), *map(p, out)) == 7  # even increment
+    assert lib.kt_sa_draws(p(pcg), p(has), p(ui), 2, 3, 2, p(cards), *map(p, out)) == 0
