@@ -108,13 +108,24 @@ class CostModelPredictor:
         if st["cap"] < b:
             cap = max(b, 2 * st["cap"])
             st["h_idx"] = torch.empty(cap, dtype=torch.int64, pin_memory=True)
+            st["h_idx32"] = torch.empty(cap, dtype=torch.int32, pin_memory=True)
             st["d_idx"] = torch.empty(cap, dtype=torch.int64, device=st["dev"])
             st["z"] = torch.empty(cap, dtype=torch.float32, device=st["dev"])
             st["h_z"] = torch.empty(cap, dtype=torch.float32, pin_memory=True)
             st["cap"] = cap
-        st["h_idx"][:b].numpy()[:] = idx
-        u = torch.empty((b, 64), dtype=torch.float32, device=st["dev"]) if want_u else None
         lib = _lib.load()
+        if not want_u:
+            # scores only: the scorer reads the uint32 indices from pinned host memory and writes
+            # the scores back into pinned host memory in place (zero-copy, no copy launches)
+            st["h_idx32"][:b].numpy().view(np.uint32)[:] = idx
+            with torch.cuda.device(st["dev"]):
+                _lib.check(lib.kt_score_indices_ex(_lib.ptr(st["tab"]), st["dims"], _lib.ptr(st["flat"]), None,
+                                                   st["h_idx32"].data_ptr(), 0, b, st["h_z"].data_ptr(), None, None,
+                                                   None, _lib.ptr(st["err"]), _lib.stream_handle()), "predict")
+                torch.cuda.current_stream().synchronize()
+            return st["h_z"][:b].numpy().astype(np.float64), None
+        st["h_idx"][:b].numpy()[:] = idx
+        u = torch.empty((b, 64), dtype=torch.float32, device=st["dev"])
         with torch.cuda.device(st["dev"]):
             st["d_idx"][:b].copy_(st["h_idx"][:b], non_blocking=True)
             _lib.check(lib.kt_score_indices(_lib.ptr(st["tab"]), st["dims"], _lib.ptr(st["flat"]),
