@@ -1013,8 +1013,11 @@ extern "C" int kt_readout(const float* h, int32_t d, int64_t B, int32_t nodes_pe
   KT_REQUIRE(d > 0, KT_E_SHAPE, "kt_readout: embedding width must be positive");
   KT_REQUIRE(nodes_per_graph > 0 || node_ptr, KT_E_ARG, "kt_readout: need nodes_per_graph or node_ptr");
   const int64_t warps = B;
+#ifndef KT_RO_BPS
+#define KT_RO_BPS 128  // readout CTAs per SM in the grid-stride launch (16: 0.86 of HBM, 64-128: 0.97, uncapped: 0.84)
+#endif
   const int64_t blocks = (warps * 32 + 255) / 256;
-  const int grid = static_cast<int>(blocks < 16 * kNumSMs ? blocks : 16 * kNumSMs);
+  const int grid = static_cast<int>(blocks < KT_RO_BPS * kNumSMs ? blocks : KT_RO_BPS * kNumSMs);
   agg::readout_kernel<<<grid, 256, 0, as_stream(stream)>>>(h, d, B, nodes_per_graph,
                                                            nodes_per_graph > 0 ? nullptr : node_ptr, agg_w, u_out);
   note_launches(1);
