@@ -60,7 +60,10 @@ static int launch_encode(const kt_spec_table* tab, const int64_t* src, int64_t B
   KT_REQUIRE(B > 0, KT_E_EMPTY, "kt_encode: empty batch");
   const int threads = 256;
   int64_t blocks = (B * KT_MAX_NODES + threads - 1) / threads;
-  if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
+#ifndef KT_ENC_BPS
+#define KT_ENC_BPS 64
+#endif
+  if (blocks > kNumSMs * KT_ENC_BPS) blocks = kNumSMs * KT_ENC_BPS;
   if (choices)
     encode_raw_kernel<true><<<(int)blocks, threads, 0, as_stream(stream)>>>(tab, src, B, out, err);
   else
