@@ -1,6 +1,8 @@
 // kt_embed_csr / kt_head_forward: embed_batch + head_forward_batch for
 // arbitrary adjacency (shared pattern or segmented CSR) and model dims
 // (model.py:185-203).  The star-layout fast path is kt_score_indices.
+#include <cstdlib>
+
 #include "kt_graph.cuh"
 
 namespace kt {
@@ -100,6 +102,94 @@ head_kernel(kt_dims dims, const float* __restrict__ params, const float* __restr
   }
 }
 
+// head_forward_batch for large batches: a CTA streams tiles of HT rows through the head with
+// the head parameters staged in shared memory; a thread owns a 4-row x 4-column block of each
+// hidden layer (one 16-byte weight load and four row reads per k, 16 FMAs) and one row of the
+// last (one-output) layer.  Every output is the same fmaf chain over k in order, then the bias,
+// as head_layer's: bit-identical to the warp-per-row kernel.
+constexpr int HT = 64;       // rows per tile
+constexpr int HTT = 256;     // threads
+__global__ void __launch_bounds__(HTT) head_tile_kernel(kt_dims dims, const float* __restrict__ params,
+                                                        const float* __restrict__ u, int64_t B,
+                                                        float* __restrict__ z_out, int hs) {
+  extern __shared__ __align__(16) float hsm[];
+  const int nh = dims.n_head, P = dims.n_head_params;
+  float* Wp = hsm;                                  // the head parameters (flat head vector order)
+  float* act0 = Wp + ((P + 3) & ~3);                // HT x hs, two buffers
+  float* act1 = act0 + HT * hs;
+  const float* hp = params + dims.off_head;
+  for (int e = threadIdx.x; e < P; e += HTT) Wp[e] = hp[e];
+  const int d0 = dims.head[0];
+  const int64_t n_tiles = (B + HT - 1) / HT;
+  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const int64_t r0 = t * HT;
+    const int rows = static_cast<int>(B - r0 < HT ? B - r0 : HT);
+    __syncthreads();  // (parameters staged / the previous tile's last layer done)
+    for (int e = threadIdx.x; e < HT * (d0 >> 2); e += HTT) {
+      const int r = e / (d0 >> 2), c = (e - r * (d0 >> 2)) * 4;
+      const float4 v = r < rows ? *reinterpret_cast<const float4*>(u + (r0 + r) * d0 + c)
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(act0 + r * hs + c) = v;
+    }
+    __syncthreads();
+    float* in = act0;
+    float* out = act1;
+    for (int i = 0; i < nh; ++i) {
+      const int din = dims.head[i], dout = dims.head[i + 1];
+      const float* W = Wp + (dims.off_hw[i] - dims.off_head);
+      const float* b = Wp + (dims.off_hb[i] - dims.off_head);
+      if (i == nh - 1) {  // one output: thread = row, k in order
+        for (int r = threadIdx.x; r < rows; r += HTT) {
+          float acc = 0.0f;
+          for (int k = 0; k < din; ++k) acc = fmaf(in[r * hs + k], W[k], acc);
+          z_out[r0 + r] = acc + b[0];
+        }
+      } else {
+        const int cq = dout >> 2;
+        for (int it = threadIdx.x; it < (HT / 4) * cq; it += HTT) {
+          const int rr = (it / cq) * 4, c = (it - (it / cq) * cq) * 4;
+          float4 a[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) a[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+          const float* x = in + rr * hs;
+#pragma unroll 4
+          for (int k = 0; k < din; ++k) {
+            const float4 w = *reinterpret_cast<const float4*>(W + k * dout + c);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float p = x[j * hs + k];
+              a[j].x = fmaf(p, w.x, a[j].x);
+              a[j].y = fmaf(p, w.y, a[j].y);
+              a[j].z = fmaf(p, w.z, a[j].z);
+              a[j].w = fmaf(p, w.w, a[j].w);
+            }
+          }
+          const float4 bb = *reinterpret_cast<const float4*>(b + c);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float4 o = make_float4(a[j].x + bb.x, a[j].y + bb.y, a[j].z + bb.z, a[j].w + bb.w);
+            o = make_float4(fmaxf(o.x, 0.f), fmaxf(o.y, 0.f), fmaxf(o.z, 0.f), fmaxf(o.w, 0.f));
+            *reinterpret_cast<float4*>(out + (rr + j) * hs + c) = o;
+          }
+        }
+        __syncthreads();
+        float* tmp = in;
+        in = out;
+        out = tmp;
+      }
+    }
+  }
+}
+
+static bool head_tile_ok(const kt_dims& d) {
+  if (d.head[d.n_head] != 1) return false;
+  for (int i = 0; i < d.n_head; ++i) {
+    if (d.head[i] % 4 || d.head[i] > 2 * KT_MAX_DIM) return false;
+    if ((d.off_hw[i] - d.off_head) % 4 || (d.off_hb[i] - d.off_head) % 4) return false;
+  }
+  return true;
+}
+
 }  // namespace fwd
 
 int check_dims(const kt_dims& d) {
@@ -168,6 +258,20 @@ int kt_head_forward(const kt_dims* dims, const float* params, const float* u, in
   KT_REQUIRE(B > 0, KT_E_EMPTY, "kt_head_forward: empty batch");
   int rc = check_dims(*dims);
   if (rc) return rc;
+  if (fwd::head_tile_ok(*dims) && (reinterpret_cast<uintptr_t>(u) & 15) == 0 &&
+      !(getenv("KT_HEADF_WARP") && getenv("KT_HEADF_WARP")[0] == '1')) {
+    int hs = 4;
+    for (int i = 0; i < dims->n_head; ++i) hs = hs > dims->head[i] ? hs : dims->head[i];
+    hs += 4;  // (row stride off a multiple of 32 words: four rows' word k in four banks)
+    const size_t smem = sizeof(float) * (((dims->n_head_params + 3) & ~3) + 2 * fwd::HT * hs);
+    static SmemAttr attr;
+    attr.ensure(fwd::head_tile_kernel, smem);
+    const int64_t tiles = (B + fwd::HT - 1) / fwd::HT;
+    const int grid = static_cast<int>(tiles < 4 * kNumSMs ? tiles : 4 * kNumSMs);
+    fwd::head_tile_kernel<<<grid, fwd::HTT, smem, as_stream(stream)>>>(*dims, params, u, B, z_out, hs);
+    note_launches(1);
+    return check_launch("kt_head_forward");
+  }
 #ifndef KT_HEADF_BPS
 #define KT_HEADF_BPS 64  // (8: 4.2 ms per 1M rows, 64: 3.7 ms)
 #endif

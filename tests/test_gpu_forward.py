@@ -17,6 +17,7 @@ from paper_2102_04199_b200 import graphs as pg
 from paper_2102_04199_b200 import kernels as pk
 from paper_2102_04199_b200 import model as pm
 from paper_2102_04199_b200 import search as ps
+from paper_2102_04199_b200.util import rng_from
 from tests._shared import corpus_graphs, device_model, oracle_params, spec_of
 
 pytestmark = pytest.mark.gpu
@@ -181,6 +182,18 @@ def test_embed_batch_general_matches_reference(cuda_device, g_encode, g_model, r
     np.testing.assert_allclose(u.double().cpu().numpy(), g_model[f"score/{rep}/u"], rtol=1e-4, atol=1e-5)
     z = pm.head_forward_batch(u, m.head)
     _assert_gflops_close(z, g_model[f"score/{rep}/z"], m.label_norm.std)
+
+
+def test_head_forward_tiled_equals_warp_kernel(cuda_device, g_model, monkeypatch):
+    """kt_head_forward's tiled kernel (64-row tiles, parameters in shared memory) computes every
+    output with the warp-per-row kernel's fmaf order: bit-identical, at any batch position."""
+    m = device_model(g_model)
+    u = torch.from_numpy(np.abs(rng_from("head-tile").normal(size=(1000, 64))).astype(np.float32)).cuda()
+    z_tile = pm.head_forward_batch(u, m.head)
+    pick = torch.tensor([0, 63, 64, 999], device=u.device)
+    assert torch.equal(pm.head_forward_batch(u[pick].contiguous(), m.head), z_tile[pick])
+    monkeypatch.setenv("KT_HEADF_WARP", "1")
+    assert torch.equal(pm.head_forward_batch(u, m.head), z_tile)
 
 
 def test_embed_graphs_mixed_sizes_matches_reference(cuda_device, g_encode, g_model):
