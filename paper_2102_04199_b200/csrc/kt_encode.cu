@@ -13,6 +13,10 @@ __global__ void __launch_bounds__(256) encode_raw_kernel(const kt_spec_table* __
                                                          double* __restrict__ out,
                                                          int32_t* __restrict__ err) {
   __shared__ int s_row_loop[64];  // node row -> loop index or -1
+  // a block's rows are consecutive in the output: staged here, then written as one contiguous
+  // run of 16-byte pieces (a thread's own row is 96 bytes: direct stores would leave every
+  // warp store instruction scattered over 3 KB)
+  __shared__ double2 s_out[256 * KT_F / 2];
   const kt_spec_table& T = *tab;
   const int N = T.n_nodes;
   for (int i = threadIdx.x; i < N && i < 64; i += blockDim.x) s_row_loop[i] = -1;
@@ -21,14 +25,14 @@ __global__ void __launch_bounds__(256) encode_raw_kernel(const kt_spec_table* __
   __syncthreads();
 
   const int64_t total = B * N;
-  for (int64_t item = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; item < total;
-       item += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < total; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t item = base + threadIdx.x;
     const int64_t g = item / N;
     const int row = static_cast<int>(item - g * N);
     double feat[KT_F];
 #pragma unroll
     for (int f = 0; f < KT_F; ++f) feat[f] = 0.0;
-    const int k = s_row_loop[row];
+    const int k = item < total ? s_row_loop[row] : -1;
     if (k >= 0) {
       int ch[KT_MAX_KNOBS];
       bool ok = true;
@@ -48,9 +52,15 @@ __global__ void __launch_bounds__(256) encode_raw_kernel(const kt_spec_table* __
         atomicOr(err, 1);
       }
     }
-    double2* o = reinterpret_cast<double2*>(out + item * KT_F);
+    if (item < total) {
 #pragma unroll
-    for (int f = 0; f < KT_F; f += 2) o[f / 2] = make_double2(feat[f], feat[f + 1]);
+      for (int f = 0; f < KT_F; f += 2) s_out[threadIdx.x * (KT_F / 2) + f / 2] = make_double2(feat[f], feat[f + 1]);
+    }
+    __syncthreads();
+    const int64_t n_items = total - base < blockDim.x ? total - base : blockDim.x;
+    double2* o = reinterpret_cast<double2*>(out + base * KT_F);
+    for (int e = threadIdx.x; e < n_items * (KT_F / 2); e += blockDim.x) o[e] = s_out[e];
+    __syncthreads();
   }
 }
 
