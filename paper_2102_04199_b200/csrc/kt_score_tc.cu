@@ -34,10 +34,10 @@
 // each region's compile-time budget):
 //   WG 0 (warps 0-3)    head: thread = TMEM lane = graph; per tile ReLU(D3 + b0) -> Z1
 //                       (TMEM, hi / lo), then ReLU(D4 + b1) . w3 + b3 -> score, top-k key
-//   WG 1 (warps 4-7)    encode: thread = graph; per row the axis' knob digit straight from
-//                       the index (two magic-number divisions), then the folded operand
-//                       row (fp64 touched / log2 / z-norm, host tables for the rest),
-//                       hi/lo split, tcgen05.st into an X slot
+//   WG 1 (warps 4-7)    encode: thread = graph; per tile the axes' knob digits straight from
+//                       the index (two magic-number divisions each) and the chained fp64
+//                       touched / log2 slots of every row; per row the table slots, hi/lo
+//                       split, tcgen05.st into an X slot
 //   WG 2-3 (8-15)       R: thread = TMEM lane = graph; ReLU(D1) split hi/lo into R (TMEM),
 //                       one warpgroup per chunk parity
 //   WG 4-5 (16-23)      readout, two warps per lane quadrant, 16 channels each: running
@@ -129,9 +129,6 @@ constexpr int NR = 2;     // R buffers
 #endif
 constexpr int N2 = 2;     // D2 buffers
 constexpr int TAB = 448;
-#ifndef KT_ENC_PIPE
-#define KT_ENC_PIPE 0
-#endif
 // per-role wait flavour: 0 = try_wait (hardware-suspended), N = probe + N ns sleeps
 #ifndef KT_SLEEP_MMA
 #define KT_SLEEP_MMA 0
@@ -204,11 +201,7 @@ struct __align__(1024) Smem {
   // the head warps (score validity, top-k key); v_free[slot] hands a slot back to the encode
   int64_t vtile[4][GT];
   unsigned int khist[2048];       // first radix digit (key >> 53) of this CTA's top-k keys
-#if KT_ENC_PIPE
-  float xstage[2][KT_MAX_LOOPS][6][GT];  // encode: feature rows of two tiles (thread-private)
-#else
-  float xstage[1][KT_MAX_LOOPS][6][GT];  // encode: a tile's feature rows (thread-private)
-#endif
+  float2 xstage[KT_MAX_LOOPS][GT];  // encode: a tile's chained feature slots (thread-private)
   // digit extraction for slot d (axes 0..5, 6 = auto_unroll knob, 7 = explicit knob):
   // choice = (v / dmult[d]) % dcard[d], both divisions by magic multiply
   unsigned long long dm_magic[8], dc_magic[8];
@@ -304,19 +297,6 @@ __device__ __forceinline__ void store_operand(const OperandRegs<N, K>& r, float*
   }
 }
 
-// 16 values -> v = hi (truncated tf32, in place), lo = exact remainder
-__device__ __forceinline__ void split16_inplace(float* v, float* lo) {
-#pragma unroll
-  for (int j = 0; j < 16; j += 2) {
-    const float2 t = make_float2(tf32_trunc(v[j]), tf32_trunc(v[j + 1]));
-    const float2 l = fsub2(make_float2(v[j], v[j + 1]), t);
-    v[j] = t.x;
-    v[j + 1] = t.y;
-    lo[j] = l.x;
-    lo[j + 1] = l.y;
-  }
-}
-
 // 16 values -> hi (truncated tf32) / lo (exact remainder) halves, packed fp32x2 subtractions
 __device__ __forceinline__ void split16(const float* v, float* hi, float* lo) {
 #pragma unroll
@@ -409,50 +389,56 @@ __device__ __forceinline__ void encode_prepare(Smem& S, const EncodeCtx& X, int6
   st.lt = 0.0;
 }
 
-// Feature row c (loop k = 2 NA - 1 - c, innermost first) of a tile into S.xstage[buf][c].
-// touched -- the product of the extents of the loops inside loop k, multiplied innermost
-// outward as np.cumprod(e[::-1]) does -- accumulates exactly in fp64, and log2(touched)
-// as the sum of the numpy log2 of those extents (log2(arith) = log2(2 touched) = that
-// + 1).  Both are functions of the extent vector only, so configs with equal features
-// score identically.
+// Phase 1, row c (loop k = 2 NA - 1 - c, innermost first): the two chained slots, normalised
+// touched and log2 touched, into S.xstage[c].  touched -- the product of the extents of the
+// loops inside loop k, multiplied innermost outward as np.cumprod(e[::-1]) does --
+// accumulates exactly in fp64, and log2(touched) as the sum of the numpy log2 of those
+// extents (log2(arith) = log2(2 touched) = that + 1).  Both are functions of the extent
+// vector only, so configs with equal features score identically.  The row's table slots
+// are gathered in the hand-over (the choice entries e / extents oi stay in registers), so
+// phase 1 -- the part of the encode that the X ring cannot hide at a tile boundary -- is
+// one 8-byte store per row.
 template <int NA>
-__device__ __forceinline__ void encode_row(Smem& S, const EncodeCtx& X, EncodeTile<NA>& st, int c, int buf) {
+__device__ __forceinline__ void encode_row(Smem& S, const EncodeCtx& X, EncodeTile<NA>& st, int c) {
   const int k = 2 * NA - 1 - c;
   const bool level = k >= NA;  // inner loop
   const int a = level ? k - NA : k;
-  float x0, x1, x2, x5;
-  if (level) {
-    const float2 ni = S.nrm_i[st.e[a]];
-    x0 = ni.x;
-    x1 = ni.y;
-    x2 = 0.0f;
-    x5 = st.unr_on && st.oi[a].y <= st.autov ? 1.0f : 0.0f;  // unroll flag
-  } else {
-    const float4 no = S.nrm_o[st.e[a]];
-    x0 = no.x;
-    x1 = no.y;
-    x2 = no.z;  // stride slot
-    x5 = 0.0f;
-  }
-  float* r = &S.xstage[buf][c][0][X.g];
-  r[0 * GT] = x0;
-  r[1 * GT] = x1;
-  r[2 * GT] = x2;
-  r[3 * GT] = static_cast<float>((st.t - X.m6) * X.r6);
-  r[4 * GT] = static_cast<float>((st.lt - X.m7) * X.r7);
-  r[5 * GT] = x5;
+  S.xstage[c][X.g] =
+      make_float2(static_cast<float>((st.t - X.m6) * X.r6), static_cast<float>((st.lt - X.m7) * X.r7));
   st.t *= static_cast<double>(level ? st.oi[a].y : st.oi[a].x);
-  const double2 l2 = S.l2[st.e[a]];
-  st.lt += level ? l2.y : l2.x;
+  const double* l2 = reinterpret_cast<const double*>(&S.l2[st.e[a]]);
+  st.lt += l2[level ? 1 : 0];
 }
 
-// Row c of a staged tile -> hi / lo split -> X slot of chunk q (tcgen05.st) -> GEMM1.
-__device__ __forceinline__ void encode_hand_over(Smem& S, const EncodeCtx& X, int c, int buf, float one, int64_t q) {
+// Phase 2, row c: the table slots (normalised extent / log2 extent, stride for an outer
+// loop, unroll flag for an inner one) and the chained slots from phase 1 -> hi / lo split
+// -> X slot of chunk q (tcgen05.st) -> GEMM1.
+template <int NA>
+__device__ __forceinline__ void encode_hand_over(Smem& S, const EncodeCtx& X, const EncodeTile<NA>& st, int c,
+                                                 int64_t q) {
+  const int k = 2 * NA - 1 - c;
+  const bool level = k >= NA;
+  const int a = level ? k - NA : k;
   float x[XK];
-  const float* r = &S.xstage[buf][c][0][X.g];
+  const float2 ch = S.xstage[c][X.g];
+  if (level) {
+    const float2 ni = S.nrm_i[st.e[a]];
+    x[0] = ni.x;
+    x[1] = ni.y;
+    x[2] = 0.0f;
+    x[5] = st.unr_on && st.oi[a].y <= st.autov ? 1.0f : 0.0f;  // unroll flag
+  } else {
+    const float4 no = S.nrm_o[st.e[a]];
+    x[0] = no.x;
+    x[1] = no.y;
+    x[2] = no.z;  // stride slot
+    x[5] = 0.0f;
+  }
+  x[3] = ch.x;
+  x[4] = ch.y;
 #pragma unroll
-  for (int f = 0; f < 6; ++f) x[f] = r[f * GT] * one;  // padding / invalid rows: all zero
-  x[6] = one;
+  for (int f = 0; f < 6; ++f) x[f] *= st.one;  // padding / invalid rows: all zero
+  x[6] = st.one;
   x[7] = 0.0f;
   float hl[16];
 #pragma unroll
@@ -477,10 +463,9 @@ __device__ __forceinline__ void encode_hand_over(Smem& S, const EncodeCtx& X, in
 }
 
 // The encode warps' loop, specialised on the axis count so every per-axis / per-row
-// quantity lives in registers.  Per tile, phase 1 computes all feature rows (no waits:
-// the rows' digit extraction and table lookups are independent, only touched / log2
-// touched chain across rows), then phase 2 hands them to GEMM1 one X slot at a time.
-// KT_ENC_PIPE=1 interleaves the next tile's phase 1 with this tile's phase 2 instead.
+// quantity lives in registers.  Per tile, the digits and table entries (prepare) and phase
+// 1 (no waits: only touched / log2 touched chain across rows), then phase 2 hands the rows
+// to GEMM1 one X slot at a time.
 template <int NA>
 __device__ __forceinline__ void encode_loop(Smem& S, const EncodeCtx& X) {
   constexpr int C = 2 * NA;
@@ -492,28 +477,6 @@ __device__ __forceinline__ void encode_loop(Smem& S, const EncodeCtx& X) {
   };
   if (X.my_tiles <= 0) return;
   int64_t q = 0;
-#if KT_ENC_PIPE
-  EncodeTile<NA> cur, nxt;
-  encode_prepare<NA>(S, X, 0, index_of(0), cur);
-  int64_t v_next = index_of(1);  // loaded a tile ahead of use
-#pragma unroll
-  for (int c = 0; c < C; ++c) encode_row<NA>(S, X, cur, c, 0);
-  for (int64_t ti = 0; ti < X.my_tiles; ++ti) {
-    const bool more = ti + 1 < X.my_tiles;
-    if (more) {
-      encode_prepare<NA>(S, X, ti + 1, v_next, nxt);
-      v_next = index_of(ti + 2);
-    }
-    const int buf = static_cast<int>(ti & 1);
-#pragma unroll
-    for (int c = 0; c < C; ++c, ++q) {
-      if (X.g == 0) TRACE(19, q);
-      if (more) encode_row<NA>(S, X, nxt, c, buf ^ 1);
-      encode_hand_over(S, X, c, buf, cur.one, q);
-    }
-    cur.one = nxt.one;
-  }
-#else
   const bool sa = X.sa->n_steps > 0;
   int64_t v_next = sa ? 0 : index_of(0);
   for (int64_t ti = 0; ti < X.my_tiles; ++ti) {
@@ -523,14 +486,13 @@ __device__ __forceinline__ void encode_loop(Smem& S, const EncodeCtx& X) {
     if (!sa) v_next = index_of(ti + 1);  // next tile's index load in flight during this tile
     if (X.g == 0) TRACE(26, ti);
 #pragma unroll
-    for (int c = 0; c < C; ++c) encode_row<NA>(S, X, st, c, 0);
-#pragma unroll 1
+    for (int c = 0; c < C; ++c) encode_row<NA>(S, X, st, c);
+#pragma unroll
     for (int c = 0; c < C; ++c, ++q) {
       if (X.g == 0) TRACE(19, q);
-      encode_hand_over(S, X, c, 0, st.one, q);
+      encode_hand_over<NA>(S, X, st, c, q);
     }
   }
-#endif
 }
 
 __global__ void __launch_bounds__(NT, 1)
@@ -880,11 +842,19 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       if (g == 0) TRACE(14, q);
       tc_fence_after();
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {  // hi in place (v), lo alongside: 48 live values, not 64
-        float lo[16];
-        split16_inplace(v + 16 * h, lo);
-        tmem_st16(tmem + lane + T_R + 64 * b + 16 * h, v + 16 * h);
-        tmem_st16(tmem + lane + T_R + 64 * b + 32 + 16 * h, lo);
+      for (int h = 0; h < 4; ++h) {  // hi in place (v), lo alongside: 40 live values
+        float lo[8];
+#pragma unroll
+        for (int j = 0; j < 8; j += 2) {
+          const float2 t = make_float2(tf32_trunc(v[8 * h + j]), tf32_trunc(v[8 * h + j + 1]));
+          const float2 l = fsub2(make_float2(v[8 * h + j], v[8 * h + j + 1]), t);
+          v[8 * h + j] = t.x;
+          v[8 * h + j + 1] = t.y;
+          lo[j] = l.x;
+          lo[j + 1] = l.y;
+        }
+        tmem_st8(tmem + lane + T_R + 64 * b + 8 * h, v + 8 * h);
+        tmem_st8(tmem + lane + T_R + 64 * b + 32 + 8 * h, lo);
       }
       if (g == 0) TRACE(15, q);
       tmem_wait_st();
@@ -1192,7 +1162,6 @@ extern "C" int kt_sa_run(const kt_spec_table* tab, const kt_dims* dims, const fl
   KT_REQUIRE(n_knobs >= 1 && n_knobs <= KT_MAX_KNOBS, KT_E_SHAPE, "kt_sa_run: 1..%d knobs", KT_MAX_KNOBS);
   KT_REQUIRE(n_steps >= 1, KT_E_EMPTY, "kt_sa_run: no steps");
   KT_REQUIRE(default_dims_tc(*dims), KT_E_UNSUPPORTED, "kt_sa_run: fused scorer needs the default dims");
-  KT_REQUIRE(!KT_ENC_PIPE, KT_E_UNSUPPORTED, "kt_sa_run: not built for the KT_ENC_PIPE encode variant");
   tcs::SaArgs a{};
   a.n_steps = n_steps;
   a.n_chains = n_chains;
