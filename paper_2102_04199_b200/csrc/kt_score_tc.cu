@@ -374,15 +374,20 @@ __device__ __forceinline__ void encode_prepare(Smem& S, const EncodeCtx& X, int6
                                                EncodeTile<NA>& st) {
   const bool ok = v64 >= 0 && static_cast<uint64_t>(v64) < X.size;
   mbar_wait(&S.v_free[ti & 3], static_cast<uint32_t>(((ti >> 2) & 1) ^ 1));  // head of tile ti-4 read it
+  if (X.g == 0) TRACE(25, ti);
   S.vtile[ti & 3][X.g] = v64;
   if (v64 != INT64_MIN && !ok) atomicOr(X.err, 1);
   const uint32_t v = ok ? static_cast<uint32_t>(v64) : 0u;
-  st.autov = S.auto_knob >= 0 ? S.auto_vals[knob_digit(S, v, 6)] : 0;
-  const int expl = S.expl_knob >= 0 ? S.expl_vals[knob_digit(S, v, 7)] : 0;
+  // branch-free: a slot without a knob has mult = card = 1 (host tables), so its digit is 0
+  // and every digit's loads and multiplies are independent
+  const int av = S.auto_vals[knob_digit(S, v, 6)], ev = S.expl_vals[knob_digit(S, v, 7)];
+  st.autov = S.auto_knob >= 0 ? av : 0;
+  const int expl = S.expl_knob >= 0 ? ev : 0;
   st.unr_on = expl != 0 && st.autov > 0;
   st.one = ok ? 1.0f : 0.0f;
 #pragma unroll
-  for (int a = 0; a < NA; ++a) st.e[a] = S.tab_off[a] + (S.axis_knob[a] >= 0 ? knob_digit(S, v, a) : 0);
+  for (int a = 0; a < NA; ++a) st.e[a] = S.tab_off[a] + knob_digit(S, v, a);
+  if (X.g == 0) TRACE(31, ti);
 #pragma unroll
   for (int a = 0; a < NA; ++a) st.oi[a] = S.oi[st.e[a]];
   st.t = 1.0;
@@ -487,6 +492,7 @@ __device__ __forceinline__ void encode_loop(Smem& S, const EncodeCtx& X) {
     if (X.g == 0) TRACE(26, ti);
 #pragma unroll
     for (int c = 0; c < C; ++c) encode_row<NA>(S, X, st, c);
+    if (X.g == 0) TRACE(30, ti + 1);
 #pragma unroll
     for (int c = 0; c < C; ++c, ++q) {
       if (X.g == 0) TRACE(19, q);
