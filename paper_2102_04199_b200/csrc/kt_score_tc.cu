@@ -35,9 +35,9 @@
 //   WG 0 (warps 0-3)    head: thread = TMEM lane = graph; per tile ReLU(D3 + b0) -> Z1
 //                       (TMEM, hi / lo), then ReLU(D4 + b1) . w3 + b3 -> score, top-k key
 //   WG 1 (warps 4-7)    encode: thread = graph; per tile the axes' knob digits straight from
-//                       the index (two magic-number divisions each) and the chained fp64
-//                       touched / log2 slots of every row; per row the table slots, hi/lo
-//                       split, tcgen05.st into an X slot
+//                       the index (two magic-number divisions each); per row the table
+//                       slots, the chained fp64 touched / log2 slots, hi/lo split,
+//                       tcgen05.st into an X slot
 //   WG 2-3 (8-15)       R: thread = TMEM lane = graph; ReLU(D1) split hi/lo into R (TMEM),
 //                       one warpgroup per chunk parity
 //   WG 4-5 (16-23)      readout, two warps per lane quadrant, 16 channels each: running
@@ -201,7 +201,6 @@ struct __align__(1024) Smem {
   // the head warps (score validity, top-k key); v_free[slot] hands a slot back to the encode
   int64_t vtile[4][GT];
   unsigned int khist[2048];       // first radix digit (key >> 53) of this CTA's top-k keys
-  float2 xstage[KT_MAX_LOOPS][GT];  // encode: a tile's chained feature slots (thread-private)
   // digit extraction for slot d (axes 0..5, 6 = auto_unroll knob, 7 = explicit knob):
   // choice = (v / dmult[d]) % dcard[d], both divisions by magic multiply
   unsigned long long dm_magic[8], dc_magic[8];
@@ -394,38 +393,27 @@ __device__ __forceinline__ void encode_prepare(Smem& S, const EncodeCtx& X, int6
   st.lt = 0.0;
 }
 
-// Phase 1, row c (loop k = 2 NA - 1 - c, innermost first): the two chained slots, normalised
-// touched and log2 touched, into S.xstage[c].  touched -- the product of the extents of the
-// loops inside loop k, multiplied innermost outward as np.cumprod(e[::-1]) does --
-// accumulates exactly in fp64, and log2(touched) as the sum of the numpy log2 of those
-// extents (log2(arith) = log2(2 touched) = that + 1).  Both are functions of the extent
-// vector only, so configs with equal features score identically.  The row's table slots
-// are gathered in the hand-over (the choice entries e / extents oi stay in registers), so
-// phase 1 -- the part of the encode that the X ring cannot hide at a tile boundary -- is
-// one 8-byte store per row.
+// Row c (loop k = 2 NA - 1 - c, innermost first) of a tile -> hi / lo split -> X slot of
+// chunk q (tcgen05.st) -> GEMM1.  The row's table slots (normalised extent / log2 extent,
+// stride for an outer loop, unroll flag for an inner one) are gathered by its choice entry
+// e; the two chained slots come from the running touched / log2 touched.  touched -- the
+// product of the extents of the loops inside loop k, multiplied innermost outward as
+// np.cumprod(e[::-1]) does -- accumulates exactly in fp64, and log2(touched) as the sum of
+// the numpy log2 of those extents (log2(arith) = log2(2 touched) = that + 1).  Both are
+// functions of the extent vector only, so configs with equal features score identically.
+// All of it is computed before the X-slot wait, so from the fifth row of a tile on it
+// overlaps the wait for GEMM1 to free a slot instead of delaying the tile's first rows.
 template <int NA>
-__device__ __forceinline__ void encode_row(Smem& S, const EncodeCtx& X, EncodeTile<NA>& st, int c) {
+__device__ __forceinline__ void encode_hand_over(Smem& S, const EncodeCtx& X, EncodeTile<NA>& st, int c,
+                                                 int64_t q) {
   const int k = 2 * NA - 1 - c;
   const bool level = k >= NA;  // inner loop
   const int a = level ? k - NA : k;
-  S.xstage[c][X.g] =
-      make_float2(static_cast<float>((st.t - X.m6) * X.r6), static_cast<float>((st.lt - X.m7) * X.r7));
-  st.t *= static_cast<double>(level ? st.oi[a].y : st.oi[a].x);
-  const double* l2 = reinterpret_cast<const double*>(&S.l2[st.e[a]]);
-  st.lt += l2[level ? 1 : 0];
-}
-
-// Phase 2, row c: the table slots (normalised extent / log2 extent, stride for an outer
-// loop, unroll flag for an inner one) and the chained slots from phase 1 -> hi / lo split
-// -> X slot of chunk q (tcgen05.st) -> GEMM1.
-template <int NA>
-__device__ __forceinline__ void encode_hand_over(Smem& S, const EncodeCtx& X, const EncodeTile<NA>& st, int c,
-                                                 int64_t q) {
-  const int k = 2 * NA - 1 - c;
-  const bool level = k >= NA;
-  const int a = level ? k - NA : k;
   float x[XK];
-  const float2 ch = S.xstage[c][X.g];
+  x[3] = static_cast<float>((st.t - X.m6) * X.r6);
+  x[4] = static_cast<float>((st.lt - X.m7) * X.r7);
+  st.t *= static_cast<double>(level ? st.oi[a].y : st.oi[a].x);
+  st.lt += reinterpret_cast<const double*>(&S.l2[st.e[a]])[level ? 1 : 0];
   if (level) {
     const float2 ni = S.nrm_i[st.e[a]];
     x[0] = ni.x;
@@ -439,8 +427,6 @@ __device__ __forceinline__ void encode_hand_over(Smem& S, const EncodeCtx& X, co
     x[2] = no.z;  // stride slot
     x[5] = 0.0f;
   }
-  x[3] = ch.x;
-  x[4] = ch.y;
 #pragma unroll
   for (int f = 0; f < 6; ++f) x[f] *= st.one;  // padding / invalid rows: all zero
   x[6] = st.one;
@@ -468,9 +454,8 @@ __device__ __forceinline__ void encode_hand_over(Smem& S, const EncodeCtx& X, co
 }
 
 // The encode warps' loop, specialised on the axis count so every per-axis / per-row
-// quantity lives in registers.  Per tile, the digits and table entries (prepare) and phase
-// 1 (no waits: only touched / log2 touched chain across rows), then phase 2 hands the rows
-// to GEMM1 one X slot at a time.
+// quantity lives in registers.  Per tile, the digits and table entries (prepare), then the
+// rows, each computed and handed to GEMM1 one X slot at a time.
 template <int NA>
 __device__ __forceinline__ void encode_loop(Smem& S, const EncodeCtx& X) {
   constexpr int C = 2 * NA;
@@ -490,9 +475,6 @@ __device__ __forceinline__ void encode_loop(Smem& S, const EncodeCtx& X) {
     encode_prepare<NA>(S, X, ti, sa ? sa_propose(S, X, ti) : v_next, st);
     if (!sa) v_next = index_of(ti + 1);  // next tile's index load in flight during this tile
     if (X.g == 0) TRACE(26, ti);
-#pragma unroll
-    for (int c = 0; c < C; ++c) encode_row<NA>(S, X, st, c);
-    if (X.g == 0) TRACE(30, ti + 1);
 #pragma unroll
     for (int c = 0; c < C; ++c, ++q) {
       if (X.g == 0) TRACE(19, q);
