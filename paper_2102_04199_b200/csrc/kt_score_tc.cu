@@ -76,9 +76,6 @@ using namespace kt::tc;
 #ifndef KT_R2
 #define KT_R2 1  // two R warpgroups, one per chunk parity
 #endif
-#ifndef KT_G2_UNROLL
-#define KT_G2_UNROLL 1  // GEMM2 issue loop unrolled over its two buffers
-#endif
 #ifndef KT_R_ISSUE
 #define KT_R_ISSUE 0  // 1: the R warpgroups issue their chunks' GEMM2 themselves (no separate MMA warp)
 #endif
@@ -89,6 +86,9 @@ constexpr int NT = 128 * NWG;  // (roles by warpgroup, see the header)
 // registers per lane; the launch gives each REG_BASE, the roles rebalance them
 constexpr int REG_BASE = (512 / NWG) & ~7;
 #if KT_R2
+#ifndef KT_ENC_NEXT
+#define KT_ENC_NEXT 0
+#endif
 #ifndef KT_REG_HEAD
 #define KT_REG_HEAD 48
 #endif
@@ -112,7 +112,10 @@ static_assert(REG_HEAD + REG_ENC + (1 + KT_R2) * REG_R + 2 * REG_RO + REG_MMA <=
 constexpr int GT = 128;   // graphs per tile (one TMEM lane each)
 constexpr int H = 64;
 constexpr int XK = 8;     // folded layer-1 operand width (one tf32 K-step)
-constexpr int XS = 4;     // X ring slots
+#ifndef KT_XS
+#define KT_XS 4
+#endif
+constexpr int XS = KT_XS;  // X ring slots
 #ifndef KT_DR
 #define KT_DR 0
 #endif
@@ -127,7 +130,10 @@ constexpr int N1 = NB, NR = NB;
 constexpr int N1 = 2;     // D1 buffers
 constexpr int NR = 2;     // R buffers
 #endif
-constexpr int N2 = 2;     // D2 buffers
+#ifndef KT_N2
+#define KT_N2 2
+#endif
+constexpr int N2 = KT_N2;  // D2 buffers
 constexpr int TAB = 448;
 // per-role wait flavour: 0 = try_wait (hardware-suspended), N = probe + N ns sleeps
 #ifndef KT_SLEEP_MMA
@@ -368,29 +374,51 @@ struct EncodeTile {
   double t, lt;
 };
 
+// The unroll knobs' values (used by the inner loops' rows) from a 32-bit config index.
 template <int NA>
-__device__ __forceinline__ void encode_prepare(Smem& S, const EncodeCtx& X, int64_t ti, int64_t v64,
-                                               EncodeTile<NA>& st) {
-  const bool ok = v64 >= 0 && static_cast<uint64_t>(v64) < X.size;
-  mbar_wait(&S.v_free[ti & 3], static_cast<uint32_t>(((ti >> 2) & 1) ^ 1));  // head of tile ti-4 read it
-  if (X.g == 0) TRACE(25, ti);
-  S.vtile[ti & 3][X.g] = v64;
-  if (v64 != INT64_MIN && !ok) atomicOr(X.err, 1);
-  const uint32_t v = ok ? static_cast<uint32_t>(v64) : 0u;
+__device__ __forceinline__ void encode_knobs(Smem& S, uint32_t v, EncodeTile<NA>& st) {
   // branch-free: a slot without a knob has mult = card = 1 (host tables), so its digit is 0
   // and every digit's loads and multiplies are independent
   const int av = S.auto_vals[knob_digit(S, v, 6)], ev = S.expl_vals[knob_digit(S, v, 7)];
   st.autov = S.auto_knob >= 0 ? av : 0;
   const int expl = S.expl_knob >= 0 ? ev : 0;
   st.unr_on = expl != 0 && st.autov > 0;
+}
+
+// Axis a's choice entry and (outer, inner) extents.
+template <int NA>
+__device__ __forceinline__ void encode_axis(Smem& S, uint32_t v, EncodeTile<NA>& st, int a) {
+  st.e[a] = S.tab_off[a] + knob_digit(S, v, a);
+  st.oi[a] = S.oi[st.e[a]];
+}
+
+__device__ __forceinline__ bool index_ok(const EncodeCtx& X, int64_t v64) {
+  return v64 >= 0 && static_cast<uint64_t>(v64) < X.size;
+}
+
+// Tile ti's per-graph state that does not need the digits: the index published for the
+// head, the padding / invalid flag, the chain's start.
+template <int NA>
+__device__ __forceinline__ void encode_begin(Smem& S, const EncodeCtx& X, int64_t ti, int64_t v64, EncodeTile<NA>& st) {
+  const bool ok = index_ok(X, v64);
+  mbar_wait(&S.v_free[ti & 3], static_cast<uint32_t>(((ti >> 2) & 1) ^ 1));  // head of tile ti-4 read it
+  if (X.g == 0) TRACE(25, ti);
+  S.vtile[ti & 3][X.g] = v64;
+  if (v64 != INT64_MIN && !ok) atomicOr(X.err, 1);
   st.one = ok ? 1.0f : 0.0f;
-#pragma unroll
-  for (int a = 0; a < NA; ++a) st.e[a] = S.tab_off[a] + knob_digit(S, v, a);
-  if (X.g == 0) TRACE(31, ti);
-#pragma unroll
-  for (int a = 0; a < NA; ++a) st.oi[a] = S.oi[st.e[a]];
   st.t = 1.0;
   st.lt = 0.0;
+}
+
+template <int NA>
+__device__ __forceinline__ void encode_prepare(Smem& S, const EncodeCtx& X, int64_t ti, int64_t v64,
+                                               EncodeTile<NA>& st) {
+  encode_begin<NA>(S, X, ti, v64, st);
+  const uint32_t v = index_ok(X, v64) ? static_cast<uint32_t>(v64) : 0u;
+  encode_knobs<NA>(S, v, st);
+#pragma unroll
+  for (int a = 0; a < NA; ++a) encode_axis<NA>(S, v, st, a);
+  if (X.g == 0) TRACE(31, ti);
 }
 
 // Row c (loop k = 2 NA - 1 - c, innermost first) of a tile -> hi / lo split -> X slot of
@@ -405,7 +433,7 @@ __device__ __forceinline__ void encode_prepare(Smem& S, const EncodeCtx& X, int6
 // overlaps the wait for GEMM1 to free a slot instead of delaying the tile's first rows.
 template <int NA>
 __device__ __forceinline__ void encode_hand_over(Smem& S, const EncodeCtx& X, EncodeTile<NA>& st, int c,
-                                                 int64_t q) {
+                                                 int64_t q, uint32_t vn, bool pre) {
   const int k = 2 * NA - 1 - c;
   const bool level = k >= NA;  // inner loop
   const int a = level ? k - NA : k;
@@ -427,6 +455,12 @@ __device__ __forceinline__ void encode_hand_over(Smem& S, const EncodeCtx& X, En
     x[2] = no.z;  // stride slot
     x[5] = 0.0f;
   }
+#if KT_ENC_NEXT
+  if (!level && pre) {  // axis a's last row in this tile: its registers take the next tile's entry
+    if (a == NA - 1) encode_knobs<NA>(S, vn, st);  // the first outer row: no inner rows left
+    encode_axis<NA>(S, vn, st, a);
+  }
+#endif
 #pragma unroll
   for (int f = 0; f < 6; ++f) x[f] *= st.one;  // padding / invalid rows: all zero
   x[6] = st.one;
@@ -468,6 +502,26 @@ __device__ __forceinline__ void encode_loop(Smem& S, const EncodeCtx& X) {
   if (X.my_tiles <= 0) return;
   int64_t q = 0;
   const bool sa = X.sa->n_steps > 0;
+#if KT_ENC_NEXT
+  if (!sa) {
+    // the next tile's digits and extents are computed in this tile's outer rows (before
+    // their X-slot waits), so a tile boundary only publishes the index and resets the chain
+    int64_t v_cur = index_of(0), v_next = index_of(1);
+    EncodeTile<NA> st;
+    encode_prepare<NA>(S, X, 0, v_cur, st);
+    for (int64_t ti = 0; ti < X.my_tiles; ++ti) {
+      if (ti > 0) encode_begin<NA>(S, X, ti, v_cur, st);
+      const bool pre = ti + 1 < X.my_tiles;
+      const uint32_t vn = index_ok(X, v_next) ? static_cast<uint32_t>(v_next) : 0u;
+      const int64_t v_after = index_of(ti + 2);  // in flight during this tile
+#pragma unroll
+      for (int c = 0; c < C; ++c, ++q) encode_hand_over<NA>(S, X, st, c, q, vn, pre);
+      v_cur = v_next;
+      v_next = v_after;
+    }
+    return;
+  }
+#endif
   int64_t v_next = sa ? 0 : index_of(0);
   for (int64_t ti = 0; ti < X.my_tiles; ++ti) {
     EncodeTile<NA> st;
@@ -478,7 +532,7 @@ __device__ __forceinline__ void encode_loop(Smem& S, const EncodeCtx& X) {
 #pragma unroll
     for (int c = 0; c < C; ++c, ++q) {
       if (X.g == 0) TRACE(19, q);
-      encode_hand_over<NA>(S, X, st, c, q);
+      encode_hand_over<NA>(S, X, st, c, q, 0u, false);
     }
   }
 }
@@ -694,36 +748,6 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         if (++c == C) c = 0;
       }
     } else if (warp == 4 * WG_MMA + 1 && !(KT_R2 && KT_R_ISSUE && !KT_DR)) {
-#if KT_G2_UNROLL
-      // unrolled over the two R / D2 buffers (NR == N2 == 2): buffer addresses are constants
-      static_assert(NR == 2 && N2 == 2, "GEMM2 unroll needs 2-deep R / D2 rings");
-      auto g2 = [&](int64_t q, int b, uint32_t ph) {
-        if ((tid & 31) == 0) TRACE(17, q);
-        mbar_wait(&S.r_full[b], ph);
-        mbar_wait(&S.d2_empty[b], ph ^ 1);
-        __syncwarp();
-        tc_fence_after();
-        if ((tid & 31) == 0) TRACE(18, q);
-        const uint32_t rh = tmem + T_R + 64 * b, rl = rh + 32, d = tmem + T_D2 + 32 * b;
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            mma_tf32_ts(d, rh + 8 * kk, kdesc(S.b2h, 32, kk), id32, kk > 0);
-            mma_tf32_ts(d, rh + 8 * kk, kdesc(S.b2l, 32, kk), id32, 1);
-            mma_tf32_ts(d, rl + 8 * kk, kdesc(S.b2h, 32, kk), id32, 1);
-          }
-          mma_commit(&S.r_empty[b]);
-          mma_commit(&S.d2_full[b]);
-          TRACE(2, q);
-        }
-        __syncwarp();
-      };
-      uint32_t ph = 0;
-      for (int64_t q = 0; q < n_chunks; q += 2, ph ^= 1u) {
-        g2(q, 0, ph);
-        if (q + 1 < n_chunks) g2(q + 1, 1, ph);
-      }
-#else
       Ring<NR> rr;
       Ring<N2> r2;
       for (int64_t q = 0; q < n_chunks; ++q, rr.next(), r2.next()) {
@@ -746,7 +770,6 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         }
         __syncwarp();
       }
-#endif
     } else if (warp == 4 * WG_MMA + 2) {
       for (int64_t t = 0; t < my_tiles; ++t) {
         const uint32_t ph = static_cast<uint32_t>(t & 1);
