@@ -86,9 +86,6 @@ constexpr int NT = 128 * NWG;  // (roles by warpgroup, see the header)
 // registers per lane; the launch gives each REG_BASE, the roles rebalance them
 constexpr int REG_BASE = (512 / NWG) & ~7;
 #if KT_R2
-#ifndef KT_ENC_NEXT
-#define KT_ENC_NEXT 0
-#endif
 #ifndef KT_REG_HEAD
 #define KT_REG_HEAD 48
 #endif
@@ -433,7 +430,7 @@ __device__ __forceinline__ void encode_prepare(Smem& S, const EncodeCtx& X, int6
 // overlaps the wait for GEMM1 to free a slot instead of delaying the tile's first rows.
 template <int NA>
 __device__ __forceinline__ void encode_hand_over(Smem& S, const EncodeCtx& X, EncodeTile<NA>& st, int c,
-                                                 int64_t q, uint32_t vn, bool pre) {
+                                                 int64_t q) {
   const int k = 2 * NA - 1 - c;
   const bool level = k >= NA;  // inner loop
   const int a = level ? k - NA : k;
@@ -455,12 +452,6 @@ __device__ __forceinline__ void encode_hand_over(Smem& S, const EncodeCtx& X, En
     x[2] = no.z;  // stride slot
     x[5] = 0.0f;
   }
-#if KT_ENC_NEXT
-  if (!level && pre) {  // axis a's last row in this tile: its registers take the next tile's entry
-    if (a == NA - 1) encode_knobs<NA>(S, vn, st);  // the first outer row: no inner rows left
-    encode_axis<NA>(S, vn, st, a);
-  }
-#endif
 #pragma unroll
   for (int f = 0; f < 6; ++f) x[f] *= st.one;  // padding / invalid rows: all zero
   x[6] = st.one;
@@ -502,26 +493,6 @@ __device__ __forceinline__ void encode_loop(Smem& S, const EncodeCtx& X) {
   if (X.my_tiles <= 0) return;
   int64_t q = 0;
   const bool sa = X.sa->n_steps > 0;
-#if KT_ENC_NEXT
-  if (!sa) {
-    // the next tile's digits and extents are computed in this tile's outer rows (before
-    // their X-slot waits), so a tile boundary only publishes the index and resets the chain
-    int64_t v_cur = index_of(0), v_next = index_of(1);
-    EncodeTile<NA> st;
-    encode_prepare<NA>(S, X, 0, v_cur, st);
-    for (int64_t ti = 0; ti < X.my_tiles; ++ti) {
-      if (ti > 0) encode_begin<NA>(S, X, ti, v_cur, st);
-      const bool pre = ti + 1 < X.my_tiles;
-      const uint32_t vn = index_ok(X, v_next) ? static_cast<uint32_t>(v_next) : 0u;
-      const int64_t v_after = index_of(ti + 2);  // in flight during this tile
-#pragma unroll
-      for (int c = 0; c < C; ++c, ++q) encode_hand_over<NA>(S, X, st, c, q, vn, pre);
-      v_cur = v_next;
-      v_next = v_after;
-    }
-    return;
-  }
-#endif
   int64_t v_next = sa ? 0 : index_of(0);
   for (int64_t ti = 0; ti < X.my_tiles; ++ti) {
     EncodeTile<NA> st;
@@ -532,7 +503,7 @@ __device__ __forceinline__ void encode_loop(Smem& S, const EncodeCtx& X) {
 #pragma unroll
     for (int c = 0; c < C; ++c, ++q) {
       if (X.g == 0) TRACE(19, q);
-      encode_hand_over<NA>(S, X, st, c, q, 0u, false);
+      encode_hand_over<NA>(S, X, st, c, q);
     }
   }
 }
