@@ -36,6 +36,7 @@ constexpr int MAXK = 1024;
 constexpr int CAP = 4096;  // selection buffer (keys at or below the final prefix)
 constexpr int NB = 2048;   // bins per pass (11-bit digits)
 constexpr int PASSES = 6;
+constexpr int KB = 4;  // keys per thread per batch of loads
 constexpr unsigned long long EMPTY = ~0ull;
 
 // Workspace: [counters 64 B][3 x NB bins][CAP keys].  All bins and counters are zero
@@ -153,10 +154,17 @@ __device__ void histogram(const Src& src, const Sel& sel, unsigned int* hist, un
   const int db = digit_bits(pass);
   const int shift = 64 - nbits - db;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * NT;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x; i < src.B; i += stride) {
-    const unsigned long long key = key_at(src, i);
-    if (nbits == 0 || (key >> (64 - nbits)) == prefix)
-      atomicAdd(&h[static_cast<int>((key >> shift) & ((1u << db) - 1))], 1u);
+  // KB keys per thread in flight (one HBM round trip per KB keys, not per key)
+  for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x; i0 < src.B; i0 += KB * stride) {
+    unsigned long long kk[KB];
+#pragma unroll
+    for (int j = 0; j < KB; ++j) kk[j] = i0 + j * stride < src.B ? key_at(src, i0 + j * stride) : 0ull;
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      const unsigned long long key = kk[j];
+      if (i0 + j * stride < src.B && (nbits == 0 || (key >> (64 - nbits)) == prefix))
+        atomicAdd(&h[static_cast<int>((key >> shift) & ((1u << db) - 1))], 1u);
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < (1 << db); i += NT)
@@ -201,12 +209,18 @@ __global__ void __launch_bounds__(NT) select_kernel(Src src, Counters* ctr, unsi
     const int nbits = sel.nbits;
     const unsigned long long prefix = sel.prefix;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * NT;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x; i < src.B; i += stride) {
-      const unsigned long long key = key_at(src, i);
-      const unsigned long long kp = nbits == 0 ? 0ull : key >> (64 - nbits);
-      if (kp <= prefix) {
-        const unsigned int slot = atomicAdd(&ctr->taken, 1u);
-        if (slot < static_cast<unsigned int>(CAP)) buf[slot] = key;
+    for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x; i0 < src.B; i0 += KB * stride) {
+      unsigned long long kk[KB];
+#pragma unroll
+      for (int j = 0; j < KB; ++j) kk[j] = i0 + j * stride < src.B ? key_at(src, i0 + j * stride) : 0ull;
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        const unsigned long long key = kk[j];
+        const unsigned long long kp = nbits == 0 ? 0ull : key >> (64 - nbits);
+        if (i0 + j * stride < src.B && kp <= prefix) {
+          const unsigned int slot = atomicAdd(&ctr->taken, 1u);
+          if (slot < static_cast<unsigned int>(CAP)) buf[slot] = key;
+        }
       }
     }
   }
