@@ -87,10 +87,10 @@ constexpr int NT = 128 * NWG;  // (roles by warpgroup, see the header)
 constexpr int REG_BASE = (512 / NWG) & ~7;
 #if KT_R2
 #ifndef KT_REG_HEAD
-#define KT_REG_HEAD 48
+#define KT_REG_HEAD 56
 #endif
 #ifndef KT_REG_ENC
-#define KT_REG_ENC 80
+#define KT_REG_ENC 72
 #endif
 #ifndef KT_REG_R
 #define KT_REG_R 56
