@@ -55,9 +55,9 @@ t0 = buf[0, 0]
 print("chunk " + " ".join(f"{n:>9s}" for n in ["P_arrive", "G1_issued", "G2_issued", "E1_go", "E1_ld", "E1_rfree", "E1_st", "E1_stw", "E1_done", "E2_go", "E2_done"]))
 for q in range(40):
     print(f"{q:5d} " + " ".join(f"{buf[e, q] - t0:9d}" for e in (0, 1, 2, 5, 13, 14, 15, 16, 6, 7, 8)))
-print("producer tile: start v_free_ok digits_done prepared rows_done")
+print("producer tile: start v_free_ok digits_done prepared")
 for ti in range(5):
-    print(ti, *(buf[e, ti] - t0 for e in (24, 25, 31, 26)), buf[30, ti + 1] - t0)
+    print(ti, *(buf[e, ti] - t0 for e in (24, 25, 31, 26)))
 print("producer q: row_start computed x_empty_ok arrive | g1start g1commit")
 for q in range(16, 40):
     print(q, buf[19, q] - t0, buf[20, q] - t0, buf[21, q] - t0, buf[0, q] - t0, "|", buf[22, q] - t0, buf[1, q] - t0)
