@@ -146,7 +146,7 @@ constexpr int TAB = 448;
 #define KT_SLEEP_ENC 0
 #endif
 #ifndef KT_HEAD_SLEEP
-#define KT_HEAD_SLEEP 128  // ns between probes of the head warpgroup's (long) waits (0: hardware wait)
+#define KT_HEAD_SLEEP 64  // ns between probes of the head warpgroup's (long) waits (0: hardware wait)
 #endif
 #ifndef KT_HEAD_SLEEP_Z
 #define KT_HEAD_SLEEP_Z 128  // the head MMA warp's wait for Z1
