@@ -29,7 +29,7 @@
 // a deterministic function of the features, so equal features still score equal.  GEMM1
 // is one K-step instead of two and an X slot is 16 TMEM columns instead of 32.
 //
-// Warp roles (896 threads = 7 warpgroups with the default KT_R2, 1 CTA / SM, 512 TMEM
+// Warp roles (896 threads = 7 warpgroups, 1 CTA / SM, 512 TMEM
 // columns; registers rebalanced per warpgroup with setmaxnreg, which ptxas also takes as
 // each region's compile-time budget):
 //   WG 0 (warps 0-3)    head: thread = TMEM lane = graph; per tile ReLU(D3 + b0) -> Z1
@@ -73,19 +73,12 @@ namespace tcs {
 
 using namespace kt::tc;
 
-#ifndef KT_R2
-#define KT_R2 1  // two R warpgroups, one per chunk parity
-#endif
-#ifndef KT_R_ISSUE
-#define KT_R_ISSUE 0  // 1: the R warpgroups issue their chunks' GEMM2 themselves (no separate MMA warp)
-#endif
-constexpr int WG_R = 2, WG_RO = WG_R + 1 + KT_R2, WG_MMA = WG_RO + 2;  // warpgroup of each role
+constexpr int WG_R = 2, WG_RO = WG_R + 2, WG_MMA = WG_RO + 2;  // warpgroup of each role
 constexpr int NWG = WG_MMA + 1;
 constexpr int NT = 128 * NWG;  // (roles by warpgroup, see the header)
 // per-warpgroup register budgets (setmaxnreg): the NWG warps of an SMSP share its 512
 // registers per lane; the launch gives each REG_BASE, the roles rebalance them
 constexpr int REG_BASE = (512 / NWG) & ~7;
-#if KT_R2
 #ifndef KT_REG_HEAD
 #define KT_REG_HEAD 56
 #endif
@@ -102,10 +95,7 @@ constexpr int REG_BASE = (512 / NWG) & ~7;
 #define KT_REG_MMA 56
 #endif
 constexpr int REG_HEAD = KT_REG_HEAD, REG_ENC = KT_REG_ENC, REG_R = KT_REG_R, REG_RO = KT_REG_RO, REG_MMA = KT_REG_MMA;
-#else
-constexpr int REG_HEAD = 72, REG_ENC = 80, REG_R = 56, REG_RO = 104, REG_MMA = 64;
-#endif
-static_assert(REG_HEAD + REG_ENC + (1 + KT_R2) * REG_R + 2 * REG_RO + REG_MMA <= NWG * REG_BASE, "register budget");
+static_assert(REG_HEAD + REG_ENC + 2 * REG_R + 2 * REG_RO + REG_MMA <= NWG * REG_BASE, "register budget");
 constexpr int GT = 128;   // graphs per tile (one TMEM lane each)
 constexpr int H = 64;
 constexpr int XK = 8;     // folded layer-1 operand width (one tf32 K-step)
@@ -113,20 +103,8 @@ constexpr int XK = 8;     // folded layer-1 operand width (one tf32 K-step)
 #define KT_XS 4
 #endif
 constexpr int XS = KT_XS;  // X ring slots
-#ifndef KT_DR
-#define KT_DR 0
-#endif
-#if KT_DR
-// D1 and R share buffers: GEMM1 writes D1 into columns 0-31 of DR[b], the R warps
-// overwrite them with R hi and put R lo in columns 32-63, GEMM2 reads both; a buffer
-// returns to GEMM1 when GEMM2 is done with it.  Three buffers in the TMEM two D1 + two R
-// buffers took, so GEMM1, R and GEMM2 each run up to three chunks apart.
-constexpr int NB = 3;     // DR buffers
-constexpr int N1 = NB, NR = NB;
-#else
 constexpr int N1 = 2;     // D1 buffers
 constexpr int NR = 2;     // R buffers
-#endif
 #ifndef KT_N2
 #define KT_N2 2
 #endif
@@ -154,17 +132,10 @@ constexpr int TAB = 448;
 
 // TMEM column map (512 allocated)
 constexpr uint32_t T_X = 0;                  // X[s]: hi at 16 s, lo at 16 s + 8
-#if KT_DR
-constexpr uint32_t T_D1 = T_X + 16 * XS;     // DR[b] at T_D1 + 64 b: D1, then R hi (cols 0-31) / lo (32-63)
-constexpr uint32_t T_R = T_D1;
-constexpr int D1_STRIDE = 64;
-constexpr uint32_t T_D2 = T_R + 64 * NR;     // D2[b] at T_D2 + 32 b
-#else
 constexpr uint32_t T_D1 = T_X + 16 * XS;     // D1[b] at T_D1 + 32 b
 constexpr uint32_t T_R = T_D1 + 32 * N1;     // R[b]: hi at T_R + 64 b, lo at +32
 constexpr int D1_STRIDE = 32;
 constexpr uint32_t T_D2 = T_R + 64 * NR;     // D2[b] at T_D2 + 32 b
-#endif
 constexpr uint32_t T_D34 = T_D2 + 32 * N2;   // head accumulator: D3, then D4 (64 columns)
 constexpr uint32_t T_Z = T_D34 + 64;         // head A operand, U then Z1 = ReLU(D3 + b0): hi at T_Z, lo at +64
 static_assert(T_Z + 128 <= 512, "TMEM budget: 512 columns");
@@ -699,11 +670,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         const int s = rx.i, b = r1.i;
         if ((tid & 31) == 0) TRACE(22, q);
         wait_bar(&S.x_full[s], rx.ph);
-#if KT_DR
-        wait_bar(&S.r_empty[b], r1.ph ^ 1);  // GEMM2 of chunk q - NB is done
-#else
         wait_bar(&S.d1_empty[b], r1.ph ^ 1);
-#endif
         if ((tid & 31) == 0) TRACE(23, q);
         const uint32_t xh = tmem + T_X + 16 * s, xl = xh + XK, d = tmem + T_D1 + D1_STRIDE * b;
         const int k = C - 1 - c;
@@ -718,7 +685,7 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
         __syncwarp();
         if (++c == C) c = 0;
       }
-    } else if (warp == 4 * WG_MMA + 1 && !(KT_R2 && KT_R_ISSUE && !KT_DR)) {
+    } else if (warp == 4 * WG_MMA + 1) {
       Ring<NR> rr;
       Ring<N2> r2;
       for (int64_t q = 0; q < n_chunks; ++q, rr.next(), r2.next()) {
@@ -790,17 +757,11 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
     const int quad = warp & 3;
     const int g = 32 * quad + (tid & 31);
     const uint32_t lane = static_cast<uint32_t>((32 * quad) << 16);
-#if KT_R2
     // two R warpgroups, chunks of parity wg - WG_R each: buffer (q % 2) is theirs alone
     static_assert(N1 == 2 && NR == 2, "R parity split needs 2-deep D1 / R rings");
     Ring<1> r1, rr;
     r1.i = rr.i = wg - WG_R;
     for (int64_t q = wg - WG_R; q < n_chunks; q += 2, r1.ph ^= 1u, rr.ph ^= 1u) {
-#else
-    Ring<N1> r1;
-    Ring<NR> rr;
-    for (int64_t q = 0; q < n_chunks; ++q, r1.next(), rr.next()) {
-#endif
       const int b1 = r1.i, b = rr.i;
       role_wait<KT_SLEEP_R>(&S.d1_full[b1], r1.ph);
       __syncwarp();
@@ -811,15 +772,11 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       tmem_ld16(tmem + lane + T_D1 + D1_STRIDE * b1 + 16, v + 16);
       tmem_wait_ld();
       if (g == 0) TRACE(13, q);
-#if !KT_DR
       tc_fence_before();
       warp_arrive(&S.d1_empty[b1]);
-#endif
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = relu(v[j]);
-#if !KT_DR  // (with shared DR buffers the buffer is this stage's until it arrives r_full)
       role_wait<KT_SLEEP_R>(&S.r_empty[b], rr.ph ^ 1);  // GEMM2 of q-NR read R[b]
-#endif
       __syncwarp();
       if (g == 0) TRACE(14, q);
       tc_fence_after();
@@ -842,37 +799,8 @@ score_tc_kernel(const kt_spec_table* __restrict__ tab, kt_dims dims, const float
       tmem_wait_st();
       if (g == 0) TRACE(16, q);
       tc_fence_before();
-#if KT_R2 && KT_R_ISSUE && !KT_DR
-      // GEMM2 of this chunk straight from the warpgroup that produced its operand: a named
-      // barrier over the 4 warps replaces the r_full hand-off to an MMA warp (whose wake-up and
-      // issue slots on a busy SMSP set the chunk cadence)
-      named_sync(1 + (wg - WG_R), 128);
-      if (g == 0) TRACE(6, q);
-      if (quad == 0) {
-        tc_fence_after();
-        role_wait<0>(&S.d2_empty[b], rr.ph ^ 1);  // readout of chunk q - 2 read D2[b]
-        __syncwarp();
-        tc_fence_after();
-        if ((tid & 31) == 0) TRACE(18, q);
-        const uint32_t id32 = idesc_tf32(128, 32);
-        const uint32_t rh = tmem + T_R + 64 * b, rl = rh + 32, d = tmem + T_D2 + 32 * b;
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            mma_tf32_ts(d, rh + 8 * kk, kdesc(S.b2h, 32, kk), id32, kk > 0);
-            mma_tf32_ts(d, rh + 8 * kk, kdesc(S.b2l, 32, kk), id32, 1);
-            mma_tf32_ts(d, rl + 8 * kk, kdesc(S.b2h, 32, kk), id32, 1);
-          }
-          mma_commit(&S.r_empty[b]);
-          mma_commit(&S.d2_full[b]);
-          TRACE(2, q);
-        }
-        __syncwarp();
-      }
-#else
       warp_arrive(&S.r_full[b]);
       if (g == 0) TRACE(6, q);
-#endif
     }
   } else if (wg >= WG_RO && wg < WG_MMA) {
     setmaxnreg<REG_RO>();
